@@ -1,0 +1,184 @@
+/*
+ * npcg.h -- C ABI of libnpcg.so, the B200 (sm_100a) NeuralPCG solve path.
+ *
+ * The reference (`pcgkit`, pure Python + numba) has no FFI: its boundary is
+ * the duck-typed Python API listed next to each entry point below. This
+ * header is the drop-in replacement a binding (ctypes / cffi / pybind) would
+ * bind instead of those Python functions; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch types. "host" pointers are
+ *    ordinary CPU memory, "device" pointers are CUDA global memory on the
+ *    current device. Streams are cudaStream_t passed as void*.
+ *  - Batches: B systems (or B right-hand sides) that share one sparsity
+ *    pattern. Vectors are laid out RHS-minor: v[i*B + b] (n x B, row major).
+ *    Matrix / factor values are either shared ([nnz]) or per system
+ *    ([nnz*B], value of system b for slot p at p*B + b); the `*_batched`
+ *    flags select which.
+ *  - Return codes map 1:1 onto pcgkit.errors (pkg/src/pcgkit/errors.py):
+ *    see NPCG_ERR_*. npcg_last_error() gives the message (thread local).
+ *  - No CPU fallback: every compute entry point launches CUDA kernels and
+ *    fails with NPCG_ERR_CUDA when no sm_100a device is usable.
+ */
+#ifndef NPCG_H
+#define NPCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NPCG_ABI_VERSION 1
+
+/* ---- status codes (pkg/src/pcgkit/errors.py:4-78) ---------------------- */
+#define NPCG_OK                 0
+#define NPCG_ERR_DIMENSION      1  /* DimensionMismatchError (errors.py:8)   */
+#define NPCG_ERR_INVALID_FACTOR 2  /* InvalidFactorError     (errors.py:23)  */
+#define NPCG_ERR_NOT_SPD        3  /* NotSpdError(pivot)     (errors.py:12)  */
+#define NPCG_ERR_BREAKDOWN      4  /* BreakdownError         (errors.py:47)  */
+#define NPCG_ERR_CUDA           5  /* device / launch failure                */
+#define NPCG_ERR_DATA_FORMAT    6  /* DataFormatError        (errors.py:56)  */
+#define NPCG_ERR_ARGUMENT       7  /* ValueError (bad handle / option)       */
+
+/* per-system solve status written by npcg_pcg_solve */
+#define NPCG_STATUS_ACTIVE     0
+#define NPCG_STATUS_CONVERGED  1   /* SolveReport.converged = True           */
+#define NPCG_STATUS_MAXITER    2   /* converged = False (pcg.py:171-176)     */
+#define NPCG_STATUS_BREAKDOWN  3   /* pcg.py:136-140 would raise             */
+
+typedef struct npcg_pattern npcg_pattern;   /* analysed sparsity pattern   */
+typedef struct npcg_gnn npcg_gnn;           /* device-resident GNN weights */
+typedef struct npcg_solver npcg_solver;     /* PCG workspace for (pattern, B) */
+
+const char *npcg_last_error(void);
+int npcg_abi_version(void);
+/* 1 when a CUDA device with compute capability 10.0 is visible. */
+int npcg_device_ok(void);
+
+/* ---- patterns -----------------------------------------------------------
+ * Replaces the pattern work of SparseMatrixCsr.__post_init__ (sparse.py:44-65),
+ * has_full_diagonal / is_symmetric (sparse.py:133-147),
+ * graph_from_system's edge_pair_index (gnn.py:83-88) and
+ * A.strict_lower() (sparse.py:149-153), done once per mesh.
+ *
+ * Input: host CSR with int64 indices, exactly the reference layout.
+ * flags: NPCG_PATTERN_FACTOR requests the triangular-solve schedules
+ * (requires structural symmetry and a full diagonal; returns
+ * NPCG_ERR_DATA_FORMAT otherwise, the error graph_from_system raises).
+ */
+#define NPCG_PATTERN_FACTOR 1
+int npcg_pattern_create(int64_t n, const int64_t *row_ptr_host,
+                        const int64_t *col_idx_host, int flags, npcg_pattern **out);
+int npcg_pattern_destroy(npcg_pattern *p);
+
+typedef struct {
+    int64_t n, nnz, nnz_lower;
+    int32_t full_diagonal, structurally_symmetric, has_factor_schedule;
+    int32_t levels_lower, levels_upper;   /* global level-set depths */
+    int32_t chunks;                       /* contiguous row chunks    */
+    int32_t chunk_rows;                   /* rows per chunk           */
+    int32_t window;                       /* smem ring depth (levels) */
+    int32_t max_level_width;              /* rows per chunk-local level */
+} npcg_pattern_info;
+int npcg_pattern_get_info(const npcg_pattern *p, npcg_pattern_info *info);
+
+/* Device views owned by the pattern (int32). Any may be NULL. */
+int npcg_pattern_device_arrays(const npcg_pattern *p, const int32_t **row_ptr,
+                               const int32_t **col_idx, const int32_t **diag_pos,
+                               const int32_t **pair, const int32_t **lower_slot);
+
+/* Exact value-symmetry test on device for B systems (sparse.py:137-147):
+ * writes ok[b] = 1 when vals[p] == vals[pair[p]] bitwise for every p. */
+int npcg_check_symmetric_values(const npcg_pattern *p, int B, const double *vals,
+                                int vals_batched, int32_t *ok_host, void *stream);
+
+/* ---- elementary kernels (unit parity) -----------------------------------
+ * y = A x for a batch: spmv (sparse.py:213-219, 255-262). */
+int npcg_spmv(const npcg_pattern *A, int B, const double *vals, int vals_batched,
+              const double *x, double *y, void *stream);
+
+/* Factor values on the pattern: S[p] for every off-diagonal slot p holds
+ * L'_{ij} of the unit-lower factor with S symmetric (S[p] == S[pair[p]]).
+ * From strict-lower values in A.strict_lower() slot order (gnn.py:299-311,
+ * preconditioners.py:70-85): */
+int npcg_factor_from_lower(const npcg_pattern *F, int B, const double *lower_vals,
+                           int lower_batched, double *S, void *stream);
+/* ... and back (for LowerFactor views): */
+int npcg_factor_to_lower(const npcg_pattern *F, int B, const double *S,
+                         double *lower_vals, void *stream);
+
+/* z = P^{-1} r with P = (I+L') D (I+L')^T: forward unit solve, D^{-1} scale,
+ * backward transpose solve (sparse.py:222-239, 265-275). D > 0 is the
+ * caller's contract (LowerFactor validation, sparse.py:187-192). */
+int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int S_batched,
+                            const double *D, int D_batched, const double *r, double *z,
+                            void *stream);
+
+/* ---- GNN (gnn.py:106-318) ------------------------------------------------
+ * Weights in the reference's checkpoint layout: for each layer of
+ * _layer_specs order (gnn.py:130-147), W[fan_in][fan_out] row-major then
+ * b[fan_out], concatenated. `width` is the latent F (FEATURE_WIDTH). */
+typedef struct {
+    int32_t width;        /* F: 16 or 64 */
+    int32_t h, l;         /* encoder/decoder hidden width, hidden layers (l == 1) */
+    int32_t h_mp, l_mp;   /* processor hidden width, hidden layers (l_mp == 1) */
+    int32_t n_mp;         /* message-passing rounds */
+    int32_t normalize;    /* GnnHyperParams.normalize */
+    int32_t with_x0_head; /* node_dec present in the weight blob */
+} npcg_gnn_desc;
+int npcg_gnn_create(const npcg_gnn_desc *desc, const double *weights_host,
+                    int64_t n_weights, npcg_gnn **out);
+int npcg_gnn_destroy(npcg_gnn *g);
+
+/* build_learned (gnn.py:314-318) for B systems sharing A's pattern:
+ * runs the GNN on (A_b, rhs_b), symmetrises (gnn.py:284-296) and writes the
+ * factor values S ([nnz*B] or [nnz] when B == 1) and D = diag(A)
+ * ([n*B], layout like vectors). edge_out (nullable) receives the raw edge
+ * scalars M ([nnz*B]); x0_out (nullable) the node head (gnn.py:321-327).
+ * Returns NPCG_ERR_NOT_SPD with *pivot set when some diag(A) <= 0. */
+int npcg_gnn_build_factor(const npcg_gnn *g, const npcg_pattern *A, int B,
+                          const double *A_vals, int A_batched, const double *rhs,
+                          double *S, double *D, double *edge_out, double *x0_out,
+                          int64_t *pivot, void *stream);
+
+/* ---- PCG (pcg.py:75-176) ---------------------------------------------------- */
+typedef struct {
+    int32_t n_thresholds;         /* SolveOptions.thresholds (strictly decreasing) */
+    double thresholds[16];
+    int64_t max_iter;             /* SolveOptions.max_iter or 10*n */
+    int32_t absolute;             /* SolveOptions.absolute */
+    int32_t check_every;          /* host polls convergence every k passes (0 = auto) */
+} npcg_solve_opts;
+
+typedef struct {
+    /* all host arrays, caller allocated */
+    int32_t *status;              /* [B] NPCG_STATUS_* */
+    int64_t *iterations;          /* [B] SolveReport.iterations */
+    int64_t *iterations_to;       /* [B][n_thresholds], -1 = not crossed */
+    double *seconds_to;           /* [B][n_thresholds] device-clock seconds */
+    double *final_relative_residual; /* [B] */
+    double *history;              /* [B][history_cap] ||r_k||, nullable */
+    int64_t history_cap;          /* entries per system (>= max_iter+1 for full) */
+    int64_t *breakdown_iteration; /* [B] k where p'Ap <= 0, else 0 */
+} npcg_solve_report;
+
+/* Solver workspace for a (A pattern, factor pattern, B) triple. F may be
+ * NULL (identity preconditioner, pcg.py:64-72) or equal A. */
+int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B,
+                       npcg_solver **out);
+int npcg_solver_destroy(npcg_solver *s);
+
+/* Batched pcg_solve: all pointers except opts/report are device pointers.
+ * x0 nullable (SolveOptions.x0). S/D ignored when the solver has F == NULL.
+ * Per-system breakdown is reported in report->status; the function itself
+ * returns NPCG_OK unless arguments / CUDA fail. Synchronises `stream`. */
+int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int A_batched,
+                   const double *S, int S_batched, const double *D, int D_batched,
+                   const double *b, double *x, const double *x0,
+                   const npcg_solve_opts *opts, npcg_solve_report *report, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NPCG_H */

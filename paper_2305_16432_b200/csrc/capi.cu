@@ -1,0 +1,650 @@
+// capi.cu -- extern "C" entry points of libnpcg.so (include/npcg.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/npcg.h"
+#include "gnn.cuh"
+#include "kernels.cuh"
+#include "pattern.h"
+
+using namespace npcg;
+
+struct npcg_pattern : public npcg::Pattern {};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define NPCG_CUDA(call)                                                                   \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(NPCG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class T>
+cudaError_t dalloc(T **p, size_t count) {
+    return cudaMalloc((void **)p, std::max<size_t>(count, 1) * sizeof(T));
+}
+
+// Pick the batch group width G (columns per unit) and chunk size for a solve.
+struct SolvePlan {
+    int G = 1, groups = 1, R = 1, use_ring = 1;
+    SchedSet *set = nullptr;
+};
+
+int plan_solve(Pattern *F, int B, SolvePlan &plan, std::string &err) {
+    int G = 1;
+    while (G * 2 <= std::min(B, 8)) G *= 2;
+    if (const char *env = std::getenv("NPCG_GROUP")) {
+        int v = std::atoi(env);
+        if (v >= 1 && v <= kMaxGroup && (v & (v - 1)) == 0) G = std::min(v, std::max(1, B));
+    }
+    for (;;) {
+        const int R = choose_chunk_rows(F->n, B, G);
+        SchedSet *set = F->schedule(R, err);
+        if (!set) return NPCG_ERR_CUDA;
+        const size_t smem = std::max(trsv_smem_bytes(set->fwd, G), trsv_smem_bytes(set->bwd, G));
+        if (smem <= 160 * 1024 || G == 1) {
+            plan.G = G;
+            plan.groups = (B + G - 1) / G;
+            plan.R = R;
+            plan.set = set;
+            plan.use_ring = smem <= 160 * 1024 ? 1 : 0;
+            if (const char *env = std::getenv("NPCG_NO_RING")) plan.use_ring = env[0] == '1' ? 0 : plan.use_ring;
+            return NPCG_OK;
+        }
+        G /= 2;
+    }
+}
+
+int check_stream_device() {
+    int dev = 0, major = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(NPCG_ERR_CUDA, "no CUDA device");
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (major != 10) return fail(NPCG_ERR_CUDA, "libnpcg is built for sm_100a (B200) only");
+    return NPCG_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// solver workspace
+// ---------------------------------------------------------------------------
+struct npcg_solver {
+    const Pattern *A = nullptr;
+    Pattern *F = nullptr;
+    std::unique_ptr<npcg_pattern> identity;  // when F == NULL
+    int B = 1;
+    SolvePlan plan;
+    double *R = nullptr, *P = nullptr, *Z = nullptr, *AP = nullptr, *Y = nullptr;
+    // state
+    int *status = nullptr, *phase = nullptr, *pflag = nullptr;
+    long long *k = nullptr, *bd = nullptr, *iter_to = nullptr;
+    unsigned long long *t_to = nullptr, *t_start = nullptr;
+    double *scale = nullptr, *rz = nullptr, *alpha = nullptr, *beta = nullptr, *rel = nullptr,
+           *final_rel = nullptr;
+    double *history = nullptr;
+    long long history_cap = 0;
+    int *active_count = nullptr, *drift_count = nullptr, *progress = nullptr;
+    Ctl *ctl = nullptr;
+    double *partial = nullptr;
+    int *h_active = nullptr;  // pinned
+    ~npcg_solver() {
+        void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
+                        alpha, beta, rel, final_rel, history, active_count, drift_count, progress, ctl, partial};
+        for (void *p : ptrs)
+            if (p) cudaFree(p);
+        if (h_active) cudaFreeHost(h_active);
+    }
+};
+
+extern "C" {
+
+const char *npcg_last_error(void) { return g_err.c_str(); }
+int npcg_abi_version(void) { return NPCG_ABI_VERSION; }
+
+int npcg_device_ok(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return 0;
+    int dev = 0, major = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    return major == 10 ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+int npcg_pattern_create(int64_t n, const int64_t *rp, const int64_t *col, int flags, npcg_pattern **out) {
+    if (!out) return fail(NPCG_ERR_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (n < 0 || !rp || (n > 0 && !col && rp[n] > 0))
+        return fail(NPCG_ERR_DIMENSION, "row_ptr must have length n+1");
+    // sparse.py:44-65 invariants
+    if (rp[0] != 0) return fail(NPCG_ERR_DIMENSION, "row_ptr endpoints disagree with nnz");
+    const int64_t nnz = rp[n];
+    if (nnz >= (1ll << 31) || n >= (1ll << 31)) return fail(NPCG_ERR_DIMENSION, "pattern exceeds int32 indexing");
+    for (int64_t i = 0; i < n; ++i)
+        if (rp[i + 1] < rp[i]) return fail(NPCG_ERR_DIMENSION, "row_ptr must be non-decreasing");
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            if (col[p] < 0 || col[p] >= n) return fail(NPCG_ERR_DIMENSION, "column index out of range");
+            if (p > rp[i] && col[p] <= col[p - 1])
+                return fail(NPCG_ERR_DIMENSION, "columns must strictly increase within rows");
+        }
+    if (int rc = check_stream_device()) return rc;
+    auto P = std::make_unique<npcg_pattern>();
+    P->n = n;
+    P->nnz = nnz;
+    P->h_rp.assign(rp, rp + n + 1);
+    P->h_col.assign(col, col + nnz);
+    P->h_dp.assign(n, -1);
+    P->h_pair.assign(nnz, -1);
+    int64_t ndiag = 0, npair = 0;
+    std::vector<int32_t> lower;
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            const int64_t j = col[p];
+            if (j == i) {
+                P->h_dp[i] = (int32_t)p;
+                ++ndiag;
+            }
+            if (j < i) lower.push_back((int32_t)p);
+            // reverse edge (j, i): binary search in row j (gnn.py:86-88)
+            const int64_t *b0 = col + rp[j], *b1 = col + rp[j + 1];
+            const int64_t *f = std::lower_bound(b0, b1, i);
+            if (f != b1 && *f == i) {
+                P->h_pair[p] = (int32_t)(f - col);
+                ++npair;
+            }
+        }
+    P->full_diag = ndiag == n;
+    P->symmetric = npair == nnz;
+    P->nnz_lower = (int64_t)lower.size();
+    P->factor_ok = P->full_diag && P->symmetric;
+    if ((flags & NPCG_PATTERN_FACTOR) && !P->full_diag)
+        return fail(NPCG_ERR_DATA_FORMAT, "matrix is missing explicit diagonal entries");
+    if ((flags & NPCG_PATTERN_FACTOR) && !P->symmetric)
+        return fail(NPCG_ERR_DATA_FORMAT, "matrix pattern is not symmetric");
+    NPCG_CUDA(dalloc(&P->rp, n + 1));
+    NPCG_CUDA(dalloc(&P->col, nnz));
+    NPCG_CUDA(dalloc(&P->dp, n));
+    NPCG_CUDA(dalloc(&P->pair, nnz));
+    NPCG_CUDA(dalloc(&P->lower_slot, lower.size()));
+    NPCG_CUDA(dalloc(&P->src, nnz));
+    {
+        std::vector<int32_t> src(nnz);
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t p = rp[i]; p < rp[i + 1]; ++p) src[p] = (int32_t)i;
+        if (nnz) NPCG_CUDA(cudaMemcpy(P->src, src.data(), nnz * 4, cudaMemcpyHostToDevice));
+    }
+    NPCG_CUDA(cudaMemcpy(P->rp, P->h_rp.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+    if (nnz) NPCG_CUDA(cudaMemcpy(P->col, P->h_col.data(), nnz * 4, cudaMemcpyHostToDevice));
+    if (n) NPCG_CUDA(cudaMemcpy(P->dp, P->h_dp.data(), n * 4, cudaMemcpyHostToDevice));
+    if (nnz) NPCG_CUDA(cudaMemcpy(P->pair, P->h_pair.data(), nnz * 4, cudaMemcpyHostToDevice));
+    if (!lower.empty())
+        NPCG_CUDA(cudaMemcpy(P->lower_slot, lower.data(), lower.size() * 4, cudaMemcpyHostToDevice));
+    *out = P.release();
+    return NPCG_OK;
+}
+
+int npcg_pattern_destroy(npcg_pattern *p) {
+    delete p;
+    return NPCG_OK;
+}
+
+int npcg_pattern_get_info(const npcg_pattern *pc, npcg_pattern_info *info) {
+    if (!pc || !info) return fail(NPCG_ERR_ARGUMENT, "NULL argument");
+    npcg_pattern *p = const_cast<npcg_pattern *>(pc);
+    std::memset(info, 0, sizeof(*info));
+    info->n = p->n;
+    info->nnz = p->nnz;
+    info->nnz_lower = p->nnz_lower;
+    info->full_diagonal = p->full_diag;
+    info->structurally_symmetric = p->symmetric;
+    info->has_factor_schedule = p->factor_ok;
+    if (p->factor_ok) {  // report the most recently built schedule, if any (never builds one)
+        std::lock_guard<std::mutex> lock(p->mu);
+        if (p->scheds.empty()) return NPCG_OK;
+        SchedSet *s = p->scheds.rbegin()->second.get();
+        info->levels_lower = s->fwd.levels_global;
+        info->levels_upper = s->bwd.levels_global;
+        info->chunks = s->fwd.chunks;
+        info->chunk_rows = s->fwd.chunk_rows;
+        info->window = std::max(s->fwd.window, s->bwd.window);
+        info->max_level_width = std::max(s->fwd.maxw, s->bwd.maxw);
+    }
+    return NPCG_OK;
+}
+
+int npcg_pattern_device_arrays(const npcg_pattern *p, const int32_t **row_ptr, const int32_t **col_idx,
+                               const int32_t **diag_pos, const int32_t **pair, const int32_t **lower_slot) {
+    if (!p) return fail(NPCG_ERR_ARGUMENT, "NULL pattern");
+    if (row_ptr) *row_ptr = p->rp;
+    if (col_idx) *col_idx = p->col;
+    if (diag_pos) *diag_pos = p->dp;
+    if (pair) *pair = p->pair;
+    if (lower_slot) *lower_slot = p->lower_slot;
+    return NPCG_OK;
+}
+
+int npcg_check_symmetric_values(const npcg_pattern *p, int B, const double *vals, int vb, int32_t *ok_host,
+                                void *stream) {
+    if (!p || !ok_host || B < 1) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int b = 0; b < B; ++b) ok_host[b] = p->symmetric ? 1 : 0;
+    if (!p->symmetric || p->nnz == 0) return NPCG_OK;
+    int *d_ok = nullptr;
+    NPCG_CUDA(dalloc(&d_ok, B));
+    NPCG_CUDA(cudaMemcpyAsync(d_ok, ok_host, B * 4, cudaMemcpyHostToDevice, s));
+    symmetric_check_kernel<<<std::min<long long>((p->nnz * B + 255) / 256, 4096), 256, 0, s>>>(p->nnz, B, vb,
+                                                                                           p->pair, vals, d_ok);
+    NPCG_CUDA(cudaGetLastError());
+    NPCG_CUDA(cudaMemcpyAsync(ok_host, d_ok, B * 4, cudaMemcpyDeviceToHost, s));
+    NPCG_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d_ok);
+    return NPCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+int npcg_spmv(const npcg_pattern *A, int B, const double *vals, int vb, const double *x, double *y, void *stream) {
+    if (!A || B < 1 || B > kMaxBatch) return fail(NPCG_ERR_ARGUMENT, "bad pattern or batch");
+    if (A->n == 0) return NPCG_OK;
+    SpmvArgs a;
+    a.n = (int)A->n;
+    a.B = B;
+    a.rp = A->rp;
+    a.col = A->col;
+    a.vals = vals;
+    a.vb = vb;
+    a.X = x;
+    a.Y = y;
+    a.op = SPMV_PLAIN;
+    NPCG_CUDA(launch_spmv(a, (cudaStream_t)stream));
+    return NPCG_OK;
+}
+
+int npcg_factor_from_lower(const npcg_pattern *F, int B, const double *lower, int lb, double *S, void *stream) {
+    if (!F || B < 1) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    if (!F->factor_ok) return fail(NPCG_ERR_DATA_FORMAT, "pattern cannot carry a factor");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (F->nnz) NPCG_CUDA(cudaMemsetAsync(S, 0, (size_t)F->nnz * B * 8, s));
+    if (F->nnz_lower) {
+        const long long work = F->nnz_lower * (long long)B;
+        factor_from_lower_kernel<<<(int)std::min<long long>((work + 255) / 256, 8192), 256, 0, s>>>(
+            (int)F->nnz_lower, B, lb, F->lower_slot, F->pair, lower, S);
+        NPCG_CUDA(cudaGetLastError());
+    }
+    return NPCG_OK;
+}
+
+int npcg_factor_to_lower(const npcg_pattern *F, int B, const double *S, double *lower, void *stream) {
+    if (!F || B < 1) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    if (F->nnz_lower) {
+        const long long work = F->nnz_lower * (long long)B;
+        factor_to_lower_kernel<<<(int)std::min<long long>((work + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(
+            (int)F->nnz_lower, B, F->lower_slot, S, lower);
+        NPCG_CUDA(cudaGetLastError());
+    }
+    return NPCG_OK;
+}
+
+static int make_identity_pattern(int64_t n, std::unique_ptr<npcg_pattern> &out) {
+    std::vector<int64_t> rp(n + 1), col(n);
+    for (int64_t i = 0; i <= n; ++i) rp[i] = i;
+    for (int64_t i = 0; i < n; ++i) col[i] = i;
+    npcg_pattern *p = nullptr;
+    int rc = npcg_pattern_create(n, rp.data(), col.data(), NPCG_PATTERN_FACTOR, &p);
+    out.reset(p);
+    return rc;
+}
+
+// ---------------------------------------------------------------------------
+int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg_solver **out) {
+    if (!A || !out || B < 1 || B > kMaxBatch) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    if (F && F->n != A->n) return fail(NPCG_ERR_DIMENSION, "factor and matrix disagree on dimension");
+    auto s = std::make_unique<npcg_solver>();
+    s->A = A;
+    s->B = B;
+    if (F) {
+        s->F = const_cast<npcg_pattern *>(F);
+    } else {
+        if (int rc = make_identity_pattern(A->n, s->identity)) return rc;
+        s->F = s->identity.get();
+    }
+    std::string err;
+    if (int rc = plan_solve(s->F, B, s->plan, err)) return fail(rc, err);
+    const size_t nB = (size_t)A->n * B;
+    NPCG_CUDA(dalloc(&s->R, nB));
+    NPCG_CUDA(dalloc(&s->P, nB));
+    NPCG_CUDA(dalloc(&s->Z, nB));
+    NPCG_CUDA(dalloc(&s->AP, nB));
+    NPCG_CUDA(dalloc(&s->Y, nB));
+    NPCG_CUDA(dalloc(&s->status, B));
+    NPCG_CUDA(dalloc(&s->phase, B));
+    NPCG_CUDA(dalloc(&s->pflag, B));
+    NPCG_CUDA(dalloc(&s->k, B));
+    NPCG_CUDA(dalloc(&s->bd, B));
+    NPCG_CUDA(dalloc(&s->iter_to, (size_t)B * kMaxThresholds));
+    NPCG_CUDA(dalloc(&s->t_to, (size_t)B * kMaxThresholds));
+    NPCG_CUDA(dalloc(&s->t_start, 1));
+    NPCG_CUDA(dalloc(&s->scale, B));
+    NPCG_CUDA(dalloc(&s->rz, B));
+    NPCG_CUDA(dalloc(&s->alpha, B));
+    NPCG_CUDA(dalloc(&s->beta, B));
+    NPCG_CUDA(dalloc(&s->rel, B));
+    NPCG_CUDA(dalloc(&s->final_rel, B));
+    NPCG_CUDA(dalloc(&s->active_count, 1));
+    NPCG_CUDA(dalloc(&s->drift_count, 1));
+    const int chunks = s->plan.set->fwd.chunks;
+    const size_t units = (size_t)chunks * s->plan.groups;
+    NPCG_CUDA(dalloc(&s->progress, units));
+    NPCG_CUDA(cudaMemset(s->progress, 0, std::max<size_t>(units, 1) * 4));
+    NPCG_CUDA(dalloc(&s->ctl, 1));
+    NPCG_CUDA(cudaMemset(s->ctl, 0, sizeof(Ctl)));
+    NPCG_CUDA(cudaMemset(s->drift_count, 0, 4));
+    const size_t part = std::max<size_t>((size_t)kReduceBlocksPerSm * num_sms() * B, units * s->plan.G);
+    NPCG_CUDA(dalloc(&s->partial, part));
+    NPCG_CUDA(cudaMallocHost((void **)&s->h_active, sizeof(int)));
+    *out = s.release();
+    return NPCG_OK;
+}
+
+int npcg_solver_destroy(npcg_solver *s) {
+    delete s;
+    return NPCG_OK;
+}
+
+static SolveState make_state(npcg_solver *s, const npcg_solve_opts *o) {
+    SolveState st{};
+    st.status = s->status;
+    st.phase = s->phase;
+    st.pflag = s->pflag;
+    st.k = s->k;
+    st.breakdown_at = s->bd;
+    st.scale = s->scale;
+    st.rz = s->rz;
+    st.alpha = s->alpha;
+    st.beta = s->beta;
+    st.rel = s->rel;
+    st.final_rel = s->final_rel;
+    st.iter_to = s->iter_to;
+    st.t_to = s->t_to;
+    st.history = s->history;
+    st.history_cap = s->history_cap;
+    st.t_start = s->t_start;
+    st.active_count = s->active_count;
+    st.T = o->n_thresholds;
+    for (int t = 0; t < o->n_thresholds; ++t) st.thr[t] = o->thresholds[t];
+    st.max_iter = o->max_iter;
+    st.absolute = o->absolute;
+    return st;
+}
+
+static TrsvArgs trsv_args(npcg_solver *s, bool upper, int mode, const double *S, int sb, const double *D, int db) {
+    TrsvArgs t;
+    const Pattern *F = s->F;
+    t.n = (int)F->n;
+    t.B = s->B;
+    t.G = s->plan.G;
+    t.groups = s->plan.groups;
+    t.upper = upper;
+    t.mode = mode;
+    t.use_ring = s->plan.use_ring;
+    t.rp = F->rp;
+    t.dp = F->dp;
+    t.col = F->col;
+    t.dep = s->plan.set->dep;
+    t.sched = upper ? s->plan.set->bwd : s->plan.set->fwd;
+    t.units = t.sched.chunks * t.groups;
+    t.S = S;
+    t.s_batched = sb;
+    t.D = D;
+    t.d_batched = db;
+    t.progress = s->progress;
+    t.ctl = s->ctl;
+    t.partial = s->partial;
+    t.drift_count = s->drift_count;
+    return t;
+}
+
+int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int sb, const double *D, int db,
+                            const double *r, double *z, void *stream) {
+    if (!F || B < 1 || B > kMaxBatch) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    if (!F->factor_ok) return fail(NPCG_ERR_DATA_FORMAT, "pattern cannot carry a factor");
+    if (F->n == 0) return NPCG_OK;
+    // a throw-away solver supplies the schedule, scratch and counters
+    npcg_solver *s = nullptr;
+    if (int rc = npcg_solver_create(F, F, B, &s)) return rc;
+    std::unique_ptr<npcg_solver> guard(s);
+    cudaStream_t st = (cudaStream_t)stream;
+    TrsvArgs f = trsv_args(s, false, TRSV_PLAIN, S, sb, D, db);
+    f.in = r;
+    f.out = s->Y;
+    NPCG_CUDA(launch_trsv(f, st));
+    TrsvArgs b = trsv_args(s, true, TRSV_PLAIN, S, sb, D, db);
+    b.in = s->Y;
+    b.out = z;
+    NPCG_CUDA(launch_trsv(b, st));
+    NPCG_CUDA(cudaStreamSynchronize(st));
+    return NPCG_OK;
+}
+
+int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S, int sb, const double *D, int db,
+                   const double *bvec, double *x, const double *x0, const npcg_solve_opts *o,
+                   npcg_solve_report *rep, void *stream) {
+    if (!s || !o || !rep || !bvec || !x) return fail(NPCG_ERR_ARGUMENT, "NULL argument");
+    if (o->n_thresholds < 1 || o->n_thresholds > kMaxThresholds)
+        return fail(NPCG_ERR_DIMENSION, "at least one threshold required");
+    for (int t = 0; t < o->n_thresholds; ++t) {
+        if (!(o->thresholds[t] > 0.0 && o->thresholds[t] < 1.0))
+            return fail(NPCG_ERR_DIMENSION, "thresholds must lie in (0, 1)");
+        if (t && !(o->thresholds[t] < o->thresholds[t - 1]))
+            return fail(NPCG_ERR_DIMENSION, "thresholds must be strictly decreasing");
+    }
+    if (o->max_iter < 1) return fail(NPCG_ERR_DIMENSION, "max_iter must be at least 1");
+    const int B = s->B, T = o->n_thresholds;
+    const int n = (int)s->A->n;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool identity = s->identity != nullptr;
+    // identity preconditioner: S unused, D = 1
+    static double *ones = nullptr;
+    static size_t ones_n = 0;
+    if (identity) {
+        if (ones_n < (size_t)n) {
+            if (ones) cudaFree(ones);
+            NPCG_CUDA(dalloc(&ones, n));
+            std::vector<double> h(n, 1.0);
+            NPCG_CUDA(cudaMemcpy(ones, h.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
+            ones_n = n;
+        }
+        S = ones;  // never read: identity pattern has no off-diagonal entries
+        sb = 0;
+        D = ones;
+        db = 0;
+    }
+    // history buffer
+    const long long cap = rep->history ? std::max<long long>(rep->history_cap, 1) : 1;
+    if (cap > s->history_cap || !s->history) {
+        if (s->history) cudaFree(s->history);
+        s->history = nullptr;
+        NPCG_CUDA(dalloc(&s->history, (size_t)cap * B));
+        s->history_cap = cap;
+    }
+    SolveState sst = make_state(s, o);
+    sst.history_cap = rep->history ? cap : 1;
+    if (n == 0) {
+        for (int b = 0; b < B; ++b) {
+            rep->status[b] = NPCG_STATUS_CONVERGED;
+            rep->iterations[b] = 0;
+        }
+        return NPCG_OK;
+    }
+    const long long nB = (long long)n * B;
+    const int ew_grid = (int)std::min<long long>((nB + 255) / 256, 4 * 1024);
+
+    init_state_kernel<<<(B + 127) / 128, 128, 0, st>>>(sst, B, cap);
+    NPCG_CUDA(cudaGetLastError());
+    normb_kernel<<<std::min(kReduceBlocksPerSm * num_sms(), std::max(1, n / 64)), kSpmvThreads, 0, st>>>(
+        n, B, bvec, sst, s->partial, s->ctl);
+    NPCG_CUDA(cudaGetLastError());
+    init_x_kernel<<<ew_grid, 256, 0, st>>>(nB, B, x0, x, sst);
+    NPCG_CUDA(cudaGetLastError());
+
+    SpmvArgs sp;
+    sp.n = n;
+    sp.B = B;
+    sp.rp = s->A->rp;
+    sp.col = s->A->col;
+    sp.vals = A_vals;
+    sp.vb = ab;
+    sp.st = sst;
+    sp.partial = s->partial;
+    sp.ctl = s->ctl;
+    sp.drift_count = s->drift_count;
+    // r = b - A x0 (or b)
+    SpmvArgs init = sp;
+    init.op = SPMV_RESID_INIT;
+    init.X = x;
+    init.Bv = bvec;
+    init.R = s->R;
+    init.has_x = x0 != nullptr;
+    NPCG_CUDA(launch_spmv(init, st));
+
+    SpmvArgs apdot = sp;
+    apdot.op = SPMV_APDOT;
+    apdot.X = s->P;
+    apdot.Y = s->AP;
+    SpmvArgs drift = sp;
+    drift.op = SPMV_RESID_DRIFT;
+    drift.X = x;
+    drift.Bv = bvec;
+    drift.R = s->R;
+    TrsvArgs fw = trsv_args(s, false, TRSV_PCG, S, sb, D, db);
+    fw.in = s->R;
+    fw.out = s->Y;
+    fw.R = s->R;
+    fw.X = x;
+    fw.P = s->P;
+    fw.AP = s->AP;
+    fw.st = sst;
+    TrsvArgs bw = trsv_args(s, true, TRSV_PCG, S, sb, D, db);
+    bw.in = s->Y;
+    bw.out = s->Z;
+    bw.R = s->R;
+    bw.st = sst;
+
+    int check = o->check_every > 0 ? o->check_every : 8;
+    const long long max_passes = 2 * o->max_iter + 8;
+    long long passes = 0;
+    for (;;) {
+        for (int q = 0; q < check; ++q) {
+            NPCG_CUDA(launch_spmv(apdot, st));
+            NPCG_CUDA(launch_trsv(fw, st));
+            NPCG_CUDA(launch_spmv(drift, st));
+            NPCG_CUDA(launch_trsv(bw, st));
+            pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, sst);
+            NPCG_CUDA(cudaGetLastError());
+        }
+        passes += check;
+        count_active_kernel<<<1, 256, 0, st>>>(sst, B);
+        NPCG_CUDA(cudaMemcpyAsync(s->h_active, s->active_count, 4, cudaMemcpyDeviceToHost, st));
+        NPCG_CUDA(cudaStreamSynchronize(st));
+        if (*s->h_active == 0 || passes >= max_passes) break;
+        if (check < 64) check *= 2;
+    }
+    // report
+    std::vector<int> status(B);
+    NPCG_CUDA(cudaMemcpy(status.data(), s->status, B * 4, cudaMemcpyDeviceToHost));
+    bool any_max = false;
+    for (int b = 0; b < B; ++b) any_max |= status[b] == ST_MAXITER || status[b] == ST_ACTIVE;
+    if (any_max) {
+        // columns still ACTIVE after the pass budget count as max-iter
+        SpmvArgs fin = sp;
+        fin.op = SPMV_RESID_FINAL;
+        fin.X = x;
+        fin.Bv = bvec;
+        NPCG_CUDA(launch_spmv(fin, st));
+    }
+    std::vector<long long> kk(B), itto((size_t)B * T), bdv(B);
+    std::vector<unsigned long long> tto((size_t)B * T);
+    unsigned long long t0 = 0;
+    NPCG_CUDA(cudaMemcpyAsync(kk.data(), s->k, B * 8, cudaMemcpyDeviceToHost, st));
+    NPCG_CUDA(cudaMemcpyAsync(bdv.data(), s->bd, B * 8, cudaMemcpyDeviceToHost, st));
+    NPCG_CUDA(cudaMemcpyAsync(itto.data(), s->iter_to, (size_t)B * T * 8, cudaMemcpyDeviceToHost, st));
+    NPCG_CUDA(cudaMemcpyAsync(tto.data(), s->t_to, (size_t)B * T * 8, cudaMemcpyDeviceToHost, st));
+    NPCG_CUDA(cudaMemcpyAsync(&t0, s->t_start, 8, cudaMemcpyDeviceToHost, st));
+    NPCG_CUDA(cudaMemcpyAsync(rep->final_relative_residual, s->final_rel, B * 8, cudaMemcpyDeviceToHost, st));
+    NPCG_CUDA(cudaStreamSynchronize(st));
+    long long kmax = 0;
+    for (int b = 0; b < B; ++b) {
+        rep->status[b] = status[b] == ST_ACTIVE ? NPCG_STATUS_MAXITER : status[b];
+        rep->iterations[b] = kk[b];
+        if (rep->breakdown_iteration) rep->breakdown_iteration[b] = bdv[b];
+        kmax = std::max(kmax, kk[b]);
+        for (int t = 0; t < T; ++t) {
+            rep->iterations_to[(size_t)b * T + t] = itto[(size_t)b * T + t];
+            rep->seconds_to[(size_t)b * T + t] =
+                itto[(size_t)b * T + t] >= 0 ? (double)(tto[(size_t)b * T + t] - t0) * 1e-9 : -1.0;
+        }
+    }
+    if (rep->history) {
+        const long long w = std::min<long long>(kmax + 1, cap);
+        NPCG_CUDA(cudaMemcpy2DAsync(rep->history, (size_t)rep->history_cap * 8, s->history, (size_t)cap * 8,
+                                    (size_t)w * 8, B, cudaMemcpyDeviceToHost, st));
+        NPCG_CUDA(cudaStreamSynchronize(st));
+    }
+    return NPCG_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// GNN
+// ---------------------------------------------------------------------------
+struct npcg_gnn : public npcg::GnnDev {};
+
+extern "C" {
+
+int npcg_gnn_create(const npcg_gnn_desc *desc, const double *weights, int64_t n_weights, npcg_gnn **out) {
+    if (!desc || !weights || !out) return fail(NPCG_ERR_ARGUMENT, "NULL argument");
+    *out = nullptr;
+    if (int rc = check_stream_device()) return rc;
+    auto g = std::make_unique<npcg_gnn>();
+    std::string err = gnn_init(*g, *desc, weights, n_weights);
+    if (!err.empty()) return fail(NPCG_ERR_DIMENSION, err);
+    *out = g.release();
+    return NPCG_OK;
+}
+
+int npcg_gnn_destroy(npcg_gnn *g) {
+    delete g;
+    return NPCG_OK;
+}
+
+int npcg_gnn_build_factor(const npcg_gnn *g, const npcg_pattern *A, int B, const double *A_vals, int ab,
+                          const double *rhs, double *S, double *D, double *edge_out, double *x0_out, int64_t *pivot,
+                          void *stream) {
+    if (!g || !A || !A_vals || !rhs || !S || !D || B < 1 || B > kMaxBatch) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    if (!A->full_diag) return fail(NPCG_ERR_DATA_FORMAT, "matrix is missing explicit diagonal entries");
+    if (!A->symmetric) return fail(NPCG_ERR_DATA_FORMAT, "matrix values are not symmetric");
+    int64_t piv = -1;
+    std::string err;
+    const int rc = gnn_build(*g, *A, B, A_vals, ab, rhs, S, D, edge_out, x0_out, &piv, (cudaStream_t)stream, err);
+    if (pivot) *pivot = piv;
+    if (rc) return fail(rc, err);
+    return NPCG_OK;
+}
+
+}  // extern "C"

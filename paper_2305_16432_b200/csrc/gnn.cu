@@ -1,0 +1,540 @@
+// gnn.cu -- sm_100a kernels for the learned preconditioner's GNN
+// (reference: pkg/src/pcgkit/gnn.py:227-318 over autodiff.py:113-253).
+//
+// Reference-mode network, fp32 arithmetic (north_star: "fp32 GNN"), input
+// statistics and all factor assembly in fp64:
+//   v = MLP_node_enc((b - mu_b)/sd_b)          e = MLP_edge_enc((A - mu_A)/sd_A)
+//   repeat n_mp: agg_i = sum_{p in row i} e_p * v_{col p}
+//                v = MLP_mp.node([v | agg]);  e = MLP_mp.edge([e | v_src | v_dst])
+//   M = MLP_edge_dec(e);  L'_s = (M_s + M_pair(s)) / 2;  D = diag(A)
+// The per-round MLPs run as register-tiled fp32 GEMM tiles from shared
+// memory inside persistent CTAs (weights loaded once per CTA); the
+// encoders / decoders are one thread per item with weights broadcast
+// from shared memory. Nothing is atomically accumulated: aggregation is a
+// CSR row walk in stored order, so the pass is deterministic.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "gnn.cuh"
+#include "kernels.cuh"
+
+namespace npcg {
+
+constexpr int kGnnThreads = 256;
+constexpr int kMaxHidden = 128;
+
+GnnDev::~GnnDev() {
+    if (w) cudaFree(w);
+}
+
+std::string gnn_init(GnnDev &g, const npcg_gnn_desc &d, const double *weights, int64_t n_weights) {
+    if (d.l != 1 || d.l_mp != 1) return "GPU GNN supports l == l_mp == 1 (one hidden layer per MLP)";
+    if (d.width != 16 && d.width != 64) return "latent width must be 16 or 64";
+    if (d.n_mp < 1 || d.n_mp > 16) return "n_mp must be in [1, 16]";
+    if (d.h < 1 || d.h > kMaxHidden) return "encoder/decoder hidden width must be in [1, 128]";
+    const int F = d.width, hm = d.h_mp;
+    const bool ok_hm = (F == 16 && (hm == 8 || hm == 16 || hm == 32)) || (F == 64 && (hm == 32 || hm == 64));
+    if (!ok_hm) return "unsupported (width, h_mp) combination";
+    g.d = d;
+    int64_t off = 0;
+    auto layer = [&](LayerOff &L, int fi, int fo) {
+        L.w = off;
+        off += (int64_t)fi * fo;
+        L.b = off;
+        off += fo;
+    };
+    layer(g.node_enc[0], 1, d.h);
+    layer(g.node_enc[1], d.h, F);
+    layer(g.edge_enc[0], 1, d.h);
+    layer(g.edge_enc[1], d.h, F);
+    for (int r = 0; r < d.n_mp; ++r) {
+        layer(g.mp_node[r][0], 2 * F, hm);
+        layer(g.mp_node[r][1], hm, F);
+        layer(g.mp_edge[r][0], 3 * F, hm);
+        layer(g.mp_edge[r][1], hm, F);
+    }
+    layer(g.edge_dec[0], F, d.h);
+    layer(g.edge_dec[1], d.h, 1);
+    if (d.with_x0_head) {
+        layer(g.node_dec[0], F, d.h);
+        layer(g.node_dec[1], d.h, 1);
+    }
+    if (off != n_weights) return "weight blob length does not match the hyper-parameters";
+    std::vector<float> h(off);
+    for (int64_t i = 0; i < off; ++i) h[i] = (float)weights[i];
+    if (cudaMalloc(&g.w, std::max<int64_t>(off, 1) * sizeof(float)) != cudaSuccess) return "cudaMalloc failed";
+    if (cudaMemcpy(g.w, h.data(), off * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+        return "cudaMemcpy failed";
+    g.n_floats = off;
+    return "";
+}
+
+// ---------------------------------------------------------------------------
+// per-column mean / population std (gnn.py:42-51), fp64, fixed order
+// ---------------------------------------------------------------------------
+__global__ void colstat_partial_kernel(long long count, int B, const double *x, const double *mean,
+                                       double *partial) {
+    __shared__ double red[kGnnThreads];
+    const int cols = B < kGnnThreads ? B : kGnnThreads;
+    const int rows_per = kGnnThreads / cols;
+    for (int b0 = 0; b0 < B; b0 += cols) {
+        const int b = b0 + threadIdx.x % cols, r0 = threadIdx.x / cols;
+        double s = 0.0;
+        if (b < B && r0 < rows_per) {
+            const double mu = mean ? mean[b] : 0.0;
+            for (long long i = (long long)blockIdx.x * rows_per + r0; i < count; i += (long long)gridDim.x * rows_per) {
+                const double v = x[(size_t)i * B + b];
+                s = mean ? __dadd_rn(s, __dmul_rn(v - mu, v - mu)) : __dadd_rn(s, v);
+            }
+        }
+        red[threadIdx.x] = s;
+        __syncthreads();
+        if (threadIdx.x < cols && b0 + threadIdx.x < B) {
+            double t = 0.0;
+            for (int q = 0; q < rows_per; ++q) t = __dadd_rn(t, red[q * cols + threadIdx.x]);
+            partial[(size_t)blockIdx.x * B + b0 + threadIdx.x] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// mode 0: out = sum/count (mean); mode 1: out = sqrt(sum/count) or 1 if 0.
+__global__ void colstat_final_kernel(long long count, int B, int nblk, const double *partial, double *out,
+                                     int mode) {
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        double t = 0.0;
+        for (int k = 0; k < nblk; ++k) t = __dadd_rn(t, partial[(size_t)k * B + b]);
+        if (count == 0) {
+            out[b] = mode ? 1.0 : 0.0;
+            continue;
+        }
+        const double m = t / (double)count;
+        if (mode == 0) out[b] = m;
+        else {
+            const double sd = sqrt(m);
+            out[b] = sd > 0.0 ? sd : 1.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// encoders: scalar input -> h -> F  (gnn.py:247-248)
+// items are (system b, index i); input x[i*xs + b*xb]; out[(b*count + i)*F]
+// ---------------------------------------------------------------------------
+template <int F>
+__global__ void __launch_bounds__(kGnnThreads) encode_kernel(long long count, int B, const double *x, int xb,
+                                                             const double *mean, const double *sd, int normalize,
+                                                             const float *W1, const float *b1, const float *W2,
+                                                             const float *b2, int h, float *out) {
+    __shared__ float sW1[kMaxHidden], sb1[kMaxHidden];
+    __shared__ __align__(16) float sW2[kMaxHidden * F];
+    __shared__ __align__(16) float sb2[F];
+    for (int k = threadIdx.x; k < h; k += blockDim.x) {
+        sW1[k] = W1[k];
+        sb1[k] = b1[k];
+    }
+    for (int k = threadIdx.x; k < h * F; k += blockDim.x) sW2[k] = W2[k];
+    for (int k = threadIdx.x; k < F; k += blockDim.x) sb2[k] = b2[k];
+    __syncthreads();
+    const long long total = count * B;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(q / count);
+        const long long i = q % count;
+        double xv = xb ? x[(size_t)i * B + b] : x[i];
+        if (normalize) xv = (xv - mean[b]) / sd[b];
+        const float xf = (float)xv;
+        float acc[F];
+#pragma unroll
+        for (int f = 0; f < F; ++f) acc[f] = sb2[f];
+        for (int k = 0; k < h; ++k) {
+            const float hk = fmaxf(fmaf(xf, sW1[k], sb1[k]), 0.0f);
+            const float4 *w4 = reinterpret_cast<const float4 *>(sW2 + k * F);
+#pragma unroll
+            for (int f4 = 0; f4 < F / 4; ++f4) {
+                const float4 w = w4[f4];
+                acc[4 * f4 + 0] = fmaf(hk, w.x, acc[4 * f4 + 0]);
+                acc[4 * f4 + 1] = fmaf(hk, w.y, acc[4 * f4 + 1]);
+                acc[4 * f4 + 2] = fmaf(hk, w.z, acc[4 * f4 + 2]);
+                acc[4 * f4 + 3] = fmaf(hk, w.w, acc[4 * f4 + 3]);
+            }
+        }
+        float4 *o4 = reinterpret_cast<float4 *>(out + ((size_t)b * count + i) * F);
+#pragma unroll
+        for (int f4 = 0; f4 < F / 4; ++f4) o4[f4] = make_float4(acc[4 * f4], acc[4 * f4 + 1], acc[4 * f4 + 2], acc[4 * f4 + 3]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// register-tiled  OUT[TE][N] = act(XT^T[TE][K] . W[K][N] + b[N])  from smem
+// XT is K x (TE+PAD) (transposed input), W is K x N.
+// ---------------------------------------------------------------------------
+template <int TE, int N>
+struct TileShape {
+    static constexpr int PER = TE * N / kGnnThreads;
+    static constexpr int TN = PER >= 4 ? 4 : PER;
+    static constexpr int TM = PER / TN;
+    static constexpr int COLG = N / TN;  // column groups
+    static_assert(TE * N % kGnnThreads == 0, "tile must cover the block");
+    static_assert(COLG * (TE / TM) == kGnnThreads, "tile shape");
+};
+
+constexpr int kPad = 4;
+
+template <int TE, int K, int N, bool RELU>
+__device__ __forceinline__ void tile_gemm(const float *XT, const float *W, const float *bias,
+                                          float (&acc)[TileShape<TE, N>::TM][TileShape<TE, N>::TN]) {
+    using S = TileShape<TE, N>;
+    const int cx = threadIdx.x % S::COLG, ry = threadIdx.x / S::COLG;
+    const int n0 = cx * S::TN, m0 = ry * S::TM;
+#pragma unroll
+    for (int a = 0; a < S::TM; ++a)
+#pragma unroll
+        for (int c = 0; c < S::TN; ++c) acc[a][c] = bias[n0 + c];
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+        float xv[S::TM], wv[S::TN];
+#pragma unroll
+        for (int a = 0; a < S::TM; ++a) xv[a] = XT[k * (TE + kPad) + m0 + a];
+        if constexpr (S::TN == 4) {
+            const float4 w = *reinterpret_cast<const float4 *>(W + k * N + n0);
+            wv[0] = w.x;
+            wv[1] = w.y;
+            wv[2] = w.z;
+            wv[3] = w.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < S::TN; ++c) wv[c] = W[k * N + n0 + c];
+        }
+#pragma unroll
+        for (int a = 0; a < S::TM; ++a)
+#pragma unroll
+            for (int c = 0; c < S::TN; ++c) acc[a][c] = fmaf(xv[a], wv[c], acc[a][c]);
+    }
+    if (RELU) {
+#pragma unroll
+        for (int a = 0; a < S::TM; ++a)
+#pragma unroll
+            for (int c = 0; c < S::TN; ++c) acc[a][c] = fmaxf(acc[a][c], 0.0f);
+    }
+}
+
+// One message-passing half-round. NODE: in = [v | agg] (K = 2F), out -> v_out.
+// EDGE: in = [e | v_src | v_dst] (K = 3F), out -> e (in place).
+template <int F, int H, int TE, bool NODE>
+__global__ void __launch_bounds__(kGnnThreads) mp_kernel(int n, long long m, int B, const int *rp,
+                                                         const int *col, const int *src, const float *W1,
+                                                         const float *b1, const float *W2, const float *b2,
+                                                         float *e, const float *v, float *v_out) {
+    constexpr int K1 = NODE ? 2 * F : 3 * F;
+    extern __shared__ __align__(16) float smem[];
+    float *sW1 = smem;                  // K1 x H
+    float *sW2 = sW1 + K1 * H;          // H x F
+    float *sb1 = sW2 + H * F;           // H
+    float *sb2 = sb1 + H;               // F
+    float *XT = sb2 + F;                // K1 x (TE+PAD)
+    float *HT = XT + K1 * (TE + kPad);  // H x (TE+PAD)
+    for (int q = threadIdx.x; q < K1 * H; q += blockDim.x) sW1[q] = W1[q];
+    for (int q = threadIdx.x; q < H * F; q += blockDim.x) sW2[q] = W2[q];
+    for (int q = threadIdx.x; q < H; q += blockDim.x) sb1[q] = b1[q];
+    for (int q = threadIdx.x; q < F; q += blockDim.x) sb2[q] = b2[q];
+    const long long items = NODE ? (long long)n : m;
+    const long long tiles_per = (items + TE - 1) / TE;
+    const long long tiles = tiles_per * B;
+    using S1 = TileShape<TE, H>;
+    using S2 = TileShape<TE, F>;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int b = (int)(tile / tiles_per);
+        const long long base = (tile % tiles_per) * TE;
+        const float *eb = e + (size_t)b * m * F;
+        const float *vb = v + (size_t)b * n * F;
+        __syncthreads();  // previous tile done with XT / HT (and weights loaded)
+        // gather the input tile, transposed: XT[c][t]
+        for (int q = threadIdx.x; q < TE * K1; q += blockDim.x) {
+            const int t = q / K1, c = q % K1;
+            const long long it = base + t;
+            float val = 0.0f;
+            if (it < items) {
+                if (NODE) {
+                    if (c < F) {
+                        val = vb[(size_t)it * F + c];
+                    } else {  // agg_i = sum_p e_p * v_col(p), CSR order (autodiff.py:221-243)
+                        const int f = c - F;
+                        float s = 0.0f;
+                        for (int p = rp[it]; p < rp[it + 1]; ++p)
+                            s = fmaf(eb[(size_t)p * F + f], vb[(size_t)col[p] * F + f], s);
+                        val = s;
+                    }
+                } else {
+                    if (c < F) val = eb[(size_t)it * F + c];
+                    else if (c < 2 * F) val = vb[(size_t)src[it] * F + (c - F)];
+                    else val = vb[(size_t)col[it] * F + (c - 2 * F)];
+                }
+            }
+            XT[c * (TE + kPad) + t] = val;
+        }
+        __syncthreads();
+        {
+            float acc[S1::TM][S1::TN];
+            tile_gemm<TE, K1, H, true>(XT, sW1, sb1, acc);
+            const int cx = threadIdx.x % S1::COLG, ry = threadIdx.x / S1::COLG;
+#pragma unroll
+            for (int a = 0; a < S1::TM; ++a)
+#pragma unroll
+                for (int c = 0; c < S1::TN; ++c) HT[(cx * S1::TN + c) * (TE + kPad) + ry * S1::TM + a] = acc[a][c];
+        }
+        __syncthreads();
+        {
+            float acc[S2::TM][S2::TN];
+            tile_gemm<TE, H, F, false>(HT, sW2, sb2, acc);
+            const int cx = threadIdx.x % S2::COLG, ry = threadIdx.x / S2::COLG;
+            float *outb = NODE ? v_out + (size_t)b * n * F : e + (size_t)b * m * F;
+#pragma unroll
+            for (int a = 0; a < S2::TM; ++a) {
+                const long long it = base + ry * S2::TM + a;
+                if (it >= items) continue;
+                float *o = outb + (size_t)it * F + cx * S2::TN;
+                if constexpr (S2::TN == 4) {
+                    *reinterpret_cast<float4 *>(o) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < S2::TN; ++c) o[c] = acc[a][c];
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// decoders: F -> h -> 1 (gnn.py:259-262); out[i*B + b] (vector layout), fp64
+// ---------------------------------------------------------------------------
+template <int F>
+__global__ void __launch_bounds__(kGnnThreads) decode_kernel(long long count, int B, const float *x,
+                                                             const float *W1, const float *b1, const float *W2,
+                                                             const float *b2, int h, double *out) {
+    __shared__ __align__(16) float sW1T[kMaxHidden * F];  // [h][F]
+    __shared__ float sb1[kMaxHidden], sW2[kMaxHidden];
+    for (int q = threadIdx.x; q < h * F; q += blockDim.x) {
+        const int k = q / F, c = q % F;
+        sW1T[q] = W1[c * h + k];
+    }
+    for (int k = threadIdx.x; k < h; k += blockDim.x) {
+        sb1[k] = b1[k];
+        sW2[k] = W2[k];
+    }
+    __syncthreads();
+    const float bout = b2[0];
+    const long long total = count * B;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(q / count);
+        const long long i = q % count;
+        float xr[F];
+        const float4 *x4 = reinterpret_cast<const float4 *>(x + ((size_t)b * count + i) * F);
+#pragma unroll
+        for (int f4 = 0; f4 < F / 4; ++f4) {
+            const float4 t = x4[f4];
+            xr[4 * f4] = t.x;
+            xr[4 * f4 + 1] = t.y;
+            xr[4 * f4 + 2] = t.z;
+            xr[4 * f4 + 3] = t.w;
+        }
+        float o = bout;
+        for (int k = 0; k < h; ++k) {
+            float a = sb1[k];
+            const float4 *w4 = reinterpret_cast<const float4 *>(sW1T + k * F);
+#pragma unroll
+            for (int f4 = 0; f4 < F / 4; ++f4) {
+                const float4 w = w4[f4];
+                a = fmaf(xr[4 * f4], w.x, a);
+                a = fmaf(xr[4 * f4 + 1], w.y, a);
+                a = fmaf(xr[4 * f4 + 2], w.z, a);
+                a = fmaf(xr[4 * f4 + 3], w.w, a);
+            }
+            o = fmaf(fmaxf(a, 0.0f), sW2[k], o);
+        }
+        out[(size_t)i * B + b] = (double)o;
+    }
+}
+
+// L'_s = 0.5 (M_s + M_pair(s)) on every off-diagonal slot (gnn.py:284-296);
+// S is symmetric by construction since fp addition commutes.
+__global__ void symm_kernel(long long nnz, int B, const int *pair, const int *src, const int *col, const double *M,
+                            double *S, int *nonfinite) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nnz * B;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long p = q / B;
+        const int b = (int)(q % B);
+        double s = 0.0;
+        if (src[p] != col[p]) {
+            s = 0.5 * (M[q] + M[(size_t)pair[p] * B + b]);
+            if (!isfinite(s)) *nonfinite = 1;
+        }
+        S[q] = s;
+    }
+}
+
+// D = diag(A) (gnn.py:301-304); records the first row with d <= 0 and
+// non-finite diagonals (LowerFactor validation, sparse.py:189-190).
+__global__ void diag_kernel(int n, int B, const int *dp, const double *A, int ab, double *D, int *bad_row,
+                            int *nonfinite) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < (long long)n * B;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(q / B), b = (int)(q % B);
+        const double d = ab ? A[(size_t)dp[i] * B + b] : A[dp[i]];
+        D[q] = d;
+        if (d <= 0.0) atomicMin(bad_row, i);
+        if (!isfinite(d)) *nonfinite = 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+template <int F, int H, int TE>
+static cudaError_t run_rounds(const GnnDev &g, const Pattern &A, int B, float *e, float *v, float *v2,
+                              float **v_final, cudaStream_t s) {
+    const int n = (int)A.n;
+    const long long m = A.nnz;
+    const size_t smem_node = sizeof(float) * ((2 * F) * H + H * F + H + F + (2 * F) * (TE + kPad) + H * (TE + kPad));
+    const size_t smem_edge = sizeof(float) * ((3 * F) * H + H * F + H + F + (3 * F) * (TE + kPad) + H * (TE + kPad));
+    cudaFuncSetAttribute(mp_kernel<F, H, TE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_node);
+    cudaFuncSetAttribute(mp_kernel<F, H, TE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_edge);
+    int occ_n = 1, occ_e = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_n, mp_kernel<F, H, TE, true>, kGnnThreads, smem_node);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, mp_kernel<F, H, TE, false>, kGnnThreads, smem_edge);
+    const long long tn = ((long long)n + TE - 1) / TE * B, te = (m + TE - 1) / TE * B;
+    const int gn = (int)std::max<long long>(1, std::min<long long>(tn, (long long)std::max(occ_n, 1) * num_sms()));
+    const int ge = (int)std::max<long long>(1, std::min<long long>(te, (long long)std::max(occ_e, 1) * num_sms()));
+    for (int r = 0; r < g.d.n_mp; ++r) {
+        const float *w = g.w;
+        mp_kernel<F, H, TE, true><<<gn, kGnnThreads, smem_node, s>>>(
+            n, m, B, A.rp, A.col, A.src, w + g.mp_node[r][0].w, w + g.mp_node[r][0].b, w + g.mp_node[r][1].w,
+            w + g.mp_node[r][1].b, e, v, v2);
+        std::swap(v, v2);
+        mp_kernel<F, H, TE, false><<<ge, kGnnThreads, smem_edge, s>>>(
+            n, m, B, A.rp, A.col, A.src, w + g.mp_edge[r][0].w, w + g.mp_edge[r][0].b, w + g.mp_edge[r][1].w,
+            w + g.mp_edge[r][1].b, e, v, nullptr);
+    }
+    *v_final = v;
+    return cudaGetLastError();
+}
+
+template <int F>
+static cudaError_t encode(const GnnDev &g, long long count, int B, const double *x, int xb, const double *mean,
+                          const double *sd, const LayerOff *L, float *out, cudaStream_t s) {
+    const long long total = count * B;
+    const int grid = (int)std::max<long long>(1, std::min<long long>((total + kGnnThreads - 1) / kGnnThreads, 8 * num_sms()));
+    encode_kernel<F><<<grid, kGnnThreads, 0, s>>>(count, B, x, xb, mean, sd, g.d.normalize, g.w + L[0].w,
+                                                   g.w + L[0].b, g.w + L[1].w, g.w + L[1].b, g.d.h, out);
+    return cudaGetLastError();
+}
+
+template <int F>
+static cudaError_t decode(const GnnDev &g, long long count, int B, const float *x, const LayerOff *L, double *out,
+                          cudaStream_t s) {
+    const long long total = count * B;
+    const int grid = (int)std::max<long long>(1, std::min<long long>((total + kGnnThreads - 1) / kGnnThreads, 8 * num_sms()));
+    decode_kernel<F><<<grid, kGnnThreads, 0, s>>>(count, B, x, g.w + L[0].w, g.w + L[0].b, g.w + L[1].w,
+                                                   g.w + L[1].b, g.d.h, out);
+    return cudaGetLastError();
+}
+
+static cudaError_t stats(long long count, int B, const double *x, double *mean, double *sd, double *partial,
+                         cudaStream_t s) {
+    const int nblk = (int)std::max<long long>(1, std::min<long long>((count + 1023) / 1024, 2 * num_sms()));
+    colstat_partial_kernel<<<nblk, kGnnThreads, 0, s>>>(count, B, x, nullptr, partial);
+    colstat_final_kernel<<<1, kGnnThreads, 0, s>>>(count, B, nblk, partial, mean, 0);
+    colstat_partial_kernel<<<nblk, kGnnThreads, 0, s>>>(count, B, x, mean, partial);
+    colstat_final_kernel<<<1, kGnnThreads, 0, s>>>(count, B, nblk, partial, sd, 1);
+    return cudaGetLastError();
+}
+
+template <int F>
+static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_vals, int ab, const double *rhs,
+                   double *S, double *D, double *edge_out, double *x0_out, int64_t *pivot, cudaStream_t s,
+                   std::string &err) {
+    const int n = (int)A.n;
+    const long long m = A.nnz;
+    float *e = nullptr, *v = nullptr, *v2 = nullptr;
+    double *M = nullptr, *st = nullptr;
+    int *flags = nullptr;
+    float *vfin = nullptr;
+    const int Bs = ab ? B : 1;  // systems with distinct A values
+    auto ck = [&](cudaError_t c) {
+        if (c != cudaSuccess && err.empty()) err = cudaGetErrorString(c);
+        return c == cudaSuccess;
+    };
+    bool ok = ck(cudaMallocAsync((void **)&e, sizeof(float) * std::max<long long>(m * F * B, 1), s)) &&
+              ck(cudaMallocAsync((void **)&v, sizeof(float) * std::max<long long>((long long)n * F * B, 1), s)) &&
+              ck(cudaMallocAsync((void **)&v2, sizeof(float) * std::max<long long>((long long)n * F * B, 1), s)) &&
+              ck(cudaMallocAsync((void **)&M, sizeof(double) * std::max<long long>(m * B, 1), s)) &&
+              ck(cudaMallocAsync((void **)&st, sizeof(double) * (4 * B + 2 * num_sms() * (size_t)B + 8), s)) &&
+              ck(cudaMallocAsync((void **)&flags, sizeof(int) * 4, s));
+    int h_flags[4] = {n, 0, 0, 0};  // bad_row, nonfinite diag, nonfinite L'
+    if (ok) {
+        double *mb = st, *sb = st + B, *ma = st + 2 * B, *sa = st + 3 * B, *partial = st + 4 * B;
+        ok = ck(cudaMemcpyAsync(flags, h_flags, sizeof(h_flags), cudaMemcpyHostToDevice, s));
+        if (ok && g.d.normalize) {
+            ok = ck(stats(n, B, rhs, mb, sb, partial, s)) && ck(stats(m, Bs, A_vals, ma, sa, partial, s));
+            if (ok && Bs != B) {  // shared A: broadcast its statistics to every system
+                for (int b = 1; b < B && ok; ++b)
+                    ok = ck(cudaMemcpyAsync(ma + b, ma, 8, cudaMemcpyDeviceToDevice, s)) &&
+                         ck(cudaMemcpyAsync(sa + b, sa, 8, cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        if (ok) ok = ck(encode<F>(g, n, B, rhs, 1, mb, sb, g.node_enc, v, s));
+        if (ok) ok = ck(encode<F>(g, m, B, A_vals, ab, ma, sa, g.edge_enc, e, s));
+        if (ok) {
+            const int hm = g.d.h_mp;
+            cudaError_t c = cudaErrorInvalidValue;
+            if (F == 16 && hm == 16) c = run_rounds<16, 16, 64>(g, A, B, e, v, v2, &vfin, s);
+            else if (F == 16 && hm == 8) c = run_rounds<16, 8, 64>(g, A, B, e, v, v2, &vfin, s);
+            else if (F == 16 && hm == 32) c = run_rounds<16, 32, 64>(g, A, B, e, v, v2, &vfin, s);
+            else if (F == 64 && hm == 64) c = run_rounds<64, 64, 32>(g, A, B, e, v, v2, &vfin, s);
+            else if (F == 64 && hm == 32) c = run_rounds<64, 32, 32>(g, A, B, e, v, v2, &vfin, s);
+            ok = ck(c);
+        }
+        double *Mout = edge_out ? edge_out : M;
+        if (ok) ok = ck(decode<F>(g, m, B, e, g.edge_dec, Mout, s));
+        if (ok && x0_out && g.d.with_x0_head) ok = ck(decode<F>(g, n, B, vfin, g.node_dec, x0_out, s));
+        if (ok) {
+            const int grid = (int)std::min<long long>((m * B + 255) / 256 + 1, 8192);
+            symm_kernel<<<grid, 256, 0, s>>>(m, B, A.pair, A.src, A.col, Mout, S, flags + 2);
+            diag_kernel<<<(int)std::min<long long>(((long long)n * B + 255) / 256 + 1, 8192), 256, 0, s>>>(
+                n, B, A.dp, A_vals, ab, D, flags, flags + 1);
+            ok = ck(cudaGetLastError());
+        }
+        if (ok) ok = ck(cudaMemcpyAsync(h_flags, flags, sizeof(h_flags), cudaMemcpyDeviceToHost, s)) &&
+                     ck(cudaStreamSynchronize(s));
+    }
+    cudaFreeAsync(e, s);
+    cudaFreeAsync(v, s);
+    cudaFreeAsync(v2, s);
+    cudaFreeAsync(M, s);
+    cudaFreeAsync(st, s);
+    cudaFreeAsync(flags, s);
+    if (!ok) return NPCG_ERR_CUDA;
+    if (h_flags[0] < n) {
+        *pivot = h_flags[0];
+        err = "nonpositive diagonal entry at row " + std::to_string(h_flags[0]);
+        return NPCG_ERR_NOT_SPD;
+    }
+    if (h_flags[1]) {
+        err = "diagonal must be finite and strictly positive";
+        return NPCG_ERR_INVALID_FACTOR;
+    }
+    if (h_flags[2]) {
+        err = "factor values must be finite";
+        return NPCG_ERR_INVALID_FACTOR;
+    }
+    return NPCG_OK;
+}
+
+int gnn_build(const GnnDev &g, const Pattern &A, int B, const double *A_vals, int ab, const double *rhs, double *S,
+              double *D, double *edge_out, double *x0_out, int64_t *pivot, cudaStream_t s, std::string &err) {
+    if (g.d.width == 16) return build_F<16>(g, A, B, A_vals, ab, rhs, S, D, edge_out, x0_out, pivot, s, err);
+    return build_F<64>(g, A, B, A_vals, ab, rhs, S, D, edge_out, x0_out, pivot, s, err);
+}
+
+}  // namespace npcg

@@ -1,0 +1,227 @@
+"""Seeded synthetic inputs for the BASELINE.json configs (input generation,
+not the solve path).
+
+The reference ships P1 FEM assembly (pkg/src/pcgkit/fem.py:42-215) as a
+per-element Python loop over unjittered grids (mesh.py:149-178). The
+configs need jittered grids, per-element coefficients and random-field
+right-hand sides, so this module generates them, vectorised in numpy.
+The arithmetic per element and the scatter order follow fem.py:42-69 and
+fem.py:116-134 exactly (COO in element order, lexsort + reduceat), so the
+assembled matrices are bitwise symmetric -- graph_from_system requires it
+(gnn.py:79-82) -- and, on the same vertices, bitwise equal to the
+reference's own assembly (pinned in tests/test_inputs.py against goldens
+produced by pcgkit.fem).
+
+Seeds: np.random.SeedSequence(1000 * cfg + 17).spawn(B), one stream per
+system / right-hand side; draws in the order jitter, coefficients, RHS.
+Random fields use random Fourier features (squared-exponential
+covariance): f(x) = sqrt(2/R) sum_r cos(w_r . x + phi_r), w ~ N(0, l^-2 I).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .sparse import SparseMatrixCsr
+
+MASS_TEMPLATE = np.array([[2.0, 1.0, 1.0], [1.0, 2.0, 1.0], [1.0, 1.0, 2.0]]) / 12.0
+GRF_FEATURES = 64
+
+
+@dataclass
+class Mesh2D:
+    vertices: np.ndarray   # (nv, 2)
+    triangles: np.ndarray  # (nt, 3) counter-clockwise
+    boundary: np.ndarray   # (nv,) bool
+
+
+def unit_square(k: int, jitter: float = 0.0, rng: np.random.Generator | None = None) -> Mesh2D:
+    """(k+1)^2 vertices, cells split along the (1,1) diagonal, vertex and
+    triangle order of mesh.generate_unit_square (mesh.py:149-178); interior
+    vertices moved by U[-jitter, jitter] * h per coordinate."""
+    axis = np.arange(k + 1) / k
+    xs, ys = np.meshgrid(axis, axis, indexing="xy")
+    v = np.column_stack([xs.ravel(), ys.ravel()])
+    boundary = ((xs == 0.0) | (xs == 1.0) | (ys == 0.0) | (ys == 1.0)).ravel()
+    if jitter > 0.0:
+        inner = np.flatnonzero(~boundary)
+        v[inner] += rng.uniform(-1.0, 1.0, size=(len(inner), 2)) * (jitter / k)
+    ix, iy = np.meshgrid(np.arange(k), np.arange(k), indexing="xy")
+    a = (iy * (k + 1) + ix).ravel()
+    b, c, d = a + 1, a + k + 2, a + k + 1
+    tris = np.empty((2 * k * k, 3), dtype=np.int64)
+    tris[0::2] = np.column_stack([a, b, c])
+    tris[1::2] = np.column_stack([a, c, d])
+    return Mesh2D(v, tris, boundary)
+
+
+def element_blocks(mesh: Mesh2D):
+    """Per-element 3x3 stiffness and mass blocks, (nt, 3, 3) each, with the
+    operation order of fem.element_stiffness / element_mass."""
+    p = mesh.vertices[mesh.triangles]
+    twice = (p[:, 1, 0] - p[:, 0, 0]) * (p[:, 2, 1] - p[:, 0, 1]) - \
+        (p[:, 1, 1] - p[:, 0, 1]) * (p[:, 2, 0] - p[:, 0, 0])
+    if np.any(twice <= 0.0):
+        raise ValueError("degenerate or clockwise triangle (reduce the jitter)")
+    bs = np.stack([p[:, 1, 1] - p[:, 2, 1], p[:, 2, 1] - p[:, 0, 1], p[:, 0, 1] - p[:, 1, 1]], axis=1)
+    cs = np.stack([p[:, 2, 0] - p[:, 1, 0], p[:, 0, 0] - p[:, 2, 0], p[:, 1, 0] - p[:, 0, 0]], axis=1)
+    K = (bs[:, :, None] * bs[:, None, :] + cs[:, :, None] * cs[:, None, :]) / (2.0 * np.abs(twice))[:, None, None]
+    M = (np.abs(twice) / 2.0)[:, None, None] * MASS_TEMPLATE[None]
+    return K, M
+
+
+class Assembler:
+    """Scatter of per-element blocks into the fixed CSR pattern, in element
+    order (fem.py:116-134); the sort is computed once per mesh."""
+
+    def __init__(self, n_vertices: int, triangles: np.ndarray):
+        rows = np.repeat(triangles, 3, axis=1).ravel()
+        cols = np.tile(triangles, (1, 3)).ravel()
+        order = np.lexsort((cols, rows))
+        r, c = rows[order], cols[order]
+        head = np.ones(len(r), dtype=bool)
+        head[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+        self.order = order
+        self.starts = np.flatnonzero(head)
+        self.n = n_vertices
+        self.row_ptr = np.zeros(n_vertices + 1, dtype=np.int64)
+        np.cumsum(np.bincount(r[self.starts], minlength=n_vertices), out=self.row_ptr[1:])
+        self.col_idx = np.ascontiguousarray(c[self.starts])
+
+    def values(self, blocks: np.ndarray) -> np.ndarray:
+        return np.add.reduceat(blocks.reshape(-1)[self.order], self.starts)
+
+    def matrix(self, values) -> SparseMatrixCsr:
+        return SparseMatrixCsr(self.n, self.row_ptr, self.col_idx, values)
+
+
+class Restriction:
+    """Symmetric restriction to free vertices (SparseMatrixCsr.submatrix,
+    sparse.py:155-163), precomputed once per (pattern, free set)."""
+
+    def __init__(self, A: SparseMatrixCsr, free: np.ndarray):
+        remap = -np.ones(A.n, dtype=np.int64)
+        remap[free] = np.arange(len(free), dtype=np.int64)
+        rows = remap[A.row_indices()]
+        cols = remap[A.col_idx]
+        self.sel = np.flatnonzero((rows >= 0) & (cols >= 0))
+        # rows stay sorted by (row, col) after restriction: no duplicates possible
+        rr, cc = rows[self.sel], cols[self.sel]
+        self.free = free
+        self.n = len(free)
+        self.row_ptr = np.zeros(self.n + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rr, minlength=self.n), out=self.row_ptr[1:])
+        self.col_idx = np.ascontiguousarray(cc)
+
+    def matrix(self, values_full) -> SparseMatrixCsr:
+        return SparseMatrixCsr(self.n, self.row_ptr, self.col_idx, np.ascontiguousarray(values_full[self.sel]))
+
+
+def grf_2d(points: np.ndarray, rng: np.random.Generator, length: float, n_features: int = GRF_FEATURES):
+    """Squared-exponential Gaussian random field sampled at points (RFF)."""
+    w = rng.standard_normal((n_features, points.shape[1])) / length
+    phi = rng.uniform(0.0, 2.0 * np.pi, size=n_features)
+    # phases in float32: the field is a random input, not a checked quantity
+    ph = (points @ w.T + phi).astype(np.float32)
+    return np.sqrt(2.0 / n_features) * np.cos(ph).sum(axis=1, dtype=np.float64)
+
+
+def gaussian_bumps(points: np.ndarray, rng: np.random.Generator, count=8, width=(0.05, 0.2)):
+    centers = rng.uniform(0.0, 1.0, size=(count, 2))
+    widths = rng.uniform(width[0], width[1], size=count)
+    amps = rng.standard_normal(count)
+    d2 = ((points[:, None, :] - centers[None, :, :]) ** 2).sum(axis=2)
+    return (amps[None, :] * np.exp(-d2 / (2.0 * widths[None, :] ** 2))).sum(axis=1)
+
+
+def streams(cfg: int, count: int):
+    return [np.random.default_rng(s) for s in np.random.SeedSequence(1000 * cfg + 17).spawn(count)]
+
+
+# ---------------------------------------------------------------------------
+# configs (BASELINE.json "configs")
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Problem:
+    name: str
+    A: SparseMatrixCsr         # shared pattern (values of system 0)
+    rhs: np.ndarray            # (n, B)
+    values: np.ndarray | None  # (nnz, B) for distinct systems, else None
+    rtol: float
+    max_iter: int | None
+    meta: dict
+
+
+def heat_2d(k=32, jitter=0.2, dt=1e-2, alpha=1.0, cfg=1, batch=1) -> Problem:
+    """Config 1: heat step A = M + dt*alpha*K on a jittered k x k square, no
+    Dirichlet rows (n = (k+1)^2); b = M u0, u0 = 8 Gaussian bumps."""
+    rngs = streams(cfg, batch)
+    vals, rhs = [], []
+    A0 = None
+    for rng in rngs:
+        mesh = unit_square(k, jitter, rng)
+        K, M = element_blocks(mesh)
+        asm = Assembler(len(mesh.vertices), mesh.triangles)
+        Kv, Mv = asm.values(K), asm.values(M)
+        A = asm.matrix(Mv + (dt * alpha) * Kv)
+        Mm = asm.matrix(Mv)
+        u0 = gaussian_bumps(mesh.vertices, rng)
+        b = Mm.to_dense() @ u0 if A.n <= 4096 else _host_spmv(Mm, u0)
+        A0 = A0 or A
+        vals.append(A.values)
+        rhs.append(b)
+    values = None if batch == 1 else np.stack(vals, axis=1)
+    if values is not None:
+        A0 = A0.with_values(values[:, 0].copy())
+    return Problem("heat2d", A0, np.stack(rhs, axis=1), values, 1e-8, 2000,
+                   {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg})
+
+
+def poisson_2d(k=256, jitter=0.2, batch=64, cfg=2) -> Problem:
+    """Config 2: Poisson stiffness on a jittered k x k square, full-boundary
+    Dirichlet eliminated (n = (k-1)^2); B right-hand sides (M f)[free], f a
+    squared-exponential GRF with length scale U[0.05, 0.3]."""
+    rngs = streams(cfg, batch)
+    mesh = unit_square(k, jitter, rngs[0])  # one shared mesh (one L' for all RHS)
+    K, M = element_blocks(mesh)
+    asm = Assembler(len(mesh.vertices), mesh.triangles)
+    Kv, Mv = asm.values(K), asm.values(M)
+    free = np.flatnonzero(~mesh.boundary)
+    red = Restriction(asm.matrix(Kv), free)
+    A = red.matrix(Kv)
+    Mm = asm.matrix(Mv)
+    rhs = np.empty((len(free), batch))
+    for j, rng in enumerate(rngs):
+        f = grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3))
+        rhs[:, j] = _host_spmv(Mm, f)[free]
+    return Problem("poisson2d", A, rhs, None, 1e-8, None, {"k": k, "jitter": jitter, "cfg": cfg})
+
+
+def wave_2d(k=512, jitter=0.2, dt=1e-3, sigma=0.5, batch=32, cfg=3, first=0) -> Problem:
+    """Config 3: implicit wave step A = M + dt^2 K_c, c = exp(sigma * GRF) per
+    element; b = M g with g a GRF; distinct A per system, one shared mesh
+    topology (jitter drawn from the config stream, shared)."""
+    rngs = streams(cfg, first + batch)[first:]
+    mesh = unit_square(k, jitter, np.random.default_rng(np.random.SeedSequence(1000 * cfg + 17).entropy))
+    K, M = element_blocks(mesh)
+    asm = Assembler(len(mesh.vertices), mesh.triangles)
+    Mv = asm.values(M)
+    Mm = asm.matrix(Mv)
+    cent = mesh.vertices[mesh.triangles].mean(axis=1)
+    vals = np.empty((len(asm.col_idx), batch))
+    rhs = np.empty((len(mesh.vertices), batch))
+    for j, rng in enumerate(rngs):
+        c = np.exp(sigma * grf_2d(cent, rng, rng.uniform(0.05, 0.3)))
+        Kc = asm.values(K * c[:, None, None])
+        vals[:, j] = Mv + (dt * dt) * Kc
+        rhs[:, j] = _host_spmv(Mm, grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3)))
+    A = asm.matrix(np.ascontiguousarray(vals[:, 0]))
+    return Problem("wave2d", A, rhs, vals, 1e-8, None, {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg})
+
+
+def _host_spmv(A: SparseMatrixCsr, x):
+    """Input-generation helper (not the solve path): y = A x in numpy."""
+    return np.add.reduceat(A.values * x[A.col_idx], A.row_ptr[:-1]) if A.nnz else np.zeros(A.n)
