@@ -149,7 +149,18 @@ typedef struct {
     int64_t max_iter;             /* SolveOptions.max_iter or 10*n */
     int32_t absolute;             /* SolveOptions.absolute */
     int32_t check_every;          /* host polls convergence every k passes (0 = auto) */
+    int32_t profile;              /* 1: time every kernel launch with CUDA events */
+    int32_t reserved;
 } npcg_solve_opts;
+
+/* kernel classes reported by a profiled solve */
+#define NPCG_PROF_SPMV_APDOT 0    /* Ap = A p, p.Ap, alpha            */
+#define NPCG_PROF_TRSV_FWD   1    /* x,r update + forward unit solve  */
+#define NPCG_PROF_SPMV_DRIFT 2    /* b - A x at threshold crossings   */
+#define NPCG_PROF_TRSV_BWD   3    /* D^-1 + backward solve + r.z      */
+#define NPCG_PROF_PUPD       4    /* p = z + beta p                   */
+#define NPCG_PROF_OTHER      5    /* setup / polling / final residual */
+#define NPCG_PROF_SLOTS      8
 
 typedef struct {
     /* all host arrays, caller allocated */
@@ -161,7 +172,14 @@ typedef struct {
     double *history;              /* [B][history_cap] ||r_k||, nullable */
     int64_t history_cap;          /* entries per system (>= max_iter+1 for full) */
     int64_t *breakdown_iteration; /* [B] k where p'Ap <= 0, else 0 */
+    double *kernel_ms;            /* [NPCG_PROF_SLOTS] summed launch times (profile) */
+    int64_t *kernel_launches;     /* [NPCG_PROF_SLOTS] launches per class (profile) */
+    int64_t passes;               /* out: kernel-sequence passes executed */
 } npcg_solve_report;
+
+/* Kernel launches issued by this library since it was loaded (all entry
+ * points), for launch accounting in benchmarks. */
+int64_t npcg_launch_count(void);
 
 /* Solver workspace for a (A pattern, factor pattern, B) triple. F may be
  * NULL (identity preconditioner, pcg.py:64-72) or equal A. */

@@ -57,14 +57,21 @@ class GnnDesc(ctypes.Structure):
 class SolveOpts(ctypes.Structure):
     _fields_ = [("n_thresholds", ctypes.c_int32), ("thresholds", ctypes.c_double * MAX_THRESHOLDS),
                 ("max_iter", ctypes.c_int64), ("absolute", ctypes.c_int32),
-                ("check_every", ctypes.c_int32)]
+                ("check_every", ctypes.c_int32), ("profile", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+PROF_SLOTS = 8
+PROF_NAMES = ("spmv_apdot", "trsv_fwd", "spmv_drift", "trsv_bwd", "pupd", "other")
 
 
 class SolveReportC(ctypes.Structure):
     _fields_ = [("status", ctypes.c_void_p), ("iterations", ctypes.c_void_p),
                 ("iterations_to", ctypes.c_void_p), ("seconds_to", ctypes.c_void_p),
                 ("final_relative_residual", ctypes.c_void_p), ("history", ctypes.c_void_p),
-                ("history_cap", ctypes.c_int64), ("breakdown_iteration", ctypes.c_void_p)]
+                ("history_cap", ctypes.c_int64), ("breakdown_iteration", ctypes.c_void_p),
+                ("kernel_ms", ctypes.c_void_p), ("kernel_launches", ctypes.c_void_p),
+                ("passes", ctypes.c_int64)]
 
 
 P = ctypes.c_void_p
@@ -92,6 +99,7 @@ SIGNATURES = {
     "npcg_solver_destroy": (I32, [P]),
     "npcg_pcg_solve": (I32, [P, P, I32, P, I32, P, I32, P, P, P, ctypes.POINTER(SolveOpts),
                              ctypes.POINTER(SolveReportC), P]),
+    "npcg_launch_count": (I64, []),
 }
 
 _lib = None

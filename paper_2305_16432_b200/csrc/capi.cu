@@ -248,7 +248,7 @@ int npcg_check_symmetric_values(const npcg_pattern *p, int B, const double *vals
     int *d_ok = nullptr;
     NPCG_CUDA(dalloc(&d_ok, B));
     NPCG_CUDA(cudaMemcpyAsync(d_ok, ok_host, B * 4, cudaMemcpyHostToDevice, s));
-    symmetric_check_kernel<<<std::min<long long>((p->nnz * B + 255) / 256, 4096), 256, 0, s>>>(p->nnz, B, vb,
+    note_launch(); symmetric_check_kernel<<<std::min<long long>((p->nnz * B + 255) / 256, 4096), 256, 0, s>>>(p->nnz, B, vb,
                                                                                            p->pair, vals, d_ok);
     NPCG_CUDA(cudaGetLastError());
     NPCG_CUDA(cudaMemcpyAsync(ok_host, d_ok, B * 4, cudaMemcpyDeviceToHost, s));
@@ -282,7 +282,7 @@ int npcg_factor_from_lower(const npcg_pattern *F, int B, const double *lower, in
     if (F->nnz) NPCG_CUDA(cudaMemsetAsync(S, 0, (size_t)F->nnz * B * 8, s));
     if (F->nnz_lower) {
         const long long work = F->nnz_lower * (long long)B;
-        factor_from_lower_kernel<<<(int)std::min<long long>((work + 255) / 256, 8192), 256, 0, s>>>(
+        note_launch(); factor_from_lower_kernel<<<(int)std::min<long long>((work + 255) / 256, 8192), 256, 0, s>>>(
             (int)F->nnz_lower, B, lb, F->lower_slot, F->pair, lower, S);
         NPCG_CUDA(cudaGetLastError());
     }
@@ -293,7 +293,7 @@ int npcg_factor_to_lower(const npcg_pattern *F, int B, const double *S, double *
     if (!F || B < 1) return fail(NPCG_ERR_ARGUMENT, "bad argument");
     if (F->nnz_lower) {
         const long long work = F->nnz_lower * (long long)B;
-        factor_to_lower_kernel<<<(int)std::min<long long>((work + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(
+        note_launch(); factor_to_lower_kernel<<<(int)std::min<long long>((work + 255) / 256, 8192), 256, 0, (cudaStream_t)stream>>>(
             (int)F->nnz_lower, B, F->lower_slot, S, lower);
         NPCG_CUDA(cudaGetLastError());
     }
@@ -494,12 +494,12 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     const long long nB = (long long)n * B;
     const int ew_grid = (int)std::min<long long>((nB + 255) / 256, 4 * 1024);
 
-    init_state_kernel<<<(B + 127) / 128, 128, 0, st>>>(sst, B, cap);
+    note_launch(); init_state_kernel<<<(B + 127) / 128, 128, 0, st>>>(sst, B, cap);
     NPCG_CUDA(cudaGetLastError());
-    normb_kernel<<<std::min(kReduceBlocksPerSm * num_sms(), std::max(1, n / 64)), kSpmvThreads, 0, st>>>(
+    note_launch(); normb_kernel<<<std::min(kReduceBlocksPerSm * num_sms(), std::max(1, n / 64)), kSpmvThreads, 0, st>>>(
         n, B, bvec, sst, s->partial, s->ctl);
     NPCG_CUDA(cudaGetLastError());
-    init_x_kernel<<<ew_grid, 256, 0, st>>>(nB, B, x0, x, sst);
+    note_launch(); init_x_kernel<<<ew_grid, 256, 0, st>>>(nB, B, x0, x, sst);
     NPCG_CUDA(cudaGetLastError());
 
     SpmvArgs sp;
@@ -545,28 +545,81 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     bw.R = s->R;
     bw.st = sst;
 
+    // Optional per-launch timing (npcg_solve_opts.profile): a start/stop
+    // event pair around every launch of the loop, summed per kernel class.
+    const bool prof = o->profile != 0;
+    struct Ev {
+        cudaEvent_t a, b;
+        int slot;
+    };
+    std::vector<Ev> pool, used;
+    double prof_ms[NPCG_PROF_SLOTS] = {0};
+    long long prof_n[NPCG_PROF_SLOTS] = {0};
+    auto timed = [&](int slot, auto &&launch) -> cudaError_t {
+        if (!prof) return launch();
+        Ev e;
+        if (pool.empty()) {
+            cudaEventCreate(&e.a);
+            cudaEventCreate(&e.b);
+        } else {
+            e = pool.back();
+            pool.pop_back();
+        }
+        e.slot = slot;
+        cudaEventRecord(e.a, st);
+        cudaError_t c = launch();
+        cudaEventRecord(e.b, st);
+        used.push_back(e);
+        return c;
+    };
+    auto harvest = [&]() {
+        for (Ev &e : used) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e.a, e.b);
+            prof_ms[e.slot] += ms;
+            prof_n[e.slot] += 1;
+            pool.push_back(e);
+        }
+        used.clear();
+    };
+    auto pupd = [&]() {
+        note_launch();
+        pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, sst);
+        return cudaGetLastError();
+    };
+
     int check = o->check_every > 0 ? o->check_every : 8;
     const long long max_passes = 2 * o->max_iter + 8;
     long long passes = 0;
     for (;;) {
         for (int q = 0; q < check; ++q) {
-            NPCG_CUDA(launch_spmv(apdot, st));
-            NPCG_CUDA(launch_trsv(fw, st));
-            NPCG_CUDA(launch_spmv(drift, st));
-            NPCG_CUDA(launch_trsv(bw, st));
-            pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, sst);
-            NPCG_CUDA(cudaGetLastError());
+            NPCG_CUDA(timed(NPCG_PROF_SPMV_APDOT, [&] { return launch_spmv(apdot, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return launch_trsv(fw, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_SPMV_DRIFT, [&] { return launch_spmv(drift, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return launch_trsv(bw, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
         }
         passes += check;
-        count_active_kernel<<<1, 256, 0, st>>>(sst, B);
+        note_launch(); count_active_kernel<<<1, 256, 0, st>>>(sst, B);
         NPCG_CUDA(cudaMemcpyAsync(s->h_active, s->active_count, 4, cudaMemcpyDeviceToHost, st));
         NPCG_CUDA(cudaStreamSynchronize(st));
+        harvest();
         if (*s->h_active == 0 || passes >= max_passes) break;
         if (check < 64) check *= 2;
     }
+    for (Ev &e : pool) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    rep->passes = passes;
+    if (rep->kernel_ms)
+        for (int q = 0; q < NPCG_PROF_SLOTS; ++q) rep->kernel_ms[q] = prof_ms[q];
+    if (rep->kernel_launches)
+        for (int q = 0; q < NPCG_PROF_SLOTS; ++q) rep->kernel_launches[q] = prof_n[q];
     // report
     std::vector<int> status(B);
-    NPCG_CUDA(cudaMemcpy(status.data(), s->status, B * 4, cudaMemcpyDeviceToHost));
+    NPCG_CUDA(cudaMemcpyAsync(status.data(), s->status, B * 4, cudaMemcpyDeviceToHost, st));
+    NPCG_CUDA(cudaStreamSynchronize(st));
     bool any_max = false;
     for (int b = 0; b < B; ++b) any_max |= status[b] == ST_MAXITER || status[b] == ST_ACTIVE;
     if (any_max) {
@@ -648,3 +701,5 @@ int npcg_gnn_build_factor(const npcg_gnn *g, const npcg_pattern *A, int B, const
 }
 
 }  // extern "C"
+
+extern "C" int64_t npcg_launch_count(void) { return (int64_t)launch_count(); }

@@ -408,11 +408,11 @@ static cudaError_t run_rounds(const GnnDev &g, const Pattern &A, int B, float *e
     const int ge = (int)std::max<long long>(1, std::min<long long>(te, (long long)std::max(occ_e, 1) * num_sms()));
     for (int r = 0; r < g.d.n_mp; ++r) {
         const float *w = g.w;
-        mp_kernel<F, H, TE, true><<<gn, kGnnThreads, smem_node, s>>>(
+        note_launch(); mp_kernel<F, H, TE, true><<<gn, kGnnThreads, smem_node, s>>>(
             n, m, B, A.rp, A.col, A.src, w + g.mp_node[r][0].w, w + g.mp_node[r][0].b, w + g.mp_node[r][1].w,
             w + g.mp_node[r][1].b, e, v, v2);
         std::swap(v, v2);
-        mp_kernel<F, H, TE, false><<<ge, kGnnThreads, smem_edge, s>>>(
+        note_launch(); mp_kernel<F, H, TE, false><<<ge, kGnnThreads, smem_edge, s>>>(
             n, m, B, A.rp, A.col, A.src, w + g.mp_edge[r][0].w, w + g.mp_edge[r][0].b, w + g.mp_edge[r][1].w,
             w + g.mp_edge[r][1].b, e, v, nullptr);
     }
@@ -425,7 +425,7 @@ static cudaError_t encode(const GnnDev &g, long long count, int B, const double 
                           const double *sd, const LayerOff *L, float *out, cudaStream_t s) {
     const long long total = count * B;
     const int grid = (int)std::max<long long>(1, std::min<long long>((total + kGnnThreads - 1) / kGnnThreads, 8 * num_sms()));
-    encode_kernel<F><<<grid, kGnnThreads, 0, s>>>(count, B, x, xb, mean, sd, g.d.normalize, g.w + L[0].w,
+    note_launch(); encode_kernel<F><<<grid, kGnnThreads, 0, s>>>(count, B, x, xb, mean, sd, g.d.normalize, g.w + L[0].w,
                                                    g.w + L[0].b, g.w + L[1].w, g.w + L[1].b, g.d.h, out);
     return cudaGetLastError();
 }
@@ -435,7 +435,7 @@ static cudaError_t decode(const GnnDev &g, long long count, int B, const float *
                           cudaStream_t s) {
     const long long total = count * B;
     const int grid = (int)std::max<long long>(1, std::min<long long>((total + kGnnThreads - 1) / kGnnThreads, 8 * num_sms()));
-    decode_kernel<F><<<grid, kGnnThreads, 0, s>>>(count, B, x, g.w + L[0].w, g.w + L[0].b, g.w + L[1].w,
+    note_launch(); decode_kernel<F><<<grid, kGnnThreads, 0, s>>>(count, B, x, g.w + L[0].w, g.w + L[0].b, g.w + L[1].w,
                                                    g.w + L[1].b, g.d.h, out);
     return cudaGetLastError();
 }
@@ -443,10 +443,10 @@ static cudaError_t decode(const GnnDev &g, long long count, int B, const float *
 static cudaError_t stats(long long count, int B, const double *x, double *mean, double *sd, double *partial,
                          cudaStream_t s) {
     const int nblk = (int)std::max<long long>(1, std::min<long long>((count + 1023) / 1024, 2 * num_sms()));
-    colstat_partial_kernel<<<nblk, kGnnThreads, 0, s>>>(count, B, x, nullptr, partial);
-    colstat_final_kernel<<<1, kGnnThreads, 0, s>>>(count, B, nblk, partial, mean, 0);
-    colstat_partial_kernel<<<nblk, kGnnThreads, 0, s>>>(count, B, x, mean, partial);
-    colstat_final_kernel<<<1, kGnnThreads, 0, s>>>(count, B, nblk, partial, sd, 1);
+    note_launch(); colstat_partial_kernel<<<nblk, kGnnThreads, 0, s>>>(count, B, x, nullptr, partial);
+    note_launch(); colstat_final_kernel<<<1, kGnnThreads, 0, s>>>(count, B, nblk, partial, mean, 0);
+    note_launch(); colstat_partial_kernel<<<nblk, kGnnThreads, 0, s>>>(count, B, x, mean, partial);
+    note_launch(); colstat_final_kernel<<<1, kGnnThreads, 0, s>>>(count, B, nblk, partial, sd, 1);
     return cudaGetLastError();
 }
 
@@ -500,8 +500,8 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
         if (ok && x0_out && g.d.with_x0_head) ok = ck(decode<F>(g, n, B, vfin, g.node_dec, x0_out, s));
         if (ok) {
             const int grid = (int)std::min<long long>((m * B + 255) / 256 + 1, 8192);
-            symm_kernel<<<grid, 256, 0, s>>>(m, B, A.pair, A.src, A.col, Mout, S, flags + 2);
-            diag_kernel<<<(int)std::min<long long>(((long long)n * B + 255) / 256 + 1, 8192), 256, 0, s>>>(
+            note_launch(); symm_kernel<<<grid, 256, 0, s>>>(m, B, A.pair, A.src, A.col, Mout, S, flags + 2);
+            note_launch(); diag_kernel<<<(int)std::min<long long>(((long long)n * B + 255) / 256 + 1, 8192), 256, 0, s>>>(
                 n, B, A.dp, A_vals, ab, D, flags, flags + 1);
             ok = ck(cudaGetLastError());
         }

@@ -9,6 +9,8 @@
 // sparse.py:213-239; only dot products / norms (reductions) differ in
 // order from numpy's BLAS ddot. Reductions are fixed-order (no float
 // atomics), so the path is run-to-run deterministic.
+#include <atomic>
+
 #include "kernels.cuh"
 
 namespace npcg {
@@ -516,6 +518,10 @@ __global__ void symmetric_check_kernel(long long nnz, int B, int vb, const int *
 // host launch helpers
 // ===========================================================================
 
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
 int num_sms() {
     static int sms = 0;
     if (!sms) {
@@ -547,7 +553,7 @@ cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s) {
         if (smem > 48 * 1024)                                                                 \
             cudaFuncSetAttribute(spmv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                  (int)smem);                                                  \
-        spmv_kernel<T><<<grid, kSpmvThreads, smem, s>>>(a);                                   \
+        note_launch(); spmv_kernel<T><<<grid, kSpmvThreads, smem, s>>>(a);                                   \
         break;
     switch (TL) {
         NPCG_SPMV_CASE(1)
@@ -576,7 +582,7 @@ cudaError_t launch_trsv(const TrsvArgs &a, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trsv_kernel, kTrsvThreads, smem);
     if (per_sm < 1) per_sm = 1;
     const int grid = std::max(1, std::min(a.units, per_sm * num_sms()));
-    trsv_kernel<<<grid, kTrsvThreads, smem, s>>>(a);
+    note_launch(); trsv_kernel<<<grid, kTrsvThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

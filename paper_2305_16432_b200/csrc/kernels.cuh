@@ -76,6 +76,8 @@ __global__ void symmetric_check_kernel(long long nnz, int B, int vb, const int *
                                        int *ok);
 
 int num_sms();
+void note_launch();          // launch accounting (npcg_launch_count)
+long long launch_count();
 cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s);
 cudaError_t launch_trsv(const TrsvArgs &a, cudaStream_t s);
 size_t trsv_smem_bytes(const Schedule &S, int G);

@@ -169,7 +169,7 @@ def heat_2d(k=32, jitter=0.2, dt=1e-2, alpha=1.0, cfg=1, batch=1) -> Problem:
         A = asm.matrix(Mv + (dt * alpha) * Kv)
         Mm = asm.matrix(Mv)
         u0 = gaussian_bumps(mesh.vertices, rng)
-        b = Mm.to_dense() @ u0 if A.n <= 4096 else _host_spmv(Mm, u0)
+        b = _host_spmv(Mm, u0)
         A0 = A0 or A
         vals.append(A.values)
         rhs.append(b)
@@ -180,12 +180,15 @@ def heat_2d(k=32, jitter=0.2, dt=1e-2, alpha=1.0, cfg=1, batch=1) -> Problem:
                    {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg})
 
 
-def poisson_2d(k=256, jitter=0.2, batch=64, cfg=2) -> Problem:
+def poisson_2d(k=256, jitter=0.2, batch=64, cfg=2, first=0) -> Problem:
     """Config 2: Poisson stiffness on a jittered k x k square, full-boundary
     Dirichlet eliminated (n = (k-1)^2); B right-hand sides (M f)[free], f a
-    squared-exponential GRF with length scale U[0.05, 0.3]."""
-    rngs = streams(cfg, batch)
-    mesh = unit_square(k, jitter, rngs[0])  # one shared mesh (one L' for all RHS)
+    squared-exponential GRF with length scale U[0.05, 0.3]. ``first`` skips
+    that many RHS streams (one batch per rank); the mesh is always the one
+    drawn from stream 0."""
+    rngs = streams(cfg, first + batch)[first:]
+    mesh_rng = rngs[0] if first == 0 else streams(cfg, 1)[0]
+    mesh = unit_square(k, jitter, mesh_rng)  # one shared mesh (one L' for all RHS)
     K, M = element_blocks(mesh)
     asm = Assembler(len(mesh.vertices), mesh.triangles)
     Kv, Mv = asm.values(K), asm.values(M)
@@ -223,5 +226,13 @@ def wave_2d(k=512, jitter=0.2, dt=1e-3, sigma=0.5, batch=32, cfg=3, first=0) -> 
 
 
 def _host_spmv(A: SparseMatrixCsr, x):
-    """Input-generation helper (not the solve path): y = A x in numpy."""
-    return np.add.reduceat(A.values * x[A.col_idx], A.row_ptr[:-1]) if A.nnz else np.zeros(A.n)
+    """Input-generation helper (not the solve path): y = A x in numpy, each
+    row summed sequentially in stored order like sparse.py:213-219, so
+    loads such as b = M u0 match the reference's assembly bitwise."""
+    deg = np.diff(A.row_ptr)
+    y = np.zeros(A.n)
+    for k in range(int(deg.max()) if A.n else 0):
+        rows = np.flatnonzero(deg > k)
+        p = A.row_ptr[rows] + k
+        y[rows] += A.values[p] * x[A.col_idx[p]]
+    return y

@@ -105,7 +105,7 @@ def pcg_solve(A: SparseMatrixCsr, b, P=None, opts: SolveOptions | None = None):
 
 
 def pcg_solve_batch(A, B_rhs, P=None, opts: SolveOptions | None = None, *, values=None,
-                    with_history=True):
+                    with_history=True, profile=False):
     """Batched solve: B_rhs is (n, B). A is shared, or ``values`` (nnz, B)
     gives B distinct matrices on A's pattern. P is None or a (batched)
     FactorPreconditioner. Returns (X (n, B), [SolveReport] * B); breakdown is
@@ -119,11 +119,14 @@ def pcg_solve_batch(A, B_rhs, P=None, opts: SolveOptions | None = None, *, value
     if fac is False:
         raise TypeError("pcg_solve_batch needs a device preconditioner (FactorPreconditioner) or None")
     X, reps = _pcg_device(A, Bm, fac, opts, batch=Bm.shape[1], values=values,
-                          with_history=with_history)
+                          with_history=with_history, profile=profile)
     return (X if on_dev else X.cpu().numpy()), reps
 
 
-def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True):
+LAST_PROFILE: dict = {}  # filled by a profiled solve: per-kernel-class ms / launches / passes
+
+
+def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True, profile=False):
     torch = _torch()
     n, B = A.n, batch
     if B < 1 or B > _native.MAX_BATCH:
@@ -154,6 +157,9 @@ def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True):
     o.max_iter = max_iter
     o.absolute = int(opts.absolute)
     o.check_every = 0
+    o.profile = int(profile)
+    kms = np.zeros(_native.PROF_SLOTS, dtype=np.float64)
+    kn = np.zeros(_native.PROF_SLOTS, dtype=np.int64)
     x0 = None if opts.x0 is None else to_device(opts.x0).view(n, 1).expand(n, B).contiguous()
     X = torch.empty((n, B), dtype=torch.float64, device="cuda")
     status = np.zeros(B, dtype=np.int32)
@@ -173,10 +179,16 @@ def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True):
     rep.history = hist.ctypes.data if with_history else None
     rep.history_cap = cap
     rep.breakdown_iteration = bd.ctypes.data
+    rep.kernel_ms = kms.ctypes.data
+    rep.kernel_launches = kn.ctypes.data
     _native.check(lib.npcg_pcg_solve(
         solver, _native.ptr(vals), vb, _native.ptr(S), int(sb), _native.ptr(D), int(db),
         _native.ptr(Bm), _native.ptr(X), _native.ptr(x0), ctypes.byref(o), ctypes.byref(rep),
         _native.stream_handle()))
+    LAST_PROFILE.clear()
+    LAST_PROFILE.update(passes=int(rep.passes), iterations=iters.copy(),
+                        kernel_ms={k: float(kms[i]) for i, k in enumerate(_native.PROF_NAMES)},
+                        kernel_launches={k: int(kn[i]) for i, k in enumerate(_native.PROF_NAMES)})
     reports = []
     for b in range(B):
         k = int(iters[b])
