@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -41,32 +42,49 @@ cudaError_t dalloc(T **p, size_t count) {
 
 // Pick the batch group width G (columns per unit) and chunk size for a solve.
 struct SolvePlan {
-    int G = 1, groups = 1, R = 1, use_ring = 1;
+    int G = 1, groups = 1, R = 1;
     SchedSet *set = nullptr;
 };
 
+// Columns per unit (G) and rows per chunk (R). G = 1 keeps every level's
+// items on distinct rows and gives B independent pipelines; the shared-
+// memory ring (window x level width x G doubles) must fit, otherwise the
+// chunks are made smaller (narrower levels).
 int plan_solve(Pattern *F, int B, SolvePlan &plan, std::string &err) {
     int G = 1;
-    while (G * 2 <= std::min(B, 8)) G *= 2;
     if (const char *env = std::getenv("NPCG_GROUP")) {
         int v = std::atoi(env);
         if (v >= 1 && v <= kMaxGroup && (v & (v - 1)) == 0) G = std::min(v, std::max(1, B));
     }
+    if (B % 2) G = 1;  // 16-byte vector staging needs an even column stride
+    int R = choose_chunk_rows(F->n, B, G);
+    size_t cap = 110 * 1024;
+    if (const char *env = std::getenv("NPCG_SMEM_KB")) cap = (size_t)std::max(16, std::atoi(env)) * 1024;
     for (;;) {
-        const int R = choose_chunk_rows(F->n, B, G);
         SchedSet *set = F->schedule(R, err);
         if (!set) return NPCG_ERR_CUDA;
-        const size_t smem = std::max(trsv_smem_bytes(set->fwd, G), trsv_smem_bytes(set->bwd, G));
-        if (smem <= 160 * 1024 || G == 1) {
+        // worst case: batched factor values staged per column
+        const size_t smem = std::max(trsv_smem_plan(set->fwd, G, 1).total, trsv_smem_plan(set->bwd, G, 1).total);
+        if (smem <= cap || R <= 64) {
+            if (smem > 220 * 1024) {
+                err = "triangular-solve ring does not fit in shared memory";
+                return NPCG_ERR_ARGUMENT;
+            }
             plan.G = G;
             plan.groups = (B + G - 1) / G;
             plan.R = R;
             plan.set = set;
-            plan.use_ring = smem <= 160 * 1024 ? 1 : 0;
-            if (const char *env = std::getenv("NPCG_NO_RING")) plan.use_ring = env[0] == '1' ? 0 : plan.use_ring;
+            if (std::getenv("NPCG_VERBOSE"))
+                fprintf(stderr,
+                        "[npcg] plan n=%lld B=%d G=%d R=%d chunks=%d units=%d | fwd maxw=%d words=%d se=%d x=%d "
+                        "W=%d levels=%d | bwd maxw=%d W=%d | smem=%zu\n",
+                        (long long)F->n, B, G, R, set->fwd.chunks, set->fwd.chunks * plan.groups, set->fwd.maxw,
+                        set->fwd.max_words, set->fwd.max_se, set->fwd.maxx, set->fwd.window,
+                        set->fwd.max_chunk_levels, set->bwd.maxw, set->bwd.window, smem);
             return NPCG_OK;
         }
-        G /= 2;
+        if (G > 1) G /= 2;
+        else R = (R + 1) / 2;
     }
 }
 
@@ -98,13 +116,16 @@ struct npcg_solver {
            *final_rel = nullptr;
     double *history = nullptr;
     long long history_cap = 0;
-    int *active_count = nullptr, *drift_count = nullptr, *progress = nullptr;
+    int *active_count = nullptr, *drift_count = nullptr;
     Ctl *ctl = nullptr;
     double *partial = nullptr;
+    double *S_fwd = nullptr, *S_bwd = nullptr;  // factor entries in schedule order
+    size_t S_cap = 0;
     int *h_active = nullptr;  // pinned
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
-                        alpha, beta, rel, final_rel, history, active_count, drift_count, progress, ctl, partial};
+                        alpha, beta, rel, final_rel, history, active_count, drift_count, ctl, partial,
+                        S_fwd, S_bwd};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_active) cudaFreeHost(h_active);
@@ -349,14 +370,16 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     NPCG_CUDA(dalloc(&s->drift_count, 1));
     const int chunks = s->plan.set->fwd.chunks;
     const size_t units = (size_t)chunks * s->plan.groups;
-    NPCG_CUDA(dalloc(&s->progress, units));
-    NPCG_CUDA(cudaMemset(s->progress, 0, std::max<size_t>(units, 1) * 4));
     NPCG_CUDA(dalloc(&s->ctl, 1));
     NPCG_CUDA(cudaMemset(s->ctl, 0, sizeof(Ctl)));
     NPCG_CUDA(cudaMemset(s->drift_count, 0, 4));
     const size_t part = std::max<size_t>((size_t)kReduceBlocksPerSm * num_sms() * B, units * s->plan.G);
     NPCG_CUDA(dalloc(&s->partial, part));
     NPCG_CUDA(cudaMallocHost((void **)&s->h_active, sizeof(int)));
+    // triangular-solve outputs start unsolved (sentinel), see kernels.cu
+    launch_fill_sentinel((long long)nB, s->Y, 0);
+    launch_fill_sentinel((long long)nB, s->Z, 0);
+    NPCG_CUDA(cudaDeviceSynchronize());
     *out = s.release();
     return NPCG_OK;
 }
@@ -392,7 +415,28 @@ static SolveState make_state(npcg_solver *s, const npcg_solve_opts *o) {
     return st;
 }
 
-static TrsvArgs trsv_args(npcg_solver *s, bool upper, int mode, const double *S, int sb, const double *D, int db) {
+// Gather the factor entries (CSR order, symmetric S) into each direction's
+// schedule order; done once per solve call, not per iteration.
+static int stage_factor(npcg_solver *s, const double *S, int sb, cudaStream_t st) {
+    const Schedule &f = s->plan.set->fwd, &b = s->plan.set->bwd;
+    const size_t cols = sb ? (size_t)s->plan.groups * s->plan.G : 1;
+    const size_t need = (size_t)std::max<int64_t>(std::max(f.padded_entries, b.padded_entries), 2) * cols;
+    if (need > s->S_cap) {
+        if (s->S_fwd) cudaFree(s->S_fwd);
+        if (s->S_bwd) cudaFree(s->S_bwd);
+        s->S_fwd = s->S_bwd = nullptr;
+        s->S_cap = 0;
+        NPCG_CUDA(dalloc(&s->S_fwd, need));
+        NPCG_CUDA(dalloc(&s->S_bwd, need));
+        s->S_cap = need;
+    }
+    launch_factor_pack(f, s->B, s->plan.G, sb, S, s->S_fwd, st);
+    launch_factor_pack(b, s->B, s->plan.G, sb, S, s->S_bwd, st);
+    NPCG_CUDA(cudaGetLastError());
+    return NPCG_OK;
+}
+
+static TrsvArgs trsv_args(npcg_solver *s, bool upper, int mode, int sb, const double *D, int db) {
     TrsvArgs t;
     const Pattern *F = s->F;
     t.n = (int)F->n;
@@ -401,18 +445,12 @@ static TrsvArgs trsv_args(npcg_solver *s, bool upper, int mode, const double *S,
     t.groups = s->plan.groups;
     t.upper = upper;
     t.mode = mode;
-    t.use_ring = s->plan.use_ring;
-    t.rp = F->rp;
-    t.dp = F->dp;
-    t.col = F->col;
-    t.dep = s->plan.set->dep;
     t.sched = upper ? s->plan.set->bwd : s->plan.set->fwd;
     t.units = t.sched.chunks * t.groups;
-    t.S = S;
+    t.S = upper ? s->S_bwd : s->S_fwd;
     t.s_batched = sb;
     t.D = D;
     t.d_batched = db;
-    t.progress = s->progress;
     t.ctl = s->ctl;
     t.partial = s->partial;
     t.drift_count = s->drift_count;
@@ -429,11 +467,13 @@ int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int s
     if (int rc = npcg_solver_create(F, F, B, &s)) return rc;
     std::unique_ptr<npcg_solver> guard(s);
     cudaStream_t st = (cudaStream_t)stream;
-    TrsvArgs f = trsv_args(s, false, TRSV_PLAIN, S, sb, D, db);
-    f.in = r;
+    if (int rc = stage_factor(s, S, sb, st)) return rc;
+    launch_fill_sentinel((long long)F->n * B, z, st);  // consumers poll z for solved values
+    TrsvArgs f = trsv_args(s, false, TRSV_PLAIN, sb, D, db);
+    f.in = const_cast<double *>(r);  // read only in the forward solve
     f.out = s->Y;
     NPCG_CUDA(launch_trsv(f, st));
-    TrsvArgs b = trsv_args(s, true, TRSV_PLAIN, S, sb, D, db);
+    TrsvArgs b = trsv_args(s, true, TRSV_PLAIN, sb, D, db);
     b.in = s->Y;
     b.out = z;
     NPCG_CUDA(launch_trsv(b, st));
@@ -531,7 +571,11 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     drift.X = x;
     drift.Bv = bvec;
     drift.R = s->R;
-    TrsvArgs fw = trsv_args(s, false, TRSV_PCG, S, sb, D, db);
+    if (!identity)
+        if (int rc = stage_factor(s, S, sb, st)) return rc;
+    launch_fill_sentinel(nB, s->Y, st);  // re-arm in case an earlier call was interrupted
+    launch_fill_sentinel(nB, s->Z, st);
+    TrsvArgs fw = trsv_args(s, false, TRSV_PCG, sb, D, db);
     fw.in = s->R;
     fw.out = s->Y;
     fw.R = s->R;
@@ -539,7 +583,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     fw.P = s->P;
     fw.AP = s->AP;
     fw.st = sst;
-    TrsvArgs bw = trsv_args(s, true, TRSV_PCG, S, sb, D, db);
+    TrsvArgs bw = trsv_args(s, true, TRSV_PCG, sb, D, db);
     bw.in = s->Y;
     bw.out = s->Z;
     bw.R = s->R;

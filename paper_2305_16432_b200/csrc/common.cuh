@@ -6,6 +6,11 @@
 namespace npcg {
 
 constexpr int kMaxThresholds = 16;
+constexpr int kMaxGroup = 32;  // columns per triangular-solve unit
+
+int num_sms();
+void note_launch();  // launch accounting (npcg_launch_count)
+long long launch_count();
 
 // ---- memory-model helpers (PTX, gpu scope) --------------------------------
 __device__ __forceinline__ int ld_acquire(const int *p) {

@@ -115,15 +115,31 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_kernel(SpmvArgs a) {
         for (int k = 0; k < kMaxCpl; ++k) acc[k] = 0.0;
         const bool use_x = a.op != SPMV_RESID_INIT || a.has_x;
         if (use_x) {
-            for (int p = p0; p < p1; ++p) {
-                const size_t j = (size_t)a.col[p] * B;
-                const double vs = a.vb ? 0.0 : a.vals[p];
+            // Batches of 8 entries: every index / value / operand load of the
+            // batch is issued before the first add, so a row costs one memory
+            // round trip per 8 entries; the adds stay in stored order.
+            for (int pb = p0; pb < p1; pb += 8) {
+                const int m = min(8, p1 - pb);
+                int cj[8];
+                double vv[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    cj[q] = q < m ? a.col[pb + q] : 0;
+                    vv[q] = (q < m && !a.vb) ? a.vals[pb + q] : 0.0;
+                }
 #pragma unroll
                 for (int k = 0; k < kMaxCpl; ++k) {
                     const int b = lane + k * TL;
                     if (k < cpl && b < B) {
-                        const double v = a.vb ? a.vals[(size_t)p * B + b] : vs;
-                        acc[k] = __dadd_rn(acc[k], __dmul_rn(v, a.X[j + b]));
+                        double xv[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            xv[q] = q < m ? a.X[(size_t)cj[q] * B + b] : 0.0;
+                            if (a.vb && q < m) vv[q] = a.vals[(size_t)(pb + q) * B + b];
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (q < m) acc[k] = __dadd_rn(acc[k], __dmul_rn(vv[q], xv[q]));
                     }
                 }
             }
@@ -191,192 +207,6 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_kernel(SpmvArgs a) {
     if (threadIdx.x == 0) {
         a.ctl->done = 0;
         if (a.op == SPMV_RESID_DRIFT) *a.drift_count = 0;
-    }
-}
-
-// ===========================================================================
-// Chunked sync-free triangular solves.
-//   forward : y_i = r_i - sum_{j<i} L'_ij y_j          rows ascending
-//   backward: z_j = y_j / D_j - sum_{i>j} L'_ij z_i    rows descending
-// Work unit = (chunk of contiguous rows, group of G batch columns). A CTA
-// walks the chunk's local levels; values of the last `window` levels live in
-// a shared-memory ring, older / foreign ones are read from global memory
-// after the producer chunk published its progress (release/acquire).
-// ===========================================================================
-
-__device__ __forceinline__ int trsv_col_op(const TrsvArgs &a, int b) {
-    if (a.mode == TRSV_PLAIN) return TOP_SOLVE;
-    const SolveState &st = a.st;
-    if (st.status[b] != ST_ACTIVE) return TOP_SKIP;
-    const int ph = st.phase[b];
-    if (!a.upper) return ph == PH_ITER ? TOP_UPDATE : (ph == PH_INIT ? TOP_SOLVE : TOP_SKIP);
-    return (ph == PH_ITER || ph == PH_INIT) ? TOP_SOLVE : TOP_SKIP;
-}
-
-__device__ void trsv_epilogue(const TrsvArgs &a, int b, double total) {
-    const SolveState &st = a.st;
-    if (st.status[b] != ST_ACTIVE) {
-        if (a.upper) st.pflag[b] = PF_NONE;
-        return;
-    }
-    const int ph = st.phase[b];
-    if (!a.upper) {  // forward: residual norm of the updated r (pcg.py:143-150, 166)
-        if (ph != PH_ITER) return;
-        const double rn = sqrt(total);
-        const long long k = st.k[b];
-        push_history(st, b, k, rn);
-        const double rel = rn / st.scale[b];
-        st.rel[b] = rel;
-        if (rel <= st.thr[st.T - 1]) {
-            st.phase[b] = PH_DRIFT;
-            atomicAdd(a.drift_count, 1);
-        } else {
-            record(st, b, k, rel);
-        }
-        return;
-    }
-    // backward: r.z and the direction update (pcg.py:128-130, 167-171)
-    if (ph == PH_ITER) {
-        st.beta[b] = total / st.rz[b];
-        st.rz[b] = total;
-        st.pflag[b] = PF_UPDATE;
-    } else if (ph == PH_INIT) {
-        st.rz[b] = total;
-        st.pflag[b] = PF_COPY;
-        st.phase[b] = PH_ITER;
-    } else if (ph == PH_RESTART) {
-        st.phase[b] = PH_INIT;
-        st.pflag[b] = PF_NONE;
-    } else {
-        st.pflag[b] = PF_NONE;
-    }
-}
-
-__global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(TrsvArgs a) {
-    extern __shared__ double ring[];  // window * maxw * G
-    __shared__ int s_unit, s_last;
-    __shared__ int s_op[kMaxGroup];
-    __shared__ double s_red[kTrsvThreads];
-    const int tid = threadIdx.x;
-    const int G = a.G, B = a.B;
-    const int lane = tid % G;  // kTrsvThreads % G == 0
-    const Schedule &S = a.sched;
-    const int W = S.window, maxw = S.maxw;
-
-    for (;;) {
-        if (tid == 0) s_unit = atomicAdd(&a.ctl->next_unit, 1);
-        __syncthreads();
-        const int u = s_unit;
-        if (u >= a.units) {
-            if (tid == 0 && atomicAdd(&a.ctl->exited, 1) == (int)gridDim.x - 1) {
-                a.ctl->next_unit = 0;  // every CTA has fetched its last unit
-                a.ctl->exited = 0;
-            }
-            return;
-        }
-        const int c = u / a.groups, g = u % a.groups;
-        if (tid < G) {
-            const int b = g * G + tid;
-            s_op[tid] = b < B ? trsv_col_op(a, b) : TOP_SKIP;
-        }
-        __syncthreads();
-        const int b = g * G + lane;
-        const int op = s_op[lane];
-        const bool any = __syncthreads_or(op != TOP_SKIP);
-        double acc2 = 0.0;
-        if (any) {
-            const int L0 = S.chunk_lvl[c], L1 = S.chunk_lvl[c + 1];
-            int *my_prog = a.progress + (size_t)c * a.groups + g;
-            for (int L = L0; L < L1; ++L) {
-                if (tid < 32) {  // external requirements of this level
-                    for (int q = S.req_ptr[L] + tid; q < S.req_ptr[L + 1]; q += 32) {
-                        const int *pr = a.progress + (size_t)S.req_chunk[q] * a.groups + g;
-                        const int need = S.req_lvl[q];
-                        while (ld_acquire(pr) <= need) {
-                        }
-                    }
-                }
-                __syncthreads();
-                if (tid == 0 && L > L0) st_release(my_prog, L - L0);
-                const int s0 = S.lvl_ptr[L], s1 = S.lvl_ptr[L + 1];
-                const int ring_base = ((L - L0) % W) * maxw;
-                if (op != TOP_SKIP) {
-                    for (int it = tid; it < (s1 - s0) * G; it += kTrsvThreads) {
-                        const int s = s0 + it / G;
-                        const int i = S.rows[s];
-                        const size_t vi = (size_t)i * B + b;
-                        double acc;
-                        if (!a.upper) {
-                            if (op == TOP_UPDATE) {  // x += a p ; r -= a Ap (pcg.py:141-142)
-                                const double al = a.st.alpha[b];
-                                a.X[vi] = __dadd_rn(a.X[vi], __dmul_rn(al, a.P[vi]));
-                                acc = __dsub_rn(a.R[vi], __dmul_rn(al, a.AP[vi]));
-                                a.R[vi] = acc;
-                                acc2 = __dadd_rn(acc2, __dmul_rn(acc, acc));
-                            } else {
-                                acc = a.in[vi];
-                            }
-                            const int p0 = a.rp[i], p1 = a.dp[i];
-                            for (int p = p0; p < p1; ++p) {
-                                const int d = a.dep[p];
-                                const double sv = a.s_batched ? a.S[(size_t)p * B + b] : a.S[p];
-                                double yj;
-                                if (a.use_ring && d >= 0) yj = ring[d * G + lane];
-                                else yj = __ldcg(&a.out[(size_t)(a.use_ring ? -d - 1 : a.col[p]) * B + b]);
-                                acc = __dsub_rn(acc, __dmul_rn(sv, yj));
-                            }
-                        } else {
-                            const double dv = a.d_batched ? a.D[vi] : a.D[i];
-                            acc = __ddiv_rn(a.in[vi], dv);
-                            const int p0 = a.dp[i] + 1, p1 = a.rp[i + 1];
-                            for (int p = p1 - 1; p >= p0; --p) {  // scatter order of sparse.py:236-239
-                                const int d = a.dep[p];
-                                const double sv = a.s_batched ? a.S[(size_t)p * B + b] : a.S[p];
-                                double zj;
-                                if (a.use_ring && d >= 0) zj = ring[d * G + lane];
-                                else zj = __ldcg(&a.out[(size_t)(a.use_ring ? -d - 1 : a.col[p]) * B + b]);
-                                acc = __dsub_rn(acc, __dmul_rn(sv, zj));
-                            }
-                            if (a.mode == TRSV_PCG) acc2 = __dadd_rn(acc2, __dmul_rn(a.R[vi], acc));
-                        }
-                        if (a.use_ring) ring[(ring_base + (s - s0)) * G + lane] = acc;
-                        a.out[vi] = acc;
-                    }
-                }
-            }
-            __syncthreads();
-            if (tid == 0) st_release(my_prog, L1 - L0);
-        }
-        // per-unit partial (fixed order: threads with the same lane, ascending)
-        if (a.mode == TRSV_PCG) {
-            s_red[tid] = acc2;
-            __syncthreads();
-            if (tid < G) {
-                double s = 0.0;
-                for (int t = tid; t < kTrsvThreads; t += G) s = __dadd_rn(s, s_red[t]);
-                a.partial[(size_t)u * G + tid] = s;
-            }
-        }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) s_last = atomicAdd(&a.ctl->done, 1) == a.units - 1;
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            if (a.mode == TRSV_PCG) {
-                for (int bb = tid; bb < B; bb += kTrsvThreads) {
-                    const int gg = bb / G, ll = bb % G;
-                    double s = 0.0;
-                    for (int cc = 0; cc < S.chunks; ++cc)
-                        s = __dadd_rn(s, __ldcg(&a.partial[((size_t)cc * a.groups + gg) * G + ll]));
-                    trsv_epilogue(a, bb, s);
-                }
-            }
-            for (int q = tid; q < S.chunks * a.groups; q += kTrsvThreads) a.progress[q] = 0;
-            if (tid == 0) a.ctl->done = 0;
-            __threadfence();
-        }
-        __syncthreads();
     }
 }
 
@@ -459,12 +289,14 @@ __global__ void init_x_kernel(long long nB, int B, const double *x0, double *x, 
 }
 
 // p = z + beta p  |  p = z   (pcg.py:129, 170)
-__global__ void pupd_kernel(long long nB, int B, const double *z, double *p, SolveState st) {
+__global__ void pupd_kernel(long long nB, int B, double *z, double *p, SolveState st) {
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nB; q += (long long)gridDim.x * blockDim.x) {
         const int b = (int)(q % B);
         const int f = st.pflag[b];
-        if (f == PF_UPDATE) p[q] = __dadd_rn(z[q], __dmul_rn(st.beta[b], p[q]));
-        else if (f == PF_COPY) p[q] = z[q];
+        if (f == PF_NONE) continue;
+        const double zq = z[q];
+        p[q] = f == PF_UPDATE ? __dadd_rn(zq, __dmul_rn(st.beta[b], p[q])) : zq;
+        reinterpret_cast<long long *>(z)[q] = (long long)kSentinel;  // re-arm for the next backward solve
     }
 }
 
@@ -564,25 +396,6 @@ cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s) {
         NPCG_SPMV_CASE(32)
     }
 #undef NPCG_SPMV_CASE
-    return cudaGetLastError();
-}
-
-size_t trsv_smem_bytes(const Schedule &S, int G) {
-    return (size_t)S.window * S.maxw * G * sizeof(double);
-}
-
-cudaError_t launch_trsv(const TrsvArgs &a, cudaStream_t s) {
-    const size_t smem = a.use_ring ? trsv_smem_bytes(a.sched, a.G) : 0;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trsv_kernel, kTrsvThreads, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int grid = std::max(1, std::min(a.units, per_sm * num_sms()));
-    note_launch(); trsv_kernel<<<grid, kTrsvThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

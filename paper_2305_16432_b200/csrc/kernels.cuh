@@ -4,14 +4,13 @@
 
 #include "common.cuh"
 #include "pattern.h"
+#include "trsv.cuh"
 
 namespace npcg {
 
 constexpr int kSpmvThreads = 256;
-constexpr int kTrsvThreads = 128;
 constexpr int kMaxBatch = 256;   // columns per solver call
 constexpr int kMaxCpl = 8;       // columns per lane (kMaxBatch / 32)
-constexpr int kMaxGroup = 32;    // columns per triangular-solve unit
 constexpr int kReduceBlocksPerSm = 2;
 
 enum SpmvOp : int {
@@ -39,34 +38,10 @@ struct SpmvArgs {
     int *drift_count = nullptr;
 };
 
-enum TrsvMode : int { TRSV_PLAIN = 0, TRSV_PCG = 1 };
-enum TrsvOp : int { TOP_SKIP = 0, TOP_SOLVE = 1, TOP_UPDATE = 2 };
-
-struct TrsvArgs {
-    int n = 0, B = 1, G = 1, groups = 1, units = 0;
-    int upper = 0, mode = TRSV_PLAIN, use_ring = 1;
-    const int *rp = nullptr, *dp = nullptr, *col = nullptr, *dep = nullptr;
-    Schedule sched{};
-    const double *S = nullptr;
-    int s_batched = 0;
-    const double *D = nullptr;
-    int d_batched = 0;
-    const double *in = nullptr;  // fwd: r (plain) ; bwd: y
-    double *out = nullptr;       // fwd: y ; bwd: z
-    // PCG fusion (forward: x/r update; backward: r.z)
-    double *R = nullptr, *X = nullptr;
-    const double *P = nullptr, *AP = nullptr;
-    SolveState st{};
-    double *partial = nullptr;
-    int *progress = nullptr;
-    Ctl *ctl = nullptr;
-    int *drift_count = nullptr;
-};
-
 __global__ void init_state_kernel(SolveState st, int B, long long hist_cap_init);
 __global__ void normb_kernel(int n, int B, const double *v, SolveState st, double *partial, Ctl *ctl);
 __global__ void init_x_kernel(long long nB, int B, const double *x0, double *x, SolveState st);
-__global__ void pupd_kernel(long long nB, int B, const double *z, double *p, SolveState st);
+__global__ void pupd_kernel(long long nB, int B, double *z, double *p, SolveState st);
 __global__ void count_active_kernel(SolveState st, int B);
 __global__ void factor_from_lower_kernel(int nnz_lower, int B, int lb, const int *lower_slot,
                                          const int *pair, const double *lower, double *S);
@@ -75,11 +50,6 @@ __global__ void factor_to_lower_kernel(int nnz_lower, int B, const int *lower_sl
 __global__ void symmetric_check_kernel(long long nnz, int B, int vb, const int *pair, const double *vals,
                                        int *ok);
 
-int num_sms();
-void note_launch();          // launch accounting (npcg_launch_count)
-long long launch_count();
 cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s);
-cudaError_t launch_trsv(const TrsvArgs &a, cudaStream_t s);
-size_t trsv_smem_bytes(const Schedule &S, int G);
 
 }  // namespace npcg

@@ -30,8 +30,7 @@ static T *upload(const std::vector<T> &v) {
 }
 
 static void free_schedule(Schedule &s) {
-    int32_t **ptrs[] = {&s.rows, &s.lvl_ptr, &s.chunk_lvl, &s.req_ptr,
-                        &s.req_chunk, &s.req_lvl, &s.row_slot};
+    int32_t **ptrs[] = {&s.packed, &s.lvl_woff, &s.lvl_meta, &s.chunk_lvl, &s.sperm};
     for (auto p : ptrs) {
         if (*p) cudaFree(*p);
         *p = nullptr;
@@ -41,7 +40,6 @@ static void free_schedule(Schedule &s) {
 SchedSet::~SchedSet() {
     free_schedule(fwd);
     free_schedule(bwd);
-    if (dep) cudaFree(dep);
 }
 
 Pattern::~Pattern() {
@@ -51,15 +49,52 @@ Pattern::~Pattern() {
         if (*p) cudaFree(*p);
 }
 
-// Build one direction. `upper` selects the backward (transpose) solve:
-// rows are visited in descending order and depend on their upper entries.
-static std::string build_direction(const Pattern &P, int32_t R, bool upper,
-                                   Schedule &S, std::vector<int32_t> &dep_h) {
+// Build one direction. `upper` selects the backward (transpose) solve: rows
+// are visited in descending order, depend on their upper entries, and each
+// row's entries are accumulated in descending column order -- the order in
+// which the reference's column scatter (sparse.py:236-239) subtracts them.
+// Chunk boundaries near multiples of R, preferring rows that do not depend on
+// their predecessor (row i-1 absent from row i's lower pattern). On meshes in
+// natural order those are the starts of grid lines; cutting there keeps the
+// chunk-local level structure aligned with the global one (window ~3 levels).
+// A cut inside a line would make the next chunk's first levels wait on the
+// previous chunk's last ones and serialise the chunks.
+static std::vector<int32_t> chunk_bounds(const Pattern &P, int32_t R) {
+    const int32_t n = (int32_t)P.n;
+    std::vector<int32_t> cand;
+    for (int32_t i = 1; i < n; ++i) {
+        bool dep_prev = false;
+        for (int32_t p = P.h_rp[i]; p < P.h_dp[i]; ++p) dep_prev |= P.h_col[p] == i - 1;
+        if (!dep_prev) cand.push_back(i);
+    }
+    std::vector<int32_t> b{0};
+    while (b.back() < n) {
+        const int64_t target = (int64_t)b.back() + R;
+        if (target >= n) break;
+        int32_t cut = (int32_t)target;
+        auto it = std::lower_bound(cand.begin(), cand.end(), (int32_t)target);
+        int64_t best = -1;
+        if (it != cand.end()) best = *it;
+        if (it != cand.begin() && *(it - 1) > b.back()) {
+            const int32_t lo = *(it - 1);
+            if (best < 0 || target - lo <= best - target) best = lo;
+        }
+        if (best > b.back() && std::llabs(best - target) <= R / 2) cut = (int32_t)best;
+        b.push_back(cut);
+    }
+    b.push_back(n);
+    return b;
+}
+
+static std::string build_direction(const Pattern &P, int32_t R, bool upper, Schedule &S) {
     const int32_t n = (int32_t)P.n;
     const auto &rp = P.h_rp, &col = P.h_col, &dp = P.h_dp;
-    const int32_t C = n == 0 ? 0 : (n + R - 1) / R;
-    // processing index of the chunk holding row i
-    auto chunk_of = [&](int32_t i) { return upper ? (C - 1 - i / R) : i / R; };
+    const std::vector<int32_t> bounds = n ? chunk_bounds(P, R) : std::vector<int32_t>{0};
+    const int32_t C = (int32_t)bounds.size() - 1;
+    std::vector<int32_t> cid(n);
+    for (int32_t c = 0; c < C; ++c)
+        for (int32_t i = bounds[c]; i < bounds[c + 1]; ++i) cid[i] = upper ? C - 1 - c : c;
+    auto chunk_of = [&](int32_t i) { return cid[i]; };
     auto dep_begin = [&](int32_t i) { return upper ? dp[i] + 1 : rp[i]; };
     auto dep_end = [&](int32_t i) { return upper ? rp[i + 1] : dp[i]; };
 
@@ -84,58 +119,80 @@ static std::string build_direction(const Pattern &P, int32_t R, bool upper,
             if (chunk_of(j) == chunk_of(i)) window = std::max(window, lvl[i] - lvl[j] + 1);
         }
 
-    // per chunk: level counts -> offsets
-    std::vector<int32_t> chunk_lvl(C + 1, 0);
-    std::vector<int32_t> nlev(C, 0);
+    std::vector<int32_t> chunk_lvl(C + 1, 0), nlev(C, 0);
     for (int32_t i = 0; i < n; ++i) nlev[chunk_of(i)] = std::max(nlev[chunk_of(i)], lvl[i] + 1);
     for (int32_t c = 0; c < C; ++c) chunk_lvl[c + 1] = chunk_lvl[c] + nlev[c];
     const int32_t TL = chunk_lvl[C];
-    std::vector<int32_t> lvl_cnt(TL + 1, 0);
-    for (int32_t i = 0; i < n; ++i) lvl_cnt[chunk_lvl[chunk_of(i)] + lvl[i] + 1]++;
     std::vector<int32_t> lvl_ptr(TL + 1, 0);
+    for (int32_t i = 0; i < n; ++i) lvl_ptr[chunk_lvl[chunk_of(i)] + lvl[i] + 1]++;
     int32_t maxw = 1, max_chunk_levels = 0;
     for (int32_t L = 0; L < TL; ++L) {
-        lvl_ptr[L + 1] = lvl_ptr[L] + lvl_cnt[L + 1];
-        maxw = std::max(maxw, lvl_cnt[L + 1]);
+        maxw = std::max(maxw, lvl_ptr[L + 1]);
+        lvl_ptr[L + 1] += lvl_ptr[L];
     }
     for (int32_t c = 0; c < C; ++c) max_chunk_levels = std::max(max_chunk_levels, nlev[c]);
-    // rows in (chunk, level, row-visit order): stable counting sort
-    std::vector<int32_t> rows(n), fill(lvl_ptr.begin(), lvl_ptr.end() - 1), pos(n), slot(n);
+    // rows in (chunk, level, visit order): stable counting sort
+    std::vector<int32_t> rows(n), fill(lvl_ptr.begin(), lvl_ptr.end() - 1), pos(n);
     for (int32_t t = 0; t < n; ++t) {
         const int32_t i = upper ? n - 1 - t : t;
         const int32_t L = chunk_lvl[chunk_of(i)] + lvl[i];
         pos[i] = fill[L] - lvl_ptr[L];
         rows[fill[L]++] = i;
     }
-    for (int32_t i = 0; i < n; ++i) slot[i] = (lvl[i] % window) * maxw + pos[i];
-    // dependency operands and external requirements
-    std::vector<int32_t> req_ptr(TL + 1, 0), req_chunk, req_lvl;
-    std::vector<int32_t> best;  // scratch: per level, max needed level per chunk
-    for (int32_t c = 0; c < C; ++c) {
-        for (int32_t l = 0; l < nlev[c]; ++l) {
-            const int32_t L = chunk_lvl[c] + l;
-            std::vector<std::pair<int32_t, int32_t>> need;  // (chunk, level)
-            for (int32_t s = lvl_ptr[L]; s < lvl_ptr[L + 1]; ++s) {
-                const int32_t i = rows[s];
-                for (int32_t p = dep_begin(i); p < dep_end(i); ++p) {
-                    const int32_t j = col[p];
-                    const int32_t cj = chunk_of(j);
-                    if (cj == c) {
-                        dep_h[p] = slot[j];
-                    } else {
-                        dep_h[p] = -(j + 1);
-                        need.emplace_back(cj, lvl[j]);
-                    }
+    // Packed per-level blocks (int32 words, every section padded to 16 B so a
+    // level is one TMA bulk copy):
+    //   rows[nrow] | eoff[nrow+1] (entry offsets within the level) |
+    //   dep[ne] (>=0 ring slot, <0: -(x+1) = index into xrow) | xrow[nx]
+    // Factor values live in a separate array in the same level order, each
+    // level padded to an even entry count (sperm maps it back to CSR).
+    auto pad4 = [](int64_t x) { return (x + 3) & ~int64_t(3); };
+    std::vector<int32_t> packed, lvl_woff(TL + 1, 0), meta(4 * (size_t)TL, 0), sperm;
+    int32_t max_words = 0, max_se = 0, maxx = 0;
+    int64_t entries = 0;
+    for (int32_t L = 0; L < TL; ++L) {
+        const int32_t s0 = lvl_ptr[L], s1 = lvl_ptr[L + 1], nrow = s1 - s0;
+        std::vector<int32_t> eoff{0}, dep, xrow, perm;
+        for (int32_t s = s0; s < s1; ++s) {
+            const int32_t i = rows[s];
+            const int32_t ci = chunk_of(i);
+            auto push = [&](int32_t p) {
+                const int32_t j = col[p];
+                if (chunk_of(j) == ci) {
+                    dep.push_back((lvl[j] % window) * maxw + pos[j]);
+                } else {
+                    xrow.push_back(j);
+                    dep.push_back(-(int32_t)xrow.size());
                 }
-            }
-            std::sort(need.begin(), need.end());
-            for (size_t k = 0; k < need.size(); ++k) {
-                if (k + 1 < need.size() && need[k + 1].first == need[k].first) continue;
-                req_chunk.push_back(need[k].first);
-                req_lvl.push_back(need[k].second);
-            }
-            req_ptr[L + 1] = (int32_t)req_chunk.size();
+                perm.push_back(p);
+            };
+            if (upper)
+                for (int32_t p = dep_end(i) - 1; p >= dep_begin(i); --p) push(p);
+            else
+                for (int32_t p = dep_begin(i); p < dep_end(i); ++p) push(p);
+            eoff.push_back((int32_t)dep.size());
         }
+        const int32_t ne = (int32_t)dep.size(), nx = (int32_t)xrow.size();
+        const int64_t w0 = (int64_t)packed.size();
+        auto put = [&](const std::vector<int32_t> &v, int64_t len) {
+            packed.insert(packed.end(), v.begin(), v.end());
+            packed.resize(packed.size() + (pad4(len) - len), 0);
+        };
+        put(std::vector<int32_t>(rows.begin() + s0, rows.begin() + s1), nrow);
+        put(eoff, nrow + 1);
+        put(dep, ne);
+        put(xrow, nx);
+        lvl_woff[L + 1] = (int32_t)packed.size();
+        max_words = std::max<int32_t>(max_words, (int32_t)(packed.size() - w0));
+        const int32_t se = (ne + 1) & ~1;
+        meta[4 * L + 0] = nrow;
+        meta[4 * L + 1] = ne;
+        meta[4 * L + 2] = nx;
+        meta[4 * L + 3] = (int32_t)sperm.size();
+        sperm.insert(sperm.end(), perm.begin(), perm.end());
+        sperm.resize(sperm.size() + (se - ne), -1);
+        max_se = std::max(max_se, se);
+        maxx = std::max(maxx, nx);
+        entries += ne;
     }
     free_schedule(S);
     S.chunks = C;
@@ -145,14 +202,17 @@ static std::string build_direction(const Pattern &P, int32_t R, bool upper,
     S.total_levels = TL;
     S.max_chunk_levels = max_chunk_levels;
     S.levels_global = levels_global;
-    S.rows = upload(rows);
-    S.lvl_ptr = upload(lvl_ptr);
+    S.entries = entries;
+    S.padded_entries = (int64_t)sperm.size();
+    S.max_words = max_words;
+    S.max_se = max_se;
+    S.maxx = maxx;
+    S.packed = upload(packed);
+    S.lvl_woff = upload(lvl_woff);
+    S.lvl_meta = upload(meta);
     S.chunk_lvl = upload(chunk_lvl);
-    S.req_ptr = upload(req_ptr);
-    S.req_chunk = upload(req_chunk);
-    S.req_lvl = upload(req_lvl);
-    S.row_slot = upload(slot);
-    if (!S.rows || !S.lvl_ptr || !S.chunk_lvl || !S.req_ptr || !S.req_chunk || !S.req_lvl || !S.row_slot)
+    S.sperm = upload(sperm);
+    if (!S.packed || !S.lvl_woff || !S.lvl_meta || !S.chunk_lvl || !S.sperm)
         return "cudaMalloc failed for the solve schedule";
     return "";
 }
@@ -168,15 +228,9 @@ SchedSet *Pattern::schedule(int32_t R, std::string &err) {
     auto it = scheds.find(R);
     if (it != scheds.end()) return it->second.get();
     auto set = std::make_unique<SchedSet>();
-    std::vector<int32_t> dep_h(nnz, 0);
-    err = build_direction(*this, R, false, set->fwd, dep_h);
-    if (err.empty()) err = build_direction(*this, R, true, set->bwd, dep_h);
+    err = build_direction(*this, R, false, set->fwd);
+    if (err.empty()) err = build_direction(*this, R, true, set->bwd);
     if (!err.empty()) return nullptr;
-    set->dep = upload(dep_h);
-    if (!set->dep) {
-        err = "cudaMalloc failed for the dependency operands";
-        return nullptr;
-    }
     SchedSet *raw = set.get();
     scheds.emplace(R, std::move(set));
     return raw;
@@ -189,9 +243,11 @@ int32_t choose_chunk_rows(int64_t n, int B, int G) {
     }
     if (n <= 0) return 1;
     const int groups = (B + G - 1) / G;
-    // aim for ~3 resident units per SM across all groups, chunks of >= 256 rows
-    int64_t chunks = (3 * 148 + groups - 1) / groups;
-    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, n / 256));
+    // The solve is latency bound along the level chain; extra chunks only add
+    // hand-offs. Use just enough chunks for ~2 resident units per SM, each of
+    // at least 4096 rows.
+    int64_t chunks = (2 * 148 + groups - 1) / groups;
+    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, n / 4096));
     return (int32_t)((n + chunks - 1) / chunks);
 }
 

@@ -1,22 +1,29 @@
 // pattern.h -- device-resident analysis of one sparsity pattern (internal).
 #pragma once
 #include <cstdint>
-#include <string>
 #include <map>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <vector>
 
 namespace npcg {
 
 // One direction (forward = lower rows ascending, backward = upper rows
-// descending) of the chunked triangular-solve schedule. Rows are split into
-// contiguous chunks; inside a chunk rows are grouped by chunk-local level
-// (longest intra-chunk dependency chain). A CTA owning a (chunk, batch
-// group) unit walks its levels with one __syncthreads per level, keeping
-// the freshly solved values in a shared-memory ring of `window` levels.
-// Dependencies on earlier chunks are satisfied by per-(chunk, group)
-// progress counters published with release stores.
+// descending) of the chunked triangular-solve schedule.
+//
+// Rows are split into `chunks` contiguous ranges; inside a chunk rows are
+// grouped by chunk-local level (longest chain of intra-chunk dependencies).
+// A CTA owning a (chunk, batch-column group) unit walks its levels with one
+// __syncthreads per level and keeps the last `window` levels of solved
+// values in a shared-memory ring. Values from earlier chunks are read from
+// global memory: every solved value is published with a relaxed store over
+// a sentinel NaN, so a consumer simply polls the value itself -- no fences,
+// no counters (kernels.cu).
+//
+// All per-entry data is stored in schedule order, so the entries of one
+// level are one contiguous block that can be prefetched into L1 a few
+// levels ahead of use.
 struct Schedule {
     int32_t chunks = 0;       // number of chunks (processing order)
     int32_t chunk_rows = 0;   // rows per chunk (last may be short)
@@ -25,23 +32,21 @@ struct Schedule {
     int32_t total_levels = 0; // sum over chunks of their level counts
     int32_t max_chunk_levels = 0;
     int32_t levels_global = 0;
-    bool smem_ok = true;      // ring fits; else all deps read from global
-    // device arrays
-    int32_t *rows = nullptr;      // [n] row ids in (chunk, level, position) order
-    int32_t *lvl_ptr = nullptr;   // [total_levels+1] offsets into rows
-    int32_t *chunk_lvl = nullptr; // [chunks+1] offsets into lvl_ptr
-    int32_t *req_ptr = nullptr;   // [total_levels+1] offsets into req_*
-    int32_t *req_chunk = nullptr; // external requirement: chunk (processing index)
-    int32_t *req_lvl = nullptr;   //   ... must have completed this local level
-    int32_t *row_slot = nullptr;  // [n] ring slot of each row (level%W*maxw+pos)
+    int64_t entries = 0;          // strict-triangle entries (= nnz_lower)
+    int64_t padded_entries = 0;   // factor-value slots (levels padded to even counts)
+    int32_t max_words = 0;        // largest packed level block (int32 words)
+    int32_t max_se = 0;           // largest padded entry count of a level
+    int32_t maxx = 0;             // most foreign dependencies in one level
+    // device arrays (see pattern.cpp build_direction for the packed layout)
+    int32_t *packed = nullptr;    // per-level blocks: rows | eoff | dep | xrow
+    int32_t *lvl_woff = nullptr;  // [total_levels+1] word offset of each block
+    int32_t *lvl_meta = nullptr;  // [total_levels][4] nrow, ne, nx, factor offset
+    int32_t *chunk_lvl = nullptr; // [chunks+1] first level of each chunk
+    int32_t *sperm = nullptr;     // [padded_entries] CSR position (or -1) of a factor slot
 };
 
-// Both directions for one chunk size, plus the per-entry operand array:
-// dep[p] >= 0 is a ring slot (same chunk), dep[p] < 0 encodes row -(dep+1).
-// Lower entries carry forward operands, upper entries backward operands.
 struct SchedSet {
     Schedule fwd, bwd;
-    int32_t *dep = nullptr;
     ~SchedSet();
 };
 

@@ -1,0 +1,49 @@
+// trsv.cuh -- launch interface of the level-pipelined triangular solves.
+#pragma once
+#include "common.cuh"
+#include "pattern.h"
+
+namespace npcg {
+
+constexpr int kTrsvThreads = 256;
+constexpr int kTrsvPD = 4;  // pipeline depth in levels (struct 2*PD ahead, vectors PD ahead)
+
+enum TrsvMode : int { TRSV_PLAIN = 0, TRSV_PCG = 1 };
+enum TrsvOp : int { TOP_SKIP = 0, TOP_SOLVE = 1, TOP_UPDATE = 2, TOP_RESET = 3 };
+
+// Unsolved marker for triangular-solve outputs (a NaN payload arithmetic
+// never produces); consumers poll until the value differs from it.
+constexpr unsigned long long kSentinel = 0xFFF4BADC0FFEE000ull;
+
+struct TrsvArgs {
+    int n = 0, B = 1, G = 1, groups = 1, units = 0;
+    int upper = 0, mode = TRSV_PLAIN;
+    Schedule sched{};
+    const double *S = nullptr;  // factor values, packed in this direction's level order
+    int s_batched = 0;          // S laid out [group][padded entries][G]
+    const double *D = nullptr;
+    int d_batched = 0;
+    double *in = nullptr;   // forward: r ; backward: y (re-armed after use in PCG mode)
+    double *out = nullptr;  // forward: y ; backward: z (must start as sentinels)
+    double *R = nullptr, *X = nullptr;
+    const double *P = nullptr, *AP = nullptr;
+    SolveState st{};
+    double *partial = nullptr;
+    Ctl *ctl = nullptr;
+    int *drift_count = nullptr;
+};
+
+// Shared-memory layout (bytes) of one CTA.
+struct TrsvSmem {
+    unsigned ring_off = 0, lvl_off = 0, mbar_off = 0, struct_off = 0, data_off = 0, total = 0;
+    int lvl_n = 0, struct_bytes = 0, sval_off = 0, data_bytes = 0, ext_off = 0, slab = 0;
+};
+
+TrsvSmem trsv_smem_plan(const Schedule &S, int G, int s_batched);
+cudaError_t launch_trsv(const TrsvArgs &a, cudaStream_t s);
+// factor values (CSR order, symmetric S) -> packed level order of `sched`
+void launch_factor_pack(const Schedule &sched, int B, int G, int s_batched, const double *S, double *packed,
+                        cudaStream_t s);
+void launch_fill_sentinel(long long count, double *p, cudaStream_t s);
+
+}  // namespace npcg
