@@ -13,7 +13,7 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnpcg.so")
+LIB_PATH = os.environ.get("NPCG_LIB") or os.path.join(_HERE, "libnpcg.so")
 
 # status / error codes (npcg.h)
 OK = 0

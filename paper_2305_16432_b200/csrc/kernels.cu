@@ -115,31 +115,15 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_kernel(SpmvArgs a) {
         for (int k = 0; k < kMaxCpl; ++k) acc[k] = 0.0;
         const bool use_x = a.op != SPMV_RESID_INIT || a.has_x;
         if (use_x) {
-            // Batches of 8 entries: every index / value / operand load of the
-            // batch is issued before the first add, so a row costs one memory
-            // round trip per 8 entries; the adds stay in stored order.
-            for (int pb = p0; pb < p1; pb += 8) {
-                const int m = min(8, p1 - pb);
-                int cj[8];
-                double vv[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    cj[q] = q < m ? a.col[pb + q] : 0;
-                    vv[q] = (q < m && !a.vb) ? a.vals[pb + q] : 0.0;
-                }
+            for (int p = p0; p < p1; ++p) {
+                const size_t j = (size_t)a.col[p] * B;
+                const double vs = a.vb ? 0.0 : a.vals[p];
 #pragma unroll
                 for (int k = 0; k < kMaxCpl; ++k) {
                     const int b = lane + k * TL;
                     if (k < cpl && b < B) {
-                        double xv[8];
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            xv[q] = q < m ? a.X[(size_t)cj[q] * B + b] : 0.0;
-                            if (a.vb && q < m) vv[q] = a.vals[(size_t)(pb + q) * B + b];
-                        }
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            if (q < m) acc[k] = __dadd_rn(acc[k], __dmul_rn(vv[q], xv[q]));
+                        const double v = a.vb ? a.vals[(size_t)p * B + b] : vs;
+                        acc[k] = __dadd_rn(acc[k], __dmul_rn(v, a.X[j + b]));
                     }
                 }
             }
