@@ -194,6 +194,13 @@ def peak_hbm():
 _CPU = {}
 
 
+def _cpu_worker_init():
+    # one BLAS thread per worker process: the reference solve is sequential and
+    # the parent's BLAS pool (already loaded) would otherwise oversubscribe
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+
+
 def _cpu_solve(j):
     from oracle import port
     A, F, rhs = _CPU["A"], _CPU["F"], _CPU["rhs"]
@@ -220,11 +227,10 @@ def cpu_reference(prob, model, steps, warmup, cores=None):
     _CPU.update(A=A, F=F, rhs=prob.rhs)
     B = prob.rhs.shape[1]
     per_round = min(cores, B)
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     ctx = mp.get_context("fork")
     rounds = []
     its = []
-    with ctx.Pool(per_round) as pool:
+    with ctx.Pool(per_round, initializer=_cpu_worker_init) as pool:
         for s in range(warmup + steps):
             cols = [(s * per_round + j) % B for j in range(per_round)]
             t = time.perf_counter()
