@@ -121,11 +121,14 @@ struct npcg_solver {
     double *partial = nullptr;
     double *S_fwd = nullptr, *S_bwd = nullptr;  // factor entries in schedule order
     size_t S_cap = 0;
+    LineSched *ls = nullptr;  // line-wavefront schedule (owned by the pattern) or null
+    int line_K = 0;
+    int *xpend = nullptr;
     int *h_active = nullptr;  // pinned
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
                         alpha, beta, rel, final_rel, history, active_count, drift_count, ctl, partial,
-                        S_fwd, S_bwd};
+                        S_fwd, S_bwd, xpend};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_active) cudaFreeHost(h_active);
@@ -346,6 +349,13 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     }
     std::string err;
     if (int rc = plan_solve(s->F, B, s->plan, err)) return fail(rc, err);
+    if (LineSched *ls = s->F->line_schedule()) {
+        const int K = std::min(line_batch_for(ls->fwd), line_batch_for(ls->bwd));
+        if (K > 0) {
+            s->ls = ls;
+            s->line_K = K;
+        }
+    }
     const size_t nB = (size_t)A->n * B;
     NPCG_CUDA(dalloc(&s->R, nB));
     NPCG_CUDA(dalloc(&s->P, nB));
@@ -353,6 +363,7 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     NPCG_CUDA(dalloc(&s->AP, nB));
     NPCG_CUDA(dalloc(&s->Y, nB));
     NPCG_CUDA(dalloc(&s->status, B));
+    NPCG_CUDA(dalloc(&s->xpend, B));
     NPCG_CUDA(dalloc(&s->phase, B));
     NPCG_CUDA(dalloc(&s->pflag, B));
     NPCG_CUDA(dalloc(&s->k, B));
@@ -392,6 +403,7 @@ int npcg_solver_destroy(npcg_solver *s) {
 static SolveState make_state(npcg_solver *s, const npcg_solve_opts *o) {
     SolveState st{};
     st.status = s->status;
+    st.xpend = s->xpend;
     st.phase = s->phase;
     st.pflag = s->pflag;
     st.k = s->k;
@@ -418,9 +430,16 @@ static SolveState make_state(npcg_solver *s, const npcg_solve_opts *o) {
 // Gather the factor entries (CSR order, symmetric S) into each direction's
 // schedule order; done once per solve call, not per iteration.
 static int stage_factor(npcg_solver *s, const double *S, int sb, cudaStream_t st) {
-    const Schedule &f = s->plan.set->fwd, &b = s->plan.set->bwd;
-    const size_t cols = sb ? (size_t)s->plan.groups * s->plan.G : 1;
-    const size_t need = (size_t)std::max<int64_t>(std::max(f.padded_entries, b.padded_entries), 2) * cols;
+    size_t need;
+    if (s->ls) {
+        const LineDir &f = s->ls->fwd;
+        need = (size_t)f.steps_pad * f.md * f.T * (sb ? s->B : 1);
+        need = std::max(need, (size_t)s->ls->bwd.steps_pad * s->ls->bwd.md * s->ls->bwd.T * (sb ? s->B : 1));
+    } else {
+        const Schedule &f = s->plan.set->fwd, &b = s->plan.set->bwd;
+        const size_t cols = sb ? (size_t)s->plan.groups * s->plan.G : 1;
+        need = (size_t)std::max<int64_t>(std::max(f.padded_entries, b.padded_entries), 2) * cols;
+    }
     if (need > s->S_cap) {
         if (s->S_fwd) cudaFree(s->S_fwd);
         if (s->S_bwd) cudaFree(s->S_bwd);
@@ -430,30 +449,69 @@ static int stage_factor(npcg_solver *s, const double *S, int sb, cudaStream_t st
         NPCG_CUDA(dalloc(&s->S_bwd, need));
         s->S_cap = need;
     }
-    launch_factor_pack(f, s->B, s->plan.G, sb, S, s->S_fwd, st);
-    launch_factor_pack(b, s->B, s->plan.G, sb, S, s->S_bwd, st);
+    if (s->ls) {  // S batched is laid out S[p * B + b]
+        launch_line_factor_pack(s->ls->fwd, s->B, sb, sb ? s->B : 1, 1, S, s->S_fwd, st);
+        launch_line_factor_pack(s->ls->bwd, s->B, sb, sb ? s->B : 1, 1, S, s->S_bwd, st);
+    } else {
+        launch_factor_pack(s->plan.set->fwd, s->B, s->plan.G, sb, S, s->S_fwd, st);
+        launch_factor_pack(s->plan.set->bwd, s->B, s->plan.G, sb, S, s->S_bwd, st);
+    }
     NPCG_CUDA(cudaGetLastError());
     return NPCG_OK;
 }
 
-static TrsvArgs trsv_args(npcg_solver *s, bool upper, int mode, int sb, const double *D, int db) {
-    TrsvArgs t;
+// One direction of P^{-1}: the line-wavefront kernel when the pattern
+// qualifies, else the chunked level kernel. Vectors are RHS-minor (i*B + b).
+struct Tri {
+    bool line = false;
+    TrsvArgs v;
+    LineArgs l;
+    void io(double *in, double *out, double *R, const double *AP, const SolveState &st) {
+        v.in = l.in = in;
+        v.out = l.out = out;
+        v.R = l.R = R;
+        v.AP = l.AP = AP;
+        v.st = l.st = st;
+    }
+    cudaError_t launch(cudaStream_t s) const { return line ? launch_trsv_line(l, s) : launch_trsv(v, s); }
+};
+
+static Tri tri_args(npcg_solver *s, bool upper, int mode, int sb, const double *D, int db) {
+    Tri t;
+    t.line = s->ls != nullptr;
+    if (t.line) {
+        LineArgs &l = t.l;
+        l.B = s->B;
+        l.K = s->line_K;
+        l.upper = upper;
+        l.mode = mode;
+        l.rs = s->B;
+        l.cs = 1;
+        l.dir = upper ? s->ls->bwd : s->ls->fwd;
+        l.S = upper ? s->S_bwd : s->S_fwd;
+        l.s_batched = sb;
+        l.D = D;
+        l.d_batched = db;
+        l.drift_count = s->drift_count;
+        return t;
+    }
+    TrsvArgs &v = t.v;
     const Pattern *F = s->F;
-    t.n = (int)F->n;
-    t.B = s->B;
-    t.G = s->plan.G;
-    t.groups = s->plan.groups;
-    t.upper = upper;
-    t.mode = mode;
-    t.sched = upper ? s->plan.set->bwd : s->plan.set->fwd;
-    t.units = t.sched.chunks * t.groups;
-    t.S = upper ? s->S_bwd : s->S_fwd;
-    t.s_batched = sb;
-    t.D = D;
-    t.d_batched = db;
-    t.ctl = s->ctl;
-    t.partial = s->partial;
-    t.drift_count = s->drift_count;
+    v.n = (int)F->n;
+    v.B = s->B;
+    v.G = s->plan.G;
+    v.groups = s->plan.groups;
+    v.upper = upper;
+    v.mode = mode;
+    v.sched = upper ? s->plan.set->bwd : s->plan.set->fwd;
+    v.units = v.sched.chunks * v.groups;
+    v.S = upper ? s->S_bwd : s->S_fwd;
+    v.s_batched = sb;
+    v.D = D;
+    v.d_batched = db;
+    v.ctl = s->ctl;
+    v.partial = s->partial;
+    v.drift_count = s->drift_count;
     return t;
 }
 
@@ -468,15 +526,13 @@ int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int s
     std::unique_ptr<npcg_solver> guard(s);
     cudaStream_t st = (cudaStream_t)stream;
     if (int rc = stage_factor(s, S, sb, st)) return rc;
-    launch_fill_sentinel((long long)F->n * B, z, st);  // consumers poll z for solved values
-    TrsvArgs f = trsv_args(s, false, TRSV_PLAIN, sb, D, db);
-    f.in = const_cast<double *>(r);  // read only in the forward solve
-    f.out = s->Y;
-    NPCG_CUDA(launch_trsv(f, st));
-    TrsvArgs b = trsv_args(s, true, TRSV_PLAIN, sb, D, db);
-    b.in = s->Y;
-    b.out = z;
-    NPCG_CUDA(launch_trsv(b, st));
+    if (!s->ls) launch_fill_sentinel((long long)F->n * B, z, st);  // level kernel polls z
+    Tri f = tri_args(s, false, TRSV_PLAIN, sb, D, db);
+    f.io(const_cast<double *>(r), s->Y, nullptr, nullptr, SolveState{});  // r is only read
+    NPCG_CUDA(f.launch(st));
+    Tri b = tri_args(s, true, TRSV_PLAIN, sb, D, db);
+    b.io(s->Y, z, nullptr, nullptr, SolveState{});
+    NPCG_CUDA(b.launch(st));
     NPCG_CUDA(cudaStreamSynchronize(st));
     return NPCG_OK;
 }
@@ -571,23 +627,17 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     drift.X = x;
     drift.Bv = bvec;
     drift.R = s->R;
-    if (!identity)
-        if (int rc = stage_factor(s, S, sb, st)) return rc;
-    launch_fill_sentinel(nB, s->Y, st);  // re-arm in case an earlier call was interrupted
-    launch_fill_sentinel(nB, s->Z, st);
-    TrsvArgs fw = trsv_args(s, false, TRSV_PCG, sb, D, db);
-    fw.in = s->R;
-    fw.out = s->Y;
-    fw.R = s->R;
-    fw.X = x;
-    fw.P = s->P;
-    fw.AP = s->AP;
-    fw.st = sst;
-    TrsvArgs bw = trsv_args(s, true, TRSV_PCG, sb, D, db);
-    bw.in = s->Y;
-    bw.out = s->Z;
-    bw.R = s->R;
-    bw.st = sst;
+    drift.P = s->P;
+    // identity: S = ones is never referenced (no off-diagonal slots), packs to zeros
+    if (int rc = stage_factor(s, S, sb, st)) return rc;
+    if (!s->ls) {  // the level kernel's outputs start unsolved (re-armed every pass)
+        launch_fill_sentinel(nB, s->Y, st);
+        launch_fill_sentinel(nB, s->Z, st);
+    }
+    Tri fw = tri_args(s, false, TRSV_PCG, sb, D, db);
+    fw.io(s->R, s->Y, s->R, s->AP, sst);
+    Tri bw = tri_args(s, true, TRSV_PCG, sb, D, db);
+    bw.io(s->Y, s->Z, s->R, nullptr, sst);
 
     // Optional per-launch timing (npcg_solve_opts.profile): a start/stop
     // event pair around every launch of the loop, summed per kernel class.
@@ -628,7 +678,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     };
     auto pupd = [&]() {
         note_launch();
-        pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, sst);
+        pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, x, sst, s->ls ? 0 : 1);
         return cudaGetLastError();
     };
 
@@ -638,9 +688,9 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     for (;;) {
         for (int q = 0; q < check; ++q) {
             NPCG_CUDA(timed(NPCG_PROF_SPMV_APDOT, [&] { return launch_spmv(apdot, st); }));
-            NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return launch_trsv(fw, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return fw.launch(st); }));
             NPCG_CUDA(timed(NPCG_PROF_SPMV_DRIFT, [&] { return launch_spmv(drift, st); }));
-            NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return launch_trsv(bw, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return bw.launch(st); }));
             NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
         }
         passes += check;

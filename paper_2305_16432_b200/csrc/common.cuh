@@ -37,11 +37,15 @@ enum Status : int { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BREAKDOW
 //               b - A x (pcg.py:147-165).
 //  PH_RESTART : drift found; skip the rest of this pass, next pass is PH_INIT.
 enum Phase : int { PH_INIT = 0, PH_ITER = 1, PH_DRIFT = 2, PH_RESTART = 3 };
-enum PFlag : int { PF_NONE = 0, PF_UPDATE = 1, PF_COPY = 2 };
+// What pupd does for a column at the end of a pass. PF_X: apply the pending
+// x += alpha p of this pass first (the update is deferred out of the
+// triangular solve; the drift check reads x + alpha p on the fly).
+enum PFlag : int { PF_NONE = 0, PF_UPDATE = 1, PF_COPY = 2, PF_X = 4 };
 
 struct SolveState {
     // per column [B]
     int *status, *phase, *pflag;
+    int *xpend;                // 1 while this pass's x += alpha p is pending
     long long *k;              // iterations
     long long *breakdown_at;
     double *scale, *rz, *alpha, *beta, *rel, *final_rel;
@@ -80,6 +84,46 @@ __device__ __forceinline__ void record(const SolveState &st, int b, long long k,
 
 __device__ __forceinline__ void push_history(const SolveState &st, int b, long long k, double v) {
     if (k < st.history_cap) st.history[(size_t)b * st.history_cap + k] = v;
+}
+
+// Forward-solve epilogue: residual norm of the updated r (pcg.py:143-150, 166).
+__device__ inline void fwd_epilogue(const SolveState &st, int b, double total, int *drift_count) {
+    if (st.status[b] != ST_ACTIVE || st.phase[b] != PH_ITER) return;
+    const double rn = sqrt(total);
+    const long long k = st.k[b];
+    push_history(st, b, k, rn);
+    const double rel = rn / st.scale[b];
+    st.rel[b] = rel;
+    if (rel <= st.thr[st.T - 1]) {
+        st.phase[b] = PH_DRIFT;
+        atomicAdd(drift_count, 1);
+    } else {
+        record(st, b, k, rel);
+    }
+}
+
+// Backward-solve epilogue: r.z and what pupd does next (pcg.py:128-130, 167-171).
+__device__ inline void bwd_epilogue(const SolveState &st, int b, double total) {
+    int f = PF_NONE;
+    if (st.status[b] == ST_ACTIVE) {
+        const int ph = st.phase[b];
+        if (ph == PH_ITER) {
+            st.beta[b] = total / st.rz[b];
+            st.rz[b] = total;
+            f = PF_UPDATE;
+        } else if (ph == PH_INIT) {
+            st.rz[b] = total;
+            f = PF_COPY;
+            st.phase[b] = PH_ITER;
+        } else if (ph == PH_RESTART) {
+            st.phase[b] = PH_INIT;
+        }
+    }
+    if (st.xpend[b]) {  // converged, restarted or iterating: x_{k+1} = x_k + alpha p_k
+        f |= PF_X;
+        st.xpend[b] = 0;
+    }
+    st.pflag[b] = f;
 }
 
 }  // namespace npcg

@@ -50,6 +50,7 @@ __device__ void spmv_epilogue(const SpmvArgs &a, int b, double total) {
                 return;
             }
             st.alpha[b] = st.rz[b] / pAp;
+            st.xpend[b] = 1;  // x += alpha p happens in pupd (pcg.py:141)
             return;
         }
         case SPMV_RESID_INIT: {  // pcg.py:111-126
@@ -123,7 +124,10 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_kernel(SpmvArgs a) {
                     const int b = lane + k * TL;
                     if (k < cpl && b < B) {
                         const double v = a.vb ? a.vals[(size_t)p * B + b] : vs;
-                        acc[k] = __dadd_rn(acc[k], __dmul_rn(v, a.X[j + b]));
+                        double xv = a.X[j + b];
+                        if (a.op == SPMV_RESID_DRIFT && a.st.xpend[b])  // x_{k+1} not yet stored
+                            xv = __dadd_rn(xv, __dmul_rn(a.st.alpha[b], a.P[j + b]));
+                        acc[k] = __dadd_rn(acc[k], __dmul_rn(v, xv));
                     }
                 }
             }
@@ -205,6 +209,7 @@ __global__ void init_state_kernel(SolveState st, int B, long long hist_cap_init)
     st.status[b] = ST_ACTIVE;
     st.phase[b] = PH_INIT;
     st.pflag[b] = PF_NONE;
+    st.xpend[b] = 0;
     st.k[b] = 0;
     st.breakdown_at[b] = 0;
     st.rz[b] = st.alpha[b] = st.beta[b] = st.rel[b] = st.final_rel[b] = 0.0;
@@ -273,14 +278,18 @@ __global__ void init_x_kernel(long long nB, int B, const double *x0, double *x, 
 }
 
 // p = z + beta p  |  p = z   (pcg.py:129, 170)
-__global__ void pupd_kernel(long long nB, int B, double *z, double *p, SolveState st) {
+__global__ void pupd_kernel(long long nB, int B, double *z, double *p, double *x, SolveState st, int rearm) {
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nB; q += (long long)gridDim.x * blockDim.x) {
         const int b = (int)(q % B);
         const int f = st.pflag[b];
         if (f == PF_NONE) continue;
-        const double zq = z[q];
-        p[q] = f == PF_UPDATE ? __dadd_rn(zq, __dmul_rn(st.beta[b], p[q])) : zq;
-        reinterpret_cast<long long *>(z)[q] = (long long)kSentinel;  // re-arm for the next backward solve
+        const double pq = p[q];
+        if (f & PF_X) x[q] = __dadd_rn(x[q], __dmul_rn(st.alpha[b], pq));  // pcg.py:141
+        if (f & (PF_UPDATE | PF_COPY)) {
+            const double zq = z[q];
+            p[q] = (f & PF_UPDATE) ? __dadd_rn(zq, __dmul_rn(st.beta[b], pq)) : zq;  // pcg.py:129, 170
+            if (rearm) reinterpret_cast<long long *>(z)[q] = (long long)kSentinel;  // for the next backward solve
+        }
     }
 }
 

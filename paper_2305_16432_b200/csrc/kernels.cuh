@@ -30,6 +30,7 @@ struct SpmvArgs {
     double *Y = nullptr;
     const double *Bv = nullptr;
     double *R = nullptr;
+    const double *P = nullptr;  // drift check: x + alpha p for columns with a pending update
     int op = SPMV_PLAIN;
     int has_x = 1;
     SolveState st{};
@@ -41,7 +42,7 @@ struct SpmvArgs {
 __global__ void init_state_kernel(SolveState st, int B, long long hist_cap_init);
 __global__ void normb_kernel(int n, int B, const double *v, SolveState st, double *partial, Ctl *ctl);
 __global__ void init_x_kernel(long long nB, int B, const double *x0, double *x, SolveState st);
-__global__ void pupd_kernel(long long nB, int B, double *z, double *p, SolveState st);
+__global__ void pupd_kernel(long long nB, int B, double *z, double *p, double *x, SolveState st, int rearm);
 __global__ void count_active_kernel(SolveState st, int B);
 __global__ void factor_from_lower_kernel(int nnz_lower, int B, int lb, const int *lower_slot,
                                          const int *pair, const double *lower, double *S);

@@ -217,6 +217,112 @@ static std::string build_direction(const Pattern &P, int32_t R, bool upper, Sche
     return "";
 }
 
+LineSched::~LineSched() {
+    for (LineDir *d : {&fwd, &bwd}) {
+        if (d->line_row0) cudaFree(d->line_row0);
+        if (d->line_len) cudaFree(d->line_len);
+        if (d->desc) cudaFree(d->desc);
+        if (d->vperm) cudaFree(d->vperm);
+    }
+}
+
+// One direction of the line schedule; false when the pattern does not
+// qualify (too many lines, deep cross-line window, wide rows).
+static bool build_lines(const Pattern &P, bool upper, LineDir &D) {
+    const int32_t n = (int32_t)P.n;
+    const auto &rp = P.h_rp, &col = P.h_col, &dp = P.h_dp;
+    std::vector<int32_t> starts{0};
+    for (int32_t i = 1; i < n; ++i) {
+        bool dep_prev = false;
+        for (int32_t p = rp[i]; p < dp[i]; ++p) dep_prev |= col[p] == i - 1;
+        if (!dep_prev) starts.push_back(i);
+    }
+    starts.push_back(n);
+    const int32_t L = (int32_t)starts.size() - 1;
+    if (n == 0 || L > 1024) return false;
+    std::vector<int32_t> line(n), pos(n), lvl(n, 0);
+    for (int32_t l = 0; l < L; ++l)
+        for (int32_t i = starts[l]; i < starts[l + 1]; ++i) {
+            line[i] = l;
+            pos[i] = upper ? starts[l + 1] - 1 - i : i - starts[l];
+        }
+    auto dep_begin = [&](int32_t i) { return upper ? dp[i] + 1 : rp[i]; };
+    auto dep_end = [&](int32_t i) { return upper ? rp[i + 1] : dp[i]; };
+    int32_t steps = 0, md = 1, span = 1;
+    for (int32_t t = 0; t < n; ++t) {
+        const int32_t i = upper ? n - 1 - t : t;
+        int32_t l = 0;
+        for (int32_t p = dep_begin(i); p < dep_end(i); ++p) l = std::max(l, lvl[col[p]] + 1);
+        lvl[i] = l;
+        steps = std::max(steps, l + 1);
+        md = std::max(md, dep_end(i) - dep_begin(i));
+    }
+    const int32_t prev_off = upper ? 1 : -1;
+    for (int32_t i = 0; i < n; ++i)
+        for (int32_t p = dep_begin(i); p < dep_end(i); ++p) {
+            const int32_t j = col[p];
+            if (j == i + prev_off && line[j] == line[i]) continue;  // carried in a register
+            span = std::max(span, lvl[i] - lvl[j] + 1);
+        }
+    int32_t W = 1;
+    while (W < span) W <<= 1;
+    if (W > 16 || md > 8) return false;
+    const int32_t MD = md <= 2 ? 2 : (md <= 3 ? 3 : (md <= 4 ? 4 : 8));
+    const int32_t T = (L + 31) & ~31;
+    const int32_t zslot = L * W;
+    const int32_t K = kLineBatch;
+    const int32_t SP = (steps + K - 1) / K * K;
+    std::vector<int16_t> desc((size_t)SP * MD * T, (int16_t)zslot);
+    std::vector<int32_t> row0(T, -1), llen(T, 0), vperm((size_t)SP * MD * T, -1);
+    for (int32_t s = 0; s < SP; ++s)
+        for (int32_t t = 0; t < T; ++t) desc[((size_t)s * MD) * T + t] = kNoRow;
+    for (int32_t l = 0; l < L; ++l) {
+        const int32_t a = starts[l], b = starts[l + 1];
+        row0[l] = upper ? b - 1 : a;
+        llen[l] = b - a;
+        for (int32_t k = 0; k < b - a; ++k) {
+            const int32_t i = upper ? b - 1 - k : a + k;
+            const size_t base = (size_t)lvl[i] * MD * T + l;
+            int32_t e = 0;
+            auto push = [&](int32_t p) {
+                const int32_t j = col[p];
+                desc[base + (size_t)e * T] =
+                    (int16_t)((j == i + prev_off && line[j] == line[i]) ? -1 : line[j] * W + (pos[j] & (W - 1)));
+                vperm[base + (size_t)e * T] = p;
+                ++e;
+            };
+            if (upper)
+                for (int32_t p = dep_end(i) - 1; p >= dep_begin(i); --p) push(p);
+            else
+                for (int32_t p = dep_begin(i); p < dep_end(i); ++p) push(p);
+            for (; e < MD; ++e) desc[base + (size_t)e * T] = (int16_t)zslot;  // 0 * (zero cell): exact
+        }
+    }
+    D.nlines = L;
+    D.T = T;
+    D.steps = steps;
+    D.steps_pad = SP;
+    D.window = W;
+    D.md = MD;
+    D.zslot = zslot;
+    D.line_row0 = upload(row0);
+    D.line_len = upload(llen);
+    D.desc = upload(desc);
+    D.vperm = upload(vperm);
+    return D.line_row0 && D.line_len && D.desc && D.vperm;
+}
+
+LineSched *Pattern::line_schedule() {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!factor_ok) return nullptr;
+    if (!lines) {
+        lines = std::make_unique<LineSched>();
+        lines->ok = !std::getenv("NPCG_NO_LINES") && build_lines(*this, false, lines->fwd) &&
+                    build_lines(*this, true, lines->bwd);
+    }
+    return lines->ok ? lines.get() : nullptr;
+}
+
 SchedSet *Pattern::schedule(int32_t R, std::string &err) {
     std::lock_guard<std::mutex> lock(mu);
     if (!factor_ok) {

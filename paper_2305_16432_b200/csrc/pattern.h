@@ -50,6 +50,34 @@ struct SchedSet {
     ~SchedSet();
 };
 
+// Line-wavefront schedule (trsv_line.cu): the rows split into "lines",
+// maximal runs in which every row depends on its predecessor (grid lines of
+// a mesh in natural order). One thread owns one line and walks its rows in
+// solve order; step s of the CTA solves every row whose level is s, so the
+// in-line dependency stays in a register and the cross-line ones are read
+// from a per-line shared-memory ring of the last `window` values.
+// Per (step, thread) the schedule stores MD dependency descriptors and the
+// matching factor slots, step-major: desc[step][e][T] (int16) with
+//   -1 = previous row of the line, >= 0 = ring slot, zslot = padding,
+//   desc[.][0] = kNoRow when the thread has no row at that step,
+// and vperm[step][e][T] = CSR position of the factor value (-1 = padding).
+// Only built when the whole pattern fits one CTA (lines <= 1024, window <= 16).
+constexpr int32_t kLineBatch = 6;          // steps staged per batch
+constexpr int16_t kNoRow = -2;             // desc[.][0]: thread idle at this step
+
+struct LineDir {
+    int32_t nlines = 0, T = 0, steps = 0, steps_pad = 0, window = 1, md = 1, zslot = 0;
+    int32_t *line_row0 = nullptr;  // [T] first row of each thread in solve order (-1: idle)
+    int32_t *line_len = nullptr;   // [T] rows of each thread's line
+    int16_t *desc = nullptr;       // [steps_pad][md][T]
+    int32_t *vperm = nullptr;      // [steps_pad][md][T]
+};
+struct LineSched {
+    bool ok = false;
+    LineDir fwd, bwd;
+    ~LineSched();
+};
+
 struct Pattern {
     int64_t n = 0, nnz = 0, nnz_lower = 0;
     bool full_diag = false, symmetric = false, factor_ok = false;
@@ -58,10 +86,13 @@ struct Pattern {
     int32_t *lower_slot = nullptr; // [nnz_lower] CSR position of each strict-lower entry
     int32_t *src = nullptr;        // [nnz] row of each stored entry (edge source, gnn.py:83)
     std::map<int32_t, std::unique_ptr<SchedSet>> scheds;  // by chunk rows
+    std::unique_ptr<LineSched> lines;                      // built on first use
     std::mutex mu;
     ~Pattern();
     // Schedule for `chunk_rows` (built on first use); nullptr + err on failure.
     SchedSet *schedule(int32_t chunk_rows, std::string &err);
+    // Line schedule, or nullptr when the pattern does not qualify.
+    LineSched *line_schedule();
 };
 
 // Rows per chunk for a solve over B columns in groups of G (heuristic,

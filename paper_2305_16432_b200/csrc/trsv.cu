@@ -86,43 +86,9 @@ __device__ __forceinline__ int trsv_col_op(const TrsvArgs &a, int b) {
     return ph == PH_RESTART ? TOP_RESET : TOP_SKIP;  // forward wrote y: re-arm it
 }
 
-__device__ void trsv_epilogue(const TrsvArgs &a, int b, double total) {
-    const SolveState &st = a.st;
-    if (st.status[b] != ST_ACTIVE) {
-        if (a.upper) st.pflag[b] = PF_NONE;
-        return;
-    }
-    const int ph = st.phase[b];
-    if (!a.upper) {  // forward: residual norm of the updated r (pcg.py:143-150, 166)
-        if (ph != PH_ITER) return;
-        const double rn = sqrt(total);
-        const long long k = st.k[b];
-        push_history(st, b, k, rn);
-        const double rel = rn / st.scale[b];
-        st.rel[b] = rel;
-        if (rel <= st.thr[st.T - 1]) {
-            st.phase[b] = PH_DRIFT;
-            atomicAdd(a.drift_count, 1);
-        } else {
-            record(st, b, k, rel);
-        }
-        return;
-    }
-    // backward: r.z and the direction update (pcg.py:128-130, 167-171)
-    if (ph == PH_ITER) {
-        st.beta[b] = total / st.rz[b];
-        st.rz[b] = total;
-        st.pflag[b] = PF_UPDATE;
-    } else if (ph == PH_INIT) {
-        st.rz[b] = total;
-        st.pflag[b] = PF_COPY;
-        st.phase[b] = PH_ITER;
-    } else if (ph == PH_RESTART) {
-        st.phase[b] = PH_INIT;
-        st.pflag[b] = PF_NONE;
-    } else {
-        st.pflag[b] = PF_NONE;
-    }
+__device__ __forceinline__ void trsv_epilogue(const TrsvArgs &a, int b, double total) {
+    if (a.upper) bwd_epilogue(a.st, b, total);
+    else fwd_epilogue(a.st, b, total, a.drift_count);
 }
 
 // ---- the kernel -----------------------------------------------------------------
@@ -193,11 +159,7 @@ struct Trsv {
                 };
                 if (!UPPER) {
                     cp(d0, a.in + vi);  // r (PCG: in == R)
-                    if (PCG && c.uop == TOP_UPDATE) {
-                        cp(d0 + slab, a.AP + vi);
-                        cp(d0 + 2 * slab, a.X + vi);
-                        cp(d0 + 3 * slab, a.P + vi);
-                    }
+                    if (PCG && c.uop == TOP_UPDATE) cp(d0 + slab, a.AP + vi);
                 } else {
                     cp(d0, a.in + vi);
                     if (a.d_batched) cp(d0 + slab, a.D + vi);
@@ -311,9 +273,8 @@ struct Trsv {
                             }
                             double acc;
                             if (!UPPER) {
-                                if (PCG && op == TOP_UPDATE) {  // x += a p ; r -= a Ap (pcg.py:141-142)
+                                if (PCG && op == TOP_UPDATE) {  // r -= a Ap (pcg.py:142); x += a p is in pupd
                                     const double al = a.st.alpha[b];
-                                    a.X[vi] = __dadd_rn(dv[2 * slab + it], __dmul_rn(al, dv[3 * slab + it]));
                                     acc = __dsub_rn(dv[it], __dmul_rn(al, dv[slab + it]));
                                     a.R[vi] = acc;
                                     acc2 = __dadd_rn(acc2, __dmul_rn(acc, acc));
