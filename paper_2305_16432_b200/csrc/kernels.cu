@@ -93,77 +93,102 @@ __device__ void spmv_epilogue(const SpmvArgs &a, int b, double total) {
     }
 }
 
-template <int TL>
-__global__ void __launch_bounds__(kSpmvThreads) spmv_kernel(SpmvArgs a) {
-    constexpr int TEAMS = kSpmvThreads / TL;
-    extern __shared__ double red[];  // TEAMS * B (reducing ops)
-    __shared__ unsigned char s_act[kMaxBatch];
-    __shared__ int s_last;
-    const int team = threadIdx.x / TL, lane = threadIdx.x % TL;
+// X columns are read VW at a time (VW = 2: 16-byte loads when B is even).
+// Row entries are consumed in groups of CH: all column indices of a group
+// first, then all the X rows they name, so a team keeps CH independent
+// loads in flight instead of a col -> x dependency per entry; products are
+// still accumulated in entry order (bitwise the reference's row sum).
+// Teams of >= 8 lanes own a contiguous block of rows: lane l holds entry
+// p0 + l of the current row (one coalesced load, broadcast by shuffles) and
+// the next row's entries are fetched while the current row's X loads fly.
+template <int VW>
+struct VecT;
+template <>
+struct VecT<1> {
+    using type = double;
+    static __device__ __forceinline__ void get(type v, double *o) { o[0] = v; }
+};
+template <>
+struct VecT<2> {
+    using type = double2;
+    static __device__ __forceinline__ void get(type v, double *o) {
+        o[0] = v.x;
+        o[1] = v.y;
+    }
+};
+
+// Row epilogue for one VW-column slot: store / fused dot / residual.
+template <int VW>
+__device__ __forceinline__ void spmv_row_pre(const SpmvArgs &a, size_t ri, int b, double *own) {
+    // the row's own operand (p for p.Ap, b for r = b - Ax), loaded before the
+    // row's sum so its latency overlaps the gathers
+#pragma unroll
+    for (int v = 0; v < VW; ++v)
+        own[v] = a.op == SPMV_APDOT ? a.X[ri + b + v] : (a.op == SPMV_PLAIN ? 0.0 : a.Bv[ri + b + v]);
+}
+
+template <int VW>
+__device__ __forceinline__ void spmv_row_out(const SpmvArgs &a, size_t ri, int b, const double *acc,
+                                             const double *own, const unsigned char *s_act, double *pt) {
+#pragma unroll
+    for (int v = 0; v < VW; ++v) {
+        const int bv = b + v;
+        if (!s_act[bv]) continue;
+        switch (a.op) {
+            case SPMV_PLAIN: a.Y[ri + bv] = acc[v]; break;
+            case SPMV_APDOT: {
+                a.Y[ri + bv] = acc[v];
+                pt[v] = __dadd_rn(pt[v], __dmul_rn(own[v], acc[v]));
+                break;
+            }
+            default: {  // residual r = b - A x
+                const double rt = __dsub_rn(own[v], acc[v]);
+                if (a.op != SPMV_RESID_FINAL) a.R[ri + bv] = rt;
+                pt[v] = __dadd_rn(pt[v], __dmul_rn(rt, rt));
+            }
+        }
+    }
+}
+
+// acc += vals[e] * x[col[e]] over CH entries whose columns are in jj (-1 = none).
+template <int CH, int VW, bool VB>
+__device__ __forceinline__ void spmv_group(const SpmvArgs &a, const int *jj, const double *vs, int e0, int b,
+                                           bool drift, const bool *xp, const double *al, double *acc) {
+    using V = typename VecT<VW>::type;
     const int B = a.B;
-    if (a.op == SPMV_RESID_DRIFT && *a.drift_count == 0) return;  // nothing drifted
-    for (int b = threadIdx.x; b < B; b += blockDim.x) s_act[b] = spmv_col_active(a, b) ? 1 : 0;
-    __syncthreads();
-    const int cpl = (B + TL - 1) / TL;
-    double part[kMaxCpl];
+    double vv[VB ? CH : 1][VW], xv[CH][VW];
 #pragma unroll
-    for (int k = 0; k < kMaxCpl; ++k) part[k] = 0.0;
-
-    for (int row = blockIdx.x * TEAMS + team; row < a.n; row += gridDim.x * TEAMS) {
-        const int p0 = a.rp[row], p1 = a.rp[row + 1];
-        double acc[kMaxCpl];
+    for (int c = 0; c < CH; ++c) {
+        if (jj[c] < 0) continue;
+        const size_t j = (size_t)jj[c] * B + b;
+        if constexpr (VB) VecT<VW>::get(*reinterpret_cast<const V *>(a.vals + (size_t)(e0 + c) * B + b), vv[c]);
+        VecT<VW>::get(*reinterpret_cast<const V *>(a.X + j), xv[c]);
+        if (drift) {  // x_{k+1} = x + alpha p not yet stored (pcg.py:141)
+            double pv[VW];
+            VecT<VW>::get(*reinterpret_cast<const V *>(a.P + j), pv);
 #pragma unroll
-        for (int k = 0; k < kMaxCpl; ++k) acc[k] = 0.0;
-        const bool use_x = a.op != SPMV_RESID_INIT || a.has_x;
-        if (use_x) {
-            for (int p = p0; p < p1; ++p) {
-                const size_t j = (size_t)a.col[p] * B;
-                const double vs = a.vb ? 0.0 : a.vals[p];
-#pragma unroll
-                for (int k = 0; k < kMaxCpl; ++k) {
-                    const int b = lane + k * TL;
-                    if (k < cpl && b < B) {
-                        const double v = a.vb ? a.vals[(size_t)p * B + b] : vs;
-                        double xv = a.X[j + b];
-                        if (a.op == SPMV_RESID_DRIFT && a.st.xpend[b])  // x_{k+1} not yet stored
-                            xv = __dadd_rn(xv, __dmul_rn(a.st.alpha[b], a.P[j + b]));
-                        acc[k] = __dadd_rn(acc[k], __dmul_rn(v, xv));
-                    }
-                }
-            }
-        }
-        const size_t ri = (size_t)row * B;
-#pragma unroll
-        for (int k = 0; k < kMaxCpl; ++k) {
-            const int b = lane + k * TL;
-            if (k >= cpl || b >= B || !s_act[b]) continue;
-            switch (a.op) {
-                case SPMV_PLAIN: a.Y[ri + b] = acc[k]; break;
-                case SPMV_APDOT: {
-                    a.Y[ri + b] = acc[k];
-                    part[k] = __dadd_rn(part[k], __dmul_rn(a.X[ri + b], acc[k]));
-                    break;
-                }
-                default: {  // residual r = b - A x
-                    const double rt = __dsub_rn(a.Bv[ri + b], acc[k]);
-                    if (a.op != SPMV_RESID_FINAL) a.R[ri + b] = rt;
-                    part[k] = __dadd_rn(part[k], __dmul_rn(rt, rt));
-                }
-            }
+            for (int v = 0; v < VW; ++v)
+                if (xp[v]) xv[c][v] = __dadd_rn(xv[c][v], __dmul_rn(al[v], pv[v]));
         }
     }
-    if (a.op == SPMV_PLAIN) return;
-
-    // block reduction per column, fixed order over teams
 #pragma unroll
-    for (int k = 0; k < kMaxCpl; ++k) {
-        const int b = lane + k * TL;
-        if (k < cpl && b < B) red[team * B + b] = part[k];
+    for (int c = 0; c < CH; ++c) {
+        if (jj[c] < 0) continue;
+#pragma unroll
+        for (int v = 0; v < VW; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(VB ? vv[VB ? c : 0][v] : vs[c], xv[c][v]));
     }
+}
+
+// Block reduction per column (fixed order over teams), then a grid reduction
+// in fixed block order by the last block to finish, which runs the control
+// epilogue. `red` holds [teams][B] partials.
+__device__ __forceinline__ void spmv_reduce_tail(const SpmvArgs &a, double *red, int teams) {
+    __shared__ int s_last;
+    const int B = a.B;
     __syncthreads();
     for (int b = threadIdx.x; b < B; b += blockDim.x) {
         double s = 0.0;
-        for (int t = 0; t < TEAMS; ++t) s = __dadd_rn(s, red[t * B + b]);
+        for (int t = 0; t < teams; ++t) s = __dadd_rn(s, red[t * B + b]);
         a.partial[(size_t)blockIdx.x * B + b] = s;
     }
     __threadfence();
@@ -172,7 +197,6 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_kernel(SpmvArgs a) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // last block: grid reduction (fixed block order) + control epilogue
     const int G = gridDim.x;
     const int per = kSpmvThreads / (B < kSpmvThreads ? B : kSpmvThreads);  // threads per column
     double *scratch = red;  // reuse
@@ -196,6 +220,286 @@ __global__ void __launch_bounds__(kSpmvThreads) spmv_kernel(SpmvArgs a) {
         a.ctl->done = 0;
         if (a.op == SPMV_RESID_DRIFT) *a.drift_count = 0;
     }
+}
+
+template <int TL, int VW, bool VB>
+__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_kernel(SpmvArgs a) {
+    constexpr int TEAMS = kSpmvThreads / TL, CH = 8;
+    extern __shared__ double red[];  // TEAMS * B (reducing ops)
+    __shared__ unsigned char s_act[kMaxBatch];
+    const int team = threadIdx.x / TL, lane = threadIdx.x % TL;
+    const int B = a.B;
+    if (a.op == SPMV_RESID_DRIFT && *a.drift_count == 0) return;  // nothing drifted
+    for (int b = threadIdx.x; b < B; b += blockDim.x) s_act[b] = spmv_col_active(a, b) ? 1 : 0;
+    __syncthreads();
+    const int cpl = (B + TL * VW - 1) / (TL * VW);  // VW-column slots per lane
+    // per-(team, column) partial sums live in shared memory; each is owned by
+    // one lane, so they accumulate in a fixed order without atomics
+    double *part = red + team * B;
+    if (a.op != SPMV_PLAIN)
+        for (int b = lane; b < B; b += TL) part[b] = 0.0;
+    const bool use_x = a.op != SPMV_RESID_INIT || a.has_x;
+    const bool drift = a.op == SPMV_RESID_DRIFT;
+    // per-slot drift state
+    auto drift_state = [&](int b, bool *xp, double *al) {
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+            xp[v] = drift && a.st.xpend[b + v];
+            al[v] = xp[v] ? a.st.alpha[b + v] : 0.0;
+        }
+    };
+
+    if constexpr (TL >= CH) {
+        // Entry stream: a team owns rows [r0, r1) and walks their entries
+        // [rp[r0], rp[r1]) in windows of TL (lane l holds entry w + l, one
+        // coalesced load), gathering CH X rows at a time regardless of where
+        // rows end; a row's result is emitted when the stream crosses its end.
+        const unsigned tmask = TL == 32 ? 0xffffffffu : (((1u << TL) - 1u) << ((threadIdx.x & 31) & ~(TL - 1)));
+        const int nteams = gridDim.x * TEAMS, gteam = blockIdx.x * TEAMS + team;
+        const int per = (a.n + nteams - 1) / nteams;
+        const int r0 = min(a.n, gteam * per), r1 = min(a.n, r0 + per);
+        if (r0 < r1) {
+#pragma unroll 1
+            for (int k = 0; k < cpl; ++k) {
+                const int b = (lane + k * TL) * VW;
+                const bool on = b < B;
+                const int bb = on ? b : 0;
+                bool xp[VW];
+                double al[VW];
+                drift_state(bb, xp, al);
+                int row = r0, wb = r0 + 1;                   // rp window: rpl = rp[wb + lane]
+                int rpl = a.rp[min(wb + lane, a.n)];
+                int wi = 0;                                  // window index of row's end
+                int rend = __shfl_sync(tmask, rpl, 0, TL);   // rp[row + 1]
+                const int E0 = a.rp[r0];
+                const int E1 = __shfl_sync(tmask, a.rp[r1], 0, TL);
+                double acc[VW], own[VW];
+#pragma unroll
+                for (int v = 0; v < VW; ++v) acc[v] = 0.0;
+                spmv_row_pre<VW>(a, (size_t)row * B, bb, own);
+                // close row (store / dot) and open the next one
+                auto next_row = [&]() {
+                    if (on) spmv_row_out<VW>(a, (size_t)row * B, b, acc, own, s_act, part + b);
+                    ++row;
+#pragma unroll
+                    for (int v = 0; v < VW; ++v) acc[v] = 0.0;
+                    if (row < r1) {
+                        spmv_row_pre<VW>(a, (size_t)row * B, bb, own);
+                        if (++wi == TL) {
+                            wb = row + 1;
+                            rpl = a.rp[min(wb + lane, a.n)];
+                            wi = 0;
+                        }
+                        rend = __shfl_sync(tmask, rpl, wi, TL);
+                    }
+                };
+                if (use_x) {
+                    for (int w = E0; w < E1; w += TL) {
+                        const int cnt = min(TL, E1 - w);
+                        const int cj = lane < cnt ? a.col[w + lane] : 0;
+                        const double cv = (!VB && lane < cnt) ? a.vals[w + lane] : 0.0;
+                        for (int g = 0; g < cnt; g += CH) {
+                            using V = typename VecT<VW>::type;
+                            double xv[CH][VW], vs[CH];
+                            double vv[VB ? CH : 1][VW];
+#pragma unroll
+                            for (int c = 0; c < CH; ++c) {
+                                const int j = __shfl_sync(tmask, cj, g + c, TL);
+                                vs[c] = __shfl_sync(tmask, cv, g + c, TL);
+                                if (g + c < cnt && on) {
+                                    const size_t jo = (size_t)j * B + b;
+                                    VecT<VW>::get(*reinterpret_cast<const V *>(a.X + jo), xv[c]);
+                                    if constexpr (VB)
+                                        VecT<VW>::get(*reinterpret_cast<const V *>(a.vals + (size_t)(w + g + c) * B + b), vv[c]);
+                                    if (drift) {  // x_{k+1} = x + alpha p not yet stored (pcg.py:141)
+                                        double pv[VW];
+                                        VecT<VW>::get(*reinterpret_cast<const V *>(a.P + jo), pv);
+#pragma unroll
+                                        for (int v = 0; v < VW; ++v)
+                                            if (xp[v]) xv[c][v] = __dadd_rn(xv[c][v], __dmul_rn(al[v], pv[v]));
+                                    }
+                                }
+                            }
+#pragma unroll
+                            for (int c = 0; c < CH; ++c) {
+                                const int ee = w + g + c;
+                                if (ee >= E1) break;
+                                while (ee == rend) next_row();  // rows ending before entry ee (incl. empty)
+#pragma unroll
+                                for (int v = 0; v < VW; ++v)
+                                    acc[v] = __dadd_rn(acc[v], __dmul_rn(VB ? vv[VB ? c : 0][v] : vs[c], xv[c][v]));
+                            }
+                        }
+                    }
+                }
+                while (row < r1) next_row();  // last row and trailing empty rows (or x = 0)
+            }
+        }
+    } else {
+        for (int row = blockIdx.x * TEAMS + team; row < a.n; row += gridDim.x * TEAMS) {
+            const int p0 = a.rp[row], p1 = a.rp[row + 1];
+            const size_t ri = (size_t)row * B;
+#pragma unroll 1
+            for (int k = 0; k < cpl; ++k) {
+                const int b = (lane + k * TL) * VW;
+                if (b >= B) continue;
+                double acc[VW], own[VW];
+#pragma unroll
+                for (int v = 0; v < VW; ++v) acc[v] = 0.0;
+                spmv_row_pre<VW>(a, ri, b, own);
+                if (use_x) {
+                    bool xp[VW];
+                    double al[VW];
+                    drift_state(b, xp, al);
+                    for (int pb = p0; pb < p1; pb += CH) {
+                        int jj[CH];
+                        double vs[CH];
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) {
+                            jj[c] = pb + c < p1 ? a.col[pb + c] : -1;
+                            vs[c] = (pb + c < p1 && !VB) ? a.vals[pb + c] : 0.0;
+                        }
+                        spmv_group<CH, VW, VB>(a, jj, vs, pb, b, drift, xp, al, acc);
+                    }
+                }
+                spmv_row_out<VW>(a, ri, b, acc, own, s_act, part + b);
+            }
+        }
+    }
+    if (a.op == SPMV_PLAIN) return;
+
+    spmv_reduce_tail(a, red, TEAMS);
+}
+
+// Warp-per-row SpMV for batches of >= 33 column groups (the common case,
+// B >= 64 RHS): one warp owns a contiguous block of rows and handles one row
+// per iteration with every lane covering VW adjacent columns, so a row's
+// entries are one coalesced index load (lane l = entry l, broadcast by
+// shuffles) and its gathers are CH unconditional 16-byte loads (padding
+// slots re-read the row's own X row; their products are masked out of the
+// sum). The op is a template parameter so the row loop has no switch, and
+// the next row's indices are fetched while the current row's gathers fly.
+template <int VW, bool VB, int OP>
+__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_warp_kernel(SpmvArgs a) {
+    constexpr int TEAMS = kSpmvThreads / 32, CH = 8;
+    using V = typename VecT<VW>::type;
+    extern __shared__ double red[];  // TEAMS * B
+    __shared__ unsigned char s_act[kMaxBatch];
+    const int team = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int B = a.B;
+    if (OP == SPMV_RESID_DRIFT && *a.drift_count == 0) return;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) s_act[b] = spmv_col_active(a, b) ? 1 : 0;
+    double *part = red + team * B;
+    if (OP != SPMV_PLAIN)
+        for (int b = lane; b < B; b += 32) part[b] = 0.0;
+    __syncthreads();
+    const int cpl = (B + 32 * VW - 1) / (32 * VW);
+    const int nteams = gridDim.x * TEAMS, gteam = blockIdx.x * TEAMS + team;
+    const int per = (a.n + nteams - 1) / nteams;
+    const int r0 = min(a.n, gteam * per), r1 = min(a.n, r0 + per);
+    const bool use_x = OP != SPMV_RESID_INIT || a.has_x;
+    const double *__restrict__ X = a.X;
+    const double *__restrict__ vals = a.vals;
+    const int *__restrict__ col = a.col;
+    for (int k = 0; k < cpl && r0 < r1; ++k) {
+        const int b = (lane + k * 32) * VW;
+        const bool on = b < B;
+        const unsigned bb = on ? b : 0;
+        bool xp[VW];
+        double al[VW];
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+            xp[v] = OP == SPMV_RESID_DRIFT && a.st.xpend[bb + v];
+            al[v] = xp[v] ? a.st.alpha[bb + v] : 0.0;
+        }
+        int wb = r0, rpl = a.rp[min(r0 + lane, a.n)];  // rp[wb + lane]
+        int p0 = __shfl_sync(0xffffffffu, rpl, 0), p1 = __shfl_sync(0xffffffffu, rpl, 1);
+        int cj = lane < p1 - p0 ? col[p0 + lane] : r0;
+        double cv = (!VB && lane < p1 - p0) ? vals[p0 + lane] : 0.0;
+        for (int row = r0; row < r1; ++row) {
+            const unsigned ri = (unsigned)row * B + bb;
+            double own[VW];
+            if (OP == SPMV_APDOT) VecT<VW>::get(*reinterpret_cast<const V *>(X + ri), own);
+            else if (OP != SPMV_PLAIN) VecT<VW>::get(*reinterpret_cast<const V *>(a.Bv + ri), own);
+            // the next row's bounds and first 32 entries
+            int w = row + 2 - wb;
+            if (w >= 32) {
+                wb = row;
+                rpl = a.rp[min(wb + lane, a.n)];
+                w = 2;
+            }
+            const int q1 = __shfl_sync(0xffffffffu, rpl, w);
+            const int cnt = p1 - p0, c0 = p0;
+            const int ccj = cj;
+            const double ccv = cv;
+            if (row + 1 < r1) {
+                cj = lane < q1 - p1 ? col[p1 + lane] : row + 1;
+                if (!VB) cv = lane < q1 - p1 ? vals[p1 + lane] : 0.0;
+            }
+            p0 = p1;
+            p1 = q1;
+            double acc[VW];
+#pragma unroll
+            for (int v = 0; v < VW; ++v) acc[v] = 0.0;
+            if (use_x) {
+                for (int g = 0; g < cnt; g += CH) {
+                    int hj = ccj;
+                    double hv = ccv;
+                    if (g >= 32 && (g & 31) == 0) {  // rows longer than 32 entries
+                        hj = lane < cnt - g ? col[c0 + g + lane] : row;
+                        hv = (!VB && lane < cnt - g) ? vals[c0 + g + lane] : 0.0;
+                    }
+                    double xv[CH][VW], vv[VB ? CH : 1][VW], vs[CH];
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        const int j = __shfl_sync(0xffffffffu, hj, (g + c) & 31);
+                        if (!VB) vs[c] = __shfl_sync(0xffffffffu, hv, (g + c) & 31);
+                        const unsigned jo = (unsigned)j * B + bb;
+                        VecT<VW>::get(*reinterpret_cast<const V *>(X + jo), xv[c]);
+                        if (VB) {
+                            const int e = g + c < cnt ? c0 + g + c : c0;
+                            VecT<VW>::get(*reinterpret_cast<const V *>(vals + (size_t)e * B + bb), vv[c]);
+                        }
+                        if (OP == SPMV_RESID_DRIFT) {  // x_{k+1} = x + alpha p not yet stored (pcg.py:141)
+                            double pv[VW];
+                            VecT<VW>::get(*reinterpret_cast<const V *>(a.P + jo), pv);
+#pragma unroll
+                            for (int v = 0; v < VW; ++v)
+                                if (xp[v]) xv[c][v] = __dadd_rn(xv[c][v], __dmul_rn(al[v], pv[v]));
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        const bool use = g + c < cnt;
+#pragma unroll
+                        for (int v = 0; v < VW; ++v) {
+                            const double s = __dadd_rn(acc[v], __dmul_rn(VB ? vv[VB ? c : 0][v] : vs[c], xv[c][v]));
+                            acc[v] = use ? s : acc[v];
+                        }
+                    }
+                }
+            }
+            if (on) {
+#pragma unroll
+                for (int v = 0; v < VW; ++v) {
+                    const int bv = b + v;
+                    if (!s_act[bv]) continue;
+                    if (OP == SPMV_PLAIN) {
+                        a.Y[ri + v] = acc[v];
+                    } else if (OP == SPMV_APDOT) {
+                        a.Y[ri + v] = acc[v];
+                        part[bv] = __dadd_rn(part[bv], __dmul_rn(own[v], acc[v]));
+                    } else {
+                        const double rt = __dsub_rn(own[v], acc[v]);
+                        if (OP != SPMV_RESID_FINAL) a.R[ri + v] = rt;
+                        part[bv] = __dadd_rn(part[bv], __dmul_rn(rt, rt));
+                    }
+                }
+            }
+        }
+    }
+    if (OP == SPMV_PLAIN) return;
+    spmv_reduce_tail(a, red, TEAMS);
 }
 
 // ===========================================================================
@@ -358,14 +662,65 @@ int num_sms() {
     return sms;
 }
 
-static int team_lanes(int B) {
+static int team_lanes(int cols) {
     int tl = 1;
-    while (tl < B && tl < 32) tl <<= 1;
+    while (tl < cols && tl < 32) tl <<= 1;
     return tl;
 }
 
+template <int TL, int VW>
+static void spmv_launch_t(const SpmvArgs &a, int grid, size_t smem, cudaStream_t s) {
+    auto kern = a.vb ? spmv_kernel<TL, VW, true> : spmv_kernel<TL, VW, false>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    note_launch();
+    kern<<<grid, kSpmvThreads, smem, s>>>(a);
+}
+
+template <int VW>
+static void spmv_launch_vw(int TL, const SpmvArgs &a, int grid, size_t smem, cudaStream_t s) {
+    switch (TL) {
+        case 1: return spmv_launch_t<1, VW>(a, grid, smem, s);
+        case 2: return spmv_launch_t<2, VW>(a, grid, smem, s);
+        case 4: return spmv_launch_t<4, VW>(a, grid, smem, s);
+        case 8: return spmv_launch_t<8, VW>(a, grid, smem, s);
+        case 16: return spmv_launch_t<16, VW>(a, grid, smem, s);
+        default: return spmv_launch_t<32, VW>(a, grid, smem, s);
+    }
+}
+
+template <int VW, bool VB, int OP>
+static void spmv_warp_t(const SpmvArgs &a, int grid, size_t smem, cudaStream_t s) {
+    auto kern = spmv_warp_kernel<VW, VB, OP>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    note_launch();
+    kern<<<grid, kSpmvThreads, smem, s>>>(a);
+}
+
+template <int VW, bool VB>
+static void spmv_warp_op(const SpmvArgs &a, int grid, size_t smem, cudaStream_t s) {
+    switch (a.op) {
+        case SPMV_PLAIN: return spmv_warp_t<VW, VB, SPMV_PLAIN>(a, grid, smem, s);
+        case SPMV_APDOT: return spmv_warp_t<VW, VB, SPMV_APDOT>(a, grid, smem, s);
+        case SPMV_RESID_INIT: return spmv_warp_t<VW, VB, SPMV_RESID_INIT>(a, grid, smem, s);
+        case SPMV_RESID_DRIFT: return spmv_warp_t<VW, VB, SPMV_RESID_DRIFT>(a, grid, smem, s);
+        default: return spmv_warp_t<VW, VB, SPMV_RESID_FINAL>(a, grid, smem, s);
+    }
+}
+
+template <int VW>
+static void spmv_warp_vw(const SpmvArgs &a, int grid, size_t smem, cudaStream_t s) {
+    if (a.vb) spmv_warp_op<VW, true>(a, grid, smem, s);
+    else spmv_warp_op<VW, false>(a, grid, smem, s);
+}
+
 cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s) {
-    const int TL = team_lanes(a.B);
+    // 16-byte column pairs when every row of every operand stays 16-byte aligned
+    auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
+    const int VW = (a.B % 2 == 0 && al16(a.X) && al16(a.Y) && al16(a.Bv) && al16(a.R) && al16(a.P) &&
+                    (!a.vb || al16(a.vals)))
+                       ? 2
+                       : 1;
+    const int TL = team_lanes((a.B + VW - 1) / VW);
     const int teams = kSpmvThreads / TL;
     long long need = (a.n + teams - 1) / teams;
     int grid;
@@ -373,22 +728,14 @@ cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s) {
     else grid = (int)std::min<long long>(std::max<long long>(need, 1), (long long)kReduceBlocksPerSm * num_sms());
     size_t smem = a.op == SPMV_PLAIN ? 0 : (size_t)teams * a.B * sizeof(double);
     smem = std::max(smem, (size_t)kSpmvThreads * sizeof(double));
-#define NPCG_SPMV_CASE(T)                                                                     \
-    case T:                                                                                   \
-        if (smem > 48 * 1024)                                                                 \
-            cudaFuncSetAttribute(spmv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 (int)smem);                                                  \
-        note_launch(); spmv_kernel<T><<<grid, kSpmvThreads, smem, s>>>(a);                                   \
-        break;
-    switch (TL) {
-        NPCG_SPMV_CASE(1)
-        NPCG_SPMV_CASE(2)
-        NPCG_SPMV_CASE(4)
-        NPCG_SPMV_CASE(8)
-        NPCG_SPMV_CASE(16)
-        NPCG_SPMV_CASE(32)
+    if (TL == 32 && (long long)a.n * a.B < (1ll << 31)) {
+        if (VW == 2) spmv_warp_vw<2>(a, grid, smem, s);
+        else spmv_warp_vw<1>(a, grid, smem, s);
+    } else if (VW == 2) {
+        spmv_launch_vw<2>(TL, a, grid, smem, s);
+    } else {
+        spmv_launch_vw<1>(TL, a, grid, smem, s);
     }
-#undef NPCG_SPMV_CASE
     return cudaGetLastError();
 }
 
