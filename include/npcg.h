@@ -181,6 +181,11 @@ typedef struct {
  * points), for launch accounting in benchmarks. */
 int64_t npcg_launch_count(void);
 
+/* Diagnostics: copies n entries of the line-solve timeline of block 0
+ * (clock64 per pipeline batch and event, [16][2048]). All zeros unless the
+ * library was built with -DNPCG_LINE_TRACE. Returns a cudaError_t code. */
+int npcg_debug_line_trace(long long *out, int n);
+
 /* Solver workspace for a (A pattern, factor pattern, B) triple. F may be
  * NULL (identity preconditioner, pcg.py:64-72) or equal A. */
 int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B,

@@ -100,6 +100,7 @@ SIGNATURES = {
     "npcg_pcg_solve": (I32, [P, P, I32, P, I32, P, I32, P, P, P, ctypes.POINTER(SolveOpts),
                              ctypes.POINTER(SolveReportC), P]),
     "npcg_launch_count": (I64, []),
+    "npcg_debug_line_trace": (I32, [P, I32]),
 }
 
 _lib = None

@@ -122,13 +122,17 @@ struct npcg_solver {
     double *S_fwd = nullptr, *S_bwd = nullptr;  // factor entries in schedule order
     size_t S_cap = 0;
     LineSched *ls = nullptr;  // line-wavefront schedule (owned by the pattern) or null
-    int line_K = 0;
+    int line_K = 0;           // pipeline stages of the line kernels
+    // line mode: R, Z, Y, AP are in line order ([b][nslot]); A re-indexed by slot
+    int *lrp = nullptr, *lcol = nullptr, *leidx = nullptr;
+    double *Dl = nullptr;  // diag in line order ([b][nslot] or [nslot])
+    size_t Dl_cap = 0;
     int *xpend = nullptr;
     int *h_active = nullptr;  // pinned
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
                         alpha, beta, rel, final_rel, history, active_count, drift_count, ctl, partial,
-                        S_fwd, S_bwd, xpend};
+                        S_fwd, S_bwd, xpend, lrp, lcol, leidx, Dl};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_active) cudaFreeHost(h_active);
@@ -350,18 +354,43 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     std::string err;
     if (int rc = plan_solve(s->F, B, s->plan, err)) return fail(rc, err);
     if (LineSched *ls = s->F->line_schedule()) {
-        const int K = std::min(line_batch_for(ls->fwd), line_batch_for(ls->bwd));
+        const int K = std::min(line_stages_for(ls->fwd), line_stages_for(ls->bwd));
         if (K > 0) {
             s->ls = ls;
             s->line_K = K;
         }
     }
     const size_t nB = (size_t)A->n * B;
-    NPCG_CUDA(dalloc(&s->R, nB));
+    const size_t vB = s->ls ? (size_t)s->ls->nslot * B : nB;  // line-order vectors
+    NPCG_CUDA(dalloc(&s->R, vB));
     NPCG_CUDA(dalloc(&s->P, nB));
-    NPCG_CUDA(dalloc(&s->Z, nB));
-    NPCG_CUDA(dalloc(&s->AP, nB));
-    NPCG_CUDA(dalloc(&s->Y, nB));
+    NPCG_CUDA(dalloc(&s->Z, vB));
+    NPCG_CUDA(dalloc(&s->AP, vB));
+    NPCG_CUDA(dalloc(&s->Y, vB));
+    if (s->ls) {  // padding slots stay zero; A's rows re-indexed by slot for the SpMV
+        for (double *v : {s->R, s->Z, s->AP, s->Y}) NPCG_CUDA(cudaMemset(v, 0, vB * 8));
+        const LineSched &ls = *s->ls;
+        std::vector<int> lrp(ls.nslot + 1, 0), lcol, leidx;
+        lcol.reserve(A->nnz);
+        leidx.reserve(A->nnz);
+        for (int q = 0; q < ls.nslot; ++q) {
+            const int i = ls.h_rowof[q];
+            if (i >= 0)
+                for (int p = A->h_rp[i]; p < A->h_rp[i + 1]; ++p) {
+                    lcol.push_back(A->h_col[p]);
+                    leidx.push_back(p);
+                }
+            lrp[q + 1] = (int)lcol.size();
+        }
+        NPCG_CUDA(dalloc(&s->lrp, lrp.size()));
+        NPCG_CUDA(dalloc(&s->lcol, std::max<size_t>(lcol.size(), 1)));
+        NPCG_CUDA(dalloc(&s->leidx, std::max<size_t>(leidx.size(), 1)));
+        NPCG_CUDA(cudaMemcpy(s->lrp, lrp.data(), lrp.size() * 4, cudaMemcpyHostToDevice));
+        if (!lcol.empty()) {
+            NPCG_CUDA(cudaMemcpy(s->lcol, lcol.data(), lcol.size() * 4, cudaMemcpyHostToDevice));
+            NPCG_CUDA(cudaMemcpy(s->leidx, leidx.data(), leidx.size() * 4, cudaMemcpyHostToDevice));
+        }
+    }
     NPCG_CUDA(dalloc(&s->status, B));
     NPCG_CUDA(dalloc(&s->xpend, B));
     NPCG_CUDA(dalloc(&s->phase, B));
@@ -387,9 +416,10 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     const size_t part = std::max<size_t>((size_t)kReduceBlocksPerSm * num_sms() * B, units * s->plan.G);
     NPCG_CUDA(dalloc(&s->partial, part));
     NPCG_CUDA(cudaMallocHost((void **)&s->h_active, sizeof(int)));
-    // triangular-solve outputs start unsolved (sentinel), see kernels.cu
-    launch_fill_sentinel((long long)nB, s->Y, 0);
-    launch_fill_sentinel((long long)nB, s->Z, 0);
+    if (!s->ls) {  // level-kernel outputs start unsolved (sentinel), see trsv.cu
+        launch_fill_sentinel((long long)nB, s->Y, 0);
+        launch_fill_sentinel((long long)nB, s->Z, 0);
+    }
     NPCG_CUDA(cudaDeviceSynchronize());
     *out = s.release();
     return NPCG_OK;
@@ -429,12 +459,10 @@ static SolveState make_state(npcg_solver *s, const npcg_solve_opts *o) {
 
 // Gather the factor entries (CSR order, symmetric S) into each direction's
 // schedule order; done once per solve call, not per iteration.
-static int stage_factor(npcg_solver *s, const double *S, int sb, cudaStream_t st) {
+static int stage_factor(npcg_solver *s, const double *S, int sb, const double *D, int db, cudaStream_t st) {
     size_t need;
     if (s->ls) {
-        const LineDir &f = s->ls->fwd;
-        need = (size_t)f.steps_pad * f.md * f.T * (sb ? s->B : 1);
-        need = std::max(need, (size_t)s->ls->bwd.steps_pad * s->ls->bwd.md * s->ls->bwd.T * (sb ? s->B : 1));
+        need = (size_t)std::max(s->ls->fwd.fac_slots, s->ls->bwd.fac_slots) * (sb ? s->B : 1);
     } else {
         const Schedule &f = s->plan.set->fwd, &b = s->plan.set->bwd;
         const size_t cols = sb ? (size_t)s->plan.groups * s->plan.G : 1;
@@ -452,6 +480,16 @@ static int stage_factor(npcg_solver *s, const double *S, int sb, cudaStream_t st
     if (s->ls) {  // S batched is laid out S[p * B + b]
         launch_line_factor_pack(s->ls->fwd, s->B, sb, sb ? s->B : 1, 1, S, s->S_fwd, st);
         launch_line_factor_pack(s->ls->bwd, s->B, sb, sb ? s->B : 1, 1, S, s->S_bwd, st);
+        // diag in line order; padding slots divide by one
+        const size_t dneed = (size_t)s->ls->nslot * (db ? s->B : 1);
+        if (dneed > s->Dl_cap) {
+            if (s->Dl) cudaFree(s->Dl);
+            s->Dl = nullptr;
+            s->Dl_cap = 0;
+            NPCG_CUDA(dalloc(&s->Dl, dneed));
+            s->Dl_cap = dneed;
+        }
+        NPCG_CUDA(launch_to_line(s->ls->nslot, db ? s->B : 1, s->ls->rowof, D, db, 1.0, s->Dl, st));
     } else {
         launch_factor_pack(s->plan.set->fwd, s->B, s->plan.G, sb, S, s->S_fwd, st);
         launch_factor_pack(s->plan.set->bwd, s->B, s->plan.G, sb, S, s->S_bwd, st);
@@ -482,15 +520,14 @@ static Tri tri_args(npcg_solver *s, bool upper, int mode, int sb, const double *
     if (t.line) {
         LineArgs &l = t.l;
         l.B = s->B;
-        l.K = s->line_K;
+        l.stages = s->line_K;
         l.upper = upper;
         l.mode = mode;
-        l.rs = s->B;
-        l.cs = 1;
+        l.nslot = s->ls->nslot;
         l.dir = upper ? s->ls->bwd : s->ls->fwd;
         l.S = upper ? s->S_bwd : s->S_fwd;
         l.s_batched = sb;
-        l.D = D;
+        l.D = s->Dl;  // staged by stage_factor
         l.d_batched = db;
         l.drift_count = s->drift_count;
         return t;
@@ -525,14 +562,26 @@ int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int s
     if (int rc = npcg_solver_create(F, F, B, &s)) return rc;
     std::unique_ptr<npcg_solver> guard(s);
     cudaStream_t st = (cudaStream_t)stream;
-    if (int rc = stage_factor(s, S, sb, st)) return rc;
-    if (!s->ls) launch_fill_sentinel((long long)F->n * B, z, st);  // level kernel polls z
-    Tri f = tri_args(s, false, TRSV_PLAIN, sb, D, db);
-    f.io(const_cast<double *>(r), s->Y, nullptr, nullptr, SolveState{});  // r is only read
-    NPCG_CUDA(f.launch(st));
-    Tri b = tri_args(s, true, TRSV_PLAIN, sb, D, db);
-    b.io(s->Y, z, nullptr, nullptr, SolveState{});
-    NPCG_CUDA(b.launch(st));
+    if (int rc = stage_factor(s, S, sb, D, db, st)) return rc;
+    if (s->ls) {  // through line order: r -> R, Y, Z -> z
+        const LineSched &ls = *s->ls;
+        NPCG_CUDA(launch_to_line(ls.nslot, B, ls.rowof, r, 1, 0.0, s->R, st));
+        Tri f = tri_args(s, false, TRSV_PLAIN, sb, D, db);
+        f.io(s->R, s->Y, nullptr, nullptr, SolveState{});
+        NPCG_CUDA(f.launch(st));
+        Tri b = tri_args(s, true, TRSV_PLAIN, sb, D, db);
+        b.io(s->Y, s->Z, nullptr, nullptr, SolveState{});
+        NPCG_CUDA(b.launch(st));
+        NPCG_CUDA(launch_from_line(ls.nslot, B, ls.rowof, s->Z, z, st));
+    } else {
+        launch_fill_sentinel((long long)F->n * B, z, st);  // level kernel polls z
+        Tri f = tri_args(s, false, TRSV_PLAIN, sb, D, db);
+        f.io(const_cast<double *>(r), s->Y, nullptr, nullptr, SolveState{});  // r is only read
+        NPCG_CUDA(f.launch(st));
+        Tri b = tri_args(s, true, TRSV_PLAIN, sb, D, db);
+        b.io(s->Y, z, nullptr, nullptr, SolveState{});
+        NPCG_CUDA(b.launch(st));
+    }
     NPCG_CUDA(cudaStreamSynchronize(st));
     return NPCG_OK;
 }
@@ -609,8 +658,17 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     sp.partial = s->partial;
     sp.ctl = s->ctl;
     sp.drift_count = s->drift_count;
+    SpmvArgs spl = sp;  // PCG ops: outputs in line order
+    if (s->ls) {
+        spl.n = s->ls->nslot;
+        spl.nslot = s->ls->nslot;
+        spl.rp = s->lrp;
+        spl.col = s->lcol;
+        spl.eidx = s->leidx;
+        spl.rowof = s->ls->rowof;
+    }
     // r = b - A x0 (or b)
-    SpmvArgs init = sp;
+    SpmvArgs init = spl;
     init.op = SPMV_RESID_INIT;
     init.X = x;
     init.Bv = bvec;
@@ -618,18 +676,18 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     init.has_x = x0 != nullptr;
     NPCG_CUDA(launch_spmv(init, st));
 
-    SpmvArgs apdot = sp;
+    SpmvArgs apdot = spl;
     apdot.op = SPMV_APDOT;
     apdot.X = s->P;
     apdot.Y = s->AP;
-    SpmvArgs drift = sp;
+    SpmvArgs drift = spl;
     drift.op = SPMV_RESID_DRIFT;
     drift.X = x;
     drift.Bv = bvec;
     drift.R = s->R;
     drift.P = s->P;
     // identity: S = ones is never referenced (no off-diagonal slots), packs to zeros
-    if (int rc = stage_factor(s, S, sb, st)) return rc;
+    if (int rc = stage_factor(s, S, sb, D, db, st)) return rc;
     if (!s->ls) {  // the level kernel's outputs start unsolved (re-armed every pass)
         launch_fill_sentinel(nB, s->Y, st);
         launch_fill_sentinel(nB, s->Z, st);
@@ -677,8 +735,9 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         used.clear();
     };
     auto pupd = [&]() {
+        if (s->ls) return launch_pupd_line(s->ls->nslot, B, s->ls->rowof, s->Z, s->P, x, sst, st);
         note_launch();
-        pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, x, sst, s->ls ? 0 : 1);
+        pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, x, sst, 1);
         return cudaGetLastError();
     };
 
@@ -797,3 +856,7 @@ int npcg_gnn_build_factor(const npcg_gnn *g, const npcg_pattern *A, int B, const
 }  // extern "C"
 
 extern "C" int64_t npcg_launch_count(void) { return (int64_t)launch_count(); }
+
+// Diagnostics: the line-solve timeline of CTA 0 (clock64 per batch and event,
+// [16][2048]); all zeros unless the library was built with -DNPCG_LINE_TRACE.
+extern "C" int npcg_debug_line_trace(long long *out, int n) { return line_trace_copy(out, n); }

@@ -502,6 +502,140 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_warp_kernel(SpmvArgs a) 
     spmv_reduce_tail(a, red, TEAMS);
 }
 
+// SpMV into line order (trsv_line.cu): rows are the slots of the factor's
+// line layout (A's CSR re-indexed by slot, padding slots empty; entries keep
+// their order, so every row sum is bitwise the natural one), X and the own
+// operand stay natural RHS-minor, and the output goes to Y[b][slot]
+// (system-major) through a per-warp [16 slots][64 columns] shared tile, so
+// each system's slots leave as 128-byte runs.
+constexpr int kLineTile = 16;
+
+template <int VW, bool VB, int OP>
+__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_line_kernel(SpmvArgs a) {
+    constexpr int TEAMS = kSpmvThreads / 32, CH = 8, TC = 32 * VW;  // tile columns
+    using V = typename VecT<VW>::type;
+    extern __shared__ double red[];  // TEAMS * B partials | TEAMS tiles [kLineTile][TC]
+    __shared__ unsigned char s_act[kMaxBatch];
+    const int team = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int B = a.B;
+    if (OP == SPMV_RESID_DRIFT && *a.drift_count == 0) return;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) s_act[b] = spmv_col_active(a, b) ? 1 : 0;
+    double *part = red + team * B;
+    double *tile = red + TEAMS * B + team * kLineTile * TC;
+    for (int b = lane; b < B; b += 32) part[b] = 0.0;
+    __syncthreads();
+    const int cpl = (B + TC - 1) / TC;
+    const int nteams = gridDim.x * TEAMS, gteam = blockIdx.x * TEAMS + team;
+    const int per = ((a.n + nteams - 1) / nteams + kLineTile - 1) / kLineTile * kLineTile;
+    const int r0 = min(a.n, gteam * per), r1 = min(a.n, r0 + per);
+    const bool use_x = OP != SPMV_RESID_INIT || a.has_x;
+    double *out = OP == SPMV_APDOT ? a.Y : a.R;
+    const long long ns = a.nslot;
+    for (int k = 0; k < cpl && r0 < r1; ++k) {
+        const int b = (lane + k * 32) * VW;
+        const bool on = b < B;
+        const unsigned bb = on ? b : 0;
+        bool xp[VW];
+        double al[VW];
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+            xp[v] = OP == SPMV_RESID_DRIFT && a.st.xpend[bb + v];
+            al[v] = xp[v] ? a.st.alpha[bb + v] : 0.0;
+        }
+        int wb = r0, rpl = a.rp[min(r0 + lane, a.n)];
+        int p0 = __shfl_sync(0xffffffffu, rpl, 0), p1 = __shfl_sync(0xffffffffu, rpl, 1);
+        int cj = lane < p1 - p0 ? a.col[p0 + lane] : 0;
+        int ce = lane < p1 - p0 ? a.eidx[p0 + lane] : 0;
+        for (int row = r0; row < r1; ++row) {
+            const int nat = a.rowof[row];
+            const unsigned ri = (unsigned)max(nat, 0) * B + bb;
+            double own[VW];
+#pragma unroll
+            for (int v = 0; v < VW; ++v) own[v] = 0.0;
+            if (nat >= 0) {
+                if (OP == SPMV_APDOT) VecT<VW>::get(*reinterpret_cast<const V *>(a.X + ri), own);
+                else VecT<VW>::get(*reinterpret_cast<const V *>(a.Bv + ri), own);
+            }
+            int w = row + 2 - wb;
+            if (w >= 32) {
+                wb = row;
+                rpl = a.rp[min(wb + lane, a.n)];
+                w = 2;
+            }
+            const int q1 = __shfl_sync(0xffffffffu, rpl, w);
+            const int cnt = p1 - p0, c0 = p0;
+            const int ccj = cj, cce = ce;
+            if (row + 1 < r1) {
+                cj = lane < q1 - p1 ? a.col[p1 + lane] : 0;
+                ce = lane < q1 - p1 ? a.eidx[p1 + lane] : 0;
+            }
+            p0 = p1;
+            p1 = q1;
+            double acc[VW];
+#pragma unroll
+            for (int v = 0; v < VW; ++v) acc[v] = 0.0;
+            if (use_x) {
+                for (int g = 0; g < cnt; g += CH) {
+                    int hj = ccj, he = cce;
+                    if (g >= 32 && (g & 31) == 0) {
+                        hj = lane < cnt - g ? a.col[c0 + g + lane] : 0;
+                        he = lane < cnt - g ? a.eidx[c0 + g + lane] : 0;
+                    }
+                    double xv[CH][VW], vv[VB ? CH : 1][VW], vs[CH];
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        const int j = __shfl_sync(0xffffffffu, hj, (g + c) & 31);
+                        const int e = __shfl_sync(0xffffffffu, he, (g + c) & 31);
+                        const unsigned jo = (unsigned)j * B + bb;
+                        VecT<VW>::get(*reinterpret_cast<const V *>(a.X + jo), xv[c]);
+                        if (VB) VecT<VW>::get(*reinterpret_cast<const V *>(a.vals + (size_t)e * B + bb), vv[c]);
+                        else vs[c] = a.vals[e];
+                        if (OP == SPMV_RESID_DRIFT) {  // x_{k+1} = x + alpha p not yet stored (pcg.py:141)
+                            double pv[VW];
+                            VecT<VW>::get(*reinterpret_cast<const V *>(a.P + jo), pv);
+#pragma unroll
+                            for (int v = 0; v < VW; ++v)
+                                if (xp[v]) xv[c][v] = __dadd_rn(xv[c][v], __dmul_rn(al[v], pv[v]));
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        const bool use = g + c < cnt;
+#pragma unroll
+                        for (int v = 0; v < VW; ++v) {
+                            const double s = __dadd_rn(acc[v], __dmul_rn(VB ? vv[VB ? c : 0][v] : vs[c], xv[c][v]));
+                            acc[v] = use ? s : acc[v];
+                        }
+                    }
+                }
+            }
+            const int ti = (row - r0) % kLineTile;
+#pragma unroll
+            for (int v = 0; v < VW; ++v) {
+                double o = acc[v];
+                if (OP != SPMV_APDOT) o = __dsub_rn(own[v], acc[v]);  // r = b - A x
+                if (on && s_act[b + v] && nat >= 0) {
+                    const double pr = OP == SPMV_APDOT ? __dmul_rn(own[v], acc[v]) : __dmul_rn(o, o);
+                    part[b + v] = __dadd_rn(part[b + v], pr);
+                }
+                tile[ti * TC + lane * VW + v] = nat >= 0 ? o : 0.0;
+            }
+            if (ti == kLineTile - 1 || row == r1 - 1) {  // flush: each column's slots as one run
+                __syncwarp();
+                const int q0 = row - ti, cntq = ti + 1;
+                for (int e = lane; e < kLineTile * TC; e += 32) {
+                    const int c = e / kLineTile, i = e % kLineTile, bc = k * TC + c;
+                    if (i < cntq && bc < B && s_act[bc] && OP != SPMV_RESID_FINAL)
+                        out[(long long)bc * ns + q0 + i] = tile[i * TC + c];
+                }
+                __syncwarp();
+            }
+        }
+    }
+    if (OP == SPMV_PLAIN) return;
+    spmv_reduce_tail(a, red, TEAMS);
+}
+
 // ===========================================================================
 // Elementwise / setup kernels
 // ===========================================================================
@@ -595,6 +729,114 @@ __global__ void pupd_kernel(long long nB, int B, double *z, double *p, double *x
             if (rearm) reinterpret_cast<long long *>(z)[q] = (long long)kSentinel;  // for the next backward solve
         }
     }
+}
+
+// Line-order variants: a block moves a tile of kLineTile slots x all columns
+// through shared memory, so the system-major line-order side ([b][slot])
+// and the natural RHS-minor side ([row][b]) are both read / written in
+// contiguous runs.
+constexpr int kPermTile = 16;
+
+// p = z + beta p | p = z ; x += alpha p   with z in line order (pcg.py:129, 141, 170)
+__global__ void __launch_bounds__(256) pupd_line_kernel(int nslot, int B, const int *rowof, const double *z,
+                                                         double *p, double *x, SolveState st) {
+    extern __shared__ double tz[];  // [kPermTile][B + 1]
+    __shared__ int s_f[kMaxBatch];
+    __shared__ double s_al[kMaxBatch], s_be[kMaxBatch];
+    const int ld = B + 1;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        s_f[b] = st.pflag[b];
+        s_al[b] = st.alpha[b];
+        s_be[b] = st.beta[b];
+    }
+    for (int q0 = blockIdx.x * kPermTile; q0 < nslot; q0 += gridDim.x * kPermTile) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPermTile * B; e += blockDim.x) {
+            const int b = e / kPermTile, i = e % kPermTile;
+            if (q0 + i < nslot) tz[i * ld + b] = z[(long long)b * nslot + q0 + i];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPermTile * B; e += blockDim.x) {
+            const int i = e / B, b = e % B;
+            if (q0 + i >= nslot) continue;
+            const int row = rowof[q0 + i];
+            const int f = s_f[b];
+            if (row < 0 || f == PF_NONE) continue;
+            const long long q = (long long)row * B + b;
+            const double pq = p[q];
+            if (f & PF_X) x[q] = __dadd_rn(x[q], __dmul_rn(s_al[b], pq));
+            if (f & (PF_UPDATE | PF_COPY)) {
+                const double zq = tz[i * ld + b];
+                p[q] = (f & PF_UPDATE) ? __dadd_rn(zq, __dmul_rn(s_be[b], pq)) : zq;
+            }
+        }
+    }
+}
+
+// dst[b][slot] = src[row(slot)][b] (natural RHS-minor, or shared [row] when
+// src_batched == 0); padding slots get `pad`.
+__global__ void __launch_bounds__(256) to_line_kernel(int nslot, int B, const int *rowof, const double *src,
+                                                       int src_batched, double pad, double *dst) {
+    extern __shared__ double tt[];  // [kPermTile][B + 1]
+    const int ld = B + 1;
+    for (int q0 = blockIdx.x * kPermTile; q0 < nslot; q0 += gridDim.x * kPermTile) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPermTile * B; e += blockDim.x) {
+            const int i = e / B, b = e % B;
+            if (q0 + i >= nslot) continue;
+            const int row = rowof[q0 + i];
+            tt[i * ld + b] = row < 0 ? pad : src[src_batched ? (long long)row * B + b : row];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPermTile * B; e += blockDim.x) {
+            const int b = e / kPermTile, i = e % kPermTile;
+            if (q0 + i < nslot) dst[(long long)b * nslot + q0 + i] = tt[i * ld + b];
+        }
+    }
+}
+
+// dst[row][b] = src[b][slot(row)]
+__global__ void __launch_bounds__(256) from_line_kernel(int nslot, int B, const int *rowof, const double *src,
+                                                         double *dst) {
+    extern __shared__ double tt[];  // [kPermTile][B + 1]
+    const int ld = B + 1;
+    for (int q0 = blockIdx.x * kPermTile; q0 < nslot; q0 += gridDim.x * kPermTile) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPermTile * B; e += blockDim.x) {
+            const int b = e / kPermTile, i = e % kPermTile;
+            if (q0 + i < nslot) tt[i * ld + b] = src[(long long)b * nslot + q0 + i];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPermTile * B; e += blockDim.x) {
+            const int i = e / B, b = e % B;
+            if (q0 + i >= nslot) continue;
+            const int row = rowof[q0 + i];
+            if (row >= 0) dst[(long long)row * B + b] = tt[i * ld + b];
+        }
+    }
+}
+
+cudaError_t launch_pupd_line(int nslot, int B, const int *rowof, const double *z, double *p, double *x,
+                             const SolveState &st, cudaStream_t s) {
+    const int grid = std::min((nslot + kPermTile - 1) / kPermTile, 8 * num_sms());
+    note_launch();
+    pupd_line_kernel<<<grid, 256, (size_t)kPermTile * (B + 1) * 8, s>>>(nslot, B, rowof, z, p, x, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_to_line(int nslot, int B, const int *rowof, const double *src, int src_batched, double pad,
+                           double *dst, cudaStream_t s) {
+    const int grid = std::min((nslot + kPermTile - 1) / kPermTile, 8 * num_sms());
+    note_launch();
+    to_line_kernel<<<grid, 256, (size_t)kPermTile * (B + 1) * 8, s>>>(nslot, B, rowof, src, src_batched, pad, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_from_line(int nslot, int B, const int *rowof, const double *src, double *dst, cudaStream_t s) {
+    const int grid = std::min((nslot + kPermTile - 1) / kPermTile, 8 * num_sms());
+    note_launch();
+    from_line_kernel<<<grid, 256, (size_t)kPermTile * (B + 1) * 8, s>>>(nslot, B, rowof, src, dst);
+    return cudaGetLastError();
 }
 
 __global__ void count_active_kernel(SolveState st, int B) {
@@ -713,7 +955,42 @@ static void spmv_warp_vw(const SpmvArgs &a, int grid, size_t smem, cudaStream_t 
     else spmv_warp_op<VW, false>(a, grid, smem, s);
 }
 
+template <int VW, bool VB, int OP>
+static void spmv_line_t(const SpmvArgs &a, int grid, size_t smem, cudaStream_t s) {
+    auto kern = spmv_line_kernel<VW, VB, OP>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    note_launch();
+    kern<<<grid, kSpmvThreads, smem, s>>>(a);
+}
+
+template <int VW, bool VB>
+static void spmv_line_op(const SpmvArgs &a, int grid, size_t smem, cudaStream_t s) {
+    switch (a.op) {
+        case SPMV_APDOT: return spmv_line_t<VW, VB, SPMV_APDOT>(a, grid, smem, s);
+        case SPMV_RESID_INIT: return spmv_line_t<VW, VB, SPMV_RESID_INIT>(a, grid, smem, s);
+        case SPMV_RESID_DRIFT: return spmv_line_t<VW, VB, SPMV_RESID_DRIFT>(a, grid, smem, s);
+        default: return spmv_line_t<VW, VB, SPMV_RESID_FINAL>(a, grid, smem, s);
+    }
+}
+
 cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s) {
+    if (a.rowof) {  // line-order output (PCG ops only)
+        if (a.op == SPMV_PLAIN) return cudaErrorInvalidValue;
+        auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
+        const int VW = (a.B % 2 == 0 && al16(a.X) && al16(a.Bv) && al16(a.P) && (!a.vb || al16(a.vals))) ? 2 : 1;
+        const int grid = (int)std::min<long long>(std::max<long long>((a.n + 8 * kLineTile - 1) / (8 * kLineTile), 1),
+                                                  (long long)kReduceBlocksPerSm * num_sms());
+        const size_t smem = ((size_t)(kSpmvThreads / 32) * a.B + (size_t)(kSpmvThreads / 32) * kLineTile * 32 * VW) *
+                            sizeof(double);
+        if (VW == 2) {
+            if (a.vb) spmv_line_op<2, true>(a, grid, smem, s);
+            else spmv_line_op<2, false>(a, grid, smem, s);
+        } else {
+            if (a.vb) spmv_line_op<1, true>(a, grid, smem, s);
+            else spmv_line_op<1, false>(a, grid, smem, s);
+        }
+        return cudaGetLastError();
+    }
     // 16-byte column pairs when every row of every operand stays 16-byte aligned
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
     const int VW = (a.B % 2 == 0 && al16(a.X) && al16(a.Y) && al16(a.Bv) && al16(a.R) && al16(a.P) &&

@@ -37,6 +37,10 @@ struct SpmvArgs {
     double *partial = nullptr;
     Ctl *ctl = nullptr;
     int *drift_count = nullptr;
+    // line-order output (rowof != null): rp/col index slots, eidx maps an
+    // entry to its natural position in vals, outputs are [b][nslot]
+    const int *eidx = nullptr, *rowof = nullptr;
+    int nslot = 0;
 };
 
 __global__ void init_state_kernel(SolveState st, int B, long long hist_cap_init);
@@ -52,5 +56,11 @@ __global__ void symmetric_check_kernel(long long nnz, int B, int vb, const int *
                                        int *ok);
 
 cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s);
+// line-order helpers (vectors [b][slot], see pattern.h LineSched)
+cudaError_t launch_pupd_line(int nslot, int B, const int *rowof, const double *z, double *p, double *x,
+                             const SolveState &st, cudaStream_t s);
+cudaError_t launch_to_line(int nslot, int B, const int *rowof, const double *src, int src_batched, double pad,
+                           double *dst, cudaStream_t s);
+cudaError_t launch_from_line(int nslot, int B, const int *rowof, const double *src, double *dst, cudaStream_t s);
 
 }  // namespace npcg

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 
@@ -218,19 +219,29 @@ static std::string build_direction(const Pattern &P, int32_t R, bool upper, Sche
 }
 
 LineSched::~LineSched() {
+    if (rowof) cudaFree(rowof);
+    if (slot) cudaFree(slot);
     for (LineDir *d : {&fwd, &bwd}) {
-        if (d->line_row0) cudaFree(d->line_row0);
-        if (d->line_len) cudaFree(d->line_len);
-        if (d->desc) cudaFree(d->desc);
-        if (d->vperm) cudaFree(d->vperm);
+        void *ptrs[] = {d->line_row0, d->line_len, d->line_start, d->bslot, d->bcount, d->boff, d->sched, d->vperm};
+        for (void *q : ptrs)
+            if (q) cudaFree(q);
     }
 }
 
-// One direction of the line schedule; false when the pattern does not
-// qualify (too many lines, deep cross-line window, wide rows).
-static bool build_lines(const Pattern &P, bool upper, LineDir &D) {
+// The line schedule of a structurally symmetric pattern; false when it does
+// not qualify (too many lines, deep cross-line window, wide rows).
+//
+// Forward: rows of line l run at steps start[l] + k, start[l] the earliest
+// step at which every cross-line dependency of the line is solved a step
+// earlier (a row's dependencies lie in earlier lines or earlier in its own
+// line). Backward runs the padded step range in reverse: an upper
+// dependency j of row i has row i as a lower dependency, so it was solved
+// at a later forward step -- an earlier backward one -- and the ring window
+// that covers the forward distances covers the backward ones.
+static bool build_line_sched(const Pattern &P, LineSched &LS) {
     const int32_t n = (int32_t)P.n;
     const auto &rp = P.h_rp, &col = P.h_col, &dp = P.h_dp;
+    if (n == 0) return false;
     std::vector<int32_t> starts{0};
     for (int32_t i = 1; i < n; ++i) {
         bool dep_prev = false;
@@ -239,77 +250,144 @@ static bool build_lines(const Pattern &P, bool upper, LineDir &D) {
     }
     starts.push_back(n);
     const int32_t L = (int32_t)starts.size() - 1;
-    if (n == 0 || L > 1024) return false;
-    std::vector<int32_t> line(n), pos(n), lvl(n, 0);
+    if (L > kLineMaxLines) return false;
+    std::vector<int32_t> line(n), pos(n), lstart(L, 0);
     for (int32_t l = 0; l < L; ++l)
         for (int32_t i = starts[l]; i < starts[l + 1]; ++i) {
             line[i] = l;
-            pos[i] = upper ? starts[l + 1] - 1 - i : i - starts[l];
+            pos[i] = i - starts[l];
         }
-    auto dep_begin = [&](int32_t i) { return upper ? dp[i] + 1 : rp[i]; };
-    auto dep_end = [&](int32_t i) { return upper ? rp[i + 1] : dp[i]; };
-    int32_t steps = 0, md = 1, span = 1;
-    for (int32_t t = 0; t < n; ++t) {
-        const int32_t i = upper ? n - 1 - t : t;
-        int32_t l = 0;
-        for (int32_t p = dep_begin(i); p < dep_end(i); ++p) l = std::max(l, lvl[col[p]] + 1);
-        lvl[i] = l;
-        steps = std::max(steps, l + 1);
-        md = std::max(md, dep_end(i) - dep_begin(i));
+    int32_t steps = 0, md = 1;
+    for (int32_t l = 0; l < L; ++l) {
+        int32_t st = 0;
+        for (int32_t i = starts[l]; i < starts[l + 1]; ++i) {
+            md = std::max(md, std::max(dp[i] - rp[i], rp[i + 1] - dp[i] - 1));
+            for (int32_t p = rp[i]; p < dp[i]; ++p) {
+                const int32_t j = col[p];
+                if (line[j] != l) st = std::max(st, lstart[line[j]] + pos[j] + 1 - pos[i]);
+            }
+        }
+        lstart[l] = st;
+        steps = std::max(steps, st + starts[l + 1] - starts[l]);
     }
-    const int32_t prev_off = upper ? 1 : -1;
+    auto fstep = [&](int32_t i) { return lstart[line[i]] + pos[i]; };
+    int32_t span = 1;
     for (int32_t i = 0; i < n; ++i)
-        for (int32_t p = dep_begin(i); p < dep_end(i); ++p) {
+        for (int32_t p = rp[i]; p < dp[i]; ++p) {
             const int32_t j = col[p];
-            if (j == i + prev_off && line[j] == line[i]) continue;  // carried in a register
-            span = std::max(span, lvl[i] - lvl[j] + 1);
+            if (j == i - 1 && line[j] == line[i]) continue;  // carried in a register
+            span = std::max(span, fstep(i) - fstep(j) + 1);
         }
     int32_t W = 1;
     while (W < span) W <<= 1;
     if (W > 16 || md > 8) return false;
     const int32_t MD = md <= 2 ? 2 : (md <= 3 ? 3 : (md <= 4 ? 4 : 8));
     const int32_t T = (L + 31) & ~31;
-    const int32_t zslot = L * W;
     const int32_t K = kLineBatch;
-    const int32_t SP = (steps + K - 1) / K * K;
-    std::vector<int16_t> desc((size_t)SP * MD * T, (int16_t)zslot);
-    std::vector<int32_t> row0(T, -1), llen(T, 0), vperm((size_t)SP * MD * T, -1);
-    for (int32_t s = 0; s < SP; ++s)
-        for (int32_t t = 0; t < T; ++t) desc[((size_t)s * MD) * T + t] = kNoRow;
-    for (int32_t l = 0; l < L; ++l) {
-        const int32_t a = starts[l], b = starts[l + 1];
-        row0[l] = upper ? b - 1 : a;
-        llen[l] = b - a;
-        for (int32_t k = 0; k < b - a; ++k) {
-            const int32_t i = upper ? b - 1 - k : a + k;
-            const size_t base = (size_t)lvl[i] * MD * T + l;
-            int32_t e = 0;
-            auto push = [&](int32_t p) {
-                const int32_t j = col[p];
-                desc[base + (size_t)e * T] =
-                    (int16_t)((j == i + prev_off && line[j] == line[i]) ? -1 : line[j] * W + (pos[j] & (W - 1)));
-                vperm[base + (size_t)e * T] = p;
-                ++e;
-            };
-            if (upper)
-                for (int32_t p = dep_end(i) - 1; p >= dep_begin(i); --p) push(p);
-            else
-                for (int32_t p = dep_begin(i); p < dep_end(i); ++p) push(p);
-            for (; e < MD; ++e) desc[base + (size_t)e * T] = (int16_t)zslot;  // 0 * (zero cell): exact
+    const int32_t SP = (steps + K - 1) / K * K, nb = SP / K;
+    // active line range of every step -> slots
+    std::vector<int32_t> lo(SP, INT32_MAX), hi(SP, 0), off(SP, 0);
+    for (int32_t l = 0; l < L; ++l)
+        for (int32_t s = lstart[l]; s < lstart[l] + starts[l + 1] - starts[l]; ++s) {
+            lo[s] = std::min(lo[s], l);
+            hi[s] = std::max(hi[s], l + 1);
         }
+    std::vector<int32_t> bslot(nb), bcount(nb);
+    int32_t cur = 0;
+    for (int32_t j = 0; j < nb; ++j) {
+        bslot[j] = cur;
+        for (int32_t q = 0; q < K; ++q) {
+            const int32_t s = j * K + q;
+            if (hi[s] == 0) lo[s] = hi[s] = 0;
+            off[s] = cur;
+            cur += hi[s] - lo[s];
+        }
+        cur = (cur + kLineSlotAlign - 1) / kLineSlotAlign * kLineSlotAlign;
+        bcount[j] = cur - bslot[j];
     }
-    D.nlines = L;
-    D.T = T;
-    D.steps = steps;
-    D.steps_pad = SP;
-    D.window = W;
-    D.md = MD;
-    D.zslot = zslot;
-    D.line_row0 = upload(row0);
-    D.line_len = upload(llen);
-    D.desc = upload(desc);
-    D.vperm = upload(vperm);
-    return D.line_row0 && D.line_len && D.desc && D.vperm;
+    const int32_t nslot = cur;
+    if ((int64_t)nslot > (int64_t)4 * n + 64 * nb) return false;  // far too sparse a wavefront
+    LS.nslot = nslot;
+    LS.h_rowof.assign(nslot, -1);
+    LS.h_slot.assign(n, -1);
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t s = fstep(i);
+        const int32_t q = off[s] + line[i] - lo[s];
+        LS.h_slot[i] = q;
+        LS.h_rowof[q] = i;
+    }
+    const int32_t zslot = W * T;
+    auto build_dir = [&](bool upper, LineDir &D) -> bool {
+        std::vector<int32_t> row0(T, 0), llen(T, 0), lst(T, 0), db(nb), dc(nb);
+        for (int32_t l = 0; l < L; ++l) {
+            const int32_t len = starts[l + 1] - starts[l];
+            row0[l] = upper ? starts[l + 1] - 1 : starts[l];
+            llen[l] = len;
+            lst[l] = upper ? SP - lstart[l] - len : lstart[l];
+        }
+        std::vector<int64_t> boff(nb);
+        std::vector<int16_t> sched;
+        std::vector<int32_t> vperm;
+        int32_t maxs = 0;
+        for (int32_t jd = 0; jd < nb; ++jd) {
+            const int32_t j = upper ? nb - 1 - jd : jd;  // forward batch
+            db[jd] = bslot[j];
+            dc[jd] = bcount[j];
+            maxs = std::max(maxs, bcount[j]);
+            boff[jd] = (int64_t)sched.size();
+            for (int32_t q = 0; q < K; ++q) {  // header: int32 base per step, as int16 pairs
+                const int32_t s = upper ? j * K + (K - 1 - q) : j * K + q;
+                const int32_t base = off[s] - lo[s] - bslot[j];
+                sched.push_back((int16_t)(base & 0xffff));
+                sched.push_back((int16_t)((uint32_t)base >> 16));
+            }
+            for (int32_t u = 0; u < bcount[j]; ++u) {
+                const int32_t i = LS.h_rowof[bslot[j] + u];
+                int32_t e = 0;
+                if (i >= 0) {
+                    auto push = [&](int32_t p) {
+                        const int32_t jj = col[p];
+                        const bool prev = line[jj] == line[i] && jj == i + (upper ? 1 : -1);
+                        const int32_t pj = upper ? (starts[line[jj] + 1] - 1 - jj) : pos[jj];
+                        sched.push_back((int16_t)(prev ? -1 : (pj & (W - 1)) * T + line[jj]));
+                        vperm.push_back(p);
+                        ++e;
+                    };
+                    // the reference's summation order (sparse.py:222-239)
+                    if (upper)
+                        for (int32_t p = rp[i + 1] - 1; p > dp[i]; --p) push(p);
+                    else
+                        for (int32_t p = rp[i]; p < dp[i]; ++p) push(p);
+                }
+                // padding reads the zero cell with a zero factor: acc - 0 * 0 == acc exactly
+                for (; e < MD; ++e) {
+                    sched.push_back((int16_t)zslot);
+                    vperm.push_back(-1);
+                }
+            }
+        }
+        D.T = T;
+        D.nbatch = nb;
+        D.window = W;
+        D.md = MD;
+        D.zslot = zslot;
+        D.max_slots = maxs;
+        D.sched_words = (int64_t)sched.size();
+        D.fac_slots = (int64_t)vperm.size();
+        D.line_row0 = upload(row0);
+        D.line_len = upload(llen);
+        D.line_start = upload(lst);
+        D.bslot = upload(db);
+        D.bcount = upload(dc);
+        D.boff = upload(boff);
+        D.sched = upload(sched);
+        D.vperm = upload(vperm);
+        return D.line_row0 && D.line_len && D.line_start && D.bslot && D.bcount && D.boff && D.sched && D.vperm;
+    };
+    if (!build_dir(false, LS.fwd) || !build_dir(true, LS.bwd)) return false;
+    LS.rowof = upload(LS.h_rowof);
+    LS.slot = upload(LS.h_slot);
+    return LS.rowof && LS.slot;
 }
 
 LineSched *Pattern::line_schedule() {
@@ -317,8 +395,7 @@ LineSched *Pattern::line_schedule() {
     if (!factor_ok) return nullptr;
     if (!lines) {
         lines = std::make_unique<LineSched>();
-        lines->ok = !std::getenv("NPCG_NO_LINES") && build_lines(*this, false, lines->fwd) &&
-                    build_lines(*this, true, lines->bwd);
+        lines->ok = !std::getenv("NPCG_NO_LINES") && build_line_sched(*this, *lines);
     }
     return lines->ok ? lines.get() : nullptr;
 }

@@ -52,28 +52,49 @@ struct SchedSet {
 
 // Line-wavefront schedule (trsv_line.cu): the rows split into "lines",
 // maximal runs in which every row depends on its predecessor (grid lines of
-// a mesh in natural order). One thread owns one line and walks its rows in
-// solve order; step s of the CTA solves every row whose level is s, so the
-// in-line dependency stays in a register and the cross-line ones are read
-// from a per-line shared-memory ring of the last `window` values.
-// Per (step, thread) the schedule stores MD dependency descriptors and the
-// matching factor slots, step-major: desc[step][e][T] (int16) with
-//   -1 = previous row of the line, >= 0 = ring slot, zslot = padding,
-//   desc[.][0] = kNoRow when the thread has no row at that step,
-// and vperm[step][e][T] = CSR position of the factor value (-1 = padding).
-// Only built when the whole pattern fits one CTA (lines <= 1024, window <= 16).
-constexpr int32_t kLineBatch = 6;          // steps staged per batch
-constexpr int16_t kNoRow = -2;             // desc[.][0]: thread idle at this step
+// a mesh in natural order). One thread owns one line; lines are rigid: in
+// the forward solve row k of line l is solved at step start[l] + k, and the
+// backward solve runs the same steps in reverse. The in-line dependency
+// stays in a register, cross-line ones are read from a shared-memory ring
+// of every line's last `window` values ([window][T]).
+//
+// Line order ("slots"): the vectors the solves touch are stored step-major,
+// each step holding the contiguous range of lines active at it, so the rows
+// of a batch of kLineBatch steps are one contiguous slot range in both
+// directions and move with a single bulk copy. Slot ranges of batches are
+// padded to multiples of 8 (16-byte aligned copies); padding slots belong to
+// no row and hold zeros.
+//
+// Per batch (in a direction's order) the schedule holds a 16-byte header
+// (int32 base[kLineBatch]: slot of line 0 at each step, relative to the
+// batch's first slot) followed by [slot][md] int16 descriptors
+//   -1 = previous row of the line, >= 0 = ring slot, zslot = padding (zero);
+// vperm[slot][md] = CSR position of the matching factor value (-1 = pad).
+// Only built when the whole pattern fits one CTA (lines <= kLineMaxLines,
+// window <= 16, <= 8 dependencies per row) and the pattern is structurally
+// symmetric.
+constexpr int32_t kLineBatch = 4;      // steps per pipeline stage
+constexpr int32_t kLineMaxLines = 512;
+constexpr int32_t kLineSlotAlign = 8;  // slots per alignment unit of a batch range
 
 struct LineDir {
-    int32_t nlines = 0, T = 0, steps = 0, steps_pad = 0, window = 1, md = 1, zslot = 0;
-    int32_t *line_row0 = nullptr;  // [T] first row of each thread in solve order (-1: idle)
-    int32_t *line_len = nullptr;   // [T] rows of each thread's line
-    int16_t *desc = nullptr;       // [steps_pad][md][T]
-    int32_t *vperm = nullptr;      // [steps_pad][md][T]
+    int32_t T = 0, nbatch = 0, window = 1, md = 1, zslot = 0, max_slots = 0;
+    int64_t sched_words = 0;        // int16 words of the packed schedule
+    int64_t fac_slots = 0;          // factor values per system (= slots * md)
+    int32_t *line_row0 = nullptr;   // [T] first row of each line in solve order
+    int32_t *line_len = nullptr;    // [T] rows of each line (0: padding thread)
+    int32_t *line_start = nullptr;  // [T] step of each line's first row
+    int32_t *bslot = nullptr;       // [nbatch] first slot of each batch
+    int32_t *bcount = nullptr;      // [nbatch] slots of each batch (multiple of 8)
+    int64_t *boff = nullptr;        // [nbatch] int16 offset of each batch's schedule block
+    int16_t *sched = nullptr;       // [sched_words] per batch: header + [slot][md]
+    int32_t *vperm = nullptr;       // [fac_slots] factor CSR position (-1 = padding)
 };
 struct LineSched {
     bool ok = false;
+    int32_t nslot = 0;                    // slots per system (multiple of 8)
+    std::vector<int32_t> h_rowof, h_slot;  // slot -> row (-1: padding), row -> slot
+    int32_t *rowof = nullptr, *slot = nullptr;
     LineDir fwd, bwd;
     ~LineSched();
 };

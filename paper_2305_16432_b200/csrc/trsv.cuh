@@ -41,23 +41,24 @@ struct TrsvSmem {
 
 TrsvSmem trsv_smem_plan(const Schedule &S, int G, int s_batched);
 
-// Line-wavefront solve (trsv_line.cu): one CTA per system, one thread per line.
-// Vector element (row i, system b) lives at i * rs + b * cs.
+// Line-wavefront solve (trsv_line.cu): one CTA per system. Every vector is
+// in line order, system-major: element (slot q, system b) at b * nslot + q.
 struct LineArgs {
-    int B = 1, K = 6, upper = 0, mode = TRSV_PLAIN;
-    long long rs = 1, cs = 0;
+    int B = 1, stages = 3, upper = 0, mode = TRSV_PLAIN;
+    int nslot = 0;
     LineDir dir{};
-    const double *S = nullptr;  // factor values in line order ([b][...] when s_batched)
+    const double *S = nullptr;  // packed factor values ([b][fac_slots] when s_batched)
     int s_batched = 0;
-    const double *D = nullptr;  // diag(A): shared [n] or per system (rs, cs)
+    const double *D = nullptr;  // diag(A) in line order: [nslot] or [b][nslot] (padding 1.0)
     int d_batched = 0;
     double *in = nullptr, *out = nullptr, *R = nullptr;
     const double *AP = nullptr;
     SolveState st{};
     int *drift_count = nullptr;
 };
-size_t line_smem_bytes(const LineDir &L, int K);
-int line_batch_for(const LineDir &L);  // steps per batch that fit shared memory (0: none)
+size_t line_smem_bytes(const LineDir &L, int stages, bool upper, bool pcg);
+int line_stages_for(const LineDir &L);  // pipeline stages that fit shared memory (0: none)
+int line_trace_copy(long long *out, int n);  // debug timeline (NPCG_LINE_TRACE builds)
 cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s);
 // factor values S[p * ps + b * bs] -> line order of `L` (per system when batched)
 void launch_line_factor_pack(const LineDir &L, int B, int sb, long long ps, long long bs, const double *S,

@@ -1,38 +1,70 @@
 // trsv_line.cu -- line-wavefront triangular solves for patterns whose rows
-// form at most 1024 "lines" (runs of rows each depending on its predecessor;
-// the grid lines of a mesh in natural order).
+// form at most kLineMaxLines "lines" (runs of rows each depending on its
+// predecessor; the grid lines of a mesh in natural order).
 //
-// One CTA per right-hand side / system, one thread per line. Step s solves
-// every row whose level is s: a thread solves at most one row per step, the
-// dependency on its own previous row stays in a register and dependencies on
-// other lines are read from a shared-memory ring holding each line's last
-// `window` values, so one step costs a barrier plus a short chain of shared
-// loads and fp64 operations. Everything a step consumes is staged ahead with
-// cp.async: the schedule (dependency descriptors + factor values, laid out
-// [step][entry][thread]) as one contiguous block per batch of K steps copied
-// by the whole CTA, and each thread's vector operands (its line's rows are
-// consecutive) up to 2K rows ahead. The wait happens once per batch, not per
-// level (tools/microbench_level.cu: a per-level wait costs 150-200 cycles).
+// One CTA per right-hand side / system, warp-specialised:
+//
+//   consumers (threads 0..T-1, one per line) walk the steps. At step s every
+//     line whose rigid step range covers s solves one row: the dependency
+//     on its own previous row is a register, the cross-line ones are read
+//     from a shared-memory ring holding every line's last `window` values.
+//     A step is a handful of shared loads, an unfused fp64 chain and one
+//     named barrier over the consumer warps -- nothing else.
+//   producers (kProdWarps warps) move whole batches of kLineBatch steps.
+//     Every vector lives in line order (pattern.h), so a batch's rows are one
+//     contiguous slot range: one elected producer bulk-copies (TMA,
+//     cp.async.bulk + mbarrier) the batch's schedule block, factor values
+//     and vector slices into a stage ring, the producer warps form the
+//     right-hand sides slot by slot (r - alpha Ap forward, y / diag
+//     backward) and, once the consumers are done, accumulate the PCG dot
+//     product and bulk-store the solved slices back (TMA store). No thread
+//     issues a scattered global access.
+//
+// Stage hand-off uses named barriers: FULL[s] (producers arrive, consumers
+// sync) and EMPTY[s] (consumers arrive, producers sync), so a consumer pays
+// one barrier per step plus one per batch.
 //
 // Summation order and unfused fp64 arithmetic are those of the reference
 // (sparse.py:222-239), so results are bit-identical to pcgkit.
 #include <algorithm>
 
+#include "ptx.cuh"
 #include "trsv.cuh"
 
 namespace npcg {
 
 namespace {
 
-__device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cpa8(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+constexpr int kProdWarps = 4;
+constexpr int kProd = 32 * kProdWarps;
+constexpr int kBarCons = 1;   // consumer step barrier
+constexpr int kBarFull = 2;   // + stage (<= kLineMaxStages)
+constexpr int kBarEmpty = 6;  // + stage
+constexpr int kBarProd = 10;  // producer-only barrier
+constexpr int kLineMaxStages = 4;
+constexpr int kPrefetchBatches = 6;  // L2 prefetch distance of the bulk copies
+
+struct LineSmem {  // byte offsets into dynamic shared memory
+    size_t ring, stage0, stage_bytes, sv, v[3], total;
+};
+
+__host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
+
+__host__ __device__ inline LineSmem line_layout(int T, int W, int MD, int maxs, int NS, int nv) {
+    LineSmem m;
+    m.ring = 128;  // mbarriers first
+    m.stage0 = al128(m.ring + ((size_t)T * W + 2) * 8);
+    size_t o = al128(16 + (size_t)maxs * MD * 2);  // schedule block
+    m.sv = o;
+    o = al128(o + (size_t)maxs * MD * 8);
+    for (int i = 0; i < 3; ++i) {
+        m.v[i] = o;
+        if (i < nv) o = al128(o + (size_t)maxs * 8);
+    }
+    m.stage_bytes = o;
+    m.total = m.stage0 + NS * o;
+    return m;
 }
-__device__ __forceinline__ void cpa16(void *dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void line_epilogue(const LineArgs &a, int b, double total) {
     if (a.upper) bwd_epilogue(a.st, b, total);
@@ -41,13 +73,30 @@ __device__ __forceinline__ void line_epilogue(const LineArgs &a, int b, double t
 
 }  // namespace
 
+// Debug timeline of CTA 0 of the forward solve (build with -DNPCG_LINE_TRACE):
+// clock64 per batch and event, read back with npcg_debug_line_trace().
+constexpr int kTraceEvents = 16, kTraceBatches = 2048;
+__device__ long long g_line_trace[kTraceEvents][kTraceBatches];
+#ifdef NPCG_LINE_TRACE
+#define LTRACE(ev, j)                                                                                     \
+    do {                                                                                                  \
+        if (!UPPER && blockIdx.x == 0 && (j) < kTraceBatches) g_line_trace[ev][j] = clock64();            \
+    } while (0)
+#else
+#define LTRACE(ev, j) \
+    do {              \
+    } while (0)
+#endif
+
 template <int MD, bool UPPER, bool PCG, bool SB>
-__global__ void __launch_bounds__(1024) trsv_line_kernel(LineArgs a) {
-    extern __shared__ __align__(16) char sm[];
-    __shared__ double s_red[32];
+__global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(LineArgs a) {
+    constexpr int K = kLineBatch;
+    extern __shared__ __align__(128) char sm[];
+    __shared__ double s_red[kProdWarps];
     const LineDir &L = a.dir;
-    const int T = L.T, t = threadIdx.x, K = a.K, VR = 2 * a.K;
-    const int b = blockIdx.x;
+    const int T = L.T, NS = a.stages, W = L.window, nb = L.nbatch;
+    const int tid = threadIdx.x, b = blockIdx.x;
+    const int NT = T + kProd;  // threads taking part in FULL / EMPTY
     // what this system needs from this launch
     int op = TOP_SOLVE;
     if (PCG) {
@@ -56,133 +105,222 @@ __global__ void __launch_bounds__(1024) trsv_line_kernel(LineArgs a) {
         op = !UPPER ? (ph == PH_ITER ? TOP_UPDATE : (ph == PH_INIT ? TOP_SOLVE : TOP_SKIP))
                     : ((ph == PH_ITER || ph == PH_INIT) ? TOP_SOLVE : TOP_SKIP);
         if (op == TOP_SKIP) {
-            if (UPPER && t == 0) line_epilogue(a, b, 0.0);  // keeps pflag / restart bookkeeping
+            if (UPPER && tid == 0) line_epilogue(a, b, 0.0);  // keeps pflag / restart bookkeeping
             return;
         }
     }
-    // shared memory: ring | desc stages | factor stages | vector ring
-    const int W = L.window;
-    double *ring = reinterpret_cast<double *>(sm);
-    const size_t ring_bytes = ((size_t)T * W + 2) * 8;
-    int16_t *sdesc = reinterpret_cast<int16_t *>(sm + ((ring_bytes + 15) & ~size_t(15)));
-    const size_t desc_stage = (size_t)K * MD * T;  // elements per stage
-    double *sval = reinterpret_cast<double *>(reinterpret_cast<char *>(sdesc) + ((2 * desc_stage * 2 + 15) & ~size_t(15)));
-    double *vring = sval + 2 * desc_stage;  // [VR][3][T]
-    for (int q = t; q < T * W + 2; q += T) ring[q] = 0.0;  // the padding slot reads +0.0
-
-    const int row0 = L.line_row0[t];
-    const int len = row0 < 0 ? 0 : L.line_len[t];
-    const int dir = UPPER ? -1 : 1;
-    const long long cb = (long long)b * a.cs, rs = a.rs;
-    const double *Sb = a.S + (SB ? (size_t)b * L.steps_pad * MD * T : 0);
-    const int nb = L.steps_pad / K;
-    const double alpha = (!UPPER && PCG && op == TOP_UPDATE) ? a.st.alpha[b] : 0.0;
-
-    auto issue_struct = [&](int j) {  // whole CTA: one contiguous block per batch
-        const int16_t *gd = L.desc + (size_t)j * desc_stage;
-        int16_t *dd = sdesc + (size_t)(j & 1) * desc_stage;
-        for (int q = t; q < (int)(desc_stage / 8); q += T) cpa16(dd + 8 * q, gd + 8 * q);
-        const double *gs = Sb + (size_t)j * desc_stage;
-        double *ds = sval + (size_t)(j & 1) * desc_stage;
-        for (int q = t; q < (int)(desc_stage / 2); q += T) cpa16(ds + 2 * q, gs + 2 * q);
-    };
-    int k_iss = 0;
-    auto issue_vectors = [&](int upto) {  // this thread: rows [k_iss, upto) of its line
-        upto = min(upto, len);
-        for (; k_iss < upto; ++k_iss) {
-            const long long vi = (long long)(row0 + dir * k_iss) * rs + cb;
-            double *v = vring + (size_t)(k_iss % VR) * 3 * T + t;
-            if (!UPPER) {
-                cpa8(v, a.in + vi);  // r
-                if (PCG && op == TOP_UPDATE) cpa8(v + T, a.AP + vi);
-            } else {
-                cpa8(v, a.in + vi);  // y
-                cpa8(v + T, a.d_batched ? a.D + vi : a.D + (row0 + dir * k_iss));  // D shared: [n]
-                if (PCG) cpa8(v + 2 * T, a.R + vi);
-            }
-        }
-    };
-
-    issue_struct(0);
-    issue_vectors(VR);
-    cpa_commit();
-    double prev = 0.0, acc2 = 0.0;
-    int k = 0;  // rows of this line solved so far
-    for (int j = 0; j < nb; ++j) {
-        cpa_wait_all();
-        __syncthreads();  // batch j's schedule and the vectors issued a batch ago have landed
-        if (j + 1 < nb) issue_struct(j + 1);
-        issue_vectors(k + VR);
-        cpa_commit();
-        const int16_t *dd = sdesc + (size_t)(j & 1) * desc_stage;
-        const double *ds = sval + (size_t)(j & 1) * desc_stage;
-        for (int q = 0; q < K; ++q) {
-            const int16_t *dq = dd + (size_t)q * MD * T + t;
-            const double *sq = ds + (size_t)q * MD * T + t;
-            const int d0 = dq[0];
-            if (d0 != kNoRow) {
-                const double *v = vring + (size_t)(k % VR) * 3 * T + t;
-                double acc;
-                if (!UPPER) {
-                    if (PCG && op == TOP_UPDATE) {  // r -= alpha Ap (pcg.py:142)
-                        acc = __dsub_rn(v[0], __dmul_rn(alpha, v[T]));
-                        a.R[(long long)(row0 + k) * rs + cb] = acc;
-                        acc2 = __dadd_rn(acc2, __dmul_rn(acc, acc));
-                    } else {
-                        acc = v[0];
-                    }
-                } else {
-                    acc = __ddiv_rn(v[0], v[T]);  // z /= diag (sparse.py:273)
-                }
-                double y[MD], s[MD];
-#pragma unroll
-                for (int e = 0; e < MD; ++e) {
-                    const int d = e == 0 ? d0 : dq[(size_t)e * T];
-                    s[e] = sq[(size_t)e * T];
-                    y[e] = d == -1 ? prev : ring[d];
-                }
-#pragma unroll
-                for (int e = 0; e < MD; ++e) acc = __dsub_rn(acc, __dmul_rn(s[e], y[e]));
-                if (UPPER && PCG) acc2 = __dadd_rn(acc2, __dmul_rn(v[2 * T], acc));
-                prev = acc;
-                ring[t * W + (k & (W - 1))] = acc;
-                a.out[(long long)(row0 + dir * k) * rs + cb] = acc;
-                ++k;
-            }
-            __syncthreads();  // step done: its values are visible to the next step
-        }
+    const bool upd = !UPPER && PCG && op == TOP_UPDATE;
+    const int nv = UPPER ? (PCG ? 3 : 2) : 2;
+    const LineSmem m = line_layout(T, W, MD, L.max_slots, NS, nv);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm);
+    double *ring = reinterpret_cast<double *>(sm + m.ring);  // [W][T] + zero cell
+    auto stage_ptr = [&](int s) { return sm + m.stage0 + (size_t)s * m.stage_bytes; };
+    for (int q = tid; q < T * W + 2; q += blockDim.x) ring[q] = 0.0;
+    if (tid == T) {
+        for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], 1);
+        fence_mbar_init();
     }
-    cpa_wait_all();
-    if (PCG) {  // fixed-order block reduction of r.r (forward) or r.z (backward)
+    __syncthreads();
+
+    if (tid < T) {
+        // ------------------------------------------------------------------ consumers
+        const int t = tid, len = L.line_len[t], lst = L.line_start[t];
+        double prev = 0.0;
+        for (int j = 0; j < nb; ++j) {
+            const int s = j % NS;
+            if (t == 0) LTRACE(0, j);
+            bar_sync(kBarFull + s, NT);  // stage s holds batch j (also orders the last step's ring writes)
+            if (t == 0) LTRACE(1, j);
+            char *sp = stage_ptr(s);
+            const int *hdr = reinterpret_cast<const int *>(sp);
+            const int16_t *dsc = reinterpret_cast<const int16_t *>(sp) + 8;
+            const double *sv = reinterpret_cast<const double *>(sp + m.sv);
+            double *vin = reinterpret_cast<double *>(sp + m.v[0]);                // rhs (r / y/D)
+            double *vout = reinterpret_cast<double *>(sp + m.v[UPPER ? 0 : 1]);   // solution
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                const int kp = j * K + q - lst;  // position of this line's row solved at this step
+                if ((unsigned)kp < (unsigned)len) {
+                    const int u = hdr[q] + t;
+                    int d[MD];
+                    double v[MD];
+#pragma unroll
+                    for (int e = 0; e < MD; ++e) {
+                        d[e] = dsc[u * MD + e];
+                        v[e] = sv[u * MD + e];
+                    }
+                    double acc = vin[u];
+                    double y[MD];
+#pragma unroll
+                    for (int e = 0; e < MD; ++e) y[e] = d[e] == -1 ? prev : ring[d[e]];
+#pragma unroll
+                    for (int e = 0; e < MD; ++e) acc = __dsub_rn(acc, __dmul_rn(v[e], y[e]));
+                    prev = acc;
+                    ring[(kp & (W - 1)) * T + t] = acc;
+                    vout[u] = acc;
+                }
+                if (t == 0) LTRACE(8 + q, j);
+                if (q + 1 < K) bar_sync(kBarCons, T);  // step done: its values are visible to the next step
+            }
+            if (t == 0) LTRACE(2, j);
+            bar_arrive(kBarEmpty + s, NT);  // batch j's solution is in stage s
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------------- producers
+    const int p = tid - T;  // 0 .. kProd-1
+    const bool elect = p == 0;
+    const long long vb = (long long)b * a.nslot;
+    const double *Sb = a.S + (SB ? (size_t)b * L.fac_slots : 0);
+    const double *Db = a.D + (a.d_batched ? vb : 0);
+    const double alpha = upd ? a.st.alpha[b] : 0.0;
+    double acc2 = 0.0;
+    // sources of batch mb's stage blocks (global)
+    auto blocks = [&](int mb, const void **src, unsigned *bytes, int &nsrc) {
+        const int bs = L.bslot[mb], cnt = L.bcount[mb];
+        const long long bo = L.boff[mb];
+        nsrc = 0;
+        src[nsrc] = L.sched + bo;
+        bytes[nsrc++] = 16 + (unsigned)cnt * MD * 2;
+        src[nsrc] = Sb + (bo - 8ll * mb);
+        bytes[nsrc++] = (unsigned)cnt * MD * 8;
+        src[nsrc] = a.in + vb + bs;
+        bytes[nsrc++] = cnt * 8;
+        if (!UPPER) {
+            if (upd) {
+                src[nsrc] = a.AP + vb + bs;
+                bytes[nsrc++] = cnt * 8;
+            }
+        } else {
+            src[nsrc] = Db + bs;
+            bytes[nsrc++] = cnt * 8;
+            if (PCG) {
+                src[nsrc] = a.R + vb + bs;
+                bytes[nsrc++] = cnt * 8;
+            }
+        }
+    };
+    auto issue_load = [&](int mb) {  // elected producer: TMA of batch mb into its stage
+        const void *src[5];
+        unsigned bytes[5];
+        int nsrc;
+        blocks(mb, src, bytes, nsrc);
+        char *sp = stage_ptr(mb % NS);
+        char *dst[5] = {sp, sp + m.sv, sp + m.v[0], sp + m.v[1], sp + m.v[2]};
+        unsigned tot = 0;
+        for (int i = 0; i < nsrc; ++i) tot += bytes[i];
+        uint64_t *bar = &mbar[mb % NS];
+        mbar_expect_tx(bar, tot);
+        for (int i = 0; i < nsrc; ++i) bulk_g2s(dst[i], src[i], bytes[i], bar);
+    };
+    auto prefetch = [&](int mb) {
+        const void *src[5];
+        unsigned bytes[5];
+        int nsrc;
+        blocks(mb, src, bytes, nsrc);
+        for (int i = 0; i < nsrc; ++i) bulk_prefetch_l2(src[i], bytes[i]);
+    };
+    // batch mb is solved: dot product, then the solved slices go home
+    auto drain = [&](int mb) {
+        bar_sync(kBarEmpty + mb % NS, NT);
+        char *sp = stage_ptr(mb % NS);
+        const int bs = L.bslot[mb], cnt = L.bcount[mb];
+        if (UPPER && PCG) {  // r.z (pcg.py:167)
+            const double *z = reinterpret_cast<const double *>(sp + m.v[0]);
+            const double *r = reinterpret_cast<const double *>(sp + m.v[2]);
+            for (int u = p; u < cnt; u += kProd) acc2 = __dadd_rn(acc2, __dmul_rn(r[u], z[u]));
+        }
+        if (elect) {
+            fence_proxy_async();  // consumer / producer smem writes -> bulk-copy reads
+            if (!UPPER) {
+                if (upd) bulk_s2g(a.R + vb + bs, sp + m.v[0], cnt * 8);  // r_{k+1}
+                bulk_s2g(a.out + vb + bs, sp + m.v[1], cnt * 8);          // y
+            } else {
+                bulk_s2g(a.out + vb + bs, sp + m.v[0], cnt * 8);  // z
+            }
+            bulk_commit();
+        }
+    };
+    constexpr int D = 2;            // batch j - D is drained at iteration j
+    const int A = NS >= 3 ? 1 : 0;  // batch j + A is requested at iteration j
+    if (elect) {
+        for (int mb = 0; mb < kPrefetchBatches && mb < nb; ++mb) prefetch(mb);
+        for (int mb = 0; mb < A && mb < nb; ++mb) issue_load(mb);
+    }
+    for (int j = 0; j < nb; ++j) {
+        if (p == 0) LTRACE(3, j);
+        if (j >= D) drain(j - D);
+        if (p == 0) LTRACE(4, j);
+        const int mb = j + A;
+        if (elect && mb < nb) {
+            // the stage of batch mb last held mb - NS, drained at iteration mb - NS + D
+            if (mb - NS + D == j) bulk_wait_read<0>();
+            else bulk_wait_read<1>();
+            issue_load(mb);
+            if (mb + kPrefetchBatches < nb) prefetch(mb + kPrefetchBatches);
+        }
+        const int s = j % NS;
+        mbar_wait(&mbar[s], (j / NS) & 1);  // batch j's blocks have landed
+        if (p == 0) LTRACE(6, j);
+        char *sp = stage_ptr(s);
+        const int cnt = L.bcount[j];
+        if (upd) {  // r -= alpha Ap (pcg.py:142), r.r of the new residual
+            double *r = reinterpret_cast<double *>(sp + m.v[0]);
+            const double *ap = reinterpret_cast<const double *>(sp + m.v[1]);
+            for (int u = p; u < cnt; u += kProd) {
+                const double rn = __dsub_rn(r[u], __dmul_rn(alpha, ap[u]));
+                r[u] = rn;
+                acc2 = __dadd_rn(acc2, __dmul_rn(rn, rn));
+            }
+        } else if (UPPER) {  // z /= diag (sparse.py:273)
+            double *y = reinterpret_cast<double *>(sp + m.v[0]);
+            const double *dg = reinterpret_cast<const double *>(sp + m.v[1]);
+            for (int u = p; u < cnt; u += kProd) y[u] = __ddiv_rn(y[u], dg[u]);
+        }
+        if (p == 0) LTRACE(5, j);
+        bar_arrive(kBarFull + s, NT);
+    }
+    for (int mb = std::max(0, nb - D); mb < nb; ++mb) drain(mb);
+    if (elect) bulk_wait<0>();  // solved slices written before the CTA retires
+    if (PCG) {  // fixed-order reduction over the producer threads
         double v = acc2;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
-        if ((t & 31) == 0) s_red[t >> 5] = v;
-        __syncthreads();
-        if (t == 0) {
+        if ((p & 31) == 0) s_red[p >> 5] = v;
+        bar_sync(kBarProd, kProd);
+        if (p == 0) {
             double tot = 0.0;
-            for (int w = 0; w < (T + 31) / 32; ++w) tot = __dadd_rn(tot, s_red[w]);
+            for (int w = 0; w < kProdWarps; ++w) tot = __dadd_rn(tot, s_red[w]);
             line_epilogue(a, b, tot);
         }
     }
 }
 
-size_t line_smem_bytes(const LineDir &L, int K) {
-    const size_t ring = (((size_t)L.T * L.window + 2) * 8 + 15) & ~size_t(15);
-    const size_t st = (size_t)K * L.md * L.T;
-    return ring + ((2 * st * 2 + 15) & ~size_t(15)) + 2 * st * 8 + (size_t)2 * K * 3 * L.T * 8;
+int line_trace_copy(long long *out, int n) {
+    n = std::min(n, kTraceEvents * kTraceBatches);
+    return (int)cudaMemcpyFromSymbol(out, g_line_trace, n * sizeof(long long));
 }
 
-int line_batch_for(const LineDir &L) {
-    for (int K : {6, 3, 2, 1})
-        if (line_smem_bytes(L, K) <= 200 * 1024) return K;
+size_t line_smem_bytes(const LineDir &L, int stages, bool upper, bool pcg) {
+    return line_layout(L.T, L.window, L.md, L.max_slots, stages, upper ? (pcg ? 3 : 2) : 2).total;
+}
+
+int line_stages_for(const LineDir &L) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (optin <= 0) optin = 227 * 1024;
+    const size_t cap = (size_t)optin - 1024;  // static shared memory
+    for (int ns = kLineMaxStages; ns >= 2; --ns)
+        if (line_smem_bytes(L, ns, true, true) <= cap) return ns;
     return 0;
 }
 
 template <int MD, bool UPPER, bool PCG, bool SB>
 static cudaError_t launch_line_t(const LineArgs &a, cudaStream_t s) {
     auto kern = trsv_line_kernel<MD, UPPER, PCG, SB>;
-    const size_t smem = line_smem_bytes(a.dir, a.K);
+    const size_t smem = line_smem_bytes(a.dir, a.stages, UPPER, PCG);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -190,7 +328,7 @@ static cudaError_t launch_line_t(const LineArgs &a, cudaStream_t s) {
         configured = smem;
     }
     note_launch();
-    kern<<<a.B, a.dir.T, smem, s>>>(a);
+    kern<<<a.B, a.dir.T + kProd, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -206,6 +344,7 @@ static cudaError_t launch_line_md(const LineArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s) {
+    if (a.stages < 2 || a.stages > kLineMaxStages) return cudaErrorInvalidValue;
     switch (a.dir.md) {
         case 2: return launch_line_md<2>(a, s);
         case 3: return launch_line_md<3>(a, s);
@@ -215,7 +354,7 @@ cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s) {
     }
 }
 
-// packed[b][step][e][t] = S[b][vperm]   (batched: S laid out system-major)
+// packed[b][e] = S[vperm[e] * ps + b * bs]
 __global__ void line_factor_pack_kernel(long long per, int B, int sb, long long ps, long long bs, const int *vperm,
                                         const double *S, double *packed) {
     const long long total = per * (sb ? B : 1);
@@ -229,7 +368,7 @@ __global__ void line_factor_pack_kernel(long long per, int B, int sb, long long 
 
 void launch_line_factor_pack(const LineDir &L, int B, int sb, long long ps, long long bs, const double *S,
                              double *packed, cudaStream_t s) {
-    const long long per = (long long)L.steps_pad * L.md * L.T;
+    const long long per = L.fac_slots;
     const long long total = per * (sb ? B : 1);
     note_launch();
     line_factor_pack_kernel<<<(int)std::min<long long>((total + 255) / 256, 16384), 256, 0, s>>>(
