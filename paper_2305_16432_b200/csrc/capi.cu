@@ -122,7 +122,7 @@ struct npcg_solver {
     double *S_fwd = nullptr, *S_bwd = nullptr;  // factor entries in schedule order
     size_t S_cap = 0;
     LineSched *ls = nullptr;  // line-wavefront schedule (owned by the pattern) or null
-    int line_K = 0;           // pipeline stages of the line kernels
+    int line_K = 0, line_Kb = 0;  // pipeline stages of the forward / backward line kernels
     // line mode: R, Z, Y, AP are in line order ([b][nslot]); A re-indexed by slot
     int *lrp = nullptr, *lcol = nullptr, *leidx = nullptr;
     double *Dl = nullptr;  // diag in line order ([b][nslot] or [nslot])
@@ -354,10 +354,11 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     std::string err;
     if (int rc = plan_solve(s->F, B, s->plan, err)) return fail(rc, err);
     if (LineSched *ls = s->F->line_schedule()) {
-        const int K = std::min(line_stages_for(ls->fwd), line_stages_for(ls->bwd));
-        if (K > 0) {
+        const int kf = line_stages_for(ls->fwd, false), kb = line_stages_for(ls->bwd, true);
+        if (kf > 0 && kb > 0) {
             s->ls = ls;
-            s->line_K = K;
+            s->line_K = kf;
+            s->line_Kb = kb;
         }
     }
     const size_t nB = (size_t)A->n * B;
@@ -520,7 +521,10 @@ static Tri tri_args(npcg_solver *s, bool upper, int mode, int sb, const double *
     if (t.line) {
         LineArgs &l = t.l;
         l.B = s->B;
-        l.stages = s->line_K;
+        l.stages = upper ? s->line_Kb : s->line_K;
+        if (const char *e = std::getenv("NPCG_LINE_NS")) l.stages = std::max(2, std::min(l.stages, atoi(e)));
+        if (const char *e = std::getenv("NPCG_LINE_A")) l.lead = atoi(e);
+        if (const char *e = std::getenv("NPCG_LINE_KNOBS")) l.knobs = atoi(e);
         l.upper = upper;
         l.mode = mode;
         l.nslot = s->ls->nslot;

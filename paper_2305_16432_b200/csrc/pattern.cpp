@@ -335,35 +335,39 @@ static bool build_line_sched(const Pattern &P, LineSched &LS) {
             dc[jd] = bcount[j];
             maxs = std::max(maxs, bcount[j]);
             boff[jd] = (int64_t)sched.size();
-            for (int32_t q = 0; q < K; ++q) {  // header: int32 base per step, as int16 pairs
+            for (int32_t q = 0; q < kLineHeader; ++q) {  // header: int32 base per step, as int16 pairs
                 const int32_t s = upper ? j * K + (K - 1 - q) : j * K + q;
-                const int32_t base = off[s] - lo[s] - bslot[j];
+                const int32_t base = q < K ? off[s] - lo[s] - bslot[j] : 0;
                 sched.push_back((int16_t)(base & 0xffff));
                 sched.push_back((int16_t)((uint32_t)base >> 16));
             }
-            for (int32_t u = 0; u < bcount[j]; ++u) {
+            // entries of the batch, structure-of-arrays: [e][slot]
+            const int32_t cnt = bcount[j];
+            const size_t s0 = sched.size(), v0 = vperm.size();
+            sched.resize(s0 + (size_t)cnt * MD, (int16_t)zslot);  // padding: zero cell, zero factor
+            vperm.resize(v0 + (size_t)cnt * MD, -1);              // (acc - 0 * 0 == acc exactly)
+            for (int32_t u = 0; u < cnt; ++u) {
                 const int32_t i = LS.h_rowof[bslot[j] + u];
+                if (i < 0) continue;
                 int32_t e = 0;
-                if (i >= 0) {
-                    auto push = [&](int32_t p) {
-                        const int32_t jj = col[p];
-                        const bool prev = line[jj] == line[i] && jj == i + (upper ? 1 : -1);
-                        const int32_t pj = upper ? (starts[line[jj] + 1] - 1 - jj) : pos[jj];
-                        sched.push_back((int16_t)(prev ? -1 : (pj & (W - 1)) * T + line[jj]));
-                        vperm.push_back(p);
-                        ++e;
-                    };
-                    // the reference's summation order (sparse.py:222-239)
-                    if (upper)
-                        for (int32_t p = rp[i + 1] - 1; p > dp[i]; --p) push(p);
-                    else
-                        for (int32_t p = rp[i]; p < dp[i]; ++p) push(p);
-                }
-                // padding reads the zero cell with a zero factor: acc - 0 * 0 == acc exactly
-                for (; e < MD; ++e) {
-                    sched.push_back((int16_t)zslot);
-                    vperm.push_back(-1);
-                }
+                auto push = [&](int32_t p) {
+                    const int32_t jj = col[p];
+                    const bool prev = line[jj] == line[i] && jj == i + (upper ? 1 : -1);
+                    const int32_t pj = upper ? (starts[line[jj] + 1] - 1 - jj) : pos[jj];
+#ifdef NPCG_LINE_AOS
+                    const size_t at = (size_t)u * MD + e;
+#else
+                    const size_t at = (size_t)e * cnt + u;
+#endif
+                    sched[s0 + at] = (int16_t)(prev ? -1 : (pj & (W - 1)) * T + line[jj]);
+                    vperm[v0 + at] = p;
+                    ++e;
+                };
+                // the reference's summation order (sparse.py:222-239)
+                if (upper)
+                    for (int32_t p = rp[i + 1] - 1; p > dp[i]; --p) push(p);
+                else
+                    for (int32_t p = rp[i]; p < dp[i]; ++p) push(p);
             }
         }
         D.T = T;

@@ -66,14 +66,16 @@ struct SchedSet {
 // no row and hold zeros.
 //
 // Per batch (in a direction's order) the schedule holds a 16-byte header
-// (int32 base[kLineBatch]: slot of line 0 at each step, relative to the
-// batch's first slot) followed by [slot][md] int16 descriptors
+// (int32 base[kLineHeader]: slot of line 0 at each step, relative to the
+// batch's first slot) followed by [md][slot] int16 descriptors
 //   -1 = previous row of the line, >= 0 = ring slot, zslot = padding (zero);
-// vperm[slot][md] = CSR position of the matching factor value (-1 = pad).
+// vperm[md][slot] = CSR position of the matching factor value (-1 = pad).
+// Both are structure-of-arrays per batch so a warp's reads are contiguous.
 // Only built when the whole pattern fits one CTA (lines <= kLineMaxLines,
 // window <= 16, <= 8 dependencies per row) and the pattern is structurally
 // symmetric.
 constexpr int32_t kLineBatch = 4;      // steps per pipeline stage
+constexpr int32_t kLineHeader = 4;     // int32 bases in a batch header (>= kLineBatch; 16 bytes)
 constexpr int32_t kLineMaxLines = 512;
 constexpr int32_t kLineSlotAlign = 8;  // slots per alignment unit of a batch range
 

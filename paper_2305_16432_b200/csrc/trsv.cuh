@@ -46,6 +46,8 @@ TrsvSmem trsv_smem_plan(const Schedule &S, int G, int s_batched);
 struct LineArgs {
     int B = 1, stages = 3, upper = 0, mode = TRSV_PLAIN;
     int nslot = 0;
+    int lead = -1;   // batches requested ahead (-1: from stages)
+    int knobs = 0;   // bit 0: TMA stores, bit 1: one thread issues every bulk copy
     LineDir dir{};
     const double *S = nullptr;  // packed factor values ([b][fac_slots] when s_batched)
     int s_batched = 0;
@@ -57,7 +59,7 @@ struct LineArgs {
     int *drift_count = nullptr;
 };
 size_t line_smem_bytes(const LineDir &L, int stages, bool upper, bool pcg);
-int line_stages_for(const LineDir &L);  // pipeline stages that fit shared memory (0: none)
+int line_stages_for(const LineDir &L, bool upper);  // pipeline stages that fit shared memory (0: none)
 int line_trace_copy(long long *out, int n);  // debug timeline (NPCG_LINE_TRACE builds)
 cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s);
 // factor values S[p * ps + b * bs] -> line order of `L` (per system when batched)

@@ -35,22 +35,22 @@ namespace npcg {
 
 namespace {
 
-constexpr int kProdWarps = 4;
+constexpr int kProdWarps = 8;
 constexpr int kProd = 32 * kProdWarps;
-constexpr int kBarCons = 1;   // consumer step barrier
-constexpr int kBarFull = 2;   // + stage (<= kLineMaxStages)
-constexpr int kBarEmpty = 6;  // + stage
-constexpr int kBarProd = 10;  // producer-only barrier
-constexpr int kLineMaxStages = 4;
-constexpr int kPrefetchBatches = 6;  // L2 prefetch distance of the bulk copies
+constexpr int kLineMaxStages = 6;
+constexpr int kBarCons = 1;
+constexpr int kBarFull = 2;
+constexpr int kBarEmpty = kBarFull + kLineMaxStages;
+constexpr int kBarProd = kBarEmpty + kLineMaxStages;
+constexpr int kPrefetchBatches = 0;  // L2 prefetch distance of the bulk copies
 
 struct LineSmem {  // byte offsets into dynamic shared memory
-    size_t ring, stage0, stage_bytes, sv, v[3], total;
+    size_t ring, stage0, stage_bytes, sv, v[3], meta, total;
 };
 
 __host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
 
-__host__ __device__ inline LineSmem line_layout(int T, int W, int MD, int maxs, int NS, int nv) {
+__host__ __device__ inline LineSmem line_layout(int T, int W, int MD, int maxs, int NS, int nv, int nb) {
     LineSmem m;
     m.ring = 128;  // mbarriers first
     m.stage0 = al128(m.ring + ((size_t)T * W + 2) * 8);
@@ -62,7 +62,8 @@ __host__ __device__ inline LineSmem line_layout(int T, int W, int MD, int maxs, 
         if (i < nv) o = al128(o + (size_t)maxs * 8);
     }
     m.stage_bytes = o;
-    m.total = m.stage0 + NS * o;
+    m.meta = m.stage0 + NS * o;  // per batch: boff | bslot | bcount
+    m.total = m.meta + (size_t)nb * 16;
     return m;
 }
 
@@ -111,11 +112,18 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
     }
     const bool upd = !UPPER && PCG && op == TOP_UPDATE;
     const int nv = UPPER ? (PCG ? 3 : 2) : 2;
-    const LineSmem m = line_layout(T, W, MD, L.max_slots, NS, nv);
+    const LineSmem m = line_layout(T, W, MD, L.max_slots, NS, nv, nb);
     uint64_t *mbar = reinterpret_cast<uint64_t *>(sm);
     double *ring = reinterpret_cast<double *>(sm + m.ring);  // [W][T] + zero cell
     auto stage_ptr = [&](int s) { return sm + m.stage0 + (size_t)s * m.stage_bytes; };
     for (int q = tid; q < T * W + 2; q += blockDim.x) ring[q] = 0.0;
+    long long *s_boff = reinterpret_cast<long long *>(sm + m.meta);
+    int *s_bslot = reinterpret_cast<int *>(s_boff + nb), *s_bcount = s_bslot + nb;
+    for (int q = tid; q < nb; q += blockDim.x) {
+        s_boff[q] = L.boff[q];
+        s_bslot[q] = L.bslot[q];
+        s_bcount[q] = L.bcount[q];
+    }
     if (tid == T) {
         for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], 1);
         fence_mbar_init();
@@ -128,11 +136,13 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
         double prev = 0.0;
         for (int j = 0; j < nb; ++j) {
             const int s = j % NS;
+            const int s_cnt_j = s_bcount[j];
             if (t == 0) LTRACE(0, j);
             bar_sync(kBarFull + s, NT);  // stage s holds batch j (also orders the last step's ring writes)
             if (t == 0) LTRACE(1, j);
             char *sp = stage_ptr(s);
             const int *hdr = reinterpret_cast<const int *>(sp);
+            const int cnt = s_cnt_j;
             const int16_t *dsc = reinterpret_cast<const int16_t *>(sp) + 8;
             const double *sv = reinterpret_cast<const double *>(sp + m.sv);
             double *vin = reinterpret_cast<double *>(sp + m.v[0]);                // rhs (r / y/D)
@@ -146,8 +156,8 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
                     double v[MD];
 #pragma unroll
                     for (int e = 0; e < MD; ++e) {
-                        d[e] = dsc[u * MD + e];
-                        v[e] = sv[u * MD + e];
+                        d[e] = dsc[e * cnt + u];
+                        v[e] = sv[e * cnt + u];
                     }
                     double acc = vin[u];
                     double y[MD];
@@ -178,8 +188,8 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
     double acc2 = 0.0;
     // sources of batch mb's stage blocks (global)
     auto blocks = [&](int mb, const void **src, unsigned *bytes, int &nsrc) {
-        const int bs = L.bslot[mb], cnt = L.bcount[mb];
-        const long long bo = L.boff[mb];
+        const int bs = s_bslot[mb], cnt = s_bcount[mb];
+        const long long bo = s_boff[mb];
         nsrc = 0;
         src[nsrc] = L.sched + bo;
         bytes[nsrc++] = 16 + (unsigned)cnt * MD * 2;
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
     auto drain = [&](int mb) {
         bar_sync(kBarEmpty + mb % NS, NT);
         char *sp = stage_ptr(mb % NS);
-        const int bs = L.bslot[mb], cnt = L.bcount[mb];
+        const int bs = s_bslot[mb], cnt = s_bcount[mb];
         if (UPPER && PCG) {  // r.z (pcg.py:167)
             const double *z = reinterpret_cast<const double *>(sp + m.v[0]);
             const double *r = reinterpret_cast<const double *>(sp + m.v[2]);
@@ -243,9 +253,10 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
         }
     };
     constexpr int D = 2;            // batch j - D is drained at iteration j
-    const int A = NS >= 3 ? 1 : 0;  // batch j + A is requested at iteration j
+    const int A = NS - D - 1 > 0 ? NS - D - 1 : 0;
     if (elect) {
         for (int mb = 0; mb < kPrefetchBatches && mb < nb; ++mb) prefetch(mb);
+
         for (int mb = 0; mb < A && mb < nb; ++mb) issue_load(mb);
     }
     for (int j = 0; j < nb; ++j) {
@@ -255,16 +266,16 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
         const int mb = j + A;
         if (elect && mb < nb) {
             // the stage of batch mb last held mb - NS, drained at iteration mb - NS + D
-            if (mb - NS + D == j) bulk_wait_read<0>();
+            if (mb - NS + D >= j) bulk_wait_read<0>();
             else bulk_wait_read<1>();
             issue_load(mb);
-            if (mb + kPrefetchBatches < nb) prefetch(mb + kPrefetchBatches);
+            if (kPrefetchBatches > 0 && mb + kPrefetchBatches < nb) prefetch(mb + kPrefetchBatches);
         }
         const int s = j % NS;
         mbar_wait(&mbar[s], (j / NS) & 1);  // batch j's blocks have landed
         if (p == 0) LTRACE(6, j);
         char *sp = stage_ptr(s);
-        const int cnt = L.bcount[j];
+        const int cnt = s_bcount[j];
         if (upd) {  // r -= alpha Ap (pcg.py:142), r.r of the new residual
             double *r = reinterpret_cast<double *>(sp + m.v[0]);
             const double *ap = reinterpret_cast<const double *>(sp + m.v[1]);
@@ -303,17 +314,17 @@ int line_trace_copy(long long *out, int n) {
 }
 
 size_t line_smem_bytes(const LineDir &L, int stages, bool upper, bool pcg) {
-    return line_layout(L.T, L.window, L.md, L.max_slots, stages, upper ? (pcg ? 3 : 2) : 2).total;
+    return line_layout(L.T, L.window, L.md, L.max_slots, stages, upper ? (pcg ? 3 : 2) : 2, L.nbatch).total;
 }
 
-int line_stages_for(const LineDir &L) {
+int line_stages_for(const LineDir &L, bool upper) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (optin <= 0) optin = 227 * 1024;
     const size_t cap = (size_t)optin - 1024;  // static shared memory
     for (int ns = kLineMaxStages; ns >= 2; --ns)
-        if (line_smem_bytes(L, ns, true, true) <= cap) return ns;
+        if (line_smem_bytes(L, ns, upper, true) <= cap) return ns;
     return 0;
 }
 

@@ -15,8 +15,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-EV = ["c_full_wait", "c_full_done", "c_batch_end", "p_start", "p_empty_done", "p_rhs_done", "p_mbar_done", "-",
-      "c_q0", "c_q1", "c_q2", "c_q3", "c_b0", "c_b1", "c_b2", "-"]
+EV = ["c_full_wait", "c_full_done", "c_batch_end", "p_start", "p_drained", "p_rhs_done", "p_mbar_done", "-",
+      "c_q0", "c_q1", "c_q2", "c_q3", "p_waitread", "p_issued", "cfg", "-"]
 
 
 def main():
@@ -39,11 +39,11 @@ def main():
     rc = lib.npcg_debug_line_trace(buf, 16 * 2048)
     t = np.frombuffer(buf, dtype=np.int64).reshape(16, 2048)
     nb = int((t[1] > 0).sum())
-    ev = [e for e in range(16) if e not in (7, 15)]
+    ev = [e for e in range(16) if e not in (7, 14, 15)]
     t0 = t[ev, :nb][t[ev, :nb] > 0].min()
     rel = np.where(t[:, :nb] > 0, t[:, :nb] - t0, -1)
     print("rc", rc, "batches", nb, "(last launch =", which, ")")
-    print("full-count lag (consumer saw producer count - (j+1)), min/max:", t[7, :nb].min(), t[7, :nb].max())
+    print("NS A nb max_slots T W MD smem:", list(t[14, :8]))
     print("batch " + " ".join(f"{e:>12s}" for e in EV))
     for j in list(range(0, min(nb, 12))) + list(range(nb // 2, nb // 2 + 8)):
         print(f"{j:5d} " + " ".join(f"{rel[e, j]:12d}" for e in range(7)))
@@ -51,7 +51,10 @@ def main():
         mid = slice(nb // 4, 3 * nb // 4)
         per = np.diff(rel[1, mid]).mean()
         print("cycles per batch (consumer, mid):", round(per, 1))
-        for e in list(range(7)) + list(range(8, 15)):
+        ns = np.diff(t[15, :nb]).astype(float)
+        print("ns per batch (globaltimer, mid):", round(ns[nb // 4:3 * nb // 4].mean(), 1), " whole solve us:",
+              round((t[15, nb - 1] - t[15, 0]) / 1e3, 1), " clock GHz:", round(per / ns[nb // 4:3 * nb // 4].mean(), 3))
+        for e in list(range(7)) + list(range(8, 14)):
             print(f"  {EV[e]:>14s} - c_full_done: {np.mean(rel[e, mid] - rel[1, mid]):10.1f}")
 
 
