@@ -28,6 +28,9 @@
 // (sparse.py:222-239), so results are bit-identical to pcgkit.
 #include <algorithm>
 
+#ifndef NPCG_NO_ZERO_Y
+#define NPCG_NO_ZERO_Y 0
+#endif
 #include "ptx.cuh"
 #include "trsv.cuh"
 
@@ -173,6 +176,7 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
                 if (q + 1 < K) bar_sync(kBarCons, T);  // step done: its values are visible to the next step
             }
             if (t == 0) LTRACE(2, j);
+            fence_proxy_async();            // solution writes -> the producers' TMA store (async proxy)
             bar_arrive(kBarEmpty + s, NT);  // batch j's solution is in stage s
         }
         return;
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
             for (int u = p; u < cnt; u += kProd) acc2 = __dadd_rn(acc2, __dmul_rn(r[u], z[u]));
         }
         if (elect) {
-            fence_proxy_async();  // consumer / producer smem writes -> bulk-copy reads
+            fence_proxy_async();  // (every writer fenced before the barriers above)
             if (!UPPER) {
                 if (upd) bulk_s2g(a.R + vb + bs, sp + m.v[0], cnt * 8);  // r_{k+1}
                 bulk_s2g(a.out + vb + bs, sp + m.v[1], cnt * 8);          // y
@@ -284,12 +288,16 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
                 r[u] = rn;
                 acc2 = __dadd_rn(acc2, __dmul_rn(rn, rn));
             }
-        } else if (UPPER) {  // z /= diag (sparse.py:273)
+        } else if (!UPPER && !NPCG_NO_ZERO_Y) {  // y is written into the (unloaded) second slice: padding slots must read 0
+            double2 *y = reinterpret_cast<double2 *>(sp + m.v[1]);
+            for (int u = p; u < cnt / 2; u += kProd) y[u] = make_double2(0.0, 0.0);
+        } else {  // z /= diag (sparse.py:273)
             double *y = reinterpret_cast<double *>(sp + m.v[0]);
             const double *dg = reinterpret_cast<const double *>(sp + m.v[1]);
             for (int u = p; u < cnt; u += kProd) y[u] = __ddiv_rn(y[u], dg[u]);
         }
         if (p == 0) LTRACE(5, j);
+        if (!UPPER) fence_proxy_async();  // r_{k+1} / zeroed y writes -> their TMA store
         bar_arrive(kBarFull + s, NT);
     }
     for (int mb = std::max(0, nb - D); mb < nb; ++mb) drain(mb);
