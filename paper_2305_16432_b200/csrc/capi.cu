@@ -728,12 +728,17 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         used.push_back(e);
         return c;
     };
+    // NPCG_PROFILE_DUMP=<file>: also append every launch's (class, ms) (diagnostics)
+    FILE *dump = nullptr;
+    if (prof)
+        if (const char *path = std::getenv("NPCG_PROFILE_DUMP")) dump = std::fopen(path, "a");
     auto harvest = [&]() {
         for (Ev &e : used) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, e.a, e.b);
             prof_ms[e.slot] += ms;
             prof_n[e.slot] += 1;
+            if (dump) std::fprintf(dump, "%d %.6f\n", e.slot, ms);
             pool.push_back(e);
         }
         used.clear();
@@ -768,6 +773,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
     }
+    if (dump) std::fclose(dump);
     rep->passes = passes;
     if (rep->kernel_ms)
         for (int q = 0; q < NPCG_PROF_SLOTS; ++q) rep->kernel_ms[q] = prof_ms[q];

@@ -1,14 +1,18 @@
-"""Sweep the triangular-solve schedule knobs on the config-2 workload and
-print the average launch time per kernel class (profiled PCG, 30 passes).
+"""Per-launch kernel times of the config-1 PCG loop (profiled, 30
+iterations): median over the launches that did work (the pass budget adds
+cheap all-skip launches at the end, which a plain mean would average in).
 
-    python tools/probe_trsv.py            # one subprocess per setting
+    python tools/probe_trsv.py one          # this process
+    python tools/probe_trsv.py '[{...}]'    # one subprocess per env setting
 """
 import json
 import os
 import subprocess
 import sys
+import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NAMES = ["spmv_apdot", "trsv_fwd", "spmv_drift", "trsv_bwd", "pupd", "other"]
 
 
 def one():
@@ -18,18 +22,28 @@ def one():
     from paper_2305_16432_b200 import gnn, inputs, pcg
     k = int(os.environ.get("PROBE_K", "256"))
     B = int(os.environ.get("PROBE_B", "64"))
+    its = int(os.environ.get("PROBE_ITERS", "30"))
     prob = inputs.poisson_2d(k=k, batch=B)
     A = prob.A
-    low = A.strict_lower()
     rng = np.random.default_rng(0)
-    P = gnn.assemble_preconditioner(rng.uniform(-0.2, 0.2, low.nnz), A)
+    P = gnn.assemble_preconditioner(rng.uniform(-0.2, 0.2, A.strict_lower().nnz), A)
     rhs = torch.from_numpy(prob.rhs).cuda()
-    opts = pcg.SolveOptions(thresholds=(1e-8,), max_iter=30)
-    pcg.pcg_solve_batch(A, rhs, P, opts, with_history=False)
+    opts = pcg.SolveOptions(thresholds=(1e-14,), max_iter=its)
+    pcg.pcg_solve_batch(A, rhs, P, opts, with_history=False)  # warm-up
+    with tempfile.NamedTemporaryFile(suffix=".txt", delete=False) as f:
+        path = f.name
+    os.environ["NPCG_PROFILE_DUMP"] = path
     pcg.pcg_solve_batch(A, rhs, P, opts, with_history=False, profile=True)
-    p = pcg.LAST_PROFILE
-    ms, nl = p["kernel_ms"], p["kernel_launches"]
-    print(json.dumps({k: round(ms[k] / max(nl[k], 1) * 1e3, 1) for k in ms if nl[k]}))
+    del os.environ["NPCG_PROFILE_DUMP"]
+    d = np.loadtxt(path, ndmin=2)
+    os.unlink(path)
+    out = {}
+    for slot, name in enumerate(NAMES):
+        t = d[d[:, 0] == slot, 1] * 1e3
+        if len(t):
+            t = t[t > 0.3 * t.max()]  # launches that did work
+            out[name] = round(float(np.median(t)), 1)
+    print(json.dumps(out))
 
 
 def sweep(settings):
@@ -39,11 +53,8 @@ def sweep(settings):
         print(s, (r.stdout.strip() or r.stderr.strip()[-400:]), flush=True)
 
 
-DEFAULT = [dict(NPCG_GROUP=str(g), NPCG_CHUNK_ROWS=str(r), NPCG_PREFETCH=str(pd), NPCG_SMEM_KB="200")
-           for g in (1,) for r in (65025, 32513, 16257, 8129) for pd in (4, 8)]
-
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         one()
     else:
-        sweep(json.loads(sys.argv[1]) if len(sys.argv) > 1 else DEFAULT)
+        sweep(json.loads(sys.argv[1]) if len(sys.argv) > 1 else [{}])

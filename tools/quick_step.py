@@ -18,7 +18,11 @@ rhs = torch.from_numpy(prob.rhs).cuda()
 opts = pcg.SolveOptions(thresholds=(bench.CFG["rtol"],), max_iter=int(os.environ.get("MAXIT", "3000")))
 for it in range(2):
     t0 = time.time()
-    P = gnn.build_learned(model, A, rhs[:, 0])
+    if os.environ.get("RANDOM_FACTOR"):
+        rng = np.random.default_rng(0)
+        P = gnn.assemble_preconditioner(rng.uniform(-0.2, 0.2, A.strict_lower().nnz), A)
+    else:
+        P = gnn.build_learned(model, A, rhs[:, 0])
     torch.cuda.synchronize()
     t1 = time.time()
     X, reps = pcg.pcg_solve_batch(A, rhs, P, opts, profile=True)
