@@ -123,8 +123,13 @@ struct npcg_solver {
     size_t S_cap = 0;
     LineSched *ls = nullptr;  // line-wavefront schedule (owned by the pattern) or null
     int line_K = 0, line_Kb = 0;  // pipeline stages of the forward / backward line kernels
-    // line mode: R, Z, Y, AP are in line order ([b][nslot]); A re-indexed by slot
-    int *lrp = nullptr, *lcol = nullptr, *leidx = nullptr;
+    // line mode: every loop vector is in line order ([b][nslot])
+    // all-line-order loop: P, XL (x), BL (b) too; A as ELL by slot
+    double *XL = nullptr, *BL = nullptr;
+    int ell_width = 0;
+    int *ecol = nullptr, *eperm = nullptr;  // [ell_width][nslot]: column slot / natural CSR position (-1: none)
+    double *evals = nullptr;                // packed A values ([b][ell_width][nslot] or [ell_width][nslot])
+    size_t evals_cap = 0, partial_cap = 0;
     double *Dl = nullptr;  // diag in line order ([b][nslot] or [nslot])
     size_t Dl_cap = 0;
     int *xpend = nullptr;
@@ -132,7 +137,7 @@ struct npcg_solver {
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
                         alpha, beta, rel, final_rel, history, active_count, drift_count, ctl, partial,
-                        S_fwd, S_bwd, xpend, lrp, lcol, leidx, Dl};
+                        S_fwd, S_bwd, xpend, Dl, XL, BL, ecol, eperm, evals};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_active) cudaFreeHost(h_active);
@@ -361,36 +366,39 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
             s->line_Kb = kb;
         }
     }
+    if (s->ls) {  // A as ELL by slot (the line-order loop); rows wider than 16 keep the level path
+        const LineSched &ls = *s->ls;
+        int width = 0;
+        for (int64_t i = 0; i < A->n; ++i) width = std::max<int>(width, A->h_rp[i + 1] - A->h_rp[i]);
+        s->ell_width = width <= 4 ? 4 : width <= 8 ? 8 : width <= 12 ? 12 : width <= 16 ? 16 : 0;
+        if (!s->ell_width) s->ls = nullptr;
+    }
     const size_t nB = (size_t)A->n * B;
     const size_t vB = s->ls ? (size_t)s->ls->nslot * B : nB;  // line-order vectors
     NPCG_CUDA(dalloc(&s->R, vB));
-    NPCG_CUDA(dalloc(&s->P, nB));
+    NPCG_CUDA(dalloc(&s->P, vB));
     NPCG_CUDA(dalloc(&s->Z, vB));
     NPCG_CUDA(dalloc(&s->AP, vB));
     NPCG_CUDA(dalloc(&s->Y, vB));
-    if (s->ls) {  // padding slots stay zero; A's rows re-indexed by slot for the SpMV
-        for (double *v : {s->R, s->Z, s->AP, s->Y}) NPCG_CUDA(cudaMemset(v, 0, vB * 8));
+    if (s->ls) {  // padding slots stay zero; A as ELL by slot for the SpMV
+        NPCG_CUDA(dalloc(&s->XL, vB));
+        NPCG_CUDA(dalloc(&s->BL, vB));
+        for (double *v : {s->R, s->Z, s->AP, s->Y, s->P, s->XL, s->BL}) NPCG_CUDA(cudaMemset(v, 0, vB * 8));
         const LineSched &ls = *s->ls;
-        std::vector<int> lrp(ls.nslot + 1, 0), lcol, leidx;
-        lcol.reserve(A->nnz);
-        leidx.reserve(A->nnz);
+        const int E = s->ell_width;
+        std::vector<int> ecol((size_t)E * ls.nslot, -1), eperm((size_t)E * ls.nslot, -1);
         for (int q = 0; q < ls.nslot; ++q) {
             const int i = ls.h_rowof[q];
-            if (i >= 0)
-                for (int p = A->h_rp[i]; p < A->h_rp[i + 1]; ++p) {
-                    lcol.push_back(A->h_col[p]);
-                    leidx.push_back(p);
-                }
-            lrp[q + 1] = (int)lcol.size();
+            if (i < 0) continue;
+            for (int p = A->h_rp[i], e = 0; p < A->h_rp[i + 1]; ++p, ++e) {  // the reference's row order
+                ecol[(size_t)e * ls.nslot + q] = ls.h_slot[A->h_col[p]];
+                eperm[(size_t)e * ls.nslot + q] = p;
+            }
         }
-        NPCG_CUDA(dalloc(&s->lrp, lrp.size()));
-        NPCG_CUDA(dalloc(&s->lcol, std::max<size_t>(lcol.size(), 1)));
-        NPCG_CUDA(dalloc(&s->leidx, std::max<size_t>(leidx.size(), 1)));
-        NPCG_CUDA(cudaMemcpy(s->lrp, lrp.data(), lrp.size() * 4, cudaMemcpyHostToDevice));
-        if (!lcol.empty()) {
-            NPCG_CUDA(cudaMemcpy(s->lcol, lcol.data(), lcol.size() * 4, cudaMemcpyHostToDevice));
-            NPCG_CUDA(cudaMemcpy(s->leidx, leidx.data(), leidx.size() * 4, cudaMemcpyHostToDevice));
-        }
+        NPCG_CUDA(dalloc(&s->ecol, ecol.size()));
+        NPCG_CUDA(dalloc(&s->eperm, eperm.size()));
+        NPCG_CUDA(cudaMemcpy(s->ecol, ecol.data(), ecol.size() * 4, cudaMemcpyHostToDevice));
+        NPCG_CUDA(cudaMemcpy(s->eperm, eperm.data(), eperm.size() * 4, cudaMemcpyHostToDevice));
     }
     NPCG_CUDA(dalloc(&s->status, B));
     NPCG_CUDA(dalloc(&s->xpend, B));
@@ -414,7 +422,9 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     NPCG_CUDA(dalloc(&s->ctl, 1));
     NPCG_CUDA(cudaMemset(s->ctl, 0, sizeof(Ctl)));
     NPCG_CUDA(cudaMemset(s->drift_count, 0, 4));
-    const size_t part = std::max<size_t>((size_t)kReduceBlocksPerSm * num_sms() * B, units * s->plan.G);
+    size_t part = std::max<size_t>((size_t)kReduceBlocksPerSm * num_sms() * B, units * s->plan.G);
+    if (s->ls) part = std::max<size_t>(part, (size_t)((s->ls->nslot + kSpmvThreads - 1) / kSpmvThreads) * B);
+    s->partial_cap = part;
     NPCG_CUDA(dalloc(&s->partial, part));
     NPCG_CUDA(cudaMallocHost((void **)&s->h_active, sizeof(int)));
     if (!s->ls) {  // level-kernel outputs start unsolved (sentinel), see trsv.cu
@@ -662,20 +672,36 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     sp.partial = s->partial;
     sp.ctl = s->ctl;
     sp.drift_count = s->drift_count;
-    SpmvArgs spl = sp;  // PCG ops: outputs in line order
+    SpmvArgs spl = sp;  // PCG ops: every vector in line order
+    double *xv = x;            // the iterate the loop updates
+    const double *bv = bvec;
     if (s->ls) {
-        spl.n = s->ls->nslot;
-        spl.nslot = s->ls->nslot;
-        spl.rp = s->lrp;
-        spl.col = s->lcol;
-        spl.eidx = s->leidx;
-        spl.rowof = s->ls->rowof;
+        const int ns = s->ls->nslot, E = s->ell_width;
+        spl.n = ns;
+        spl.nslot = ns;
+        spl.ecol = s->ecol;
+        spl.ell_width = E;
+        spl.partial_cap = s->partial_cap;
+        const size_t need = (size_t)E * ns * (ab ? B : 1);
+        if (need > s->evals_cap) {
+            if (s->evals) cudaFree(s->evals);
+            s->evals = nullptr;
+            s->evals_cap = 0;
+            NPCG_CUDA(dalloc(&s->evals, need));
+            s->evals_cap = need;
+        }
+        launch_gather_pack((long long)E * ns, B, ab, ab ? B : 1, 1, s->eperm, A_vals, s->evals, st);
+        spl.evals = s->evals;
+        NPCG_CUDA(launch_to_line(ns, B, s->ls->rowof, x, 1, 0.0, s->XL, st));
+        NPCG_CUDA(launch_to_line(ns, B, s->ls->rowof, bvec, 1, 0.0, s->BL, st));
+        xv = s->XL;
+        bv = s->BL;
     }
     // r = b - A x0 (or b)
     SpmvArgs init = spl;
     init.op = SPMV_RESID_INIT;
-    init.X = x;
-    init.Bv = bvec;
+    init.X = xv;
+    init.Bv = bv;
     init.R = s->R;
     init.has_x = x0 != nullptr;
     NPCG_CUDA(launch_spmv(init, st));
@@ -686,8 +712,8 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     apdot.Y = s->AP;
     SpmvArgs drift = spl;
     drift.op = SPMV_RESID_DRIFT;
-    drift.X = x;
-    drift.Bv = bvec;
+    drift.X = xv;
+    drift.Bv = bv;
     drift.R = s->R;
     drift.P = s->P;
     // identity: S = ones is never referenced (no off-diagonal slots), packs to zeros
@@ -744,7 +770,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         used.clear();
     };
     auto pupd = [&]() {
-        if (s->ls) return launch_pupd_line(s->ls->nslot, B, s->ls->rowof, s->Z, s->P, x, sst, st);
+        if (s->ls) return launch_pupd_ell(s->ls->nslot, B, s->Z, s->P, s->XL, sst, st);
         note_launch();
         pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, x, sst, 1);
         return cudaGetLastError();
@@ -787,12 +813,13 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     for (int b = 0; b < B; ++b) any_max |= status[b] == ST_MAXITER || status[b] == ST_ACTIVE;
     if (any_max) {
         // columns still ACTIVE after the pass budget count as max-iter
-        SpmvArgs fin = sp;
+        SpmvArgs fin = spl;
         fin.op = SPMV_RESID_FINAL;
-        fin.X = x;
-        fin.Bv = bvec;
+        fin.X = xv;
+        fin.Bv = bv;
         NPCG_CUDA(launch_spmv(fin, st));
     }
+    if (s->ls) NPCG_CUDA(launch_from_line(s->ls->nslot, B, s->ls->rowof, s->XL, x, st));
     std::vector<long long> kk(B), itto((size_t)B * T), bdv(B);
     std::vector<unsigned long long> tto((size_t)B * T);
     unsigned long long t0 = 0;

@@ -181,19 +181,24 @@ __device__ __forceinline__ void spmv_group(const SpmvArgs &a, const int *jj, con
 
 // Block reduction per column (fixed order over teams), then a grid reduction
 // in fixed block order by the last block to finish, which runs the control
-// epilogue. `red` holds [teams][B] partials.
-__device__ __forceinline__ void spmv_reduce_tail(const SpmvArgs &a, double *red, int teams) {
+// epilogue. `red` holds [teams][ldr] partials of columns [b_lo, b_hi) (a
+// 2-D grid splits the columns over blockIdx.y; rows of `partial` are
+// blockIdx.x).
+__device__ __forceinline__ void spmv_reduce_tail(const SpmvArgs &a, double *red, int teams, int b_lo = 0,
+                                                 int b_hi = -1, int ldr = -1) {
     __shared__ int s_last;
     const int B = a.B;
+    if (b_hi < 0) b_hi = B;
+    if (ldr < 0) ldr = B;
     __syncthreads();
-    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    for (int b = b_lo + threadIdx.x; b < b_hi; b += blockDim.x) {
         double s = 0.0;
-        for (int t = 0; t < teams; ++t) s = __dadd_rn(s, red[t * B + b]);
+        for (int t = 0; t < teams; ++t) s = __dadd_rn(s, red[t * ldr + b - b_lo]);
         a.partial[(size_t)blockIdx.x * B + b] = s;
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&a.ctl->done, 1) == (int)gridDim.x - 1;
+    if (threadIdx.x == 0) s_last = atomicAdd(&a.ctl->done, 1) == (int)(gridDim.x * gridDim.y) - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -205,7 +210,15 @@ __device__ __forceinline__ void spmv_reduce_tail(const SpmvArgs &a, double *red,
         double s = 0.0;
         if (b < B) {
             const int lo = (int)((long long)G * sub / per), hi = (int)((long long)G * (sub + 1) / per);
-            for (int blk = lo; blk < hi; ++blk) s = __dadd_rn(s, __ldcg(&a.partial[(size_t)blk * B + b]));
+            int blk = lo;
+            for (; blk + 8 <= hi; blk += 8) {  // 8 loads in flight, summed in block order
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldcg(&a.partial[(size_t)(blk + u) * B + b]);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+            }
+            for (; blk < hi; ++blk) s = __dadd_rn(s, __ldcg(&a.partial[(size_t)blk * B + b]));
         }
         scratch[threadIdx.x] = s;
         __syncthreads();
@@ -502,140 +515,6 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_warp_kernel(SpmvArgs a) 
     spmv_reduce_tail(a, red, TEAMS);
 }
 
-// SpMV into line order (trsv_line.cu): rows are the slots of the factor's
-// line layout (A's CSR re-indexed by slot, padding slots empty; entries keep
-// their order, so every row sum is bitwise the natural one), X and the own
-// operand stay natural RHS-minor, and the output goes to Y[b][slot]
-// (system-major) through a per-warp [16 slots][64 columns] shared tile, so
-// each system's slots leave as 128-byte runs.
-constexpr int kLineTile = 16;
-
-template <int VW, bool VB, int OP>
-__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_line_kernel(SpmvArgs a) {
-    constexpr int TEAMS = kSpmvThreads / 32, CH = 8, TC = 32 * VW;  // tile columns
-    using V = typename VecT<VW>::type;
-    extern __shared__ double red[];  // TEAMS * B partials | TEAMS tiles [kLineTile][TC]
-    __shared__ unsigned char s_act[kMaxBatch];
-    const int team = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int B = a.B;
-    if (OP == SPMV_RESID_DRIFT && *a.drift_count == 0) return;
-    for (int b = threadIdx.x; b < B; b += blockDim.x) s_act[b] = spmv_col_active(a, b) ? 1 : 0;
-    double *part = red + team * B;
-    double *tile = red + TEAMS * B + team * kLineTile * TC;
-    for (int b = lane; b < B; b += 32) part[b] = 0.0;
-    __syncthreads();
-    const int cpl = (B + TC - 1) / TC;
-    const int nteams = gridDim.x * TEAMS, gteam = blockIdx.x * TEAMS + team;
-    const int per = ((a.n + nteams - 1) / nteams + kLineTile - 1) / kLineTile * kLineTile;
-    const int r0 = min(a.n, gteam * per), r1 = min(a.n, r0 + per);
-    const bool use_x = OP != SPMV_RESID_INIT || a.has_x;
-    double *out = OP == SPMV_APDOT ? a.Y : a.R;
-    const long long ns = a.nslot;
-    for (int k = 0; k < cpl && r0 < r1; ++k) {
-        const int b = (lane + k * 32) * VW;
-        const bool on = b < B;
-        const unsigned bb = on ? b : 0;
-        bool xp[VW];
-        double al[VW];
-#pragma unroll
-        for (int v = 0; v < VW; ++v) {
-            xp[v] = OP == SPMV_RESID_DRIFT && a.st.xpend[bb + v];
-            al[v] = xp[v] ? a.st.alpha[bb + v] : 0.0;
-        }
-        int wb = r0, rpl = a.rp[min(r0 + lane, a.n)];
-        int p0 = __shfl_sync(0xffffffffu, rpl, 0), p1 = __shfl_sync(0xffffffffu, rpl, 1);
-        int cj = lane < p1 - p0 ? a.col[p0 + lane] : 0;
-        int ce = lane < p1 - p0 ? a.eidx[p0 + lane] : 0;
-        for (int row = r0; row < r1; ++row) {
-            const int nat = a.rowof[row];
-            const unsigned ri = (unsigned)max(nat, 0) * B + bb;
-            double own[VW];
-#pragma unroll
-            for (int v = 0; v < VW; ++v) own[v] = 0.0;
-            if (nat >= 0) {
-                if (OP == SPMV_APDOT) VecT<VW>::get(*reinterpret_cast<const V *>(a.X + ri), own);
-                else VecT<VW>::get(*reinterpret_cast<const V *>(a.Bv + ri), own);
-            }
-            int w = row + 2 - wb;
-            if (w >= 32) {
-                wb = row;
-                rpl = a.rp[min(wb + lane, a.n)];
-                w = 2;
-            }
-            const int q1 = __shfl_sync(0xffffffffu, rpl, w);
-            const int cnt = p1 - p0, c0 = p0;
-            const int ccj = cj, cce = ce;
-            if (row + 1 < r1) {
-                cj = lane < q1 - p1 ? a.col[p1 + lane] : 0;
-                ce = lane < q1 - p1 ? a.eidx[p1 + lane] : 0;
-            }
-            p0 = p1;
-            p1 = q1;
-            double acc[VW];
-#pragma unroll
-            for (int v = 0; v < VW; ++v) acc[v] = 0.0;
-            if (use_x) {
-                for (int g = 0; g < cnt; g += CH) {
-                    int hj = ccj, he = cce;
-                    if (g >= 32 && (g & 31) == 0) {
-                        hj = lane < cnt - g ? a.col[c0 + g + lane] : 0;
-                        he = lane < cnt - g ? a.eidx[c0 + g + lane] : 0;
-                    }
-                    double xv[CH][VW], vv[VB ? CH : 1][VW], vs[CH];
-#pragma unroll
-                    for (int c = 0; c < CH; ++c) {
-                        const int j = __shfl_sync(0xffffffffu, hj, (g + c) & 31);
-                        const int e = __shfl_sync(0xffffffffu, he, (g + c) & 31);
-                        const unsigned jo = (unsigned)j * B + bb;
-                        VecT<VW>::get(*reinterpret_cast<const V *>(a.X + jo), xv[c]);
-                        if (VB) VecT<VW>::get(*reinterpret_cast<const V *>(a.vals + (size_t)e * B + bb), vv[c]);
-                        else vs[c] = a.vals[e];
-                        if (OP == SPMV_RESID_DRIFT) {  // x_{k+1} = x + alpha p not yet stored (pcg.py:141)
-                            double pv[VW];
-                            VecT<VW>::get(*reinterpret_cast<const V *>(a.P + jo), pv);
-#pragma unroll
-                            for (int v = 0; v < VW; ++v)
-                                if (xp[v]) xv[c][v] = __dadd_rn(xv[c][v], __dmul_rn(al[v], pv[v]));
-                        }
-                    }
-#pragma unroll
-                    for (int c = 0; c < CH; ++c) {
-                        const bool use = g + c < cnt;
-#pragma unroll
-                        for (int v = 0; v < VW; ++v) {
-                            const double s = __dadd_rn(acc[v], __dmul_rn(VB ? vv[VB ? c : 0][v] : vs[c], xv[c][v]));
-                            acc[v] = use ? s : acc[v];
-                        }
-                    }
-                }
-            }
-            const int ti = (row - r0) % kLineTile;
-#pragma unroll
-            for (int v = 0; v < VW; ++v) {
-                double o = acc[v];
-                if (OP != SPMV_APDOT) o = __dsub_rn(own[v], acc[v]);  // r = b - A x
-                if (on && s_act[b + v] && nat >= 0) {
-                    const double pr = OP == SPMV_APDOT ? __dmul_rn(own[v], acc[v]) : __dmul_rn(o, o);
-                    part[b + v] = __dadd_rn(part[b + v], pr);
-                }
-                tile[ti * TC + lane * VW + v] = nat >= 0 ? o : 0.0;
-            }
-            if (ti == kLineTile - 1 || row == r1 - 1) {  // flush: each column's slots as one run
-                __syncwarp();
-                const int q0 = row - ti, cntq = ti + 1;
-                for (int e = lane; e < kLineTile * TC; e += 32) {
-                    const int c = e / kLineTile, i = e % kLineTile, bc = k * TC + c;
-                    if (i < cntq && bc < B && s_act[bc] && OP != SPMV_RESID_FINAL)
-                        out[(long long)bc * ns + q0 + i] = tile[i * TC + c];
-                }
-                __syncwarp();
-            }
-        }
-    }
-    if (OP == SPMV_PLAIN) return;
-    spmv_reduce_tail(a, red, TEAMS);
-}
-
 // ===========================================================================
 // Elementwise / setup kernels
 // ===========================================================================
@@ -731,47 +610,11 @@ __global__ void pupd_kernel(long long nB, int B, double *z, double *p, double *x
     }
 }
 
-// Line-order variants: a block moves a tile of kLineTile slots x all columns
-// through shared memory, so the system-major line-order side ([b][slot])
-// and the natural RHS-minor side ([row][b]) are both read / written in
-// contiguous runs.
+// Natural <-> line order: a block moves a tile of kPermTile slots x all
+// columns through shared memory, so the system-major line-order side
+// ([b][slot]) and the natural RHS-minor side ([row][b]) are both read /
+// written in contiguous runs.
 constexpr int kPermTile = 16;
-
-// p = z + beta p | p = z ; x += alpha p   with z in line order (pcg.py:129, 141, 170)
-__global__ void __launch_bounds__(256) pupd_line_kernel(int nslot, int B, const int *rowof, const double *z,
-                                                         double *p, double *x, SolveState st) {
-    extern __shared__ double tz[];  // [kPermTile][B + 1]
-    __shared__ int s_f[kMaxBatch];
-    __shared__ double s_al[kMaxBatch], s_be[kMaxBatch];
-    const int ld = B + 1;
-    for (int b = threadIdx.x; b < B; b += blockDim.x) {
-        s_f[b] = st.pflag[b];
-        s_al[b] = st.alpha[b];
-        s_be[b] = st.beta[b];
-    }
-    for (int q0 = blockIdx.x * kPermTile; q0 < nslot; q0 += gridDim.x * kPermTile) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < kPermTile * B; e += blockDim.x) {
-            const int b = e / kPermTile, i = e % kPermTile;
-            if (q0 + i < nslot) tz[i * ld + b] = z[(long long)b * nslot + q0 + i];
-        }
-        __syncthreads();
-        for (int e = threadIdx.x; e < kPermTile * B; e += blockDim.x) {
-            const int i = e / B, b = e % B;
-            if (q0 + i >= nslot) continue;
-            const int row = rowof[q0 + i];
-            const int f = s_f[b];
-            if (row < 0 || f == PF_NONE) continue;
-            const long long q = (long long)row * B + b;
-            const double pq = p[q];
-            if (f & PF_X) x[q] = __dadd_rn(x[q], __dmul_rn(s_al[b], pq));
-            if (f & (PF_UPDATE | PF_COPY)) {
-                const double zq = tz[i * ld + b];
-                p[q] = (f & PF_UPDATE) ? __dadd_rn(zq, __dmul_rn(s_be[b], pq)) : zq;
-            }
-        }
-    }
-}
 
 // dst[b][slot] = src[row(slot)][b] (natural RHS-minor, or shared [row] when
 // src_batched == 0); padding slots get `pad`.
@@ -814,14 +657,6 @@ __global__ void __launch_bounds__(256) from_line_kernel(int nslot, int B, const 
             if (row >= 0) dst[(long long)row * B + b] = tt[i * ld + b];
         }
     }
-}
-
-cudaError_t launch_pupd_line(int nslot, int B, const int *rowof, const double *z, double *p, double *x,
-                             const SolveState &st, cudaStream_t s) {
-    const int grid = std::min((nslot + kPermTile - 1) / kPermTile, 8 * num_sms());
-    note_launch();
-    pupd_line_kernel<<<grid, 256, (size_t)kPermTile * (B + 1) * 8, s>>>(nslot, B, rowof, z, p, x, st);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_to_line(int nslot, int B, const int *rowof, const double *src, int src_batched, double pad,
@@ -955,42 +790,194 @@ static void spmv_warp_vw(const SpmvArgs &a, int grid, size_t smem, cudaStream_t 
     else spmv_warp_op<VW, false>(a, grid, smem, s);
 }
 
-template <int VW, bool VB, int OP>
-static void spmv_line_t(const SpmvArgs &a, int grid, size_t smem, cudaStream_t s) {
-    auto kern = spmv_line_kernel<VW, VB, OP>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    note_launch();
-    kern<<<grid, kSpmvThreads, smem, s>>>(a);
+// ===========================================================================
+// Line-order SpMV (every operand [b][nslot], pattern.h LineSched): A in
+// ELL form by slot -- ecol[e][slot] = slot of the e-th entry's column in
+// the reference's row order (-1 past the row's end), evals[(b)][e][slot]
+// its value. One thread owns one slot and keeps its row in registers; a
+// block walks every system over its 256 slots, so matrix data is read once
+// per block and every vector access of a warp is one contiguous 256-byte
+// run (the row's own slot) or a gather within +-2 grid lines of it (L1).
+// ===========================================================================
+constexpr int kEllCols = 32;  // systems per block (blockIdx.y picks the group)
+
+template <int E, bool VB, int OP>
+__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_ell_kernel(SpmvArgs a) {
+    constexpr int TEAMS = kSpmvThreads / 32;
+    __shared__ double red[TEAMS * kSpmvThreads];  // reused by the tail's final pass
+    __shared__ unsigned char s_act[kMaxBatch];
+    __shared__ unsigned char s_xp[kMaxBatch];
+    __shared__ double s_al[kMaxBatch];
+    const int B = a.B, ns = a.nslot, lane = threadIdx.x & 31, team = threadIdx.x >> 5;
+    const int bl = blockIdx.y * kEllCols, bh = min(B, bl + kEllCols);  // this block's columns
+    if (OP == SPMV_RESID_DRIFT && *a.drift_count == 0) return;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        s_act[b] = spmv_col_active(a, b) ? 1 : 0;
+        s_xp[b] = OP == SPMV_RESID_DRIFT && a.st.xpend[b];
+        s_al[b] = s_xp[b] ? a.st.alpha[b] : 0.0;
+    }
+    __syncthreads();
+    const int q = blockIdx.x * kSpmvThreads + threadIdx.x;
+    const bool live = q < ns;
+    const int qq = live ? q : 0;
+    // row entries past the row's end point at the row's own slot with a zero
+    // value: acc + 0 * x leaves the sum unchanged (acc starts at +0 and can
+    // never become -0), so the loop needs no predicate
+    unsigned cb[E];  // byte offsets of the column slots
+    double v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int c = live ? a.ecol[(size_t)e * ns + q] : -1;
+        cb[e] = (unsigned)(c >= 0 ? c : (live ? q : 0)) * 8u;
+        v[e] = (!VB && c >= 0) ? a.evals[(size_t)e * ns + q] : 0.0;
+    }
+    const bool use_x = OP != SPMV_RESID_INIT || a.has_x;
+    // NB systems at a time: their gathers are in flight together and their
+    // dot-product trees interleave
+    constexpr int NB = 4;
+    for (int b0 = bl; b0 < bh; b0 += NB) {
+        // every load of the NB systems first (no branch between them), then the sums
+        double xv[NB][E], own[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int b = min(b0 + u, bh - 1);
+            const size_t vb = (size_t)b * ns;
+            const char *Xb = reinterpret_cast<const char *>(a.X + vb);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                xv[u][e] = use_x ? *reinterpret_cast<const double *>(Xb + cb[e]) : 0.0;
+                if (OP == SPMV_RESID_DRIFT && s_xp[b])  // x_{k+1} = x + alpha p not yet stored (pcg.py:141)
+                    xv[u][e] = __dadd_rn(xv[u][e], __dmul_rn(s_al[b], *reinterpret_cast<const double *>(
+                                                                       reinterpret_cast<const char *>(a.P + vb) + cb[e])));
+            }
+            own[u] = OP == SPMV_APDOT ? a.X[vb + qq] : a.Bv[vb + qq];
+        }
+        double pr[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int b = b0 + u;
+            const bool on = b < bh && s_act[b] && live;
+            const size_t vb = (size_t)min(b, bh - 1) * ns;
+            double acc = 0.0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {  // sparse.py:213-219
+                const double vv = VB ? a.evals[((size_t)min(b, bh - 1) * E + e) * ns + qq] : v[e];
+                acc = __dadd_rn(acc, __dmul_rn(vv, xv[u][e]));
+            }
+            pr[u] = 0.0;
+            if (OP == SPMV_APDOT) {
+                if (on) a.Y[vb + q] = acc;
+                pr[u] = on ? __dmul_rn(own[u], acc) : 0.0;  // p.Ap (pcg.py:134)
+            } else {
+                const double r = __dsub_rn(own[u], acc);  // r = b - A x
+                if (on && OP != SPMV_RESID_FINAL) a.R[vb + q] = r;
+                pr[u] = on ? __dmul_rn(r, r) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int u = 0; u < NB; ++u) pr[u] = __dadd_rn(pr[u], __shfl_down_sync(0xffffffffu, pr[u], off));
+        if (lane == 0)
+#pragma unroll
+            for (int u = 0; u < NB; ++u)
+                if (b0 + u < bh) red[team * kEllCols + b0 + u - bl] = pr[u];
+    }
+    spmv_reduce_tail(a, red, TEAMS, bl, bh, kEllCols);
 }
 
-template <int VW, bool VB>
-static void spmv_line_op(const SpmvArgs &a, int grid, size_t smem, cudaStream_t s) {
+template <int E, bool VB>
+static void spmv_ell_op(const SpmvArgs &a, dim3 grid, cudaStream_t s) {
+    note_launch();
     switch (a.op) {
-        case SPMV_APDOT: return spmv_line_t<VW, VB, SPMV_APDOT>(a, grid, smem, s);
-        case SPMV_RESID_INIT: return spmv_line_t<VW, VB, SPMV_RESID_INIT>(a, grid, smem, s);
-        case SPMV_RESID_DRIFT: return spmv_line_t<VW, VB, SPMV_RESID_DRIFT>(a, grid, smem, s);
-        default: return spmv_line_t<VW, VB, SPMV_RESID_FINAL>(a, grid, smem, s);
+        case SPMV_APDOT: spmv_ell_kernel<E, VB, SPMV_APDOT><<<grid, kSpmvThreads, 0, s>>>(a); break;
+        case SPMV_RESID_INIT: spmv_ell_kernel<E, VB, SPMV_RESID_INIT><<<grid, kSpmvThreads, 0, s>>>(a); break;
+        case SPMV_RESID_DRIFT: spmv_ell_kernel<E, VB, SPMV_RESID_DRIFT><<<grid, kSpmvThreads, 0, s>>>(a); break;
+        default: spmv_ell_kernel<E, VB, SPMV_RESID_FINAL><<<grid, kSpmvThreads, 0, s>>>(a); break;
     }
+}
+
+template <int E>
+static void spmv_ell_e(const SpmvArgs &a, dim3 grid, cudaStream_t s) {
+    if (a.vb) spmv_ell_op<E, true>(a, grid, s);
+    else spmv_ell_op<E, false>(a, grid, s);
+}
+
+static cudaError_t launch_spmv_ell(const SpmvArgs &a, cudaStream_t s) {
+    if (a.op == SPMV_PLAIN || a.nslot <= 0) return cudaErrorInvalidValue;
+    const dim3 grid((a.nslot + kSpmvThreads - 1) / kSpmvThreads, (a.B + kEllCols - 1) / kEllCols);
+    if ((size_t)grid.x * a.B > a.partial_cap) return cudaErrorInvalidValue;
+    switch (a.ell_width) {
+        case 4: spmv_ell_e<4>(a, grid, s); break;
+        case 8: spmv_ell_e<8>(a, grid, s); break;
+        case 12: spmv_ell_e<12>(a, grid, s); break;
+        case 16: spmv_ell_e<16>(a, grid, s); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+// p = z + beta p | p = z ; x += alpha p, every vector in line order (pcg.py:129, 141, 170)
+__global__ void __launch_bounds__(256) pupd_ell_kernel(int nslot, const double *z, double *p, double *x,
+                                                        SolveState st) {
+    const int b = blockIdx.y, f = st.pflag[b];
+    if (f == PF_NONE) return;
+    const double al = st.alpha[b], be = st.beta[b];
+    const size_t vb = (size_t)b * nslot;
+    const double2 *z2 = reinterpret_cast<const double2 *>(z + vb);
+    double2 *p2 = reinterpret_cast<double2 *>(p + vb), *x2 = reinterpret_cast<double2 *>(x + vb);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nslot / 2; i += gridDim.x * blockDim.x) {
+        double2 pq = p2[i];
+        if (f & PF_X) {
+            double2 xq = x2[i];
+            xq.x = __dadd_rn(xq.x, __dmul_rn(al, pq.x));
+            xq.y = __dadd_rn(xq.y, __dmul_rn(al, pq.y));
+            x2[i] = xq;
+        }
+        if (f & (PF_UPDATE | PF_COPY)) {
+            const double2 zq = z2[i];
+            if (f & PF_UPDATE) {
+                pq.x = __dadd_rn(zq.x, __dmul_rn(be, pq.x));
+                pq.y = __dadd_rn(zq.y, __dmul_rn(be, pq.y));
+            } else {
+                pq = zq;
+            }
+            p2[i] = pq;
+        }
+    }
+}
+
+cudaError_t launch_pupd_ell(int nslot, int B, const double *z, double *p, double *x, const SolveState &st,
+                            cudaStream_t s) {
+    const int per = (nslot / 2 + 255) / 256;
+    const int gx = std::max(1, std::min(per, (4 * num_sms() + B - 1) / B));
+    note_launch();
+    pupd_ell_kernel<<<dim3(gx, B), 256, 0, s>>>(nslot, z, p, x, st);
+    return cudaGetLastError();
+}
+
+// packed[b][e] = S[perm[e] * ps + b * bs]  (0 where perm < 0)
+__global__ void gather_pack_kernel(long long per, int B, int sb, long long ps, long long bs, const int *perm,
+                                   const double *S, double *packed) {
+    const long long total = per * (sb ? B : 1);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long b = q / per, e = q % per;
+        const int p = perm[e];
+        packed[q] = p < 0 ? 0.0 : S[(long long)p * ps + b * bs];
+    }
+}
+
+void launch_gather_pack(long long per, int B, int sb, long long ps, long long bs, const int *perm, const double *S,
+                        double *packed, cudaStream_t s) {
+    const long long total = per * (sb ? B : 1);
+    note_launch();
+    gather_pack_kernel<<<(int)std::min<long long>((total + 255) / 256, 16384), 256, 0, s>>>(per, B, sb, ps, bs, perm,
+                                                                                             S, packed);
 }
 
 cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s) {
-    if (a.rowof) {  // line-order output (PCG ops only)
-        if (a.op == SPMV_PLAIN) return cudaErrorInvalidValue;
-        auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
-        const int VW = (a.B % 2 == 0 && al16(a.X) && al16(a.Bv) && al16(a.P) && (!a.vb || al16(a.vals))) ? 2 : 1;
-        const int grid = (int)std::min<long long>(std::max<long long>((a.n + 8 * kLineTile - 1) / (8 * kLineTile), 1),
-                                                  (long long)kReduceBlocksPerSm * num_sms());
-        const size_t smem = ((size_t)(kSpmvThreads / 32) * a.B + (size_t)(kSpmvThreads / 32) * kLineTile * 32 * VW) *
-                            sizeof(double);
-        if (VW == 2) {
-            if (a.vb) spmv_line_op<2, true>(a, grid, smem, s);
-            else spmv_line_op<2, false>(a, grid, smem, s);
-        } else {
-            if (a.vb) spmv_line_op<1, true>(a, grid, smem, s);
-            else spmv_line_op<1, false>(a, grid, smem, s);
-        }
-        return cudaGetLastError();
-    }
+    if (a.ecol) return launch_spmv_ell(a, s);
     // 16-byte column pairs when every row of every operand stays 16-byte aligned
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
     const int VW = (a.B % 2 == 0 && al16(a.X) && al16(a.Y) && al16(a.Bv) && al16(a.R) && al16(a.P) &&

@@ -37,10 +37,12 @@ struct SpmvArgs {
     double *partial = nullptr;
     Ctl *ctl = nullptr;
     int *drift_count = nullptr;
-    // line-order output (rowof != null): rp/col index slots, eidx maps an
-    // entry to its natural position in vals, outputs are [b][nslot]
-    const int *eidx = nullptr, *rowof = nullptr;
     int nslot = 0;
+    // line-order ELL (ecol != null): every operand [b][nslot], see spmv_ell_kernel
+    const int *ecol = nullptr;
+    const double *evals = nullptr;
+    int ell_width = 0;
+    size_t partial_cap = 0;  // doubles available at `partial`
 };
 
 __global__ void init_state_kernel(SolveState st, int B, long long hist_cap_init);
@@ -57,10 +59,13 @@ __global__ void symmetric_check_kernel(long long nnz, int B, int vb, const int *
 
 cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s);
 // line-order helpers (vectors [b][slot], see pattern.h LineSched)
-cudaError_t launch_pupd_line(int nslot, int B, const int *rowof, const double *z, double *p, double *x,
-                             const SolveState &st, cudaStream_t s);
 cudaError_t launch_to_line(int nslot, int B, const int *rowof, const double *src, int src_batched, double pad,
                            double *dst, cudaStream_t s);
 cudaError_t launch_from_line(int nslot, int B, const int *rowof, const double *src, double *dst, cudaStream_t s);
+// all-line-order PCG vectors: p / x update, and value gathers into a packed order
+cudaError_t launch_pupd_ell(int nslot, int B, const double *z, double *p, double *x, const SolveState &st,
+                            cudaStream_t s);
+void launch_gather_pack(long long per, int B, int sb, long long ps, long long bs, const int *perm, const double *S,
+                        double *packed, cudaStream_t s);
 
 }  // namespace npcg
