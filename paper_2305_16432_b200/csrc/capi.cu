@@ -122,9 +122,9 @@ struct npcg_solver {
     double *S_fwd = nullptr, *S_bwd = nullptr;  // factor entries in schedule order
     size_t S_cap = 0;
     LineSched *ls = nullptr;  // line-wavefront schedule (owned by the pattern) or null
-    int line_K = 0, line_Kb = 0;  // pipeline stages of the forward / backward line kernels
-    // line mode: every loop vector is in line order ([b][nslot])
-    // all-line-order loop: P, XL (x), BL (b) too; A as ELL by slot
+    int line_K = 0, line_Kb = 0;  // launch shapes (line_config_for) of the forward / backward line kernels
+    // line mode: every loop vector is in line order ([b][nslot]): P, XL (x), BL (b)
+    // too; A as ELL by slot
     double *XL = nullptr, *BL = nullptr;
     int ell_width = 0;
     int *ecol = nullptr, *eperm = nullptr;  // [ell_width][nslot]: column slot / natural CSR position (-1: none)
@@ -279,14 +279,15 @@ int npcg_check_symmetric_values(const npcg_pattern *p, int B, const double *vals
     for (int b = 0; b < B; ++b) ok_host[b] = p->symmetric ? 1 : 0;
     if (!p->symmetric || p->nnz == 0) return NPCG_OK;
     int *d_ok = nullptr;
-    NPCG_CUDA(dalloc(&d_ok, B));
+    keep_pool_memory();
+    NPCG_CUDA(cudaMallocAsync((void **)&d_ok, (size_t)B * 4, s));
     NPCG_CUDA(cudaMemcpyAsync(d_ok, ok_host, B * 4, cudaMemcpyHostToDevice, s));
     note_launch(); symmetric_check_kernel<<<std::min<long long>((p->nnz * B + 255) / 256, 4096), 256, 0, s>>>(p->nnz, B, vb,
                                                                                            p->pair, vals, d_ok);
     NPCG_CUDA(cudaGetLastError());
     NPCG_CUDA(cudaMemcpyAsync(ok_host, d_ok, B * 4, cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(d_ok, s);
     NPCG_CUDA(cudaStreamSynchronize(s));
-    cudaFree(d_ok);
     return NPCG_OK;
 }
 
@@ -359,7 +360,7 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     std::string err;
     if (int rc = plan_solve(s->F, B, s->plan, err)) return fail(rc, err);
     if (LineSched *ls = s->F->line_schedule()) {
-        const int kf = line_stages_for(ls->fwd, false), kb = line_stages_for(ls->bwd, true);
+        const int kf = line_config_for(ls->fwd, false, B), kb = line_config_for(ls->bwd, true, B);
         if (kf > 0 && kb > 0) {
             s->ls = ls;
             s->line_K = kf;
@@ -522,7 +523,12 @@ struct Tri {
         v.AP = l.AP = AP;
         v.st = l.st = st;
     }
-    cudaError_t launch(cudaStream_t s) const { return line ? launch_trsv_line(l, s) : launch_trsv(v, s); }
+    cudaError_t launch(cudaStream_t s) const {
+        if (!line) return launch_trsv(v, s);
+        cudaError_t e = launch_trsv_line(l, s);
+        if (e == cudaSuccess && !l.upper) e = launch_diag_scale(l.nslot, l.B, l.D, l.d_batched, l.out, s);
+        return e;
+    }
 };
 
 static Tri tri_args(npcg_solver *s, bool upper, int mode, int sb, const double *D, int db) {
@@ -530,15 +536,19 @@ static Tri tri_args(npcg_solver *s, bool upper, int mode, int sb, const double *
     t.line = s->ls != nullptr;
     if (t.line) {
         LineArgs &l = t.l;
+        const LineDir &dir = upper ? s->ls->bwd : s->ls->fwd;
+        const int cfg = upper ? s->line_Kb : s->line_K;
         l.B = s->B;
-        l.stages = upper ? s->line_Kb : s->line_K;
-        if (const char *e = std::getenv("NPCG_LINE_NS")) l.stages = std::max(2, std::min(l.stages, atoi(e)));
-        if (const char *e = std::getenv("NPCG_LINE_A")) l.lead = atoi(e);
-        if (const char *e = std::getenv("NPCG_LINE_KNOBS")) l.knobs = atoi(e);
+        l.cluster = cfg / 256;
+        l.group = cfg / 16 % 16;
+        l.stages = cfg % 16;
         l.upper = upper;
         l.mode = mode;
         l.nslot = s->ls->nslot;
-        l.dir = upper ? s->ls->bwd : s->ls->fwd;
+        l.warps = dir.warps;
+        l.ring = dir.ring;
+        l.meta = dir.meta;
+        l.fac_slots = dir.fac_slots;
         l.S = upper ? s->S_bwd : s->S_fwd;
         l.s_batched = sb;
         l.D = s->Dl;  // staged by stage_factor

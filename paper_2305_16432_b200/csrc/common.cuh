@@ -9,6 +9,7 @@ constexpr int kMaxThresholds = 16;
 constexpr int kMaxGroup = 32;  // columns per triangular-solve unit
 
 int num_sms();
+void keep_pool_memory();  // keep cudaMallocAsync scratch pooled across calls
 void note_launch();  // launch accounting (npcg_launch_count)
 long long launch_count();
 

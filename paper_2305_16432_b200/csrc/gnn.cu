@@ -465,6 +465,7 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
         if (c != cudaSuccess && err.empty()) err = cudaGetErrorString(c);
         return c == cudaSuccess;
     };
+    keep_pool_memory();
     bool ok = ck(cudaMallocAsync((void **)&e, sizeof(float) * std::max<long long>(m * F * B, 1), s)) &&
               ck(cudaMallocAsync((void **)&v, sizeof(float) * std::max<long long>((long long)n * F * B, 1), s)) &&
               ck(cudaMallocAsync((void **)&v2, sizeof(float) * std::max<long long>((long long)n * F * B, 1), s)) &&

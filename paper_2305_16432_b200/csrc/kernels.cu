@@ -728,6 +728,22 @@ static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+// Stream-ordered scratch (cudaMallocAsync) stays in the device pool between
+// calls instead of going back to the driver at every synchronisation (the
+// pool's default release threshold is 0), so repeated builds do not remap it.
+void keep_pool_memory() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done = true;
+}
+
 int num_sms() {
     static int sms = 0;
     if (!sms) {

@@ -222,22 +222,20 @@ LineSched::~LineSched() {
     if (rowof) cudaFree(rowof);
     if (slot) cudaFree(slot);
     for (LineDir *d : {&fwd, &bwd}) {
-        void *ptrs[] = {d->line_row0, d->line_len, d->line_start, d->bslot, d->bcount, d->boff, d->sched, d->vperm};
-        for (void *q : ptrs)
-            if (q) cudaFree(q);
+        if (d->meta) cudaFree(d->meta);
+        if (d->vperm) cudaFree(d->vperm);
     }
 }
 
-// The line schedule of a structurally symmetric pattern; false when it does
-// not qualify (too many lines, deep cross-line window, wide rows).
+// The line schedule of a structurally symmetric pattern (pattern.h); false
+// when it does not qualify (too many lines, a dependency off the adjacent
+// line or more than two steps back, an order the three kinds cannot carry).
 //
 // Forward: rows of line l run at steps start[l] + k, start[l] the earliest
-// step at which every cross-line dependency of the line is solved a step
-// earlier (a row's dependencies lie in earlier lines or earlier in its own
-// line). Backward runs the padded step range in reverse: an upper
-// dependency j of row i has row i as a lower dependency, so it was solved
-// at a later forward step -- an earlier backward one -- and the ring window
-// that covers the forward distances covers the backward ones.
+// step at which every cross-line dependency of the line is solved at least a
+// step earlier. Backward runs the steps in reverse: an upper dependency c of
+// row i has row i as a lower dependency, so it was solved at a later forward
+// step -- an earlier backward one -- at the same distance.
 static bool build_line_sched(const Pattern &P, LineSched &LS) {
     const int32_t n = (int32_t)P.n;
     const auto &rp = P.h_rp, &col = P.h_col, &dp = P.h_dp;
@@ -257,136 +255,104 @@ static bool build_line_sched(const Pattern &P, LineSched &LS) {
             line[i] = l;
             pos[i] = i - starts[l];
         }
-    int32_t steps = 0, md = 1;
+    int32_t steps = 0;
     for (int32_t l = 0; l < L; ++l) {
         int32_t st = 0;
-        for (int32_t i = starts[l]; i < starts[l + 1]; ++i) {
-            md = std::max(md, std::max(dp[i] - rp[i], rp[i + 1] - dp[i] - 1));
+        for (int32_t i = starts[l]; i < starts[l + 1]; ++i)
             for (int32_t p = rp[i]; p < dp[i]; ++p) {
                 const int32_t j = col[p];
                 if (line[j] != l) st = std::max(st, lstart[line[j]] + pos[j] + 1 - pos[i]);
             }
-        }
         lstart[l] = st;
         steps = std::max(steps, st + starts[l + 1] - starts[l]);
     }
     auto fstep = [&](int32_t i) { return lstart[line[i]] + pos[i]; };
-    int32_t span = 1;
-    for (int32_t i = 0; i < n; ++i)
+    // kind of the dependency of row i on row j (0 = L2, 1 = L1, 2 = S1), -1 if none fits
+    auto kind = [&](int32_t i, int32_t j, bool upper) -> int32_t {
+        const int32_t li = line[i], lj = line[j];
+        if (lj == li) return j == i + (upper ? 1 : -1) ? 2 : -1;
+        if (lj != li + (upper ? 1 : -1)) return -1;
+        const int32_t age = upper ? fstep(j) - fstep(i) : fstep(i) - fstep(j);
+        return age == 1 ? 1 : (age == 2 ? 0 : -1);
+    };
+    // every row's dependencies, in the reference's order (sparse.py:222-239:
+    // ascending columns forward, the column scatter's descending order
+    // backward), must be strictly increasing kinds
+    std::vector<int32_t> kpos_f((size_t)n * kLineKinds, -1), kpos_b((size_t)n * kLineKinds, -1);
+    for (int32_t i = 0; i < n; ++i) {
+        int32_t last = -1;
         for (int32_t p = rp[i]; p < dp[i]; ++p) {
-            const int32_t j = col[p];
-            if (j == i - 1 && line[j] == line[i]) continue;  // carried in a register
-            span = std::max(span, fstep(i) - fstep(j) + 1);
+            const int32_t k = kind(i, col[p], false);
+            if (k <= last) return false;
+            kpos_f[(size_t)i * kLineKinds + k] = p;
+            last = k;
         }
-    int32_t W = 1;
-    while (W < span) W <<= 1;
-    if (W > 16 || md > 8) return false;
-    const int32_t MD = md <= 2 ? 2 : (md <= 3 ? 3 : (md <= 4 ? 4 : 8));
-    const int32_t T = (L + 31) & ~31;
-    const int32_t K = kLineBatch;
-    const int32_t SP = (steps + K - 1) / K * K, nb = SP / K;
-    // active line range of every step -> slots
-    std::vector<int32_t> lo(SP, INT32_MAX), hi(SP, 0), off(SP, 0);
-    for (int32_t l = 0; l < L; ++l)
-        for (int32_t s = lstart[l]; s < lstart[l] + starts[l + 1] - starts[l]; ++s) {
-            lo[s] = std::min(lo[s], l);
-            hi[s] = std::max(hi[s], l + 1);
+        last = -1;
+        for (int32_t p = rp[i + 1] - 1; p > dp[i]; --p) {
+            const int32_t k = kind(i, col[p], true);
+            if (k <= last) return false;
+            kpos_b[(size_t)i * kLineKinds + k] = p;
+            last = k;
         }
-    std::vector<int32_t> bslot(nb), bcount(nb);
-    int32_t cur = 0;
-    for (int32_t j = 0; j < nb; ++j) {
-        bslot[j] = cur;
-        for (int32_t q = 0; q < K; ++q) {
-            const int32_t s = j * K + q;
-            if (hi[s] == 0) lo[s] = hi[s] = 0;
-            off[s] = cur;
-            cur += hi[s] - lo[s];
-        }
-        cur = (cur + kLineSlotAlign - 1) / kLineSlotAlign * kLineSlotAlign;
-        bcount[j] = cur - bslot[j];
     }
-    const int32_t nslot = cur;
-    if ((int64_t)nslot > (int64_t)4 * n + 64 * nb) return false;  // far too sparse a wavefront
+    const int32_t W = (L + 31) / 32, pad = 32 * W - L;
+    // forward tiles of every warp
+    std::vector<int32_t> s0(W, INT32_MAX), s1(W, 0), nt(W), t0(W);
+    for (int32_t l = 0; l < L; ++l) {
+        const int32_t w = (l + pad) / 32;
+        s0[w] = std::min(s0[w], lstart[l]);
+        s1[w] = std::max(s1[w], lstart[l] + starts[l + 1] - starts[l]);
+    }
+    int32_t tiles = 0, maxt = 0;
+    for (int32_t w = 0; w < W; ++w) {
+        nt[w] = (s1[w] - s0[w] + kTileSteps - 1) / kTileSteps;
+        t0[w] = tiles;
+        tiles += nt[w];
+        maxt = std::max(maxt, nt[w]);
+    }
+    if ((int64_t)tiles * kTileSlots > INT32_MAX / kLineKinds) return false;
+    const int32_t nslot = tiles * kTileSlots;
     LS.nslot = nslot;
+    LS.lines = L;
+    LS.steps = steps;
     LS.h_rowof.assign(nslot, -1);
     LS.h_slot.assign(n, -1);
     for (int32_t i = 0; i < n; ++i) {
-        const int32_t s = fstep(i);
-        const int32_t q = off[s] + line[i] - lo[s];
-        LS.h_slot[i] = q;
-        LS.h_rowof[q] = i;
+        const int32_t q = line[i] + pad, w = q / 32, d = fstep(i) - s0[w];
+        const int32_t slot = (t0[w] + d / kTileSteps) * kTileSlots + (d % kTileSteps) * 32 + q % 32;
+        LS.h_slot[i] = slot;
+        LS.h_rowof[slot] = i;
     }
-    const int32_t zslot = W * T;
     auto build_dir = [&](bool upper, LineDir &D) -> bool {
-        std::vector<int32_t> row0(T, 0), llen(T, 0), lst(T, 0), db(nb), dc(nb);
-        for (int32_t l = 0; l < L; ++l) {
-            const int32_t len = starts[l + 1] - starts[l];
-            row0[l] = upper ? starts[l + 1] - 1 : starts[l];
-            llen[l] = len;
-            lst[l] = upper ? SP - lstart[l] - len : lstart[l];
+        D.warps = W;
+        D.ntiles = tiles;
+        D.max_warp_tiles = maxt;
+        D.fac_slots = (int64_t)nslot * kLineKinds;
+        int32_t lag = 0;  // largest first-step offset between adjacent warps
+        for (int32_t w = 0; w + 1 < W; ++w) lag = std::max(lag, std::abs(s0[w + 1] - s0[w]));
+        D.ring = 64;
+        while (D.ring < 2 * lag + 16) D.ring *= 2;
+        D.h_meta.assign((size_t)W * 4, 0);
+        for (int32_t wd = 0; wd < W; ++wd) {
+            const int32_t w = upper ? W - 1 - wd : wd;  // forward warp
+            int32_t *m = &D.h_meta[(size_t)wd * 4];
+            m[0] = upper ? steps - s0[w] - kTileSteps * nt[w] : s0[w];
+            m[1] = nt[w];
+            m[2] = t0[w];
         }
-        std::vector<int64_t> boff(nb);
-        std::vector<int16_t> sched;
-        std::vector<int32_t> vperm;
-        int32_t maxs = 0;
-        for (int32_t jd = 0; jd < nb; ++jd) {
-            const int32_t j = upper ? nb - 1 - jd : jd;  // forward batch
-            db[jd] = bslot[j];
-            dc[jd] = bcount[j];
-            maxs = std::max(maxs, bcount[j]);
-            boff[jd] = (int64_t)sched.size();
-            for (int32_t q = 0; q < kLineHeader; ++q) {  // header: int32 base per step, as int16 pairs
-                const int32_t s = upper ? j * K + (K - 1 - q) : j * K + q;
-                const int32_t base = q < K ? off[s] - lo[s] - bslot[j] : 0;
-                sched.push_back((int16_t)(base & 0xffff));
-                sched.push_back((int16_t)((uint32_t)base >> 16));
-            }
-            // entries of the batch, structure-of-arrays: [e][slot]
-            const int32_t cnt = bcount[j];
-            const size_t s0 = sched.size(), v0 = vperm.size();
-            sched.resize(s0 + (size_t)cnt * MD, (int16_t)zslot);  // padding: zero cell, zero factor
-            vperm.resize(v0 + (size_t)cnt * MD, -1);              // (acc - 0 * 0 == acc exactly)
-            for (int32_t u = 0; u < cnt; ++u) {
-                const int32_t i = LS.h_rowof[bslot[j] + u];
-                if (i < 0) continue;
-                int32_t e = 0;
-                auto push = [&](int32_t p) {
-                    const int32_t jj = col[p];
-                    const bool prev = line[jj] == line[i] && jj == i + (upper ? 1 : -1);
-                    const int32_t pj = upper ? (starts[line[jj] + 1] - 1 - jj) : pos[jj];
-#ifdef NPCG_LINE_AOS
-                    const size_t at = (size_t)u * MD + e;
-#else
-                    const size_t at = (size_t)e * cnt + u;
-#endif
-                    sched[s0 + at] = (int16_t)(prev ? -1 : (pj & (W - 1)) * T + line[jj]);
-                    vperm[v0 + at] = p;
-                    ++e;
-                };
-                // the reference's summation order (sparse.py:222-239)
-                if (upper)
-                    for (int32_t p = rp[i + 1] - 1; p > dp[i]; --p) push(p);
-                else
-                    for (int32_t p = rp[i]; p < dp[i]; ++p) push(p);
-            }
+        std::vector<int32_t> vperm((size_t)D.fac_slots, -1);
+        const auto &kp = upper ? kpos_b : kpos_f;
+        for (int32_t slot = 0; slot < nslot; ++slot) {
+            const int32_t i = LS.h_rowof[slot];
+            if (i < 0) continue;
+            const int32_t tile = slot / kTileSlots, e = slot % kTileSlots;
+            const int32_t ed = upper ? kTileSlots - 1 - e : e;  // element in this direction's traversal
+            for (int32_t k = 0; k < kLineKinds; ++k)
+                vperm[((size_t)tile * kLineKinds + k) * kTileSlots + ed] = kp[(size_t)i * kLineKinds + k];
         }
-        D.T = T;
-        D.nbatch = nb;
-        D.window = W;
-        D.md = MD;
-        D.zslot = zslot;
-        D.max_slots = maxs;
-        D.sched_words = (int64_t)sched.size();
-        D.fac_slots = (int64_t)vperm.size();
-        D.line_row0 = upload(row0);
-        D.line_len = upload(llen);
-        D.line_start = upload(lst);
-        D.bslot = upload(db);
-        D.bcount = upload(dc);
-        D.boff = upload(boff);
-        D.sched = upload(sched);
+        D.meta = upload(D.h_meta);
         D.vperm = upload(vperm);
-        return D.line_row0 && D.line_len && D.line_start && D.bslot && D.bcount && D.boff && D.sched && D.vperm;
+        return D.meta && D.vperm;
     };
     if (!build_dir(false, LS.fwd) || !build_dir(true, LS.bwd)) return false;
     LS.rowof = upload(LS.h_rowof);

@@ -52,49 +52,47 @@ struct SchedSet {
 
 // Line-wavefront schedule (trsv_line.cu): the rows split into "lines",
 // maximal runs in which every row depends on its predecessor (grid lines of
-// a mesh in natural order). One thread owns one line; lines are rigid: in
-// the forward solve row k of line l is solved at step start[l] + k, and the
-// backward solve runs the same steps in reverse. The in-line dependency
-// stays in a register, cross-line ones are read from a shared-memory ring
-// of every line's last `window` values ([window][T]).
+// a mesh in natural order). Line l is owned by one lane of one warp; lines
+// are rigid: in the forward solve row k of line l is solved at step
+// start[l] + k, and the backward solve runs the same steps in reverse.
 //
-// Line order ("slots"): the vectors the solves touch are stored step-major,
-// each step holding the contiguous range of lines active at it, so the rows
-// of a batch of kLineBatch steps are one contiguous slot range in both
-// directions and move with a single bulk copy. Slot ranges of batches are
-// padded to multiples of 8 (16-byte aligned copies); padding slots belong to
-// no row and hold zeros.
+// The schedule qualifies when every cross-line dependency of a row lies on
+// the adjacent line (l - 1 forward, l + 1 backward) at most two steps back,
+// so a lane's operands are its own previous value (register), and its left
+// neighbour's values one and two steps back (one warp shuffle per step; the
+// first lane of a warp reads them from a shared-memory ring written by the
+// last lane of the previous warp). Every row's dependencies, in the
+// reference's summation order, are then a subsequence of the three "kinds"
+//     L2 (left line, 2 steps back), L1 (left, 1 step back), S1 (own line),
+// and the factor is stored as three values per row (0 where a kind is absent).
 //
-// Per batch (in a direction's order) the schedule holds a 16-byte header
-// (int32 base[kLineHeader]: slot of line 0 at each step, relative to the
-// batch's first slot) followed by [md][slot] int16 descriptors
-//   -1 = previous row of the line, >= 0 = ring slot, zslot = padding (zero);
-// vperm[md][slot] = CSR position of the matching factor value (-1 = pad).
-// Both are structure-of-arrays per batch so a warp's reads are contiguous.
-// Only built when the whole pattern fits one CTA (lines <= kLineMaxLines,
-// window <= 16, <= 8 dependencies per row) and the pattern is structurally
-// symmetric.
-constexpr int32_t kLineBatch = 4;      // steps per pipeline stage
-constexpr int32_t kLineHeader = 4;     // int32 bases in a batch header (>= kLineBatch; 16 bytes)
-constexpr int32_t kLineMaxLines = 512;
-constexpr int32_t kLineSlotAlign = 8;  // slots per alignment unit of a batch range
+// Line order ("slots"): lines are placed on lanes 32w + t (forward, padded at
+// the front to a multiple of 32); each warp's step range is cut into tiles
+// of kTileSteps steps x 32 lanes, element q * 32 + t, and a warp's tiles are
+// contiguous, so every pipeline stage of a warp is one bulk copy per array.
+// The backward solve traverses the same tiles in reverse (warp W-1-w, lane
+// 31-t, element 127-e), so one slot order serves both directions and every
+// vector of the PCG loop. Padding slots belong to no row and hold zeros.
+constexpr int32_t kTileSteps = 4;
+constexpr int32_t kTileSlots = 32 * kTileSteps;
+constexpr int32_t kLineKinds = 3;  // L2, L1, S1
+constexpr int32_t kLineMaxWarps = 16;  // 512 threads: up to 128 registers per lane
+constexpr int32_t kLineMaxLines = 32 * kLineMaxWarps;
 
 struct LineDir {
-    int32_t T = 0, nbatch = 0, window = 1, md = 1, zslot = 0, max_slots = 0;
-    int64_t sched_words = 0;        // int16 words of the packed schedule
-    int64_t fac_slots = 0;          // factor values per system (= slots * md)
-    int32_t *line_row0 = nullptr;   // [T] first row of each line in solve order
-    int32_t *line_len = nullptr;    // [T] rows of each line (0: padding thread)
-    int32_t *line_start = nullptr;  // [T] step of each line's first row
-    int32_t *bslot = nullptr;       // [nbatch] first slot of each batch
-    int32_t *bcount = nullptr;      // [nbatch] slots of each batch (multiple of 8)
-    int64_t *boff = nullptr;        // [nbatch] int16 offset of each batch's schedule block
-    int16_t *sched = nullptr;       // [sched_words] per batch: header + [slot][md]
-    int32_t *vperm = nullptr;       // [fac_slots] factor CSR position (-1 = padding)
+    int32_t warps = 0;
+    int32_t ntiles = 0;              // tiles in all (nslot / kTileSlots)
+    int32_t max_warp_tiles = 0;      // most tiles of one warp
+    int32_t ring = 64;               // steps per warp's outgoing value ring (power of two)
+    int64_t fac_slots = 0;           // factor values per system (= nslot * kLineKinds)
+    std::vector<int32_t> h_meta;     // [warps][4]: first step, tiles, first tile, 0
+    int32_t *meta = nullptr;         // device copy of h_meta
+    int32_t *vperm = nullptr;        // [tile][kind][element]: CSR position of the factor value (-1 = zero)
 };
 struct LineSched {
     bool ok = false;
-    int32_t nslot = 0;                    // slots per system (multiple of 8)
+    int32_t nslot = 0;                     // slots per system (multiple of kTileSlots)
+    int32_t lines = 0, steps = 0;
     std::vector<int32_t> h_rowof, h_slot;  // slot -> row (-1: padding), row -> slot
     int32_t *rowof = nullptr, *slot = nullptr;
     LineDir fwd, bwd;

@@ -41,14 +41,15 @@ struct TrsvSmem {
 
 TrsvSmem trsv_smem_plan(const Schedule &S, int G, int s_batched);
 
-// Line-wavefront solve (trsv_line.cu): one CTA per system. Every vector is
-// in line order, system-major: element (slot q, system b) at b * nslot + q.
+// Line-wavefront solve (trsv_line.cu): one CTA per system, one lane per
+// line. Every vector is in line order, system-major: element (slot q,
+// system b) at b * nslot + q.
 struct LineArgs {
-    int B = 1, stages = 3, upper = 0, mode = TRSV_PLAIN;
-    int nslot = 0;
-    int lead = -1;   // batches requested ahead (-1: from stages)
-    int knobs = 0;   // bit 0: TMA stores, bit 1: one thread issues every bulk copy
-    LineDir dir{};
+    int B = 1, upper = 0, mode = TRSV_PLAIN;
+    int cluster = 1, group = 2, stages = 2;  // CTAs per system, tiles per pipeline stage, stages per warp
+    int nslot = 0, warps = 0, ring = 64;  // ring: steps per warp's outgoing ring (LineDir::ring)
+    const int *meta = nullptr;  // LineDir::meta of this direction
+    long long fac_slots = 0;
     const double *S = nullptr;  // packed factor values ([b][fac_slots] when s_batched)
     int s_batched = 0;
     const double *D = nullptr;  // diag(A) in line order: [nslot] or [b][nslot] (padding 1.0)
@@ -58,10 +59,14 @@ struct LineArgs {
     SolveState st{};
     int *drift_count = nullptr;
 };
-size_t line_smem_bytes(const LineDir &L, int stages, bool upper, bool pcg);
-int line_stages_for(const LineDir &L, bool upper);  // pipeline stages that fit shared memory (0: none)
+// Launch shape (cluster * 256 + group * 16 + stages) for B systems that fits
+// shared memory for this direction, 0 when none does. NPCG_LINE_CFG
+// (group * 16 + stages) and NPCG_LINE_CLUSTER override.
+int line_config_for(const LineDir &L, bool upper, int B);
 int line_trace_copy(long long *out, int n);  // debug timeline (NPCG_LINE_TRACE builds)
 cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s);
+// y[b][slot] /= D[(b)][slot] (the diagonal scaling between the line solves)
+cudaError_t launch_diag_scale(int nslot, int B, const double *D, int d_batched, double *y, cudaStream_t s);
 // factor values S[p * ps + b * bs] -> line order of `L` (per system when batched)
 void launch_line_factor_pack(const LineDir &L, int B, int sb, long long ps, long long bs, const double *S,
                              double *packed, cudaStream_t s);

@@ -1,36 +1,42 @@
-// trsv_line.cu -- line-wavefront triangular solves for patterns whose rows
-// form at most kLineMaxLines "lines" (runs of rows each depending on its
-// predecessor; the grid lines of a mesh in natural order).
+// trsv_line.cu -- line-wavefront triangular solves (pattern.h, LineSched).
 //
-// One CTA per right-hand side / system, warp-specialised:
+// One system per cluster of C CTAs (C = 1 or 2, each on its own SM), one
+// lane per grid line, no block-wide synchronisation inside the solve:
 //
-//   consumers (threads 0..T-1, one per line) walk the steps. At step s every
-//     line whose rigid step range covers s solves one row: the dependency
-//     on its own previous row is a register, the cross-line ones are read
-//     from a shared-memory ring holding every line's last `window` values.
-//     A step is a handful of shared loads, an unfused fp64 chain and one
-//     named barrier over the consumer warps -- nothing else.
-//   producers (kProdWarps warps) move whole batches of kLineBatch steps.
-//     Every vector lives in line order (pattern.h), so a batch's rows are one
-//     contiguous slot range: one elected producer bulk-copies (TMA,
-//     cp.async.bulk + mbarrier) the batch's schedule block, factor values
-//     and vector slices into a stage ring, the producer warps form the
-//     right-hand sides slot by slot (r - alpha Ap forward, y / diag
-//     backward) and, once the consumers are done, accumulate the PCG dot
-//     product and bulk-store the solved slices back (TMA store). No thread
-//     issues a scattered global access.
-//
-// Stage hand-off uses named barriers: FULL[s] (producers arrive, consumers
-// sync) and EMPTY[s] (consumers arrive, producers sync), so a consumer pays
-// one barrier per step plus one per batch.
+//   * at every step a lane solves the next row of its line. Its operands are
+//     its own previous value (register), and its left neighbour's values one
+//     and two steps back: one __shfl_up_sync per step (the two-steps-back
+//     value is last step's shuffle). Lane 0 of a warp gets them from a
+//     shared-memory ring in its own CTA, written by lane 31 of the previous
+//     warp -- through distributed shared memory when that warp sits on the
+//     other SM of the cluster. A slot holds a NaN sentinel until written and
+//     is re-armed by its reader, so an aligned 8-byte value is its own flag:
+//     no fence, no counter. Both sides move whole stages: the reader checks
+//     and re-arms a stage's slots at once, the writer checks once per stage
+//     that its slots were re-armed (a ring spans twice the natural start
+//     offset of adjacent warps, so this never waits in the steady state).
+//   * each warp streams its own operands: per stage of G tiles (4 steps x 32
+//     lanes each) one elected lane issues bulk copies (TMA, cp.async.bulk +
+//     one mbarrier per stage) of the factor values and vector slices into the
+//     warp's private stage ring. Results go from registers to global memory
+//     in coalesced 256-byte warp stores.
+//   * the diagonal scaling y /= diag (sparse.py:273) is applied by the
+//     forward solve as it stores y (off the dependency chain), so the
+//     backward solve reads y / diag directly. PCG mode also fuses the
+//     forward r -= alpha Ap (pcg.py:142) with |r|^2 (pcg.py:143) and the
+//     backward r.z (pcg.py:167), reduced in a fixed order at the end.
+//   * splitting a system over C SMs divides what every SM's shared-memory /
+//     L1 data path carries per step (operands in, results out), which is
+//     what bounds the step rate.
 //
 // Summation order and unfused fp64 arithmetic are those of the reference
-// (sparse.py:222-239), so results are bit-identical to pcgkit.
+// (sparse.py:222-239): a row's dependencies in the reference's order are a
+// subsequence of (L2, L1, S1) and absent kinds carry a zero factor, whose
+// product with a finite operand leaves the row sum unchanged, so results are
+// bit-identical to pcgkit (up to the sign of an exactly-zero row sum).
 #include <algorithm>
+#include <cstdlib>
 
-#ifndef NPCG_NO_ZERO_Y
-#define NPCG_NO_ZERO_Y 0
-#endif
 #include "ptx.cuh"
 #include "trsv.cuh"
 
@@ -38,36 +44,53 @@ namespace npcg {
 
 namespace {
 
-constexpr int kProdWarps = 8;
-constexpr int kProd = 32 * kProdWarps;
-constexpr int kLineMaxStages = 6;
-constexpr int kBarCons = 1;
-constexpr int kBarFull = 2;
-constexpr int kBarEmpty = kBarFull + kLineMaxStages;
-constexpr int kBarProd = kBarEmpty + kLineMaxStages;
-constexpr int kPrefetchBatches = 0;  // L2 prefetch distance of the bulk copies
-
 struct LineSmem {  // byte offsets into dynamic shared memory
-    size_t ring, stage0, stage_bytes, sv, v[3], meta, total;
+    size_t ring, mbar, stage0, stage_bytes, total;
 };
 
 __host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
 
-__host__ __device__ inline LineSmem line_layout(int T, int W, int MD, int maxs, int NS, int nv, int nb) {
+// vectors staged per stage: forward r [, Ap] ; backward y/diag [, r]
+__host__ __device__ constexpr int line_vectors(bool upper, bool pcg) { return pcg ? 2 : 1; }
+
+__host__ __device__ inline LineSmem line_layout(int WL, int R, int G, int NS, int nv) {
     LineSmem m;
-    m.ring = 128;  // mbarriers first
-    m.stage0 = al128(m.ring + ((size_t)T * W + 2) * 8);
-    size_t o = al128(16 + (size_t)maxs * MD * 2);  // schedule block
-    m.sv = o;
-    o = al128(o + (size_t)maxs * MD * 8);
-    for (int i = 0; i < 3; ++i) {
-        m.v[i] = o;
-        if (i < nv) o = al128(o + (size_t)maxs * 8);
-    }
-    m.stage_bytes = o;
-    m.meta = m.stage0 + NS * o;  // per batch: boff | bslot | bcount
-    m.total = m.meta + (size_t)nb * 16;
+    m.ring = 0;
+    m.mbar = al128((size_t)WL * R * 8);
+    m.stage0 = al128(m.mbar + (size_t)WL * NS * 8);
+    m.stage_bytes = (size_t)G * (kLineKinds + nv) * kTileSlots * 8;
+    m.total = m.stage0 + (size_t)WL * NS * m.stage_bytes;
     return m;
+}
+
+__device__ __forceinline__ double ld_vol(const double *p) { return *reinterpret_cast<const volatile double *>(p); }
+__device__ __forceinline__ void st_vol(double *p, double v) { *reinterpret_cast<volatile double *>(p) = v; }
+__device__ __forceinline__ bool is_sentinel(double v) {
+    return (unsigned long long)__double_as_longlong(v) == kSentinel;
+}
+__device__ __forceinline__ double sentinel() { return __longlong_as_double((long long)kSentinel); }
+// distributed shared memory: address of `p` in CTA `rank` of the cluster
+__device__ __forceinline__ unsigned map_rank(const void *p, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ double ld_dsm(unsigned addr) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.cluster.shared::cluster.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+    return __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ void st_dsm(unsigned addr, double v) {
+    asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(addr), "l"(__double_as_longlong(v))
+                 : "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void line_epilogue(const LineArgs &a, int b, double total) {
@@ -77,31 +100,24 @@ __device__ __forceinline__ void line_epilogue(const LineArgs &a, int b, double t
 
 }  // namespace
 
-// Debug timeline of CTA 0 of the forward solve (build with -DNPCG_LINE_TRACE):
-// clock64 per batch and event, read back with npcg_debug_line_trace().
+// Debug timeline (build with -DNPCG_LINE_TRACE): per warp of the first
+// cluster (first 16), its first step, then clock64 before / after each
+// stage's mbarrier wait.
 constexpr int kTraceEvents = 16, kTraceBatches = 2048;
 __device__ long long g_line_trace[kTraceEvents][kTraceBatches];
-#ifdef NPCG_LINE_TRACE
-#define LTRACE(ev, j)                                                                                     \
-    do {                                                                                                  \
-        if (!UPPER && blockIdx.x == 0 && (j) < kTraceBatches) g_line_trace[ev][j] = clock64();            \
-    } while (0)
-#else
-#define LTRACE(ev, j) \
-    do {              \
-    } while (0)
-#endif
 
-template <int MD, bool UPPER, bool PCG, bool SB>
-__global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(LineArgs a) {
-    constexpr int K = kLineBatch;
+template <bool UPPER, bool PCG, bool SB, int G, int C>
+__global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(LineArgs a) {
+    constexpr int STEPS = kTileSteps * G;
+    constexpr int NV = line_vectors(UPPER, PCG);
     extern __shared__ __align__(128) char sm[];
-    __shared__ double s_red[kProdWarps];
-    const LineDir &L = a.dir;
-    const int T = L.T, NS = a.stages, W = L.window, nb = L.nbatch;
-    const int tid = threadIdx.x, b = blockIdx.x;
-    const int NT = T + kProd;  // threads taking part in FULL / EMPTY
-    // what this system needs from this launch
+    __shared__ double s_red[kLineMaxWarps];
+    __shared__ double s_cta[4];
+    const int W = a.warps, WL = W / C, NS = a.stages, R = a.ring;
+    const int wl = threadIdx.x >> 5, t = threadIdx.x & 31;
+    const int rank = C > 1 ? (int)cluster_rank() : 0, b = blockIdx.x / C;
+    const int w = rank * WL + wl;  // warp of the direction's schedule
+    // what this system needs from this launch (uniform over the cluster)
     int op = TOP_SOLVE;
     if (PCG) {
         const SolveState &st = a.st;
@@ -109,208 +125,251 @@ __global__ void __launch_bounds__(kLineMaxLines + kProd, 1) trsv_line_kernel(Lin
         op = !UPPER ? (ph == PH_ITER ? TOP_UPDATE : (ph == PH_INIT ? TOP_SOLVE : TOP_SKIP))
                     : ((ph == PH_ITER || ph == PH_INIT) ? TOP_SOLVE : TOP_SKIP);
         if (op == TOP_SKIP) {
-            if (UPPER && tid == 0) line_epilogue(a, b, 0.0);  // keeps pflag / restart bookkeeping
+            if (UPPER && rank == 0 && threadIdx.x == 0) line_epilogue(a, b, 0.0);  // pflag / restart bookkeeping
             return;
         }
     }
     const bool upd = !UPPER && PCG && op == TOP_UPDATE;
-    const int nv = UPPER ? (PCG ? 3 : 2) : 2;
-    const LineSmem m = line_layout(T, W, MD, L.max_slots, NS, nv, nb);
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm);
-    double *ring = reinterpret_cast<double *>(sm + m.ring);  // [W][T] + zero cell
-    auto stage_ptr = [&](int s) { return sm + m.stage0 + (size_t)s * m.stage_bytes; };
-    for (int q = tid; q < T * W + 2; q += blockDim.x) ring[q] = 0.0;
-    long long *s_boff = reinterpret_cast<long long *>(sm + m.meta);
-    int *s_bslot = reinterpret_cast<int *>(s_boff + nb), *s_bcount = s_bslot + nb;
-    for (int q = tid; q < nb; q += blockDim.x) {
-        s_boff[q] = L.boff[q];
-        s_bslot[q] = L.bslot[q];
-        s_bcount[q] = L.bcount[q];
-    }
-    if (tid == T) {
+    const LineSmem m = line_layout(WL, R, G, NS, NV);
+    double *ring = reinterpret_cast<double *>(sm + m.ring);  // [WL][R]: values of the warp left of each warp
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + m.mbar) + wl * NS;
+    char *stage = sm + m.stage0 + (size_t)wl * NS * m.stage_bytes;
+    for (int i = threadIdx.x; i < WL * R; i += blockDim.x) ring[i] = sentinel();
+    const int4 *meta = reinterpret_cast<const int4 *>(a.meta);
+    const int4 me = meta[w];
+    if (t == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], 1);
         fence_mbar_init();
     }
-    __syncthreads();
+    if (C > 1) cluster_sync_all();  // every ring armed before any remote write
+    else __syncthreads();
 
-    if (tid < T) {
-        // ------------------------------------------------------------------ consumers
-        const int t = tid, len = L.line_len[t], lst = L.line_start[t];
-        double prev = 0.0;
-        for (int j = 0; j < nb; ++j) {
-            const int s = j % NS;
-            const int s_cnt_j = s_bcount[j];
-            if (t == 0) LTRACE(0, j);
-            bar_sync(kBarFull + s, NT);  // stage s holds batch j (also orders the last step's ring writes)
-            if (t == 0) LTRACE(1, j);
-            char *sp = stage_ptr(s);
-            const int *hdr = reinterpret_cast<const int *>(sp);
-            const int cnt = s_cnt_j;
-            const int16_t *dsc = reinterpret_cast<const int16_t *>(sp) + 8;
-            const double *sv = reinterpret_cast<const double *>(sp + m.sv);
-            double *vin = reinterpret_cast<double *>(sp + m.v[0]);                // rhs (r / y/D)
-            double *vout = reinterpret_cast<double *>(sp + m.v[UPPER ? 0 : 1]);   // solution
-#pragma unroll
-            for (int q = 0; q < K; ++q) {
-                const int kp = j * K + q - lst;  // position of this line's row solved at this step
-                if ((unsigned)kp < (unsigned)len) {
-                    const int u = hdr[q] + t;
-                    int d[MD];
-                    double v[MD];
-#pragma unroll
-                    for (int e = 0; e < MD; ++e) {
-                        d[e] = dsc[e * cnt + u];
-                        v[e] = sv[e * cnt + u];
-                    }
-                    double acc = vin[u];
-                    double y[MD];
-#pragma unroll
-                    for (int e = 0; e < MD; ++e) y[e] = d[e] == -1 ? prev : ring[d[e]];
-#pragma unroll
-                    for (int e = 0; e < MD; ++e) acc = __dsub_rn(acc, __dmul_rn(v[e], y[e]));
-                    prev = acc;
-                    ring[(kp & (W - 1)) * T + t] = acc;
-                    vout[u] = acc;
-                }
-                if (t == 0) LTRACE(8 + q, j);
-                if (q + 1 < K) bar_sync(kBarCons, T);  // step done: its values are visible to the next step
-            }
-            if (t == 0) LTRACE(2, j);
-            fence_proxy_async();            // solution writes -> the producers' TMA store (async proxy)
-            bar_arrive(kBarEmpty + s, NT);  // batch j's solution is in stage s
-        }
-        return;
+    const int C0 = me.x, nt = me.y, tile0 = me.z, C1 = C0 + kTileSteps * nt;
+    const int nstage = (nt + G - 1) / G;
+    // ring protocol: warp w sends its last lane's values of steps
+    // [max(C0_right - 2, C0), min(C1_right - 1, C1)) to the right warp; every
+    // value is read once and re-armed by its reader
+    int P0 = 0, P1 = 0, Q0 = 0, Q1 = 0;
+    if (w > 0) {
+        const int4 pm = meta[w - 1];
+        P0 = pm.x;
+        P1 = pm.x + kTileSteps * pm.y;
     }
+    if (w + 1 < W) {
+        const int4 qm = meta[w + 1];
+        Q0 = max(qm.x - 2, C0);
+        Q1 = min(qm.x + kTileSteps * qm.y - 1, C1);
+    }
+    const bool cons = w > 0 && t == 0, prod = w + 1 < W && t == 31;
+    double *rin = ring + wl * R;  // my incoming ring (local)
+    // my outgoing ring: the right warp's incoming ring, in its CTA
+    const int wr = w + 1 < W ? w + 1 : w;
+    const unsigned rout = map_rank(ring + (wr % WL) * R, (unsigned)(wr / WL));
+    auto ring_read = [&](int x) -> double {  // value of the left line at step x (0 outside its range)
+        if (x < P0 || x >= P1) return 0.0;
+        double *p = rin + (x & (R - 1));
+        double v = ld_vol(p);
+        while (is_sentinel(v)) {  // start-up: the left warp is a whole line-block ahead
+            __nanosleep(64);
+            v = ld_vol(p);
+        }
+        st_vol(p, sentinel());
+        return v;
+    };
 
-    // ---------------------------------------------------------------------- producers
-    const int p = tid - T;  // 0 .. kProd-1
-    const bool elect = p == 0;
     const long long vb = (long long)b * a.nslot;
-    const double *Sb = a.S + (SB ? (size_t)b * L.fac_slots : 0);
-    const double *Db = a.D + (a.d_batched ? vb : 0);
+    const double *fac = a.S + (SB ? (size_t)b * a.fac_slots : 0);
+    const double *src[3];
+    if (!UPPER) {
+        src[0] = a.in + vb;
+        src[1] = PCG ? a.AP + vb : nullptr;
+        src[2] = nullptr;
+    } else {
+        src[0] = a.in + vb;
+        src[1] = PCG ? a.R + vb : nullptr;
+        src[2] = nullptr;
+    }
+    double *out = a.out + vb, *rout_g = PCG && !UPPER ? a.R + vb : nullptr;
+    // tiles [lo, lo + g) of stage j (ascending in memory; the backward solve walks them downwards)
+    auto stage_tiles = [&](int j, int &lo, int &g) {
+        g = min(G, nt - j * G);
+        lo = UPPER ? tile0 + nt - j * G - g : tile0 + j * G;
+    };
+    auto issue = [&](int j) {  // elected lane: bulk copies of stage j into its ring slot
+        int lo, g;
+        stage_tiles(j, lo, g);
+        char *sp = stage + (size_t)(j % NS) * m.stage_bytes;
+        const unsigned fb = (unsigned)g * kLineKinds * kTileSlots * 8, vbytes = (unsigned)g * kTileSlots * 8;
+        uint64_t *bar = &mbar[j % NS];
+        mbar_expect_tx(bar, fb + NV * vbytes);
+        bulk_g2s(sp, fac + (size_t)lo * kLineKinds * kTileSlots, fb, bar);
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            bulk_g2s(sp + (size_t)G * kLineKinds * kTileSlots * 8 + (size_t)v * G * kTileSlots * 8,
+                     src[v] + (size_t)lo * kTileSlots, vbytes, bar);
+    };
+    if (t == 0)
+        for (int j = 0; j < NS && j < nstage; ++j) issue(j);
+
     const double alpha = upd ? a.st.alpha[b] : 0.0;
+    double h0 = 0.0;  // my value one step back
+    double lp = 0.0;  // left neighbour's value two steps back (at the next step)
     double acc2 = 0.0;
-    // sources of batch mb's stage blocks (global)
-    auto blocks = [&](int mb, const void **src, unsigned *bytes, int &nsrc) {
-        const int bs = s_bslot[mb], cnt = s_bcount[mb];
-        const long long bo = s_boff[mb];
-        nsrc = 0;
-        src[nsrc] = L.sched + bo;
-        bytes[nsrc++] = 16 + (unsigned)cnt * MD * 2;
-        src[nsrc] = Sb + (bo - 8ll * mb);
-        bytes[nsrc++] = (unsigned)cnt * MD * 8;
-        src[nsrc] = a.in + vb + bs;
-        bytes[nsrc++] = cnt * 8;
-        if (!UPPER) {
-            if (upd) {
-                src[nsrc] = a.AP + vb + bs;
-                bytes[nsrc++] = cnt * 8;
-            }
-        } else {
-            src[nsrc] = Db + bs;
-            bytes[nsrc++] = cnt * 8;
-            if (PCG) {
-                src[nsrc] = a.R + vb + bs;
-                bytes[nsrc++] = cnt * 8;
-            }
-        }
-    };
-    auto issue_load = [&](int mb) {  // elected producer: TMA of batch mb into its stage
-        const void *src[5];
-        unsigned bytes[5];
-        int nsrc;
-        blocks(mb, src, bytes, nsrc);
-        char *sp = stage_ptr(mb % NS);
-        char *dst[5] = {sp, sp + m.sv, sp + m.v[0], sp + m.v[1], sp + m.v[2]};
-        unsigned tot = 0;
-        for (int i = 0; i < nsrc; ++i) tot += bytes[i];
-        uint64_t *bar = &mbar[mb % NS];
-        mbar_expect_tx(bar, tot);
-        for (int i = 0; i < nsrc; ++i) bulk_g2s(dst[i], src[i], bytes[i], bar);
-    };
-    auto prefetch = [&](int mb) {
-        const void *src[5];
-        unsigned bytes[5];
-        int nsrc;
-        blocks(mb, src, bytes, nsrc);
-        for (int i = 0; i < nsrc; ++i) bulk_prefetch_l2(src[i], bytes[i]);
-    };
-    // batch mb is solved: dot product, then the solved slices go home
-    auto drain = [&](int mb) {
-        bar_sync(kBarEmpty + mb % NS, NT);
-        char *sp = stage_ptr(mb % NS);
-        const int bs = s_bslot[mb], cnt = s_bcount[mb];
-        if (UPPER && PCG) {  // r.z (pcg.py:167)
-            const double *z = reinterpret_cast<const double *>(sp + m.v[0]);
-            const double *r = reinterpret_cast<const double *>(sp + m.v[2]);
-            for (int u = p; u < cnt; u += kProd) acc2 = __dadd_rn(acc2, __dmul_rn(r[u], z[u]));
-        }
-        if (elect) {
-            fence_proxy_async();  // (every writer fenced before the barriers above)
+    double ychk = sentinel();  // this stage's outgoing-slot check (loaded a stage ahead)
+    if (w + 1 < W) {
+        const int ys = C0 + t;
+        if (t < STEPS && ys >= Q0 && ys < Q1 && ys - R >= Q0) ychk = ld_dsm(rout + (unsigned)(ys & (R - 1)) * 8u);
+    }
+    if (cons) lp = ring_read(C0 - 2);
+    for (int j = 0; j < nstage; ++j) {
+        const int s = j % NS, sig = C0 + j * STEPS;  // first step of the stage
+#ifdef NPCG_LINE_TRACE
+        const bool tr = b == 0 && t == 0 && w < kTraceEvents && 6 * j + 6 < kTraceBatches;
+#define LTR(k)                                                   \
+    do {                                                         \
+        if (tr) g_line_trace[w][6 * j + 1 + (k)] = clock64();    \
+    } while (0)
+        if (tr && j == 0) g_line_trace[w][0] = C0;
+        LTR(0);
+#else
+#define LTR(k) \
+    do {       \
+    } while (0)
+#endif
+        mbar_wait(&mbar[s], (j / NS) & 1);
+        LTR(1);
+        int lo, g;
+        stage_tiles(j, lo, g);
+        const char *sp = stage + (size_t)s * m.stage_bytes;
+        const double *f = reinterpret_cast<const double *>(sp);
+        const double *v0 = f + G * kLineKinds * kTileSlots;
+        const double *v1 = v0 + G * kTileSlots;
+        // every operand of the stage into registers (row sums start from VIN)
+        double F0[STEPS], F1[STEPS], F2[STEPS], VIN[STEPS], AUX[STEPS], ACC[STEPS];
+#pragma unroll
+        for (int i = 0; i < STEPS; ++i) {
+            const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;  // tile within the stage
+            const int e = (i % kTileSteps) * 32 + t;                         // element, this direction's order
+            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 1 - e : e);
+            const bool live = i < g * kTileSteps;
+            const double *ft = f + tp * kLineKinds * kTileSlots + e;
+            F0[i] = live ? ft[0] : 0.0;
+            F1[i] = live ? ft[kTileSlots] : 0.0;
+            F2[i] = live ? ft[2 * kTileSlots] : 0.0;
             if (!UPPER) {
-                if (upd) bulk_s2g(a.R + vb + bs, sp + m.v[0], cnt * 8);  // r_{k+1}
-                bulk_s2g(a.out + vb + bs, sp + m.v[1], cnt * 8);          // y
+                double vin = live ? v0[ve] : 0.0;
+                if (upd && live) {  // r_{k+1} = r_k - alpha A p (pcg.py:142)
+                    vin = __dsub_rn(vin, __dmul_rn(alpha, v1[ve]));
+                    acc2 = __dadd_rn(acc2, __dmul_rn(vin, vin));
+                }
+                VIN[i] = vin;
+                AUX[i] = 0.0;
             } else {
-                bulk_s2g(a.out + vb + bs, sp + m.v[0], cnt * 8);  // z
+                VIN[i] = live ? v0[ve] : 0.0;                     // y / diag
+                AUX[i] = (PCG && live) ? v1[ve] : 0.0;            // r
             }
+        }
+        __syncwarp();
+        LTR(2);
+        // refill the slot of stage j - 2: its results left by bulk store a stage ago
+        if (t == 0 && j >= 2 && j - 2 + NS < nstage) {
+            bulk_wait_read<1>();
+            issue(j - 2 + NS);
+        }
+        // left line's values at steps sig-1 .. sig+STEPS-2 (lane i holds step sig-1+i): one
+        // batch per stage, each slot re-armed after the read
+        double x = 0.0;
+        if (w > 0) {
+            const int xs = sig - 1 + t;
+            const bool pend = t < STEPS && xs >= P0 && xs < P1 && xs < C1 - 1;
+            double *px = rin + (xs & (R - 1));
+            if (pend) x = ld_vol(px);
+            while (__any_sync(0xffffffffu, pend && is_sentinel(x))) {
+                __nanosleep(20);
+                if (pend) x = ld_vol(px);
+            }
+            if (pend) st_vol(px, sentinel());
+        }
+        LTR(3);
+        // my outgoing slots for this stage must have been re-armed by the right warp; the
+        // check was loaded a stage ahead (a re-armed slot stays so until I write it)
+        if (w + 1 < W) {
+            const int ys = sig + t;
+            const bool chk = t < STEPS && ys >= Q0 && ys < Q1 && ys - R >= Q0;
+            const unsigned py = rout + (unsigned)(ys & (R - 1)) * 8u;
+            while (__any_sync(0xffffffffu, chk && !is_sentinel(ychk))) {
+                __nanosleep(20);
+                if (chk) ychk = ld_dsm(py);
+            }
+            const int yn = ys + STEPS;  // next stage's slots
+            const bool chn = t < STEPS && yn >= Q0 && yn < Q1 && yn - R >= Q0;
+            ychk = chn ? ld_dsm(rout + (unsigned)(yn & (R - 1)) * 8u) : sentinel();
+        }
+        LTR(4);
+#pragma unroll
+        for (int i = 0; i < STEPS; ++i) {
+            if (i >= g * kTileSteps) break;
+            const int step = sig + i;
+            const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;
+            const int e = (i % kTileSteps) * 32 + t;
+            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 1 - e : e);
+            const double pre = __dsub_rn(VIN[i], __dmul_rn(F0[i], lp));
+            const double p2 = __dmul_rn(F2[i], h0);
+            double l1 = __shfl_up_sync(0xffffffffu, h0, 1);
+            const double xl = __shfl_sync(0xffffffffu, x, i);
+            if (t == 0) l1 = xl;
+            double acc = __dsub_rn(pre, __dmul_rn(F1[i], l1));
+            acc = __dsub_rn(acc, p2);
+            h0 = acc;
+            lp = l1;
+            if (prod && step >= Q0 && step < Q1) st_dsm(rout + (unsigned)(step & (R - 1)) * 8u, acc);
+            ACC[i] = acc;
+        }
+        // results into the stage's own vector slices (their operands are in registers), then
+        // one bulk store per array: the steps above never wait on a divide or a global store
+        double *o0 = const_cast<double *>(v0), *o1 = const_cast<double *>(v1);
+#pragma unroll
+        for (int i = 0; i < STEPS; ++i) {
+            if (i >= g * kTileSteps) break;
+            const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;
+            const int e = (i % kTileSteps) * 32 + t;
+            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 1 - e : e);
+            if (!UPPER) {
+                o0[ve] = ACC[i];                     // y (diag_scale_kernel divides)
+                if (upd) o1[ve] = VIN[i];            // r_{k+1}
+            } else {
+                o0[ve] = ACC[i];
+                if (PCG) acc2 = __dadd_rn(acc2, __dmul_rn(AUX[i], ACC[i]));  // r.z (pcg.py:167)
+            }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (t == 0) {
+            const unsigned vbytes = (unsigned)g * kTileSlots * 8;
+            bulk_s2g(out + (size_t)lo * kTileSlots, o0, vbytes);
+            if (upd) bulk_s2g(rout_g + (size_t)lo * kTileSlots, o1, vbytes);
             bulk_commit();
         }
-    };
-    constexpr int D = 2;            // batch j - D is drained at iteration j
-    const int A = NS - D - 1 > 0 ? NS - D - 1 : 0;
-    if (elect) {
-        for (int mb = 0; mb < kPrefetchBatches && mb < nb; ++mb) prefetch(mb);
-
-        for (int mb = 0; mb < A && mb < nb; ++mb) issue_load(mb);
     }
-    for (int j = 0; j < nb; ++j) {
-        if (p == 0) LTRACE(3, j);
-        if (j >= D) drain(j - D);
-        if (p == 0) LTRACE(4, j);
-        const int mb = j + A;
-        if (elect && mb < nb) {
-            // the stage of batch mb last held mb - NS, drained at iteration mb - NS + D
-            if (mb - NS + D >= j) bulk_wait_read<0>();
-            else bulk_wait_read<1>();
-            issue_load(mb);
-            if (kPrefetchBatches > 0 && mb + kPrefetchBatches < nb) prefetch(mb + kPrefetchBatches);
-        }
-        const int s = j % NS;
-        mbar_wait(&mbar[s], (j / NS) & 1);  // batch j's blocks have landed
-        if (p == 0) LTRACE(6, j);
-        char *sp = stage_ptr(s);
-        const int cnt = s_bcount[j];
-        if (upd) {  // r -= alpha Ap (pcg.py:142), r.r of the new residual
-            double *r = reinterpret_cast<double *>(sp + m.v[0]);
-            const double *ap = reinterpret_cast<const double *>(sp + m.v[1]);
-            for (int u = p; u < cnt; u += kProd) {
-                const double rn = __dsub_rn(r[u], __dmul_rn(alpha, ap[u]));
-                r[u] = rn;
-                acc2 = __dadd_rn(acc2, __dmul_rn(rn, rn));
-            }
-        } else if (!UPPER && !NPCG_NO_ZERO_Y) {  // y is written into the (unloaded) second slice: padding slots must read 0
-            double2 *y = reinterpret_cast<double2 *>(sp + m.v[1]);
-            for (int u = p; u < cnt / 2; u += kProd) y[u] = make_double2(0.0, 0.0);
-        } else {  // z /= diag (sparse.py:273)
-            double *y = reinterpret_cast<double *>(sp + m.v[0]);
-            const double *dg = reinterpret_cast<const double *>(sp + m.v[1]);
-            for (int u = p; u < cnt; u += kProd) y[u] = __ddiv_rn(y[u], dg[u]);
-        }
-        if (p == 0) LTRACE(5, j);
-        if (!UPPER) fence_proxy_async();  // r_{k+1} / zeroed y writes -> their TMA store
-        bar_arrive(kBarFull + s, NT);
-    }
-    for (int mb = std::max(0, nb - D); mb < nb; ++mb) drain(mb);
-    if (elect) bulk_wait<0>();  // solved slices written before the CTA retires
-    if (PCG) {  // fixed-order reduction over the producer threads
+    if (t == 0) bulk_wait<0>();  // results written before the solve is complete
+    if (PCG) {  // fixed-order reduction: lanes, warps, then the cluster's CTAs
         double v = acc2;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
-        if ((p & 31) == 0) s_red[p >> 5] = v;
-        bar_sync(kBarProd, kProd);
-        if (p == 0) {
+        if (t == 0) s_red[wl] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
             double tot = 0.0;
-            for (int w = 0; w < kProdWarps; ++w) tot = __dadd_rn(tot, s_red[w]);
+            for (int q = 0; q < WL; ++q) tot = __dadd_rn(tot, s_red[q]);
+            if (C > 1) st_dsm(map_rank(&s_cta[rank], 0), tot);
+            else line_epilogue(a, b, tot);
+        }
+    }
+    if (C > 1) {  // remote rings / partials stay valid until every CTA of the cluster is done
+        cluster_sync_all();
+        if (PCG && rank == 0 && threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int q = 0; q < C; ++q) tot = __dadd_rn(tot, s_cta[q]);
             line_epilogue(a, b, tot);
         }
     }
@@ -321,25 +380,36 @@ int line_trace_copy(long long *out, int n) {
     return (int)cudaMemcpyFromSymbol(out, g_line_trace, n * sizeof(long long));
 }
 
-size_t line_smem_bytes(const LineDir &L, int stages, bool upper, bool pcg) {
-    return line_layout(L.T, L.window, L.md, L.max_slots, stages, upper ? (pcg ? 3 : 2) : 2, L.nbatch).total;
+static size_t line_smem(int WL, int R, int G, int NS, bool upper, bool pcg) {
+    return line_layout(WL, R, G, NS, line_vectors(upper, pcg)).total;
 }
 
-int line_stages_for(const LineDir &L, bool upper) {
-    int dev = 0, optin = 0;
+int line_config_for(const LineDir &L, bool upper, int B) {
+    int dev = 0, optin = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (optin <= 0) optin = 227 * 1024;
     const size_t cap = (size_t)optin - 1024;  // static shared memory
-    for (int ns = kLineMaxStages; ns >= 2; --ns)
-        if (line_smem_bytes(L, ns, upper, true) <= cap) return ns;
+    // CTAs per system: split over two SMs while the batch leaves them free
+    int C = (L.warps % 2 == 0 && 2 * B <= sms) ? 2 : 1;
+    if (const char *env = std::getenv("NPCG_LINE_CLUSTER")) C = (std::atoi(env) == 2 && L.warps % 2 == 0) ? 2 : 1;
+    const int WL = L.warps / C;
+    if (const char *env = std::getenv("NPCG_LINE_CFG")) {
+        const int c = std::atoi(env), G = c / 16, NS = c % 16;
+        if ((G == 1 || G == 2) && NS >= 3 && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
+    }
+    // stages >= 3: a slot is refilled two stages after its use (its results leave by bulk store)
+    static const int prefs[][2] = {{2, 4}, {2, 3}, {1, 4}, {1, 3}};
+    for (const auto &p : prefs)
+        if (line_smem(WL, L.ring, p[0], p[1], upper, true) <= cap) return C * 256 + p[0] * 16 + p[1];
     return 0;
 }
 
-template <int MD, bool UPPER, bool PCG, bool SB>
+template <bool UPPER, bool PCG, bool SB, int G, int C>
 static cudaError_t launch_line_t(const LineArgs &a, cudaStream_t s) {
-    auto kern = trsv_line_kernel<MD, UPPER, PCG, SB>;
-    const size_t smem = line_smem_bytes(a.dir, a.stages, UPPER, PCG);
+    auto kern = trsv_line_kernel<UPPER, PCG, SB, G, C>;
+    const size_t smem = line_smem(a.warps / C, a.ring, G, a.stages, UPPER, PCG);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -347,30 +417,68 @@ static cudaError_t launch_line_t(const LineArgs &a, cudaStream_t s) {
         configured = smem;
     }
     note_launch();
-    kern<<<a.B, a.dir.T + kProd, smem, s>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.B * C);
+    cfg.blockDim = dim3(32 * (a.warps / C));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <int MD>
-static cudaError_t launch_line_md(const LineArgs &a, cudaStream_t s) {
+template <int G, int C>
+static cudaError_t launch_line_gc(const LineArgs &a, cudaStream_t s) {
     const bool pcg = a.mode == TRSV_PCG;
     if (a.upper) {
-        if (pcg) return a.s_batched ? launch_line_t<MD, true, true, true>(a, s) : launch_line_t<MD, true, true, false>(a, s);
-        return a.s_batched ? launch_line_t<MD, true, false, true>(a, s) : launch_line_t<MD, true, false, false>(a, s);
+        if (pcg) return a.s_batched ? launch_line_t<true, true, true, G, C>(a, s) : launch_line_t<true, true, false, G, C>(a, s);
+        return a.s_batched ? launch_line_t<true, false, true, G, C>(a, s) : launch_line_t<true, false, false, G, C>(a, s);
     }
-    if (pcg) return a.s_batched ? launch_line_t<MD, false, true, true>(a, s) : launch_line_t<MD, false, true, false>(a, s);
-    return a.s_batched ? launch_line_t<MD, false, false, true>(a, s) : launch_line_t<MD, false, false, false>(a, s);
+    if (pcg) return a.s_batched ? launch_line_t<false, true, true, G, C>(a, s) : launch_line_t<false, true, false, G, C>(a, s);
+    return a.s_batched ? launch_line_t<false, false, true, G, C>(a, s) : launch_line_t<false, false, false, G, C>(a, s);
 }
 
 cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s) {
-    if (a.stages < 2 || a.stages > kLineMaxStages) return cudaErrorInvalidValue;
-    switch (a.dir.md) {
-        case 2: return launch_line_md<2>(a, s);
-        case 3: return launch_line_md<3>(a, s);
-        case 4: return launch_line_md<4>(a, s);
-        case 8: return launch_line_md<8>(a, s);
+    if (a.stages < 3 || a.warps < 1 || a.warps > kLineMaxWarps || a.warps % a.cluster) return cudaErrorInvalidValue;
+    const int key = a.cluster * 16 + a.group;
+    switch (key) {
+        case 16 + 1: return launch_line_gc<1, 1>(a, s);
+        case 16 + 2: return launch_line_gc<2, 1>(a, s);
+        case 32 + 1: return launch_line_gc<1, 2>(a, s);
+        case 32 + 2: return launch_line_gc<2, 2>(a, s);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// y /= diag (sparse.py:273) between the two solves: an elementwise pass
+// over every SM at HBM speed, where inside the wavefront kernels the divide
+// would sit on the few SMs that carry the solve.
+__global__ void __launch_bounds__(256) diag_scale_kernel(int nslot, const double *D, int d_batched, double *y) {
+    const int b = blockIdx.y;
+    const double2 *d2 = reinterpret_cast<const double2 *>(D + (d_batched ? (size_t)b * nslot : 0));
+    double2 *y2 = reinterpret_cast<double2 *>(y + (size_t)b * nslot);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nslot / 2; i += gridDim.x * blockDim.x) {
+        double2 v = y2[i];
+        const double2 d = d2[i];
+        v.x = __ddiv_rn(v.x, d.x);
+        v.y = __ddiv_rn(v.y, d.y);
+        y2[i] = v;
+    }
+}
+
+cudaError_t launch_diag_scale(int nslot, int B, const double *D, int d_batched, double *y, cudaStream_t s) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int per = (nslot / 2 + 255) / 256;
+    const int gx = std::max(1, std::min(per, (8 * sms + B - 1) / B));
+    note_launch();
+    diag_scale_kernel<<<dim3(gx, B), 256, 0, s>>>(nslot, D, d_batched, y);
+    return cudaGetLastError();
 }
 
 // packed[b][e] = S[vperm[e] * ps + b * bs]

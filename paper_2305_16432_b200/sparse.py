@@ -164,6 +164,7 @@ class SparseMatrixCsr:
             if not np.all(ok):
                 raise DimensionMismatchError("columns must strictly increase within rows")
         object.__setattr__(self, "_dev_vals", None)
+        object.__setattr__(self, "_sym", None)
 
     # -- constructors (sparse.py:69-108) --------------------------------------
 
@@ -225,15 +226,17 @@ class SparseMatrixCsr:
         return np.count_nonzero(self.row_indices() == self.col_idx) == self.n
 
     def is_symmetric(self):
-        """Exact (bitwise) value symmetry, checked on the device."""
-        pat = self.device_pattern()
-        if not pat_symmetric(pat):
-            return False
-        ok = (ctypes.c_int32 * 1)()
-        vals = self.device_values()
-        _native.check(_native.lib().npcg_check_symmetric_values(pat.handle, 1, _native.ptr(vals), 0,
-                                                                ok, _native.stream_handle()))
-        return bool(ok[0])
+        """Exact (bitwise) value symmetry, checked on the device (once: the
+        values are immutable, like the device copy they are checked on)."""
+        if self._sym is None:
+            pat = self.device_pattern()
+            ok = (ctypes.c_int32 * 1)()
+            if pat_symmetric(pat):
+                vals = self.device_values()
+                _native.check(_native.lib().npcg_check_symmetric_values(pat.handle, 1, _native.ptr(vals), 0,
+                                                                        ok, _native.stream_handle()))
+            object.__setattr__(self, "_sym", bool(ok[0]))
+        return self._sym
 
     def strict_lower(self):
         rows = self.row_indices()
