@@ -397,10 +397,10 @@ int line_config_for(const LineDir &L, bool upper, int B) {
     const int WL = L.warps / C;
     if (const char *env = std::getenv("NPCG_LINE_CFG")) {
         const int c = std::atoi(env), G = c / 16, NS = c % 16;
-        if ((G == 1 || G == 2) && NS >= 3 && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
+        if (G >= 1 && G <= 3 && NS >= 3 && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
     }
     // stages >= 3: a slot is refilled two stages after its use (its results leave by bulk store)
-    static const int prefs[][2] = {{2, 4}, {2, 3}, {1, 4}, {1, 3}};
+    static const int prefs[][2] = {{3, 3}, {2, 4}, {2, 3}, {1, 4}, {1, 3}};
     for (const auto &p : prefs)
         if (line_smem(WL, L.ring, p[0], p[1], upper, true) <= cap) return C * 256 + p[0] * 16 + p[1];
     return 0;
@@ -449,8 +449,10 @@ cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s) {
     switch (key) {
         case 16 + 1: return launch_line_gc<1, 1>(a, s);
         case 16 + 2: return launch_line_gc<2, 1>(a, s);
+        case 16 + 3: return launch_line_gc<3, 1>(a, s);
         case 32 + 1: return launch_line_gc<1, 2>(a, s);
         case 32 + 2: return launch_line_gc<2, 2>(a, s);
+        case 32 + 3: return launch_line_gc<3, 2>(a, s);
         default: return cudaErrorInvalidValue;
     }
 }

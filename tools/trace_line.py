@@ -38,18 +38,18 @@ def main():
     t = np.frombuffer(buf, dtype=np.int64).reshape(16, 2048)
     t0 = min(t[w, 1] for w in range(16) if t[w, 1] > 0)
     print("rc", rc, "(last launch of the solve = backward)")
-    names = ["wait", "operands", "issue+ring in", "ring out chk", "steps->next"]
+    names = ["wait", "operands", "ring in", "ring out chk", "steps", "tail"]
     for w in range(16):
         n = int((t[w, 1:] > 0).sum()) // 6
         if n < 3:
             continue
         ev = t[w, 1:6 * n + 1].reshape(n, 6).astype(float)
         seg = np.diff(ev, axis=1)                      # within a stage
-        tail = ev[1:, 0] - ev[:-1, 5]                   # steps of stage j (to the next stage's start)
+        tail = ev[1:, 0] - ev[:-1, 5]                   # after the steps until the next stage
         per = np.median(np.diff(ev[:, 0]))
         parts = [np.median(seg[:, k]) for k in range(5)] + [np.median(tail)]
         print(f"warp {w:2d} first step {t[w, 0]:4d} stages {n:3d} cyc/stage {per:7.1f} | " +
-              " ".join(f"{nm}={v:.0f}" for nm, v in zip(["pre", *names], parts)))
+              " ".join(f"{nm}={v:.0f}" for nm, v in zip(names, parts)))
 
 if __name__ == "__main__":
     main()
