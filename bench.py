@@ -132,10 +132,11 @@ def roofline(A, nnz_lower, prof, iters, peak_gbs):
     solves, trsv_kernel) and of a whole PCG iteration.
 
     Per launch, fp64 values / int32 indices, compulsory traffic only:
-      trsv fwd: 12*nnz(L) + 4(n+1) + per active column 56 n
-                (read r, Ap, x, p; write r, x, y)
-      trsv bwd: 12*nnz(L) + 4(n+1) + 8 n (D) + per active column 24 n
-                (read y, r; write z)
+      trsv fwd: 12*nnz(L) + 4(n+1) + per active column 32 n
+                (read r, Ap; write r_{k+1}, y; the y /= diag pass is timed
+                with it and adds 8 n (diag) + 16 n per column)
+      trsv bwd: 12*nnz(L) + 4(n+1) + per active column 24 n
+                (read y/diag, r; write z)
     Whole iteration: M + B V with
       M = 12 nnz(A) + 4(n+1) + 2 (12 nnz(L) + 4(n+1)) + 8 n,  V = 104 n.
     """
@@ -145,8 +146,8 @@ def roofline(A, nnz_lower, prof, iters, peak_gbs):
     nfwd = prof["kernel_launches"]["trsv_fwd"]
     nbwd = prof["kernel_launches"]["trsv_bwd"]
     ncol = len(iters)
-    fwd_bytes = nfwd * ML + col_iters * 56 * n + ncol * 16 * n  # + the initial z = P^-1 r solves
-    bwd_bytes = nbwd * (ML + 8 * n) + (col_iters + ncol) * 24 * n
+    fwd_bytes = nfwd * (ML + 8 * n) + col_iters * 48 * n + ncol * 32 * n  # + the initial z = P^-1 r solves
+    bwd_bytes = nbwd * ML + (col_iters + ncol) * 24 * n
     t_trsv = (prof["kernel_ms"]["trsv_fwd"] + prof["kernel_ms"]["trsv_bwd"]) * 1e-3
     achieved = (fwd_bytes + bwd_bytes) / t_trsv / 1e9
     M = 12 * nnz + 4 * (n + 1) + 2 * ML + 8 * n
@@ -154,7 +155,7 @@ def roofline(A, nnz_lower, prof, iters, peak_gbs):
     t_loop = sum(prof["kernel_ms"].values()) * 1e-3
     iter_gbs = iter_bytes / t_loop / 1e9
     return {
-        "kernel": "trsv_kernel (forward + backward triangular solves)",
+        "kernel": "trsv_line_kernel (forward + backward triangular solves; forward includes diag_scale_kernel)",
         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
         "frac": round(achieved / peak_gbs, 4), "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
         "traffic": ncu_traffic(),
