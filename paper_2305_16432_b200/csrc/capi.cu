@@ -720,6 +720,12 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     apdot.op = SPMV_APDOT;
     apdot.X = s->P;
     apdot.Y = s->AP;
+    if (s->ls) {  // the drift check rides on the next APDOT launch (no separate drift SpMV)
+        apdot.merge_drift = 1;
+        apdot.X2 = xv;
+        apdot.Bv = bv;
+        apdot.R = s->R;
+    }
     SpmvArgs drift = spl;
     drift.op = SPMV_RESID_DRIFT;
     drift.X = xv;
@@ -793,7 +799,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         for (int q = 0; q < check; ++q) {
             NPCG_CUDA(timed(NPCG_PROF_SPMV_APDOT, [&] { return launch_spmv(apdot, st); }));
             NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return fw.launch(st); }));
-            NPCG_CUDA(timed(NPCG_PROF_SPMV_DRIFT, [&] { return launch_spmv(drift, st); }));
+            if (!s->ls) NPCG_CUDA(timed(NPCG_PROF_SPMV_DRIFT, [&] { return launch_spmv(drift, st); }));
             NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return bw.launch(st); }));
             NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
         }

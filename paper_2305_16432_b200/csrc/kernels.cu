@@ -24,6 +24,7 @@ __device__ __forceinline__ bool spmv_col_active(const SpmvArgs &a, int b) {
     switch (a.op) {
         case SPMV_PLAIN: return true;
         case SPMV_APDOT:
+            if (a.merge_drift && a.st.status[b] == ST_ACTIVE && a.st.phase[b] == PH_DRIFT) return true;
             return a.st.status[b] == ST_ACTIVE && a.st.phase[b] == PH_ITER && a.st.k[b] < a.st.max_iter;
         case SPMV_RESID_INIT: return a.st.status[b] == ST_ACTIVE;
         case SPMV_RESID_DRIFT: return a.st.status[b] == ST_ACTIVE && a.st.phase[b] == PH_DRIFT;
@@ -35,7 +36,10 @@ __device__ __forceinline__ bool spmv_col_active(const SpmvArgs &a, int b) {
 // Per-column control logic after the batch reduction (one thread per column).
 __device__ void spmv_epilogue(const SpmvArgs &a, int b, double total) {
     const SolveState &st = a.st;
-    switch (a.op) {
+    const int op = (a.op == SPMV_APDOT && a.merge_drift && st.status[b] == ST_ACTIVE && st.phase[b] == PH_DRIFT)
+                       ? SPMV_RESID_DRIFT
+                       : a.op;
+    switch (op) {
         case SPMV_APDOT: {  // pcg.py:134-141
             if (st.status[b] != ST_ACTIVE || st.phase[b] != PH_ITER) return;
             if (st.k[b] >= st.max_iter) {  // while k < max_iter fell through
@@ -824,6 +828,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_ell_kernel(SpmvArgs a) {
     __shared__ unsigned char s_act[kMaxBatch];
     __shared__ unsigned char s_xp[kMaxBatch];
     __shared__ double s_al[kMaxBatch];
+    __shared__ unsigned char s_dr[kMaxBatch];
     const int B = a.B, ns = a.nslot, lane = threadIdx.x & 31, team = threadIdx.x >> 5;
     const int bl = blockIdx.y * kEllCols, bh = min(B, bl + kEllCols);  // this block's columns
     if (OP == SPMV_RESID_DRIFT && *a.drift_count == 0) return;
@@ -831,6 +836,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_ell_kernel(SpmvArgs a) {
         s_act[b] = spmv_col_active(a, b) ? 1 : 0;
         s_xp[b] = OP == SPMV_RESID_DRIFT && a.st.xpend[b];
         s_al[b] = s_xp[b] ? a.st.alpha[b] : 0.0;
+        // merged drift columns: true residual from X2 (x already holds x + alpha p)
+        s_dr[b] = OP == SPMV_APDOT && a.merge_drift && a.st.status[b] == ST_ACTIVE && a.st.phase[b] == PH_DRIFT;
     }
     __syncthreads();
     const int q = blockIdx.x * kSpmvThreads + threadIdx.x;
@@ -858,7 +865,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_ell_kernel(SpmvArgs a) {
         for (int u = 0; u < NB; ++u) {
             const int b = min(b0 + u, bh - 1);
             const size_t vb = (size_t)b * ns;
-            const char *Xb = reinterpret_cast<const char *>(a.X + vb);
+            const bool dr = OP == SPMV_APDOT && s_dr[b];
+            const char *Xb = reinterpret_cast<const char *>((dr ? a.X2 : a.X) + vb);
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 xv[u][e] = use_x ? *reinterpret_cast<const double *>(Xb + cb[e]) : 0.0;
@@ -866,7 +874,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_ell_kernel(SpmvArgs a) {
                     xv[u][e] = __dadd_rn(xv[u][e], __dmul_rn(s_al[b], *reinterpret_cast<const double *>(
                                                                        reinterpret_cast<const char *>(a.P + vb) + cb[e])));
             }
-            own[u] = OP == SPMV_APDOT ? a.X[vb + qq] : a.Bv[vb + qq];
+            own[u] = (OP == SPMV_APDOT && !dr) ? a.X[vb + qq] : a.Bv[vb + qq];
         }
         double pr[NB];
 #pragma unroll
@@ -881,7 +889,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_ell_kernel(SpmvArgs a) {
                 acc = __dadd_rn(acc, __dmul_rn(vv, xv[u][e]));
             }
             pr[u] = 0.0;
-            if (OP == SPMV_APDOT) {
+            if (OP == SPMV_APDOT && !s_dr[min(b, bh - 1)]) {
                 if (on) a.Y[vb + q] = acc;
                 pr[u] = on ? __dmul_rn(own[u], acc) : 0.0;  // p.Ap (pcg.py:134)
             } else {

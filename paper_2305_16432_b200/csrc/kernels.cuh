@@ -41,6 +41,10 @@ struct SpmvArgs {
     // line-order ELL (ecol != null): every operand [b][nslot], see spmv_ell_kernel
     const int *ecol = nullptr;
     const double *evals = nullptr;
+    // APDOT only: columns in PH_DRIFT compute their true residual R = Bv - A X2
+    // in the same launch (the drift check of the previous pass, pcg.py:147-165)
+    int merge_drift = 0;
+    const double *X2 = nullptr;
     int ell_width = 0;
     size_t partial_cap = 0;  // doubles available at `partial`
 };
