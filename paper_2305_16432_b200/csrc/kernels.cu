@@ -819,7 +819,13 @@ static void spmv_warp_vw(const SpmvArgs &a, int grid, size_t smem, cudaStream_t 
 // per block and every vector access of a warp is one contiguous 256-byte
 // run (the row's own slot) or a gather within +-2 grid lines of it (L1).
 // ===========================================================================
-constexpr int kEllCols = 32;  // systems per block (blockIdx.y picks the group)
+#ifndef NPCG_ELL_COLS
+#define NPCG_ELL_COLS 32
+#endif
+#ifndef NPCG_ELL_NB
+#define NPCG_ELL_NB 4
+#endif
+constexpr int kEllCols = NPCG_ELL_COLS;  // systems per block (blockIdx.y picks the group)
 
 template <int E, bool VB, int OP>
 __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_ell_kernel(SpmvArgs a) {
@@ -857,7 +863,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_ell_kernel(SpmvArgs a) {
     const bool use_x = OP != SPMV_RESID_INIT || a.has_x;
     // NB systems at a time: their gathers are in flight together and their
     // dot-product trees interleave
-    constexpr int NB = 4;
+    constexpr int NB = NPCG_ELL_NB;
     for (int b0 = bl; b0 < bh; b0 += NB) {
         // every load of the NB systems first (no branch between them), then the sums
         double xv[NB][E], own[NB];

@@ -319,7 +319,8 @@ static bool build_line_sched(const Pattern &P, LineSched &LS) {
     LS.h_slot.assign(n, -1);
     for (int32_t i = 0; i < n; ++i) {
         const int32_t q = line[i] + pad, w = q / 32, d = fstep(i) - s0[w];
-        const int32_t slot = (t0[w] + d / kTileSteps) * kTileSlots + (d % kTileSteps) * 32 + q % 32;
+        const int32_t qs = d % kTileSteps;  // a lane's steps 2h, 2h+1 are adjacent
+        const int32_t slot = (t0[w] + d / kTileSteps) * kTileSlots + (qs >> 1) * 64 + (q % 32) * 2 + (qs & 1);
         LS.h_slot[i] = slot;
         LS.h_rowof[slot] = i;
     }

@@ -68,7 +68,8 @@ struct SchedSet {
 //
 // Line order ("slots"): lines are placed on lanes 32w + t (forward, padded at
 // the front to a multiple of 32); each warp's step range is cut into tiles
-// of kTileSteps steps x 32 lanes, element q * 32 + t, and a warp's tiles are
+// of kTileSteps steps x 32 lanes, element (q / 2) * 64 + 2 t + q % 2 (a
+// lane's two steps of a tile half are adjacent: 16-byte loads), and a warp's tiles are
 // contiguous, so every pipeline stage of a warp is one bulk copy per array.
 // The backward solve traverses the same tiles in reverse (warp W-1-w, lane
 // 31-t, element 127-e), so one slot order serves both directions and every

@@ -44,6 +44,10 @@ namespace npcg {
 
 namespace {
 
+// operand stages per warp: a slot is refilled two stages after its use (its
+// results leave by bulk store from the slot a stage later)
+constexpr int kLineStages = 3;
+
 struct LineSmem {  // byte offsets into dynamic shared memory
     size_t ring, mbar, stage0, stage_bytes, total;
 };
@@ -93,6 +97,10 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// element of (step q of a tile, lane t) in a direction's traversal order:
+// a lane's steps 2h and 2h+1 are adjacent (pattern.h)
+__device__ __forceinline__ int tile_elem(int q, int t) { return (q >> 1) * 64 + t * 2 + (q & 1); }
+
 __device__ __forceinline__ void line_epilogue(const LineArgs &a, int b, double total) {
     if (a.upper) bwd_epilogue(a.st, b, total);
     else fwd_epilogue(a.st, b, total, a.drift_count);
@@ -113,7 +121,8 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
     extern __shared__ __align__(128) char sm[];
     __shared__ double s_red[kLineMaxWarps];
     __shared__ double s_cta[4];
-    const int W = a.warps, WL = W / C, NS = a.stages, R = a.ring;
+    constexpr int NS = kLineStages;
+    const int W = a.warps, WL = W / C, R = a.ring;
     const int wl = threadIdx.x >> 5, t = threadIdx.x & 31;
     const int rank = C > 1 ? (int)cluster_rank() : 0, b = blockIdx.x / C;
     const int w = rank * WL + wl;  // warp of the direction's schedule
@@ -224,10 +233,10 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
     for (int j = 0; j < nstage; ++j) {
         const int s = j % NS, sig = C0 + j * STEPS;  // first step of the stage
 #ifdef NPCG_LINE_TRACE
-        const bool tr = b == 0 && t == 0 && w < kTraceEvents && 6 * j + 6 < kTraceBatches;
+        const bool tr = b == 0 && t == 0 && w < kTraceEvents && 10 * j + 11 < kTraceBatches;
 #define LTR(k)                                                   \
     do {                                                         \
-        if (tr) g_line_trace[w][6 * j + 1 + (k)] = clock64();    \
+        if (tr) g_line_trace[w][10 * j + 1 + (k)] = clock64();   \
     } while (0)
         if (tr && j == 0) g_line_trace[w][0] = C0;
         LTR(0);
@@ -246,28 +255,41 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
         const double *v1 = v0 + G * kTileSlots;
         // every operand of the stage into registers (row sums start from VIN)
         double F0[STEPS], F1[STEPS], F2[STEPS], VIN[STEPS], AUX[STEPS], ACC[STEPS];
+        // a lane's two steps of a tile half are adjacent (pattern.h): one 16-byte load each
 #pragma unroll
-        for (int i = 0; i < STEPS; ++i) {
+        for (int pi = 0; pi < STEPS / 2; ++pi) {
+            const int i = 2 * pi;
             const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;  // tile within the stage
-            const int e = (i % kTileSteps) * 32 + t;                         // element, this direction's order
-            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 1 - e : e);
+            const int e = tile_elem(i % kTileSteps, t);                      // element of step i, this direction
             const bool live = i < g * kTileSteps;
             const double *ft = f + tp * kLineKinds * kTileSlots + e;
-            F0[i] = live ? ft[0] : 0.0;
-            F1[i] = live ? ft[kTileSlots] : 0.0;
-            F2[i] = live ? ft[2 * kTileSlots] : 0.0;
-            if (!UPPER) {
-                double vin = live ? v0[ve] : 0.0;
-                if (upd && live) {  // r_{k+1} = r_k - alpha A p (pcg.py:142)
-                    vin = __dsub_rn(vin, __dmul_rn(alpha, v1[ve]));
-                    acc2 = __dadd_rn(acc2, __dmul_rn(vin, vin));
-                }
-                VIN[i] = vin;
-                AUX[i] = 0.0;
-            } else {
-                VIN[i] = live ? v0[ve] : 0.0;                     // y / diag
-                AUX[i] = (PCG && live) ? v1[ve] : 0.0;            // r
+            const double2 z2 = make_double2(0.0, 0.0);
+            const double2 f0 = live ? *reinterpret_cast<const double2 *>(ft) : z2;
+            const double2 f1 = live ? *reinterpret_cast<const double2 *>(ft + kTileSlots) : z2;
+            const double2 f2 = live ? *reinterpret_cast<const double2 *>(ft + 2 * kTileSlots) : z2;
+            F0[i] = f0.x, F0[i + 1] = f0.y, F1[i] = f1.x, F1[i + 1] = f1.y, F2[i] = f2.x, F2[i + 1] = f2.y;
+            // vectors are in forward tile order: the backward pair is reversed
+            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
+            double2 a0 = live ? *reinterpret_cast<const double2 *>(v0 + ve) : z2;
+            double2 a1 = (live && NV > 1) ? *reinterpret_cast<const double2 *>(v1 + ve) : z2;
+            if (UPPER) {
+                a0 = make_double2(a0.y, a0.x);
+                a1 = make_double2(a1.y, a1.x);
             }
+            if (!UPPER) {
+                if (upd && live) {  // r_{k+1} = r_k - alpha A p (pcg.py:142)
+                    a0.x = __dsub_rn(a0.x, __dmul_rn(alpha, a1.x));
+                    a0.y = __dsub_rn(a0.y, __dmul_rn(alpha, a1.y));
+                    acc2 = __dadd_rn(acc2, __dmul_rn(a0.x, a0.x));
+                    acc2 = __dadd_rn(acc2, __dmul_rn(a0.y, a0.y));
+                }
+                AUX[i] = AUX[i + 1] = 0.0;
+            } else {
+                AUX[i] = PCG ? a1.x : 0.0;  // r
+                AUX[i + 1] = PCG ? a1.y : 0.0;
+            }
+            VIN[i] = a0.x;  // r_{k+1} | y / diag
+            VIN[i + 1] = a0.y;
         }
         __syncwarp();
         LTR(2);
@@ -276,6 +298,7 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
             bulk_wait_read<1>();
             issue(j - 2 + NS);
         }
+        LTR(3);
         // left line's values at steps sig-1 .. sig+STEPS-2 (lane i holds step sig-1+i): one
         // batch per stage, each slot re-armed after the read
         double x = 0.0;
@@ -290,7 +313,7 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
             }
             if (pend) st_vol(px, sentinel());
         }
-        LTR(3);
+        LTR(4);
         // my outgoing slots for this stage must have been re-armed by the right warp; the
         // check was loaded a stage ahead (a re-armed slot stays so until I write it)
         if (w + 1 < W) {
@@ -305,14 +328,11 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
             const bool chn = t < STEPS && yn >= Q0 && yn < Q1 && yn - R >= Q0;
             ychk = chn ? ld_dsm(rout + (unsigned)(yn & (R - 1)) * 8u) : sentinel();
         }
-        LTR(4);
+        LTR(5);
 #pragma unroll
         for (int i = 0; i < STEPS; ++i) {
             if (i >= g * kTileSteps) break;
             const int step = sig + i;
-            const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;
-            const int e = (i % kTileSteps) * 32 + t;
-            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 1 - e : e);
             const double pre = __dsub_rn(VIN[i], __dmul_rn(F0[i], lp));
             const double p2 = __dmul_rn(F2[i], h0);
             double l1 = __shfl_up_sync(0xffffffffu, h0, 1);
@@ -325,31 +345,39 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
             if (prod && step >= Q0 && step < Q1) st_dsm(rout + (unsigned)(step & (R - 1)) * 8u, acc);
             ACC[i] = acc;
         }
+        LTR(6);
         // results into the stage's own vector slices (their operands are in registers), then
         // one bulk store per array: the steps above never wait on a divide or a global store
         double *o0 = const_cast<double *>(v0), *o1 = const_cast<double *>(v1);
 #pragma unroll
-        for (int i = 0; i < STEPS; ++i) {
+        for (int pi = 0; pi < STEPS / 2; ++pi) {
+            const int i = 2 * pi;
             if (i >= g * kTileSteps) break;
             const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;
-            const int e = (i % kTileSteps) * 32 + t;
-            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 1 - e : e);
+            const int e = tile_elem(i % kTileSteps, t);
+            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
             if (!UPPER) {
-                o0[ve] = ACC[i];                     // y (diag_scale_kernel divides)
-                if (upd) o1[ve] = VIN[i];            // r_{k+1}
+                *reinterpret_cast<double2 *>(o0 + ve) = make_double2(ACC[i], ACC[i + 1]);  // y (diag_scale_kernel divides)
+                if (upd) *reinterpret_cast<double2 *>(o1 + ve) = make_double2(VIN[i], VIN[i + 1]);  // r_{k+1}
             } else {
-                o0[ve] = ACC[i];
-                if (PCG) acc2 = __dadd_rn(acc2, __dmul_rn(AUX[i], ACC[i]));  // r.z (pcg.py:167)
+                *reinterpret_cast<double2 *>(o0 + ve) = make_double2(ACC[i + 1], ACC[i]);
+                if (PCG) {  // r.z (pcg.py:167)
+                    acc2 = __dadd_rn(acc2, __dmul_rn(AUX[i], ACC[i]));
+                    acc2 = __dadd_rn(acc2, __dmul_rn(AUX[i + 1], ACC[i + 1]));
+                }
             }
         }
+        LTR(7);
         fence_proxy_async();
         __syncwarp();
+        LTR(8);
         if (t == 0) {
             const unsigned vbytes = (unsigned)g * kTileSlots * 8;
             bulk_s2g(out + (size_t)lo * kTileSlots, o0, vbytes);
             if (upd) bulk_s2g(rout_g + (size_t)lo * kTileSlots, o1, vbytes);
             bulk_commit();
         }
+        LTR(9);
     }
     if (t == 0) bulk_wait<0>();  // results written before the solve is complete
     if (PCG) {  // fixed-order reduction: lanes, warps, then the cluster's CTAs
@@ -397,10 +425,10 @@ int line_config_for(const LineDir &L, bool upper, int B) {
     const int WL = L.warps / C;
     if (const char *env = std::getenv("NPCG_LINE_CFG")) {
         const int c = std::atoi(env), G = c / 16, NS = c % 16;
-        if (G >= 1 && G <= 3 && NS >= 3 && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
+        if (G >= 1 && G <= 3 && NS == kLineStages && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
     }
     // stages >= 3: a slot is refilled two stages after its use (its results leave by bulk store)
-    static const int prefs[][2] = {{3, 3}, {2, 4}, {2, 3}, {1, 4}, {1, 3}};
+    static const int prefs[][2] = {{3, kLineStages}, {2, kLineStages}, {1, kLineStages}};
     for (const auto &p : prefs)
         if (line_smem(WL, L.ring, p[0], p[1], upper, true) <= cap) return C * 256 + p[0] * 16 + p[1];
     return 0;
@@ -444,7 +472,7 @@ static cudaError_t launch_line_gc(const LineArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s) {
-    if (a.stages < 3 || a.warps < 1 || a.warps > kLineMaxWarps || a.warps % a.cluster) return cudaErrorInvalidValue;
+    if (a.stages != kLineStages || a.warps < 1 || a.warps > kLineMaxWarps || a.warps % a.cluster) return cudaErrorInvalidValue;
     const int key = a.cluster * 16 + a.group;
     switch (key) {
         case 16 + 1: return launch_line_gc<1, 1>(a, s);

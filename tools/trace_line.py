@@ -38,18 +38,17 @@ def main():
     t = np.frombuffer(buf, dtype=np.int64).reshape(16, 2048)
     t0 = min(t[w, 1] for w in range(16) if t[w, 1] > 0)
     print("rc", rc, "(last launch of the solve = backward)")
-    names = ["wait", "operands", "ring in", "ring out chk", "steps", "tail"]
+    names = ["wait", "operands", "refill", "ring in", "ring out chk", "steps", "results", "fence", "store", "loop"]
     for w in range(16):
-        n = int((t[w, 1:] > 0).sum()) // 6
+        n = int((t[w, 1:] > 0).sum()) // 10
         if n < 3:
             continue
-        ev = t[w, 1:6 * n + 1].reshape(n, 6).astype(float)
+        ev = t[w, 1:10 * n + 1].reshape(n, 10).astype(float)
         seg = np.diff(ev, axis=1)                      # within a stage
-        tail = ev[1:, 0] - ev[:-1, 5]                   # after the steps until the next stage
+        tail = ev[1:, 0] - ev[:-1, 9]                   # to the next stage
         per = np.median(np.diff(ev[:, 0]))
-        parts = [np.median(seg[:, k]) for k in range(5)] + [np.median(tail)]
-        print(f"warp {w:2d} first step {t[w, 0]:4d} stages {n:3d} cyc/stage {per:7.1f} | " +
-              " ".join(f"{nm}={v:.0f}" for nm, v in zip(names, parts)))
+        parts = [np.median(seg[:, k]) for k in range(9)] + [np.median(tail)]
+        print(f"w{w:2d} cyc/stage {per:6.0f} | " + " ".join(f"{nm}={v:.0f}" for nm, v in zip(names, parts)))
 
 if __name__ == "__main__":
     main()
