@@ -117,6 +117,7 @@ __device__ long long g_line_trace[kTraceEvents][kTraceBatches];
 template <bool UPPER, bool PCG, bool SB, int G, int C>
 __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(LineArgs a) {
     constexpr int STEPS = kTileSteps * G;
+    static_assert(2 * STEPS <= 32, "a stage pair's ring slots are checked by one warp");
     constexpr int NV = line_vectors(UPPER, PCG);
     extern __shared__ __align__(128) char sm[];
     __shared__ double s_red[kLineMaxWarps];
@@ -224,10 +225,10 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
     double h0 = 0.0;  // my value one step back
     double lp = 0.0;  // left neighbour's value two steps back (at the next step)
     double acc2 = 0.0;
-    double ychk = sentinel();  // this stage's outgoing-slot check (loaded a stage ahead)
+    double ychk = sentinel();  // this stage pair's outgoing-slot check (loaded a pair ahead)
     if (w + 1 < W) {
         const int ys = C0 + t;
-        if (t < STEPS && ys >= Q0 && ys < Q1 && ys - R >= Q0) ychk = ld_dsm(rout + (unsigned)(ys & (R - 1)) * 8u);
+        if (t < 2 * STEPS && ys >= Q0 && ys < Q1 && ys - R >= Q0) ychk = ld_dsm(rout + (unsigned)(ys & (R - 1)) * 8u);
     }
     if (cons) lp = ring_read(C0 - 2);
     for (int j = 0; j < nstage; ++j) {
@@ -314,18 +315,19 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
             if (pend) st_vol(px, sentinel());
         }
         LTR(4);
-        // my outgoing slots for this stage must have been re-armed by the right warp; the
-        // check was loaded a stage ahead (a re-armed slot stays so until I write it)
-        if (w + 1 < W) {
+        // my outgoing slots of this stage pair must have been re-armed by the right warp;
+        // checked once per two stages (lane i: step sig + i), loaded two stages ahead (a
+        // re-armed slot stays so until I write it)
+        if (w + 1 < W && (j & 1) == 0) {
             const int ys = sig + t;
-            const bool chk = t < STEPS && ys >= Q0 && ys < Q1 && ys - R >= Q0;
+            const bool chk = t < 2 * STEPS && ys >= Q0 && ys < Q1 && ys - R >= Q0;
             const unsigned py = rout + (unsigned)(ys & (R - 1)) * 8u;
             while (__any_sync(0xffffffffu, chk && !is_sentinel(ychk))) {
                 __nanosleep(20);
                 if (chk) ychk = ld_dsm(py);
             }
-            const int yn = ys + STEPS;  // next stage's slots
-            const bool chn = t < STEPS && yn >= Q0 && yn < Q1 && yn - R >= Q0;
+            const int yn = ys + 2 * STEPS;  // the next pair's slots
+            const bool chn = t < 2 * STEPS && yn >= Q0 && yn < Q1 && yn - R >= Q0;
             ychk = chn ? ld_dsm(rout + (unsigned)(yn & (R - 1)) * 8u) : sentinel();
         }
         LTR(5);
