@@ -371,7 +371,7 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
         const LineSched &ls = *s->ls;
         int width = 0;
         for (int64_t i = 0; i < A->n; ++i) width = std::max<int>(width, A->h_rp[i + 1] - A->h_rp[i]);
-        s->ell_width = width <= 4 ? 4 : width <= 8 ? 8 : width <= 12 ? 12 : width <= 16 ? 16 : 0;
+        s->ell_width = width <= 4 ? 4 : width <= 7 ? 7 : width <= 8 ? 8 : width <= 12 ? 12 : width <= 16 ? 16 : 0;
         if (!s->ell_width) s->ls = nullptr;
     }
     const size_t nB = (size_t)A->n * B;

@@ -939,6 +939,7 @@ static cudaError_t launch_spmv_ell(const SpmvArgs &a, cudaStream_t s) {
     if ((size_t)grid.x * a.B > a.partial_cap) return cudaErrorInvalidValue;
     switch (a.ell_width) {
         case 4: spmv_ell_e<4>(a, grid, s); break;
+        case 7: spmv_ell_e<7>(a, grid, s); break;
         case 8: spmv_ell_e<8>(a, grid, s); break;
         case 12: spmv_ell_e<12>(a, grid, s); break;
         case 16: spmv_ell_e<16>(a, grid, s); break;
