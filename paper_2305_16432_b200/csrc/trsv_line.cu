@@ -504,10 +504,7 @@ __global__ void __launch_bounds__(256) diag_scale_kernel(int nslot, const double
 }
 
 cudaError_t launch_diag_scale(int nslot, int B, const double *D, int d_batched, double *y, cudaStream_t s) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int per = (nslot / 2 + 255) / 256;
-    const int gx = std::max(1, std::min(per, (8 * sms + B - 1) / B));
+    const int gx = std::max(1, (nslot / 2 + 255) / 256);  // one pair per thread: the divides are latency bound
     note_launch();
     diag_scale_kernel<<<dim3(gx, B), 256, 0, s>>>(nslot, D, d_batched, y);
     return cudaGetLastError();
