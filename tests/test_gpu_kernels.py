@@ -68,7 +68,7 @@ def test_apply_inverse_chunkings_bitwise(gpu, monkeypatch, chunk_rows):
     np.testing.assert_array_equal(sparse.ldlt_apply_inverse(F, r), oF.apply_inverse(r))
 
 
-@pytest.mark.parametrize("path,k", [("lines", 26), ("levels", 27)])
+@pytest.mark.parametrize("path,k", [("lines", 26), ("lines", 64), ("lines", 96), ("levels", 27)])
 def test_apply_inverse_paths_bitwise(gpu, monkeypatch, path, k):
     """Both triangular-solve engines -- the line wavefront (line-order
     vectors) and the chunked level schedule -- give the reference's bits,
@@ -94,6 +94,21 @@ def test_apply_inverse_paths_bitwise(gpu, monkeypatch, path, k):
     for b in range(B):
         oF = port.Factor(A.n, port.Csr(A.n, low.row_ptr, low.col_idx, vals[:, b]), A.diagonal())
         np.testing.assert_array_equal(Z[:, b], oF.apply_inverse(R[:, b]))
+
+
+def test_apply_inverse_wide_grid_bitwise(gpu):
+    """A 513 x 513 grid (511 lines: 16 warps, a 2-CTA cluster per system,
+    one-tile stages): bitwise equal to the reference's solve."""
+    prob = inputs.poisson_2d(k=512, batch=1)
+    A = prob.A
+    rng = np.random.default_rng(5)
+    low = A.strict_lower()
+    vals = rng.uniform(-0.3, 0.3, size=low.nnz)
+    F = sparse.LowerFactor(A.n, sparse.SparseMatrixCsr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    R = rng.standard_normal((A.n, 2))
+    oF = port.Factor(A.n, port.Csr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    for b in range(2):
+        np.testing.assert_array_equal(sparse.ldlt_apply_inverse(F, R[:, b]), oF.apply_inverse(R[:, b]))
 
 
 _LINES_VS_LEVELS = r"""
