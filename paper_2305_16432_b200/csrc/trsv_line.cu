@@ -101,6 +101,20 @@ __device__ __forceinline__ void cluster_sync_all() {
 // a lane's steps 2h and 2h+1 are adjacent (pattern.h)
 __device__ __forceinline__ int tile_elem(int q, int t) { return (q >> 1) * 64 + t * 2 + (q & 1); }
 
+// sum of u[i] v[i] over a stage's steps in a fixed pairwise order (padding
+// steps hold zeros), so the running dot product waits on one add per stage
+template <int N>
+__device__ __forceinline__ double stage_dot(const double (&u)[N], const double (&v)[N]) {
+    double p[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) p[i] = __dmul_rn(u[i], v[i]);
+#pragma unroll
+    for (int h = 1; h < N; h <<= 1)
+#pragma unroll
+        for (int i = 0; i + h < N; i += 2 * h) p[i] = __dadd_rn(p[i], p[i + h]);
+    return p[0];
+}
+
 __device__ __forceinline__ void line_epilogue(const LineArgs &a, int b, double total) {
     if (a.upper) bwd_epilogue(a.st, b, total);
     else fwd_epilogue(a.st, b, total, a.drift_count);
@@ -234,7 +248,7 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
     for (int j = 0; j < nstage; ++j) {
         const int s = j % NS, sig = C0 + j * STEPS;  // first step of the stage
 #ifdef NPCG_LINE_TRACE
-        const bool tr = b == 0 && t == 0 && w < kTraceEvents && 10 * j + 11 < kTraceBatches;
+        const bool tr = b == 0 && t == 0 && w < kTraceEvents && 10 * j + 11 < kTraceBatches && (NPCG_LINE_TRACE != 2 || !UPPER);
 #define LTR(k)                                                   \
     do {                                                         \
         if (tr) g_line_trace[w][10 * j + 1 + (k)] = clock64();   \
@@ -256,42 +270,41 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
         const double *v1 = v0 + G * kTileSlots;
         // every operand of the stage into registers (row sums start from VIN)
         double F0[STEPS], F1[STEPS], F2[STEPS], VIN[STEPS], AUX[STEPS], ACC[STEPS];
-        // a lane's two steps of a tile half are adjacent (pattern.h): one 16-byte load each
+#pragma unroll
+        for (int i = 0; i < STEPS; ++i) ACC[i] = 0.0;  // padding steps of a partial stage
+        // a lane's two steps of a tile half are adjacent (pattern.h): one 16-byte load each.
+        // Every load is unconditional (a partial stage's missing tiles read stale slot
+        // contents, masked below), so they issue back to back
 #pragma unroll
         for (int pi = 0; pi < STEPS / 2; ++pi) {
             const int i = 2 * pi;
-            const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;  // tile within the stage
-            const int e = tile_elem(i % kTileSteps, t);                      // element of step i, this direction
-            const bool live = i < g * kTileSteps;
-            const double *ft = f + tp * kLineKinds * kTileSlots + e;
-            const double2 z2 = make_double2(0.0, 0.0);
-            const double2 f0 = live ? *reinterpret_cast<const double2 *>(ft) : z2;
-            const double2 f1 = live ? *reinterpret_cast<const double2 *>(ft + kTileSlots) : z2;
-            const double2 f2 = live ? *reinterpret_cast<const double2 *>(ft + 2 * kTileSlots) : z2;
-            F0[i] = f0.x, F0[i + 1] = f0.y, F1[i] = f1.x, F1[i + 1] = f1.y, F2[i] = f2.x, F2[i + 1] = f2.y;
+            const int tp = UPPER ? G - 1 - i / kTileSteps - (G - g) : i / kTileSteps;  // tile within the stage
+            const int tpc = tp < 0 ? 0 : tp;
+            const int e = tile_elem(i % kTileSteps, t);  // element of step i, this direction
+            const double *ft = f + tpc * kLineKinds * kTileSlots + e;
+            const double2 f0 = *reinterpret_cast<const double2 *>(ft);
+            const double2 f1 = *reinterpret_cast<const double2 *>(ft + kTileSlots);
+            const double2 f2 = *reinterpret_cast<const double2 *>(ft + 2 * kTileSlots);
             // vectors are in forward tile order: the backward pair is reversed
-            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
-            double2 a0 = live ? *reinterpret_cast<const double2 *>(v0 + ve) : z2;
-            double2 a1 = (live && NV > 1) ? *reinterpret_cast<const double2 *>(v1 + ve) : z2;
-            if (UPPER) {
-                a0 = make_double2(a0.y, a0.x);
-                a1 = make_double2(a1.y, a1.x);
+            const int ve = tpc * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
+            const double2 a0 = *reinterpret_cast<const double2 *>(v0 + ve);
+            const double2 a1 = NV > 1 ? *reinterpret_cast<const double2 *>(v1 + ve) : make_double2(0.0, 0.0);
+            const bool live = i < g * kTileSteps;
+            F0[i] = live ? f0.x : 0.0, F0[i + 1] = live ? f0.y : 0.0;
+            F1[i] = live ? f1.x : 0.0, F1[i + 1] = live ? f1.y : 0.0;
+            F2[i] = live ? f2.x : 0.0, F2[i + 1] = live ? f2.y : 0.0;
+            double v_lo = UPPER ? a0.y : a0.x, v_hi = UPPER ? a0.x : a0.y;
+            const double w_lo = UPPER ? a1.y : a1.x, w_hi = UPPER ? a1.x : a1.y;
+            if (!UPPER && PCG) {  // r_{k+1} = r_k - alpha A p (pcg.py:142); alpha = 0 unless updating
+                v_lo = upd ? __dsub_rn(v_lo, __dmul_rn(alpha, w_lo)) : v_lo;
+                v_hi = upd ? __dsub_rn(v_hi, __dmul_rn(alpha, w_hi)) : v_hi;
             }
-            if (!UPPER) {
-                if (upd && live) {  // r_{k+1} = r_k - alpha A p (pcg.py:142)
-                    a0.x = __dsub_rn(a0.x, __dmul_rn(alpha, a1.x));
-                    a0.y = __dsub_rn(a0.y, __dmul_rn(alpha, a1.y));
-                    acc2 = __dadd_rn(acc2, __dmul_rn(a0.x, a0.x));
-                    acc2 = __dadd_rn(acc2, __dmul_rn(a0.y, a0.y));
-                }
-                AUX[i] = AUX[i + 1] = 0.0;
-            } else {
-                AUX[i] = PCG ? a1.x : 0.0;  // r
-                AUX[i + 1] = PCG ? a1.y : 0.0;
-            }
-            VIN[i] = a0.x;  // r_{k+1} | y / diag
-            VIN[i + 1] = a0.y;
+            VIN[i] = live ? v_lo : 0.0;  // r_{k+1} | y / diag
+            VIN[i + 1] = live ? v_hi : 0.0;
+            AUX[i] = (UPPER && PCG && live) ? w_lo : 0.0;  // r
+            AUX[i + 1] = (UPPER && PCG && live) ? w_hi : 0.0;
         }
+        if (upd) acc2 = __dadd_rn(acc2, stage_dot(VIN, VIN));  // |r_{k+1}|^2 (pcg.py:143)
         __syncwarp();
         LTR(2);
         // refill the slot of stage j - 2: its results left by bulk store a stage ago
@@ -363,12 +376,9 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
                 if (upd) *reinterpret_cast<double2 *>(o1 + ve) = make_double2(VIN[i], VIN[i + 1]);  // r_{k+1}
             } else {
                 *reinterpret_cast<double2 *>(o0 + ve) = make_double2(ACC[i + 1], ACC[i]);
-                if (PCG) {  // r.z (pcg.py:167)
-                    acc2 = __dadd_rn(acc2, __dmul_rn(AUX[i], ACC[i]));
-                    acc2 = __dadd_rn(acc2, __dmul_rn(AUX[i + 1], ACC[i + 1]));
-                }
             }
         }
+        if (UPPER && PCG) acc2 = __dadd_rn(acc2, stage_dot(AUX, ACC));  // r.z (pcg.py:167)
         LTR(7);
         fence_proxy_async();
         __syncwarp();
