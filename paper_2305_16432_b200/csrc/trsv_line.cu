@@ -262,6 +262,12 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
 #endif
         mbar_wait(&mbar[s], (j / NS) & 1);
         LTR(1);
+        // refill the slot of stage j - 2 (its results left by bulk store a stage ago) before
+        // this stage's operand loads, so the copies do not wait for them
+        if (t == 0 && j >= 2 && j - 2 + NS < nstage) {
+            bulk_wait_read<1>();
+            issue(j - 2 + NS);
+        }
         int lo, g;
         stage_tiles(j, lo, g);
         const char *sp = stage + (size_t)s * m.stage_bytes;
@@ -307,11 +313,6 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
         if (upd) acc2 = __dadd_rn(acc2, stage_dot(VIN, VIN));  // |r_{k+1}|^2 (pcg.py:143)
         __syncwarp();
         LTR(2);
-        // refill the slot of stage j - 2: its results left by bulk store a stage ago
-        if (t == 0 && j >= 2 && j - 2 + NS < nstage) {
-            bulk_wait_read<1>();
-            issue(j - 2 + NS);
-        }
         LTR(3);
         // left line's values at steps sig-1 .. sig+STEPS-2 (lane i holds step sig-1+i): one
         // batch per stage, each slot re-armed after the read
