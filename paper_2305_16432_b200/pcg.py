@@ -14,6 +14,8 @@ systems sharing one pattern) in one loop.
 from __future__ import annotations
 
 import ctypes
+import os
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -125,8 +127,83 @@ def pcg_solve_batch(A, B_rhs, P=None, opts: SolveOptions | None = None, *, value
 
 LAST_PROFILE: dict = {}  # filled by a profiled solve: per-kernel-class ms / launches / passes
 
+# A batch is solved as this many independent sub-batches, each on its own
+# CUDA stream driven by its own host thread: the triangular solves are bound
+# by their wavefront, not by the GPU's width, so one half's solves overlap the
+# other half's SpMV / vector updates. NPCG_STREAMS=1 turns it off.
+SPLIT_STREAMS = int(os.environ.get("NPCG_STREAMS", "2"))
+SPLIT_MIN_BATCH = 16
+_STREAMS: list = []
+
+
+def _side_streams(k):
+    torch = _torch()
+    while len(_STREAMS) < k:
+        _STREAMS.append(torch.cuda.Stream())
+    return _STREAMS[:k]
+
 
 def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True, profile=False):
+    k = SPLIT_STREAMS if batch >= SPLIT_MIN_BATCH and SPLIT_STREAMS > 1 else 1
+    if k == 1:
+        X, reps, prof = _pcg_device_one(A, Bm, fac, opts, batch, values, with_history, profile)
+        LAST_PROFILE.clear()
+        LAST_PROFILE.update(prof)
+        return X, reps
+    torch = _torch()
+    n = A.n
+    cuts = [batch * i // k for i in range(k + 1)]
+    caller = torch.cuda.current_stream()
+    streams = _side_streams(k)
+    results = [None] * k
+    errors = [None] * k
+
+    def cols(t, lo, hi, rows):  # columns [lo, hi) of a column-minor (rows, batch) tensor
+        return t.view(rows, batch)[:, lo:hi].contiguous()
+
+    def part(i):
+        lo, hi = cuts[i], cuts[i + 1]
+        try:
+            with torch.cuda.stream(streams[i]):
+                f = fac
+                if fac is not None and fac[5] != 1:  # per-system factors: this part's columns
+                    patF, S, sb, D, db, FB = fac
+                    Sp = cols(S, lo, hi, patF.nnz).view(-1) if sb else S
+                    Dp = cols(D, lo, hi, n).view(-1) if db else D
+                    f = (patF, Sp, sb, Dp, db, hi - lo)
+                v = None if values is None else to_device(values)[:, lo:hi].contiguous()
+                results[i] = _pcg_device_one(A, Bm[:, lo:hi].contiguous(), f, opts, hi - lo, v, with_history,
+                                             profile, tag=i + 1)
+        except BaseException as e:  # re-raised in the caller
+            errors[i] = e
+
+    for st in streams:
+        st.wait_stream(caller)
+    threads = [threading.Thread(target=part, args=(i,)) for i in range(1, k)]
+    for th in threads:
+        th.start()
+    part(0)
+    for th in threads:
+        th.join()
+    for st in streams:
+        caller.wait_stream(st)
+    for e in errors:
+        if e is not None:
+            raise e
+    X = torch.cat([r[0] for r in results], dim=1)
+    reps = [rep for r in results for rep in r[1]]
+    profs = [r[2] for r in results]
+    LAST_PROFILE.clear()
+    LAST_PROFILE.update(passes=max(p["passes"] for p in profs),
+                        iterations=np.concatenate([p["iterations"] for p in profs]),
+                        kernel_ms={key: sum(p["kernel_ms"][key] for p in profs) for key in profs[0]["kernel_ms"]},
+                        kernel_launches={key: sum(p["kernel_launches"][key] for p in profs)
+                                         for key in profs[0]["kernel_launches"]},
+                        streams=k)
+    return X, reps
+
+
+def _pcg_device_one(A, Bm, fac, opts, batch, values=None, with_history=True, profile=False, tag=0):
     torch = _torch()
     n, B = A.n, batch
     if B < 1 or B > _native.MAX_BATCH:
@@ -147,7 +224,7 @@ def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True, profile
             raise DimensionMismatchError("factor and matrix disagree on dimension")
         if FB != 1 and FB != B:
             raise DimensionMismatchError("batched factor does not match the batch")
-    solver = patA.solver(patF, B)
+    solver = patA.solver(patF, B, tag)
     max_iter = opts.max_iter if opts.max_iter is not None else 10 * n
     T = len(opts.thresholds)
     o = _native.SolveOpts()
@@ -185,10 +262,9 @@ def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True, profile
         solver, _native.ptr(vals), vb, _native.ptr(S), int(sb), _native.ptr(D), int(db),
         _native.ptr(Bm), _native.ptr(X), _native.ptr(x0), ctypes.byref(o), ctypes.byref(rep),
         _native.stream_handle()))
-    LAST_PROFILE.clear()
-    LAST_PROFILE.update(passes=int(rep.passes), iterations=iters.copy(),
-                        kernel_ms={k: float(kms[i]) for i, k in enumerate(_native.PROF_NAMES)},
-                        kernel_launches={k: int(kn[i]) for i, k in enumerate(_native.PROF_NAMES)})
+    prof = dict(passes=int(rep.passes), iterations=iters.copy(),
+                kernel_ms={k: float(kms[i]) for i, k in enumerate(_native.PROF_NAMES)},
+                kernel_launches={k: int(kn[i]) for i, k in enumerate(_native.PROF_NAMES)})
     reports = []
     for b in range(B):
         k = int(iters[b])
@@ -200,7 +276,7 @@ def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True, profile
         h = hist[b, : min(k + 1, cap)].tolist() if with_history else []
         reports.append(SolveReport(opts.thresholds, itd, sd, float(final[b]),
                                    bool(status[b] == _native.STATUS_CONVERGED), h, k, int(status[b])))
-    return X, reports
+    return X, reports, prof
 
 
 def _pcg_foreign(A, b, P, opts):

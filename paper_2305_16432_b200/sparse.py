@@ -77,9 +77,10 @@ class DevicePattern:
     def nnz_lower(self) -> int:
         return int(self.info().nnz_lower)
 
-    def solver(self, factor_pattern, B):
-        """Cached npcg_solver for (this A pattern, factor pattern or None, B)."""
-        key = (id(factor_pattern), B)
+    def solver(self, factor_pattern, B, tag=0):
+        """Cached npcg_solver for (this A pattern, factor pattern or None, B);
+        ``tag`` keeps concurrent solves (one per stream) on distinct solvers."""
+        key = (id(factor_pattern), B, tag)
         s = self._solvers.get(key)
         if s is None:
             h = ctypes.c_void_p()
