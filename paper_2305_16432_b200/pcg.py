@@ -138,9 +138,12 @@ _STREAMS: list = []
 
 def _side_streams(k):
     torch = _torch()
-    while len(_STREAMS) < k:
-        _STREAMS.append(torch.cuda.Stream())
-    return _STREAMS[:k]
+    dev = torch.cuda.current_device()
+    mine = [st for st in _STREAMS if st.device.index == dev]
+    while len(mine) < k:
+        mine.append(torch.cuda.Stream(device=dev))
+        _STREAMS.append(mine[-1])
+    return mine[:k]
 
 
 def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True, profile=False):
@@ -161,9 +164,12 @@ def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True, profile
     def cols(t, lo, hi, rows):  # columns [lo, hi) of a column-minor (rows, batch) tensor
         return t.view(rows, batch)[:, lo:hi].contiguous()
 
+    dev = torch.cuda.current_device()
+
     def part(i):
         lo, hi = cuts[i], cuts[i + 1]
         try:
+            torch.cuda.set_device(dev)  # a new host thread starts on device 0
             with torch.cuda.stream(streams[i]):
                 f = fac
                 if fac is not None and fac[5] != 1:  # per-system factors: this part's columns
