@@ -44,8 +44,7 @@ namespace npcg {
 
 namespace {
 
-// operand stages per warp: a slot is refilled two stages after its use (its
-// results leave by bulk store from the slot a stage later)
+// operand stages per warp: a slot is refilled the stage after its use
 constexpr int kLineStages = 3;
 
 struct LineSmem {  // byte offsets into dynamic shared memory
@@ -262,56 +261,39 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
 #endif
         mbar_wait(&mbar[s], (j / NS) & 1);
         LTR(1);
-        // refill the slot of stage j - 2 (its results left by bulk store a stage ago) before
-        // this stage's operand loads, so the copies do not wait for them
-        if (t == 0 && j >= 2 && j - 2 + NS < nstage) {
-            bulk_wait_read<1>();
-            issue(j - 2 + NS);
-        }
+        // refill the slot of stage j - 1 (every lane's reads of it ended at its __syncwarp)
+        // with stage j - 1 + NS before this stage's operand loads
+        if (t == 0 && j >= 1 && j - 1 + NS < nstage) issue(j - 1 + NS);
         int lo, g;
         stage_tiles(j, lo, g);
         const char *sp = stage + (size_t)s * m.stage_bytes;
         const double *f = reinterpret_cast<const double *>(sp);
         const double *v0 = f + G * kLineKinds * kTileSlots;
         const double *v1 = v0 + G * kTileSlots;
-        // every operand of the stage into registers (row sums start from VIN)
-        double F0[STEPS], F1[STEPS], F2[STEPS], VIN[STEPS], AUX[STEPS], ACC[STEPS];
-#pragma unroll
-        for (int i = 0; i < STEPS; ++i) ACC[i] = 0.0;  // padding steps of a partial stage
-        // a lane's two steps of a tile half are adjacent (pattern.h): one 16-byte load each.
-        // Every load is unconditional (a partial stage's missing tiles read stale slot
-        // contents, masked below), so they issue back to back
-#pragma unroll
-        for (int pi = 0; pi < STEPS / 2; ++pi) {
+        const int live_steps = g * kTileSteps;
+        // a step pair's operands (a lane's two steps of a tile half are adjacent, pattern.h:
+        // one 16-byte load each), loaded one pair ahead inside the step loop so the shared-
+        // memory reads overlap the dependency chain instead of preceding it. A partial
+        // stage's lookahead reads stale slot contents, never used.
+        auto pair_ops = [&](int pi, double2 &f0, double2 &f1, double2 &f2, double2 &a0, double2 &a1) {
             const int i = 2 * pi;
             const int tp = UPPER ? G - 1 - i / kTileSteps - (G - g) : i / kTileSteps;  // tile within the stage
             const int tpc = tp < 0 ? 0 : tp;
             const int e = tile_elem(i % kTileSteps, t);  // element of step i, this direction
             const double *ft = f + tpc * kLineKinds * kTileSlots + e;
-            const double2 f0 = *reinterpret_cast<const double2 *>(ft);
-            const double2 f1 = *reinterpret_cast<const double2 *>(ft + kTileSlots);
-            const double2 f2 = *reinterpret_cast<const double2 *>(ft + 2 * kTileSlots);
+            f0 = *reinterpret_cast<const double2 *>(ft);
+            f1 = *reinterpret_cast<const double2 *>(ft + kTileSlots);
+            f2 = *reinterpret_cast<const double2 *>(ft + 2 * kTileSlots);
             // vectors are in forward tile order: the backward pair is reversed
             const int ve = tpc * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
-            const double2 a0 = *reinterpret_cast<const double2 *>(v0 + ve);
-            const double2 a1 = NV > 1 ? *reinterpret_cast<const double2 *>(v1 + ve) : make_double2(0.0, 0.0);
-            const bool live = i < g * kTileSteps;
-            F0[i] = live ? f0.x : 0.0, F0[i + 1] = live ? f0.y : 0.0;
-            F1[i] = live ? f1.x : 0.0, F1[i + 1] = live ? f1.y : 0.0;
-            F2[i] = live ? f2.x : 0.0, F2[i + 1] = live ? f2.y : 0.0;
-            double v_lo = UPPER ? a0.y : a0.x, v_hi = UPPER ? a0.x : a0.y;
-            const double w_lo = UPPER ? a1.y : a1.x, w_hi = UPPER ? a1.x : a1.y;
-            if (!UPPER && PCG) {  // r_{k+1} = r_k - alpha A p (pcg.py:142); alpha = 0 unless updating
-                v_lo = upd ? __dsub_rn(v_lo, __dmul_rn(alpha, w_lo)) : v_lo;
-                v_hi = upd ? __dsub_rn(v_hi, __dmul_rn(alpha, w_hi)) : v_hi;
-            }
-            VIN[i] = live ? v_lo : 0.0;  // r_{k+1} | y / diag
-            VIN[i + 1] = live ? v_hi : 0.0;
-            AUX[i] = (UPPER && PCG && live) ? w_lo : 0.0;  // r
-            AUX[i + 1] = (UPPER && PCG && live) ? w_hi : 0.0;
-        }
-        if (upd) acc2 = __dadd_rn(acc2, stage_dot(VIN, VIN));  // |r_{k+1}|^2 (pcg.py:143)
-        __syncwarp();
+            a0 = *reinterpret_cast<const double2 *>(v0 + ve);
+            a1 = NV > 1 ? *reinterpret_cast<const double2 *>(v1 + ve) : make_double2(0.0, 0.0);
+        };
+        double VIN[STEPS], AUX[STEPS], ACC[STEPS];  // padding steps of a partial stage stay 0
+#pragma unroll
+        for (int i = 0; i < STEPS; ++i) VIN[i] = AUX[i] = ACC[i] = 0.0;
+        double2 cf0, cf1, cf2, ca0, ca1;
+        pair_ops(0, cf0, cf1, cf2, ca0, ca1);
         LTR(2);
         LTR(3);
         // left line's values at steps sig-1 .. sig+STEPS-2 (lane i holds step sig-1+i): one
@@ -346,53 +328,63 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
         }
         LTR(5);
 #pragma unroll
-        for (int i = 0; i < STEPS; ++i) {
-            if (i >= g * kTileSteps) break;
-            const int step = sig + i;
-            const double pre = __dsub_rn(VIN[i], __dmul_rn(F0[i], lp));
-            const double p2 = __dmul_rn(F2[i], h0);
-            double l1 = __shfl_up_sync(0xffffffffu, h0, 1);
-            const double xl = __shfl_sync(0xffffffffu, x, i);
-            if (t == 0) l1 = xl;
-            double acc = __dsub_rn(pre, __dmul_rn(F1[i], l1));
-            acc = __dsub_rn(acc, p2);
-            h0 = acc;
-            lp = l1;
-            if (prod && step >= Q0 && step < Q1) st_dsm(rout + (unsigned)(step & (R - 1)) * 8u, acc);
-            ACC[i] = acc;
+        for (int pi = 0; pi < STEPS / 2; ++pi) {
+            const int i = 2 * pi;
+            if (i >= live_steps) break;
+            double2 nf0, nf1, nf2, na0, na1;
+            if (pi + 1 < STEPS / 2) pair_ops(pi + 1, nf0, nf1, nf2, na0, na1);
+            double v_lo = UPPER ? ca0.y : ca0.x, v_hi = UPPER ? ca0.x : ca0.y;
+            const double w_lo = UPPER ? ca1.y : ca1.x, w_hi = UPPER ? ca1.x : ca1.y;
+            if (!UPPER && PCG) {  // r_{k+1} = r_k - alpha A p (pcg.py:142); alpha = 0 unless updating
+                v_lo = upd ? __dsub_rn(v_lo, __dmul_rn(alpha, w_lo)) : v_lo;
+                v_hi = upd ? __dsub_rn(v_hi, __dmul_rn(alpha, w_hi)) : v_hi;
+            }
+            VIN[i] = v_lo;  // r_{k+1} | y / diag
+            VIN[i + 1] = v_hi;
+            if (UPPER && PCG) AUX[i] = w_lo, AUX[i + 1] = w_hi;  // r
+            const double F0[2] = {cf0.x, cf0.y}, F1[2] = {cf1.x, cf1.y}, F2[2] = {cf2.x, cf2.y};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int step = sig + i + h;
+                const double pre = __dsub_rn(VIN[i + h], __dmul_rn(F0[h], lp));
+                const double p2 = __dmul_rn(F2[h], h0);
+                double l1 = __shfl_up_sync(0xffffffffu, h0, 1);
+                const double xl = __shfl_sync(0xffffffffu, x, i + h);
+                if (t == 0) l1 = xl;
+                double acc = __dsub_rn(pre, __dmul_rn(F1[h], l1));
+                acc = __dsub_rn(acc, p2);
+                h0 = acc;
+                lp = l1;
+                if (prod && step >= Q0 && step < Q1) st_dsm(rout + (unsigned)(step & (R - 1)) * 8u, acc);
+                ACC[i + h] = acc;
+            }
+            if (pi + 1 < STEPS / 2) cf0 = nf0, cf1 = nf1, cf2 = nf2, ca0 = na0, ca1 = na1;
         }
+        if (upd) acc2 = __dadd_rn(acc2, stage_dot(VIN, VIN));  // |r_{k+1}|^2 (pcg.py:143)
         LTR(6);
-        // results into the stage's own vector slices (their operands are in registers), then
-        // one bulk store per array: the steps above never wait on a divide or a global store
-        double *o0 = const_cast<double *>(v0), *o1 = const_cast<double *>(v1);
+        // results straight from registers: coalesced 16-byte stores, off the dependency chain
+        double *og = out + (size_t)lo * kTileSlots, *rg = upd ? rout_g + (size_t)lo * kTileSlots : nullptr;
 #pragma unroll
         for (int pi = 0; pi < STEPS / 2; ++pi) {
             const int i = 2 * pi;
-            if (i >= g * kTileSteps) break;
+            if (i >= live_steps) break;
             const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;
             const int e = tile_elem(i % kTileSteps, t);
             const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
             if (!UPPER) {
-                *reinterpret_cast<double2 *>(o0 + ve) = make_double2(ACC[i], ACC[i + 1]);  // y (diag_scale_kernel divides)
-                if (upd) *reinterpret_cast<double2 *>(o1 + ve) = make_double2(VIN[i], VIN[i + 1]);  // r_{k+1}
+                *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i], ACC[i + 1]);  // y (diag_scale_kernel divides)
+                if (upd) *reinterpret_cast<double2 *>(rg + ve) = make_double2(VIN[i], VIN[i + 1]);  // r_{k+1}
             } else {
-                *reinterpret_cast<double2 *>(o0 + ve) = make_double2(ACC[i + 1], ACC[i]);
+                *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i + 1], ACC[i]);
             }
         }
         if (UPPER && PCG) acc2 = __dadd_rn(acc2, stage_dot(AUX, ACC));  // r.z (pcg.py:167)
         LTR(7);
-        fence_proxy_async();
+        // every lane's reads of this slot are done before the elected lane refills it
         __syncwarp();
         LTR(8);
-        if (t == 0) {
-            const unsigned vbytes = (unsigned)g * kTileSlots * 8;
-            bulk_s2g(out + (size_t)lo * kTileSlots, o0, vbytes);
-            if (upd) bulk_s2g(rout_g + (size_t)lo * kTileSlots, o1, vbytes);
-            bulk_commit();
-        }
         LTR(9);
     }
-    if (t == 0) bulk_wait<0>();  // results written before the solve is complete
     if (PCG) {  // fixed-order reduction: lanes, warps, then the cluster's CTAs
         double v = acc2;
 #pragma unroll
@@ -440,7 +432,7 @@ int line_config_for(const LineDir &L, bool upper, int B) {
         const int c = std::atoi(env), G = c / 16, NS = c % 16;
         if (G >= 1 && G <= 3 && NS == kLineStages && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
     }
-    // stages >= 3: a slot is refilled two stages after its use (its results leave by bulk store)
+    // three operand stages: two in flight while one is consumed
     static const int prefs[][2] = {{3, kLineStages}, {2, kLineStages}, {1, kLineStages}};
     for (const auto &p : prefs)
         if (line_smem(WL, L.ring, p[0], p[1], upper, true) <= cap) return C * 256 + p[0] * 16 + p[1];

@@ -48,6 +48,8 @@ def main():
         tail = ev[1:, 0] - ev[:-1, 9]                   # to the next stage
         per = np.median(np.diff(ev[:, 0]))
         parts = [np.median(seg[:, k]) for k in range(9)] + [np.median(tail)]
+        st = np.diff(ev[:, 0])
+        print(f"w{w:2d} C0={t[w,0]} start={ev[0,0]-t0:8.0f} end={ev[-1,9]-t0:8.0f} n={n} p90/stage {np.percentile(st,90):6.0f} max {st.max():6.0f} sum(wait)={seg[:,0].sum():.0f} sum(ringin)={seg[:,3].sum():.0f} sum(ringout)={seg[:,4].sum():.0f}")
         print(f"w{w:2d} cyc/stage {per:6.0f} | " + " ".join(f"{nm}={v:.0f}" for nm, v in zip(names, parts)))
 
 if __name__ == "__main__":
