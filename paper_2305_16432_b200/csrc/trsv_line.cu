@@ -44,8 +44,9 @@ namespace npcg {
 
 namespace {
 
-// operand stages per warp: a slot is refilled the stage after its use
-constexpr int kLineStages = 3;
+// operand stages per warp (a slot is refilled the stage after its use): three
+// up to 3-tile stages, two for 4-tile stages (shared memory)
+__host__ __device__ constexpr int line_stages(int G) { return G >= 4 ? 2 : 3; }
 
 struct LineSmem {  // byte offsets into dynamic shared memory
     size_t ring, mbar, stage0, stage_bytes, total;
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
     extern __shared__ __align__(128) char sm[];
     __shared__ double s_red[kLineMaxWarps];
     __shared__ double s_cta[4];
-    constexpr int NS = kLineStages;
+    constexpr int NS = line_stages(G);
     const int W = a.warps, WL = W / C, R = a.ring;
     const int wl = threadIdx.x >> 5, t = threadIdx.x & 31;
     const int rank = C > 1 ? (int)cluster_rank() : 0, b = blockIdx.x / C;
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
             ychk = chn ? ld_dsm(rout + (unsigned)(yn & (R - 1)) * 8u) : sentinel();
         }
         LTR(5);
+        double *og = out + (size_t)lo * kTileSlots, *rg = upd ? rout_g + (size_t)lo * kTileSlots : nullptr;
 #pragma unroll
         for (int pi = 0; pi < STEPS / 2; ++pi) {
             const int i = 2 * pi;
@@ -358,26 +360,22 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
                 if (prod && step >= Q0 && step < Q1) st_dsm(rout + (unsigned)(step & (R - 1)) * 8u, acc);
                 ACC[i + h] = acc;
             }
+            // results straight from registers: coalesced 16-byte stores, off the dependency chain
+            {
+                const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;
+                const int e = tile_elem(i % kTileSteps, t);
+                const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
+                if (!UPPER) {
+                    *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i], ACC[i + 1]);  // y (diag_scale_kernel divides)
+                    if (upd) *reinterpret_cast<double2 *>(rg + ve) = make_double2(VIN[i], VIN[i + 1]);  // r_{k+1}
+                } else {
+                    *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i + 1], ACC[i]);
+                }
+            }
             if (pi + 1 < STEPS / 2) cf0 = nf0, cf1 = nf1, cf2 = nf2, ca0 = na0, ca1 = na1;
         }
         if (upd) acc2 = __dadd_rn(acc2, stage_dot(VIN, VIN));  // |r_{k+1}|^2 (pcg.py:143)
         LTR(6);
-        // results straight from registers: coalesced 16-byte stores, off the dependency chain
-        double *og = out + (size_t)lo * kTileSlots, *rg = upd ? rout_g + (size_t)lo * kTileSlots : nullptr;
-#pragma unroll
-        for (int pi = 0; pi < STEPS / 2; ++pi) {
-            const int i = 2 * pi;
-            if (i >= live_steps) break;
-            const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;
-            const int e = tile_elem(i % kTileSteps, t);
-            const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
-            if (!UPPER) {
-                *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i], ACC[i + 1]);  // y (diag_scale_kernel divides)
-                if (upd) *reinterpret_cast<double2 *>(rg + ve) = make_double2(VIN[i], VIN[i + 1]);  // r_{k+1}
-            } else {
-                *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i + 1], ACC[i]);
-            }
-        }
         if (UPPER && PCG) acc2 = __dadd_rn(acc2, stage_dot(AUX, ACC));  // r.z (pcg.py:167)
         LTR(7);
         // every lane's reads of this slot are done before the elected lane refills it
@@ -430,10 +428,10 @@ int line_config_for(const LineDir &L, bool upper, int B) {
     const int WL = L.warps / C;
     if (const char *env = std::getenv("NPCG_LINE_CFG")) {
         const int c = std::atoi(env), G = c / 16, NS = c % 16;
-        if (G >= 1 && G <= 3 && NS == kLineStages && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
+        if (G >= 1 && G <= 4 && NS == line_stages(G) && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
     }
     // three operand stages: two in flight while one is consumed
-    static const int prefs[][2] = {{3, kLineStages}, {2, kLineStages}, {1, kLineStages}};
+    static const int prefs[][2] = {{4, line_stages(4)}, {3, line_stages(3)}, {2, line_stages(2)}, {1, line_stages(1)}};
     for (const auto &p : prefs)
         if (line_smem(WL, L.ring, p[0], p[1], upper, true) <= cap) return C * 256 + p[0] * 16 + p[1];
     return 0;
@@ -477,15 +475,17 @@ static cudaError_t launch_line_gc(const LineArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s) {
-    if (a.stages != kLineStages || a.warps < 1 || a.warps > kLineMaxWarps || a.warps % a.cluster) return cudaErrorInvalidValue;
+    if (a.group < 1 || a.group > 4 || a.stages != line_stages(a.group) || a.warps < 1 || a.warps > kLineMaxWarps || a.warps % a.cluster) return cudaErrorInvalidValue;
     const int key = a.cluster * 16 + a.group;
     switch (key) {
         case 16 + 1: return launch_line_gc<1, 1>(a, s);
         case 16 + 2: return launch_line_gc<2, 1>(a, s);
         case 16 + 3: return launch_line_gc<3, 1>(a, s);
+        case 16 + 4: return launch_line_gc<4, 1>(a, s);
         case 32 + 1: return launch_line_gc<1, 2>(a, s);
         case 32 + 2: return launch_line_gc<2, 2>(a, s);
         case 32 + 3: return launch_line_gc<3, 2>(a, s);
+        case 32 + 4: return launch_line_gc<4, 2>(a, s);
         default: return cudaErrorInvalidValue;
     }
 }
