@@ -201,6 +201,35 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int A_batched,
                    const double *b, double *x, const double *x0,
                    const npcg_solve_opts *opts, npcg_solve_report *report, void *stream);
 
+/* ---- P1 FEM assembly (input side) --------------
+ * Replaces pcgkit.fem.full_stiffness_and_mass / assemble's matrix part
+ * (fem.py:42-69 element blocks, fem.py:116-134 COO in element order summed by
+ * SparseMatrixCsr.from_coo after a stable (row, col) lexsort), for a fixed
+ * triangle topology and any number of vertex sets / element coefficients.
+ * Values are bit-identical to that host assembly (numpy add.reduceat order).
+ *
+ * npcg_fem_plan_create: host triangles int64 [nt][3] (counter-clockwise);
+ * builds the lexsorted triplet plan once. NPCG_ERR_DATA_FORMAT for a vertex
+ * index out of range or an empty mesh. */
+typedef struct npcg_fem_plan npcg_fem_plan;
+int npcg_fem_plan_create(int64_t n_vertices, int64_t n_triangles, const int64_t *triangles_host,
+                         npcg_fem_plan **out);
+int npcg_fem_plan_destroy(npcg_fem_plan *p);
+/* The assembled CSR pattern: *nnz always; row_ptr [n_vertices + 1] and
+ * col_idx [nnz] (host, int64, nullable) the reference's layout. */
+int npcg_fem_plan_pattern(const npcg_fem_plan *p, int64_t *nnz, int64_t *row_ptr_host, int64_t *col_idx_host);
+
+#define NPCG_FEM_K          0  /* sum of (coef_e * K_e)                    */
+#define NPCG_FEM_M          1  /* sum of M_e                                */
+#define NPCG_FEM_M_PLUS_SK  2  /* (sum M_e) + scale * (sum coef_e K_e)      */
+/* Device assembly of B systems: vertices [n_vertices][2][VB] (VB = B when
+ * vertices_batched, else 1), coef [nt][CB] nullable (CB = B when
+ * coef_batched), values out [nnz][B]. bad_dev (device int, nullable) is set
+ * to 1 when a triangle is degenerate or clockwise (fem.py raises there). */
+int npcg_fem_assemble(const npcg_fem_plan *p, int B, const double *vertices, int vertices_batched,
+                      const double *coef, int coef_batched, int mode, double scale, double *values,
+                      int *bad_dev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

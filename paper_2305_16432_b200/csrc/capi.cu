@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/npcg.h"
+#include "fem.cuh"
 #include "gnn.cuh"
 #include "kernels.cuh"
 #include "pattern.h"
@@ -913,3 +914,79 @@ extern "C" int64_t npcg_launch_count(void) { return (int64_t)launch_count(); }
 // Diagnostics: the line-solve timeline of CTA 0 (clock64 per batch and event,
 // [16][2048]); all zeros unless the library was built with -DNPCG_LINE_TRACE.
 extern "C" int npcg_debug_line_trace(long long *out, int n) { return line_trace_copy(out, n); }
+
+// ---- P1 FEM assembly (fem.cu) ---------------------------------------------
+struct npcg_fem_plan {
+    long long nv = 0, nt = 0, nnz = 0;
+    std::vector<long long> row_ptr, col;
+    int *d_starts = nullptr, *d_order = nullptr, *d_tri = nullptr;
+};
+
+extern "C" int npcg_fem_plan_create(int64_t nv, int64_t nt, const int64_t *tri, npcg_fem_plan **out) {
+    if (!out || !tri) return fail(NPCG_ERR_ARGUMENT, "null argument");
+    *out = nullptr;
+    FemPlanHost h;
+    const std::string err = fem_plan_build(nv, nt, reinterpret_cast<const long long *>(tri), h);
+    if (!err.empty()) return fail(NPCG_ERR_DATA_FORMAT, err);
+    std::unique_ptr<npcg_fem_plan> p(new npcg_fem_plan);
+    p->nv = nv;
+    p->nt = nt;
+    p->nnz = (long long)h.col.size();
+    p->row_ptr = h.row_ptr;
+    p->col.assign(h.col.begin(), h.col.end());
+    std::vector<int> t32(3 * nt);
+    for (long long q = 0; q < 3 * nt; ++q) t32[q] = (int)tri[q];
+    NPCG_CUDA(dalloc(&p->d_starts, h.starts.size()));
+    NPCG_CUDA(dalloc(&p->d_order, h.order.size()));
+    NPCG_CUDA(dalloc(&p->d_tri, t32.size()));
+    NPCG_CUDA(cudaMemcpy(p->d_starts, h.starts.data(), h.starts.size() * 4, cudaMemcpyHostToDevice));
+    NPCG_CUDA(cudaMemcpy(p->d_order, h.order.data(), h.order.size() * 4, cudaMemcpyHostToDevice));
+    NPCG_CUDA(cudaMemcpy(p->d_tri, t32.data(), t32.size() * 4, cudaMemcpyHostToDevice));
+    *out = p.release();
+    return NPCG_OK;
+}
+
+extern "C" int npcg_fem_plan_destroy(npcg_fem_plan *p) {
+    if (!p) return NPCG_OK;
+    cudaFree(p->d_starts);
+    cudaFree(p->d_order);
+    cudaFree(p->d_tri);
+    delete p;
+    return NPCG_OK;
+}
+
+extern "C" int npcg_fem_plan_pattern(const npcg_fem_plan *p, int64_t *nnz, int64_t *row_ptr, int64_t *col_idx) {
+    if (!p || !nnz) return fail(NPCG_ERR_ARGUMENT, "null argument");
+    *nnz = p->nnz;
+    if (row_ptr) std::copy(p->row_ptr.begin(), p->row_ptr.end(), row_ptr);
+    if (col_idx) std::copy(p->col.begin(), p->col.end(), col_idx);
+    return NPCG_OK;
+}
+
+extern "C" int npcg_fem_assemble(const npcg_fem_plan *p, int B, const double *vertices, int vb, const double *coef,
+                                 int cb, int mode, double scale, double *values, int *bad, void *stream) {
+    if (!p || B < 1 || !vertices || !values) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    if (mode != NPCG_FEM_K && mode != NPCG_FEM_M && mode != NPCG_FEM_M_PLUS_SK) return fail(NPCG_ERR_ARGUMENT, "bad mode");
+    cudaStream_t s = (cudaStream_t)stream;
+    int *flag = bad;
+    if (!flag) {  // a scratch flag the caller does not read
+        static thread_local int *scratch = nullptr;
+        if (!scratch) NPCG_CUDA(dalloc(&scratch, 1));
+        flag = scratch;
+    }
+    FemArgs a;
+    a.nnz = (int)p->nnz;
+    a.B = B;
+    a.starts = p->d_starts;
+    a.order = p->d_order;
+    a.tri = p->d_tri;
+    a.V = vertices;
+    a.vb = vb ? B : 1;
+    a.coef = coef;
+    a.cb = cb ? B : 1;
+    a.mode = mode;
+    a.scale = scale;
+    a.out = values;
+    NPCG_CUDA(launch_fem_assemble(a, flag, s));
+    return NPCG_OK;
+}

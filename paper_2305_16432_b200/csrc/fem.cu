@@ -1,0 +1,165 @@
+// fem.cu -- P1 triangle FEM assembly into a fixed CSR pattern, on the device
+// (the input side of the solve path).
+//
+// Reference semantics: pkg/src/pcgkit/fem.py:42-69 (element_stiffness /
+// element_mass per triangle) and fem.py:116-134 (COO triplets in element
+// order, rows = repeat(tri, 3), cols = tile(tri, 3), summed by
+// SparseMatrixCsr.from_coo after a stable (row, col) lexsort). The host mirror
+// is paper_2305_16432_b200/inputs.py (element_blocks, Assembler), which the
+// tests pin bitwise to pcgkit.fem.
+//
+// Layout: the plan keeps, per CSR slot, the run [starts[p], starts[p+1]) of
+// triplet ids (e * 9 + 3 i + j, block entry (i, j) of element e) in lexsort
+// order. One thread owns one (slot, system) pair -- system index fastest, so a
+// warp reads one coefficient row / vertex pair for all its systems -- and
+// recomputes each contributing element entry from the vertices with the
+// reference's operation order (unfused fp64), so no (nt, 3, 3) block array is
+// ever written. A slot's run is summed exactly like numpy's add.reduceat:
+// first element + pairwise_sum(rest) (sequential from -0.0 below 8 terms, eight
+// interleaved accumulators up to 128).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+#include "fem.cuh"
+
+namespace npcg {
+
+namespace {
+
+constexpr double kMassDiag = 2.0 / 12.0, kMassOff = 1.0 / 12.0;  // fem.py mass template / 12
+
+struct Elem {  // one triangle's geometry, fem.py:42-69 operation order
+    double bs[3], cs[3], twice_abs;
+    bool bad;
+};
+
+__device__ __forceinline__ Elem element(const int *tri, const double *V, int vb, int B, int b, int e) {
+    double x[3], y[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const long long v = tri[3 * (long long)e + k];
+        x[k] = V[(v * 2 + 0) * vb + (vb > 1 ? b : 0)];
+        y[k] = V[(v * 2 + 1) * vb + (vb > 1 ? b : 0)];
+    }
+    Elem E;
+    const double twice = __dsub_rn(__dmul_rn(__dsub_rn(x[1], x[0]), __dsub_rn(y[2], y[0])),
+                                   __dmul_rn(__dsub_rn(y[1], y[0]), __dsub_rn(x[2], x[0])));
+    E.bad = !(twice > 0.0);
+    E.twice_abs = fabs(twice);
+    E.bs[0] = __dsub_rn(y[1], y[2]);
+    E.bs[1] = __dsub_rn(y[2], y[0]);
+    E.bs[2] = __dsub_rn(y[0], y[1]);
+    E.cs[0] = __dsub_rn(x[2], x[1]);
+    E.cs[1] = __dsub_rn(x[0], x[2]);
+    E.cs[2] = __dsub_rn(x[1], x[0]);
+    return E;
+}
+
+// entry (i, j) of the (coefficient-scaled) stiffness or of the mass block
+template <bool MASS>
+__device__ __forceinline__ double entry(const Elem &E, int i, int j, double c, bool scaled) {
+    if (MASS) return __dmul_rn(__ddiv_rn(E.twice_abs, 2.0), i == j ? kMassDiag : kMassOff);
+    const double k = __ddiv_rn(__dadd_rn(__dmul_rn(E.bs[i], E.bs[j]), __dmul_rn(E.cs[i], E.cs[j])),
+                               __dmul_rn(2.0, E.twice_abs));
+    return scaled ? __dmul_rn(k, c) : k;  // K * c[:, None, None]
+}
+
+template <bool MASS>
+__device__ double slot_sum(const FemArgs &a, int p, int b, int *bad) {
+    const int q0 = a.starts[p], q1 = a.starts[p + 1];
+    auto term = [&](int q) -> double {
+        const int o = a.order[q], e = o / 9, l = o - 9 * e;
+        const Elem E = element(a.tri, a.V, a.vb, a.B, b, e);
+        if (E.bad) atomicOr(bad, 1);
+        const double c = (!MASS && a.coef) ? a.coef[(long long)e * a.cb + (a.cb > 1 ? b : 0)] : 1.0;
+        return entry<MASS>(E, l / 3, l % 3, c, !MASS && a.coef);
+    };
+    // numpy add.reduceat: a[0] + pairwise_sum(a[1:]) (numpy/core/src/umath/loops_utils.h)
+    const double first = term(q0);
+    const int n = q1 - q0 - 1;
+    double rest;
+    if (n < 8) {
+        rest = -0.0;  // numpy >= 2 starts the short sum at -0.0 (signed zeros survive)
+        for (int q = q0 + 1; q < q1; ++q) rest = __dadd_rn(rest, term(q));
+    } else {  // n <= 128 (checked when the plan is built)
+        double r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = term(q0 + 1 + k);
+        int i = 8;
+        for (; i < n - (n % 8); i += 8)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], term(q0 + 1 + i + k));
+        rest = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) rest = __dadd_rn(rest, term(q0 + 1 + i));
+    }
+    return __dadd_rn(first, rest);
+}
+
+__global__ void __launch_bounds__(256) fem_assemble_kernel(FemArgs a, int *bad) {
+    const long long total = (long long)a.nnz * a.B;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int p = (int)(t / a.B), b = (int)(t - (long long)p * a.B);
+        double v;
+        if (a.mode == FEM_K) {
+            v = slot_sum<false>(a, p, b, bad);
+        } else if (a.mode == FEM_M) {
+            v = slot_sum<true>(a, p, b, bad);
+        } else {  // M + s K  (heat: dt * alpha, wave: dt * dt)
+            v = __dadd_rn(slot_sum<true>(a, p, b, bad), __dmul_rn(a.scale, slot_sum<false>(a, p, b, bad)));
+        }
+        a.out[t] = v;
+    }
+}
+
+}  // namespace
+
+std::string fem_plan_build(long long nv, long long nt, const long long *tri, FemPlanHost &h) {
+    if (nv < 1 || nt < 1) return "empty mesh";
+    if (nt * 9 > (long long)INT32_MAX || nv > (long long)INT32_MAX / 2) return "mesh too large for int32 plan";
+    for (long long q = 0; q < 3 * nt; ++q)
+        if (tri[q] < 0 || tri[q] >= nv) return "triangle vertex out of range";
+    const long long m = 9 * nt;
+    std::vector<int> ord(m);
+    std::iota(ord.begin(), ord.end(), 0);
+    auto row = [&](int o) { return tri[3 * (long long)(o / 9) + (o % 9) / 3]; };
+    auto col = [&](int o) { return tri[3 * (long long)(o / 9) + (o % 9) % 3]; };
+    // np.lexsort((cols, rows)): by row, then column, ties in triplet order (stable)
+    std::stable_sort(ord.begin(), ord.end(), [&](int u, int v) {
+        const long long ru = row(u), rv = row(v);
+        return ru != rv ? ru < rv : col(u) < col(v);
+    });
+    h.order = ord;
+    h.starts.clear();
+    h.col.clear();
+    h.row_ptr.assign(nv + 1, 0);
+    for (long long q = 0; q < m; ++q) {
+        const int o = ord[q];
+        if (q == 0 || row(o) != row(ord[q - 1]) || col(o) != col(ord[q - 1])) {
+            h.starts.push_back((int)q);
+            h.col.push_back(col(o));
+            h.row_ptr[row(o) + 1] += 1;
+        }
+    }
+    h.starts.push_back((int)m);
+    for (long long i = 0; i < nv; ++i) h.row_ptr[i + 1] += h.row_ptr[i];
+    for (size_t k = 0; k + 1 < h.starts.size(); ++k)
+        if (h.starts[k + 1] - h.starts[k] > 129) return "more than 129 contributions to one entry";
+    return "";
+}
+
+cudaError_t launch_fem_assemble(const FemArgs &a, int *bad, cudaStream_t s) {
+    const long long total = (long long)a.nnz * a.B;
+    if (total == 0) return cudaSuccess;
+    const int grid = (int)std::min<long long>((total + 255) / 256, 16LL * num_sms());
+    note_launch();
+    fem_assemble_kernel<<<grid, 256, 0, s>>>(a, bad);
+    return cudaGetLastError();
+}
+
+}  // namespace npcg

@@ -236,3 +236,70 @@ def _host_spmv(A: SparseMatrixCsr, x):
         p = A.row_ptr[rows] + k
         y[rows] += A.values[p] * x[A.col_idx[p]]
     return y
+
+
+class DeviceAssembler:
+    """P1 assembly on the device (libnpcg ``npcg_fem_assemble``, csrc/fem.cu):
+    the same triangle topology as :class:`Assembler`, any number of vertex
+    sets / per-element coefficients per call, values bit-identical to
+    ``Assembler.values(element_blocks(...))`` (fem.py:42-69, 116-134).
+
+    ``values(vertices, coef=None, mode="K" | "M" | "M+sK", scale=1.0)``:
+    vertices (nv, 2) or (nv, 2, B); coef None, (nt,) or (nt, B); returns a
+    device float64 tensor (nnz,) or (nnz, B). Raises ValueError on a
+    degenerate / clockwise triangle like element_blocks."""
+
+    MODES = {"K": 0, "M": 1, "M+sK": 2}
+
+    def __init__(self, n_vertices: int, triangles: np.ndarray):
+        import ctypes
+
+        from . import _native
+        self._lib = _native.lib()
+        tri = np.ascontiguousarray(triangles, dtype=np.int64)
+        h = ctypes.c_void_p()
+        _native.check(self._lib.npcg_fem_plan_create(int(n_vertices), len(tri), tri.ctypes.data, ctypes.byref(h)))
+        self._h = h
+        nnz = ctypes.c_int64()
+        _native.check(self._lib.npcg_fem_plan_pattern(h, ctypes.byref(nnz), None, None))
+        self.n, self.nnz, self.n_triangles = int(n_vertices), int(nnz.value), len(tri)
+        self.row_ptr = np.zeros(self.n + 1, dtype=np.int64)
+        self.col_idx = np.zeros(self.nnz, dtype=np.int64)
+        _native.check(self._lib.npcg_fem_plan_pattern(h, ctypes.byref(nnz), self.row_ptr.ctypes.data,
+                                                      self.col_idx.ctypes.data))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.npcg_fem_plan_destroy(h)
+            self._h = None
+
+    def values(self, vertices, coef=None, mode: str = "K", scale: float = 1.0, check: bool = True):
+        import torch
+
+        from . import _native
+        if mode not in self.MODES:
+            raise ValueError(f"mode must be one of {sorted(self.MODES)}")
+        V = torch.as_tensor(vertices, dtype=torch.float64, device="cuda").contiguous()
+        if V.dim() not in (2, 3) or V.shape[0] != self.n or V.shape[1] != 2:
+            raise ValueError("vertices must be (n_vertices, 2) or (n_vertices, 2, B)")
+        B = V.shape[2] if V.dim() == 3 else 1
+        C = None
+        if coef is not None:
+            C = torch.as_tensor(coef, dtype=torch.float64, device="cuda").contiguous()
+            if C.shape[0] != self.n_triangles or C.dim() not in (1, 2):
+                raise ValueError("coef must be (n_triangles,) or (n_triangles, B)")
+            if C.dim() == 2:
+                if B == 1:
+                    B = C.shape[1]
+                elif C.shape[1] != B:
+                    raise ValueError("coef and vertices disagree on the batch")
+        batched = V.dim() == 3 or (C is not None and C.dim() == 2)
+        out = torch.empty((self.nnz, B) if batched else (self.nnz,), dtype=torch.float64, device="cuda")
+        bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _native.check(self._lib.npcg_fem_assemble(
+            self._h, B, _native.ptr(V), int(V.dim() == 3), _native.ptr(C), int(C is not None and C.dim() == 2),
+            self.MODES[mode], float(scale), _native.ptr(out), _native.ptr(bad), _native.stream_handle()))
+        if check and int(bad.item()):
+            raise ValueError("degenerate or clockwise triangle (reduce the jitter)")
+        return out
