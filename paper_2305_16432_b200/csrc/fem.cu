@@ -68,22 +68,16 @@ __device__ __forceinline__ double entry(const Elem &E, int i, int j, double c, b
     return scaled ? __dmul_rn(k, c) : k;  // K * c[:, None, None]
 }
 
-template <bool MASS>
-__device__ double slot_sum(const FemArgs &a, int p, int b, int *bad) {
-    const int q0 = a.starts[p], q1 = a.starts[p + 1];
-    auto term = [&](int q) -> double {
-        const int o = a.order[q], e = o / 9, l = o - 9 * e;
-        const Elem E = element(a.tri, a.V, a.vb, a.B, b, e);
-        if (E.bad) atomicOr(bad, 1);
-        const double c = (!MASS && a.coef) ? a.coef[(long long)e * a.cb + (a.cb > 1 ? b : 0)] : 1.0;
-        return entry<MASS>(E, l / 3, l % 3, c, !MASS && a.coef);
-    };
-    // numpy add.reduceat: a[0] + pairwise_sum(a[1:]) (numpy/core/src/umath/loops_utils.h)
+// numpy add.reduceat of term(q0) .. term(q1 - 1): a[0] + pairwise_sum(a[1:])
+// (numpy umath loops_utils.h: below 8 terms a sequential sum from -0.0, which
+// keeps signed zeros; up to 128 terms eight interleaved accumulators)
+template <class F>
+__device__ __forceinline__ double reduceat_run(int q0, int q1, F term) {
     const double first = term(q0);
     const int n = q1 - q0 - 1;
     double rest;
     if (n < 8) {
-        rest = -0.0;  // numpy >= 2 starts the short sum at -0.0 (signed zeros survive)
+        rest = -0.0;
         for (int q = q0 + 1; q < q1; ++q) rest = __dadd_rn(rest, term(q));
     } else {  // n <= 128 (checked when the plan is built)
         double r[8];
@@ -100,6 +94,17 @@ __device__ double slot_sum(const FemArgs &a, int p, int b, int *bad) {
     return __dadd_rn(first, rest);
 }
 
+template <bool MASS>
+__device__ double slot_sum(const FemArgs &a, int p, int b, int *bad) {
+    return reduceat_run(a.starts[p], a.starts[p + 1], [&](int q) -> double {
+        const int o = a.order[q], e = o / 9, l = o - 9 * e;
+        const Elem E = element(a.tri, a.V, a.vb, a.B, b, e);
+        if (E.bad) atomicOr(bad, 1);
+        const double c = (!MASS && a.coef) ? a.coef[(long long)e * a.cb + (a.cb > 1 ? b : 0)] : 1.0;
+        return entry<MASS>(E, l / 3, l % 3, c, !MASS && a.coef);
+    });
+}
+
 __global__ void __launch_bounds__(256) fem_assemble_kernel(FemArgs a, int *bad) {
     const long long total = (long long)a.nnz * a.B;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -114,6 +119,77 @@ __global__ void __launch_bounds__(256) fem_assemble_kernel(FemArgs a, int *bad) 
             v = __dadd_rn(slot_sum<true>(a, p, b, bad), __dmul_rn(a.scale, slot_sum<false>(a, p, b, bad)));
         }
         a.out[t] = v;
+    }
+}
+
+// Shared vertices (one mesh for the batch), two passes:
+//  prep  -- one thread per slot: the unscaled stiffness entry of every triplet
+//           of its run (geometry and divides once per mesh, not per system)
+//           into kq[q], and the whole mass sum into ms[p];
+//  batch -- one thread per (slot, system), system fastest: the coefficient
+//           products of the run summed in numpy's order. A warp's kq / order
+//           reads are broadcasts, its coefficient reads and value stores are
+//           contiguous.
+__global__ void __launch_bounds__(256) fem_prep_kernel(FemArgs a, int *bad) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < a.nnz; p += gridDim.x * blockDim.x) {
+        const int q0 = a.starts[p], q1 = a.starts[p + 1];
+        for (int q = q0; q < q1; ++q) {
+            const int o = a.order[q], e = o / 9, l = o - 9 * e;
+            const Elem E = element(a.tri, a.V, 1, a.B, 0, e);
+            if (E.bad) atomicOr(bad, 1);
+            a.kq[q] = entry<false>(E, l / 3, l % 3, 1.0, false);
+        }
+        if (a.mode != FEM_K) a.ms[p] = slot_sum<true>(a, p, 0, bad);
+    }
+}
+
+// value of item t = (slot p, system b) by the generic run walk (runs > 8)
+__device__ double batch_item_slow(const FemArgs &a, unsigned p, unsigned b) {
+    if (a.mode == FEM_M) return a.ms[p];
+    const double Ks = reduceat_run(a.starts[p], a.starts[p + 1], [&](int q) -> double {
+        const double k = a.kq[q];
+        if (!a.coef) return k;
+        return __dmul_rn(k, __ldg(&a.coef[(long long)(a.order[q] / 9) * a.cb + (a.cb > 1 ? b : 0)]));
+    });
+    return a.mode == FEM_K ? Ks : __dadd_rn(a.ms[p], __dmul_rn(a.scale, Ks));
+}
+
+// A warp per slot, lanes over the systems: lane k fetches the run's k-th
+// stiffness entry and element id (one coalesced load each), the warp
+// broadcasts them by shuffles, and every coefficient load of the run is then
+// in flight at once (lane = system: contiguous 256-byte rows), as is the
+// value store. Runs longer than 8 take the generic walk.
+__global__ void __launch_bounds__(256) fem_batch_kernel(FemArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < a.nnz; p += warps) {
+        const int q0 = a.starts[p], n = a.starts[p + 1] - q0;
+        double *o = a.out + (long long)p * a.B;
+        if (a.mode == FEM_M || n > 8) {
+            for (int b = lane; b < a.B; b += 32) o[b] = batch_item_slow(a, (unsigned)p, (unsigned)b);
+            continue;
+        }
+        const double kl = lane < n ? a.kq[q0 + lane] : 0.0;
+        const int el = (lane < n && a.coef) ? a.order[q0 + lane] / 9 : 0;
+        const double msv = a.mode != FEM_K ? a.ms[p] : 0.0;
+        for (int b0 = 0; b0 < a.B; b0 += 32) {
+            const int b = b0 + lane;
+            const bool on = b < a.B;
+            double t[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double kk = __shfl_sync(0xffffffffu, kl, k);
+                const int ek = __shfl_sync(0xffffffffu, el, k);
+                t[k] = (a.coef && k < n) ? __dmul_rn(kk, on ? __ldg(&a.coef[(long long)ek * a.cb + (a.cb > 1 ? b : 0)]) : 0.0)
+                                         : kk;
+            }
+            double rest = -0.0;  // numpy's short sum (below 8 terms): sequential from -0.0
+#pragma unroll
+            for (int k = 1; k < 8; ++k)
+                if (k < n) rest = __dadd_rn(rest, t[k]);
+            const double Ks = __dadd_rn(t[0], rest);
+            if (on) o[b] = a.mode == FEM_K ? Ks : __dadd_rn(msv, __dmul_rn(a.scale, Ks));
+        }
     }
 }
 
@@ -156,8 +232,14 @@ std::string fem_plan_build(long long nv, long long nt, const long long *tri, Fem
 cudaError_t launch_fem_assemble(const FemArgs &a, int *bad, cudaStream_t s) {
     const long long total = (long long)a.nnz * a.B;
     if (total == 0) return cudaSuccess;
-    const int grid = (int)std::min<long long>((total + 255) / 256, 16LL * num_sms());
     note_launch();
+    if (a.vb == 1 && total < (1LL << 31)) {  // one mesh: per-slot geometry shared by the batch
+        fem_prep_kernel<<<(int)std::min<long long>((a.nnz + 255) / 256, 16LL * num_sms()), 256, 0, s>>>(a, bad);
+        note_launch();
+        fem_batch_kernel<<<(int)std::min<long long>((a.nnz + 7) / 8, 32LL * num_sms()), 256, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    const int grid = (int)std::min<long long>((total + 255) / 256, 16LL * num_sms());
     fem_assemble_kernel<<<grid, 256, 0, s>>>(a, bad);
     return cudaGetLastError();
 }

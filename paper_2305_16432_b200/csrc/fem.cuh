@@ -21,6 +21,8 @@ struct FemArgs {
     int mode = FEM_K;
     double scale = 1.0;           // s of M + s K
     double *out = nullptr;        // [nnz][B]
+    double *kq = nullptr;         // plan scratch: unscaled stiffness entry per triplet [9 nt] (shared vertices)
+    double *ms = nullptr;         // plan scratch: mass sum per slot [nnz]
 };
 
 struct FemPlanHost {

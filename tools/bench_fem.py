@@ -58,6 +58,7 @@ def main():
     t0 = time.perf_counter()
     Mv = asm.values(M)
     host = []
+    a.cpu_systems = min(a.cpu_systems, a.batch)
     for b in range(a.cpu_systems):
         host.append(Mv + dt2 * asm.values(K * C[:, b, None, None]))
     t_cpu = (time.perf_counter() - t0) / a.cpu_systems
