@@ -76,8 +76,9 @@ class Assembler:
     order (fem.py:116-134); the sort is computed once per mesh."""
 
     def __init__(self, n_vertices: int, triangles: np.ndarray):
-        rows = np.repeat(triangles, 3, axis=1).ravel()
-        cols = np.tile(triangles, (1, 3)).ravel()
+        npe = triangles.shape[1]  # 3 (triangles) or 4 (tetrahedra)
+        rows = np.repeat(triangles, npe, axis=1).ravel()
+        cols = np.tile(triangles, (1, npe)).ravel()
         order = np.lexsort((cols, rows))
         r, c = rows[order], cols[order]
         head = np.ones(len(r), dtype=bool)
@@ -223,6 +224,111 @@ def wave_2d(k=512, jitter=0.2, dt=1e-3, sigma=0.5, batch=32, cfg=3, first=0) -> 
         rhs[:, j] = _host_spmv(Mm, grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3)))
     A = asm.matrix(np.ascontiguousarray(vals[:, 0]))
     return Problem("wave2d", A, rhs, vals, 1e-8, None, {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg})
+
+
+# ---------------------------------------------------------------------------
+# 3-D inputs (configs 4 and 5): Kuhn-split unit cube, P1 tetrahedra. The
+# reference has no 3-D FEM; this restates P1 on tetrahedra in the 2-D code's
+# style (element blocks in a fixed elementwise operation order, the same
+# COO lexsort / reduceat scatter), so assembled matrices are bitwise
+# symmetric as graph_from_system requires (gnn.py:79-82).
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Mesh3D:
+    vertices: np.ndarray   # (nv, 3)
+    tets: np.ndarray       # (nt, 4), positive orientation
+    boundary: np.ndarray   # (nv,) bool
+
+
+def unit_cube(k: int, jitter: float = 0.0, rng: np.random.Generator | None = None) -> Mesh3D:
+    """(k+1)^3 vertices (x fastest), every cell split into the 6 Kuhn
+    tetrahedra around its (0,0,0)-(1,1,1) diagonal; interior vertices moved by
+    U[-jitter, jitter] * h per coordinate."""
+    axis = np.arange(k + 1) / k
+    zs, ys, xs = np.meshgrid(axis, axis, axis, indexing="ij")
+    v = np.column_stack([xs.ravel(), ys.ravel(), zs.ravel()])
+    boundary = ((v == 0.0) | (v == 1.0)).any(axis=1)
+    if jitter > 0.0:
+        inner = np.flatnonzero(~boundary)
+        v[inner] += rng.uniform(-1.0, 1.0, size=(len(inner), 3)) * (jitter / k)
+    n1 = k + 1
+    step = np.array([1, n1, n1 * n1])
+    iz, iy, ix = np.meshgrid(np.arange(k), np.arange(k), np.arange(k), indexing="ij")
+    o = (iz * n1 * n1 + iy * n1 + ix).ravel()
+    tets = []
+    for perm, sign in (((0, 1, 2), 1), ((0, 2, 1), -1), ((1, 0, 2), -1), ((1, 2, 0), 1), ((2, 0, 1), 1),
+                       ((2, 1, 0), -1)):
+        a = o
+        b = a + step[perm[0]]
+        c = b + step[perm[1]]
+        d = c + step[perm[2]]
+        tets.append(np.column_stack([a, b, c, d] if sign > 0 else [a, c, b, d]))
+    tets = np.stack(tets, axis=1).reshape(-1, 4).astype(np.int64)  # cell-major, 6 per cell
+    return Mesh3D(v, tets, boundary)
+
+
+def tet_blocks(mesh: Mesh3D):
+    """Per-tetrahedron 4x4 P1 stiffness and mass blocks, (nt, 4, 4) each:
+    K_ij = |T| grad l_i . grad l_j, M_ij = |T| (1 + d_ij) / 20."""
+    p = mesh.vertices[mesh.tets]
+    e1, e2, e3 = p[:, 1] - p[:, 0], p[:, 2] - p[:, 0], p[:, 3] - p[:, 0]
+    c23, c31, c12 = np.cross(e2, e3), np.cross(e3, e1), np.cross(e1, e2)
+    det = (e1[:, 0] * c23[:, 0] + e1[:, 1] * c23[:, 1]) + e1[:, 2] * c23[:, 2]
+    if np.any(det <= 0.0):
+        raise ValueError("degenerate or inverted tetrahedron (reduce the jitter)")
+    g = np.empty((len(det), 4, 3))
+    g[:, 1], g[:, 2], g[:, 3] = c23 / det[:, None], c31 / det[:, None], c12 / det[:, None]
+    g[:, 0] = -((g[:, 1] + g[:, 2]) + g[:, 3])
+    vol = det / 6.0
+    dots = (g[:, :, None, 0] * g[:, None, :, 0] + g[:, :, None, 1] * g[:, None, :, 1]) + \
+        g[:, :, None, 2] * g[:, None, :, 2]
+    K = vol[:, None, None] * dots
+    M = (vol / 20.0)[:, None, None] * (np.ones((4, 4)) + np.eye(4))[None]
+    return K, M
+
+
+def poisson_3d(k=64, jitter=0.15, batch=128, cfg=4, first=0) -> Problem:
+    """Config 4: Poisson stiffness on a jittered Kuhn cube, full-boundary
+    Dirichlet eliminated (n = (k-1)^3); B right-hand sides (M f)[free], f a
+    3-D squared-exponential GRF with length scale U[0.05, 0.3]; one mesh."""
+    rngs = streams(cfg, first + batch)[first:]
+    mesh_rng = rngs[0] if first == 0 else streams(cfg, 1)[0]
+    mesh = unit_cube(k, jitter, mesh_rng)
+    K, M = tet_blocks(mesh)
+    asm = Assembler(len(mesh.vertices), mesh.tets)
+    Kv, Mv = asm.values(K), asm.values(M)
+    free = np.flatnonzero(~mesh.boundary)
+    red = Restriction(asm.matrix(Kv), free)
+    A = red.matrix(Kv)
+    Mm = asm.matrix(Mv)
+    rhs = np.empty((len(free), batch))
+    for j, rng in enumerate(rngs):
+        f = grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3))
+        rhs[:, j] = _host_spmv(Mm, f)[free]
+    return Problem("poisson3d", A, rhs, None, 1e-8, None, {"k": k, "jitter": jitter, "cfg": cfg})
+
+
+def heat_3d(k=128, jitter=0.15, dt=1e-3, sigma=1.0, batch=8, cfg=5, first=0) -> Problem:
+    """Config 5: A = M + dt K_kappa on a jittered Kuhn cube (no Dirichlet rows,
+    n = (k+1)^3), kappa = exp(sigma GRF) per element and system; b = M g with g
+    a GRF; distinct A per system, one mesh (rtol 1e-10)."""
+    rngs = streams(cfg, first + batch)[first:]
+    mesh = unit_cube(k, jitter, np.random.default_rng(np.random.SeedSequence(1000 * cfg + 17).entropy))
+    K, M = tet_blocks(mesh)
+    asm = Assembler(len(mesh.vertices), mesh.tets)
+    Mv = asm.values(M)
+    Mm = asm.matrix(Mv)
+    cent = mesh.vertices[mesh.tets].mean(axis=1)
+    vals = np.empty((len(asm.col_idx), batch))
+    rhs = np.empty((len(mesh.vertices), batch))
+    for j, rng in enumerate(rngs):
+        kap = np.exp(sigma * grf_2d(cent, rng, rng.uniform(0.05, 0.3)))
+        vals[:, j] = Mv + dt * asm.values(K * kap[:, None, None])
+        rhs[:, j] = _host_spmv(Mm, grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3)))
+    A = asm.matrix(np.ascontiguousarray(vals[:, 0]))
+    return Problem("heat3d", A, rhs, vals, 1e-10, None, {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg})
 
 
 def _host_spmv(A: SparseMatrixCsr, x):

@@ -1,0 +1,78 @@
+"""Configs 4 and 5 (3-D Kuhn cubes, P1 tetrahedra) at parity-test sizes:
+the triangular solves take the level-set path (3-D patterns have no line
+schedule), the GNN runs on ~12 neighbours per row. Checker: the oracle port
+(pinned to pcgkit on the goldens). Bars as in test_gpu_parity.py."""
+import numpy as np
+import pytest
+
+from oracle import port
+from paper_2305_16432_b200 import gnn, inputs, pcg, sparse
+
+pytestmark = pytest.mark.gpu
+
+L_TOL = 1e-5
+X_TOL = 1e-8
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def perturbed_model(seed, h=16, n_mp=2):
+    hyper = gnn.GnnHyperParams(l=1, h=h, n_mp=n_mp, l_mp=1, h_mp=h)
+    model = gnn.create_model(hyper, seed=seed)
+    for r in range(hyper.n_mp):  # cancel the processor output gain: non-trivial L'
+        for s in ("node", "edge"):
+            model.params[f"mp{r}.{s}.1.w"] *= 10.0
+    return model, port.Hyper(l=1, h=h, n_mp=n_mp, l_mp=1, h_mp=h)
+
+
+def test_apply_inverse_bitwise_3d(gpu):
+    A = inputs.poisson_3d(k=10, batch=1).A
+    rng = np.random.default_rng(7)
+    low = A.strict_lower()
+    vals = rng.uniform(-0.2, 0.2, size=low.nnz)
+    F = sparse.LowerFactor(A.n, sparse.SparseMatrixCsr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    oF = port.Factor(A.n, port.Csr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    for s in range(3):
+        r = rng.standard_normal(A.n)
+        np.testing.assert_array_equal(sparse.ldlt_apply_inverse(F, r), oF.apply_inverse(r))
+    x = rng.standard_normal(A.n)
+    np.testing.assert_array_equal(sparse.spmv(A, x), port.spmv(port.Csr(A.n, A.row_ptr, A.col_idx, A.values), x))
+
+
+def test_poisson_3d_shared_factor_batch(gpu):
+    """Config-4 shape: one L' from the GNN on RHS 0, a batch of GRF loads."""
+    prob = inputs.poisson_3d(k=9, batch=6)
+    A = prob.A
+    oA = port.Csr(A.n, A.row_ptr, A.col_idx, A.values)
+    model, ohp = perturbed_model(0)
+    P = gnn.build_learned(model, A, prob.rhs[:, 0])
+    oF = port.build_learned(ohp, model.params, oA, prob.rhs[:, 0])
+    assert rel(P.factor.strict_lower.values, oF.lower.values) <= L_TOL
+    thr = (1e-8,)
+    X, reps = pcg.pcg_solve_batch(A, prob.rhs, P, pcg.SolveOptions(thresholds=thr, max_iter=3000))
+    for s, rep in enumerate(reps):
+        ox, orep = port.pcg_solve(oA, prob.rhs[:, s], oF, thresholds=thr, max_iter=3000)
+        assert rep.converged and orep.converged
+        assert abs(rep.iterations - orep.iterations) <= 1, (s, rep.iterations, orep.iterations)
+        assert rel(X[:, s], ox) <= X_TOL
+
+
+def test_heat_3d_distinct_systems(gpu):
+    """Config-5 shape: distinct A (per-element exp(GRF) diffusivity) and L' per
+    system, rtol 1e-10."""
+    prob = inputs.heat_3d(k=7, batch=3)
+    A, vals = prob.A, prob.values
+    model, ohp = perturbed_model(1)
+    P = gnn.build_learned_batch(model, A, prob.rhs, values=vals)
+    thr = (1e-10,)
+    X, reps = pcg.pcg_solve_batch(A, prob.rhs, P, pcg.SolveOptions(thresholds=thr, max_iter=3000), values=vals)
+    for s, rep in enumerate(reps):
+        oA = port.Csr(A.n, A.row_ptr, A.col_idx, np.ascontiguousarray(vals[:, s]))
+        oF = port.build_learned(ohp, model.params, oA, prob.rhs[:, s])
+        assert rel(P.system_factor(s).strict_lower.values, oF.lower.values) <= L_TOL
+        ox, orep = port.pcg_solve(oA, prob.rhs[:, s], oF, thresholds=thr, max_iter=3000)
+        assert rep.converged and orep.converged
+        assert abs(rep.iterations - orep.iterations) <= 1, (s, rep.iterations, orep.iterations)
+        assert rel(X[:, s], ox) <= X_TOL

@@ -48,3 +48,26 @@ def test_sizes_of_the_configs():
     assert len(asm.col_idx) == 460289
     free = np.flatnonzero(~m.boundary)
     assert len(free) == 65025
+
+
+def test_kuhn_cube_p1_tetrahedra():
+    """3-D generator (configs 4, 5): bitwise symmetric SPD matrices, exact P1
+    identities (K 1 = 0, x'Kx = volume, total mass = volume)."""
+    mesh = inputs.unit_cube(6, 0.15, np.random.default_rng(0))
+    assert mesh.tets.shape == (6 * 6 ** 3, 4)
+    K, M = inputs.tet_blocks(mesh)
+    asm = inputs.Assembler(len(mesh.vertices), mesh.tets)
+    Kv, Mv = asm.values(K), asm.values(M)
+    Km = asm.matrix(Kv)
+    ones = np.ones(Km.n)
+    assert np.abs(inputs._host_spmv(Km, ones)).max() < 1e-14
+    x = mesh.vertices[:, 0]
+    assert abs(x @ inputs._host_spmv(Km, x) - 1.0) < 1e-13
+    assert abs(Mv.sum() - 1.0) < 1e-13
+    for p in (inputs.poisson_3d(k=6, batch=2), inputs.heat_3d(k=5, batch=2)):
+        A = p.A
+        dense = A.to_dense()
+        np.testing.assert_array_equal(dense, dense.T)
+        assert np.linalg.eigvalsh(dense).min() > 0.0
+    assert inputs.poisson_3d(k=6, batch=1).A.n == 5 ** 3
+    assert inputs.heat_3d(k=5, batch=1).A.n == 6 ** 3
