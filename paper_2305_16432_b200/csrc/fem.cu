@@ -154,11 +154,10 @@ __device__ double batch_item_slow(const FemArgs &a, unsigned p, unsigned b) {
     return a.mode == FEM_K ? Ks : __dadd_rn(a.ms[p], __dmul_rn(a.scale, Ks));
 }
 
-// A warp per slot, lanes over the systems: lane k fetches the run's k-th
-// stiffness entry and element id (one coalesced load each), the warp
-// broadcasts them by shuffles, and every coefficient load of the run is then
-// in flight at once (lane = system: contiguous 256-byte rows), as is the
-// value store. Runs longer than 8 take the generic walk.
+// A warp per slot, lanes over the systems: the run's stiffness entries and
+// element ids are warp-uniform loads, each coefficient row a contiguous
+// 256-byte load across the lanes, the values one contiguous store. Runs
+// longer than 8 take the generic walk.
 __global__ void __launch_bounds__(256) fem_batch_kernel(FemArgs a) {
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
@@ -169,26 +168,22 @@ __global__ void __launch_bounds__(256) fem_batch_kernel(FemArgs a) {
             for (int b = lane; b < a.B; b += 32) o[b] = batch_item_slow(a, (unsigned)p, (unsigned)b);
             continue;
         }
-        const double kl = lane < n ? a.kq[q0 + lane] : 0.0;
-        const int el = (lane < n && a.coef) ? a.order[q0 + lane] / 9 : 0;
         const double msv = a.mode != FEM_K ? a.ms[p] : 0.0;
         for (int b0 = 0; b0 < a.B; b0 += 32) {
             const int b = b0 + lane;
-            const bool on = b < a.B;
-            double t[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const double kk = __shfl_sync(0xffffffffu, kl, k);
-                const int ek = __shfl_sync(0xffffffffu, el, k);
-                t[k] = (a.coef && k < n) ? __dmul_rn(kk, on ? __ldg(&a.coef[(long long)ek * a.cb + (a.cb > 1 ? b : 0)]) : 0.0)
-                                         : kk;
-            }
+            const int bc = a.cb > 1 ? min(b, a.B - 1) : 0;
+            // run entries and element ids are warp-uniform loads; the coefficient
+            // row is one contiguous load across the lanes
+            auto term = [&](int q) -> double {
+                const double k = __ldg(&a.kq[q]);
+                return a.coef ? __dmul_rn(k, __ldg(&a.coef[(long long)(__ldg(&a.order[q]) / 9) * a.cb + bc])) : k;
+            };
+            const double first = term(q0);
             double rest = -0.0;  // numpy's short sum (below 8 terms): sequential from -0.0
-#pragma unroll
-            for (int k = 1; k < 8; ++k)
-                if (k < n) rest = __dadd_rn(rest, t[k]);
-            const double Ks = __dadd_rn(t[0], rest);
-            if (on) o[b] = a.mode == FEM_K ? Ks : __dadd_rn(msv, __dmul_rn(a.scale, Ks));
+#pragma unroll 2
+            for (int q = q0 + 1; q < q0 + n; ++q) rest = __dadd_rn(rest, term(q));
+            const double Ks = __dadd_rn(first, rest);
+            if (b < a.B) o[b] = a.mode == FEM_K ? Ks : __dadd_rn(msv, __dmul_rn(a.scale, Ks));
         }
     }
 }
