@@ -920,7 +920,7 @@ struct npcg_fem_plan {
     long long nv = 0, nt = 0, nnz = 0;
     std::vector<long long> row_ptr, col;
     int *d_starts = nullptr, *d_order = nullptr, *d_tri = nullptr;
-    double *d_kq = nullptr, *d_ms = nullptr;  // shared-mesh scratch (fem_prep_kernel)
+    double *d_kq = nullptr, *d_ms = nullptr, *d_mq = nullptr;  // shared-mesh scratch (fem_prep_kernel)
 };
 
 extern "C" int npcg_fem_plan_create(int64_t nv, int64_t nt, const int64_t *tri, npcg_fem_plan **out) {
@@ -942,6 +942,7 @@ extern "C" int npcg_fem_plan_create(int64_t nv, int64_t nt, const int64_t *tri, 
     NPCG_CUDA(dalloc(&p->d_tri, t32.size()));
     NPCG_CUDA(dalloc(&p->d_kq, h.order.size()));
     NPCG_CUDA(dalloc(&p->d_ms, h.col.size()));
+    NPCG_CUDA(dalloc(&p->d_mq, h.order.size()));
     NPCG_CUDA(cudaMemcpy(p->d_starts, h.starts.data(), h.starts.size() * 4, cudaMemcpyHostToDevice));
     NPCG_CUDA(cudaMemcpy(p->d_order, h.order.data(), h.order.size() * 4, cudaMemcpyHostToDevice));
     NPCG_CUDA(cudaMemcpy(p->d_tri, t32.data(), t32.size() * 4, cudaMemcpyHostToDevice));
@@ -956,6 +957,7 @@ extern "C" int npcg_fem_plan_destroy(npcg_fem_plan *p) {
     cudaFree(p->d_tri);
     cudaFree(p->d_kq);
     cudaFree(p->d_ms);
+    cudaFree(p->d_mq);
     delete p;
     return NPCG_OK;
 }
@@ -994,6 +996,8 @@ extern "C" int npcg_fem_assemble(const npcg_fem_plan *p, int B, const double *ve
     a.out = values;
     a.kq = p->d_kq;
     a.ms = p->d_ms;
+    a.mq = p->d_mq;
+    a.nt = (int)p->nt;
     NPCG_CUDA(launch_fem_assemble(a, flag, s));
     return NPCG_OK;
 }

@@ -123,24 +123,28 @@ __global__ void __launch_bounds__(256) fem_assemble_kernel(FemArgs a, int *bad) 
 }
 
 // Shared vertices (one mesh for the batch), two passes:
-//  prep  -- one thread per slot: the unscaled stiffness entry of every triplet
-//           of its run (geometry and divides once per mesh, not per system)
-//           into kq[q], and the whole mass sum into ms[p];
+//  prep  -- one thread per triplet: its unscaled stiffness and mass entries
+//           (geometry and divides once per mesh, not per system) into kq / mq,
+//           then one thread per slot sums the mass run into ms[p];
 //  batch -- one thread per (slot, system), system fastest: the coefficient
 //           products of the run summed in numpy's order. A warp's kq / order
 //           reads are broadcasts, its coefficient reads and value stores are
 //           contiguous.
 __global__ void __launch_bounds__(256) fem_prep_kernel(FemArgs a, int *bad) {
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < a.nnz; p += gridDim.x * blockDim.x) {
-        const int q0 = a.starts[p], q1 = a.starts[p + 1];
-        for (int q = q0; q < q1; ++q) {
-            const int o = a.order[q], e = o / 9, l = o - 9 * e;
-            const Elem E = element(a.tri, a.V, 1, a.B, 0, e);
-            if (E.bad) atomicOr(bad, 1);
-            a.kq[q] = entry<false>(E, l / 3, l % 3, 1.0, false);
-        }
-        if (a.mode != FEM_K) a.ms[p] = slot_sum<true>(a, p, 0, bad);
+    const int m = 9 * a.nt;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < m; q += gridDim.x * blockDim.x) {
+        const int o = a.order[q], e = o / 9, l = o - 9 * e;
+        const Elem E = element(a.tri, a.V, 1, a.B, 0, e);
+        if (E.bad) atomicOr(bad, 1);
+        a.kq[q] = entry<false>(E, l / 3, l % 3, 1.0, false);
+        if (a.mode != FEM_K) a.mq[q] = entry<true>(E, l / 3, l % 3, 1.0, false);
     }
+}
+
+// mass sum per slot from the per-triplet entries, numpy reduceat order
+__global__ void __launch_bounds__(256) fem_mass_kernel(FemArgs a) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < a.nnz; p += gridDim.x * blockDim.x)
+        a.ms[p] = reduceat_run(a.starts[p], a.starts[p + 1], [&](int q) -> double { return a.mq[q]; });
 }
 
 // value of item t = (slot p, system b) by the generic run walk (runs > 8)
@@ -229,7 +233,11 @@ cudaError_t launch_fem_assemble(const FemArgs &a, int *bad, cudaStream_t s) {
     if (total == 0) return cudaSuccess;
     note_launch();
     if (a.vb == 1 && total < (1LL << 31)) {  // one mesh: per-slot geometry shared by the batch
-        fem_prep_kernel<<<(int)std::min<long long>((a.nnz + 255) / 256, 16LL * num_sms()), 256, 0, s>>>(a, bad);
+        fem_prep_kernel<<<(int)std::min<long long>((9LL * a.nt + 255) / 256, 32LL * num_sms()), 256, 0, s>>>(a, bad);
+        if (a.mode != FEM_K) {
+            note_launch();
+            fem_mass_kernel<<<(int)std::min<long long>((a.nnz + 255) / 256, 16LL * num_sms()), 256, 0, s>>>(a);
+        }
         note_launch();
         fem_batch_kernel<<<(int)std::min<long long>((a.nnz + 7) / 8, 32LL * num_sms()), 256, 0, s>>>(a);
         return cudaGetLastError();

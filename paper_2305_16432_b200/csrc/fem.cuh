@@ -10,7 +10,7 @@ namespace npcg {
 enum FemMode : int { FEM_K = 0, FEM_M = 1, FEM_M_PLUS_SK = 2 };  // include/npcg.h NPCG_FEM_*
 
 struct FemArgs {
-    int nnz = 0, B = 1;
+    int nnz = 0, B = 1, nt = 0;
     const int *starts = nullptr;  // [nnz + 1] runs of triplet ids per CSR slot
     const int *order = nullptr;   // [9 nt] triplet ids in lexsort order
     const int *tri = nullptr;     // [nt][3]
@@ -23,6 +23,7 @@ struct FemArgs {
     double *out = nullptr;        // [nnz][B]
     double *kq = nullptr;         // plan scratch: unscaled stiffness entry per triplet [9 nt] (shared vertices)
     double *ms = nullptr;         // plan scratch: mass sum per slot [nnz]
+    double *mq = nullptr;         // plan scratch: mass entry per triplet [9 nt]
 };
 
 struct FemPlanHost {
