@@ -162,7 +162,7 @@ __device__ double batch_item_slow(const FemArgs &a, unsigned p, unsigned b) {
 // element ids are warp-uniform loads, each coefficient row a contiguous
 // 256-byte load across the lanes, the values one contiguous store. Runs
 // longer than 8 take the generic walk.
-__global__ void __launch_bounds__(256) fem_batch_kernel(FemArgs a) {
+__global__ void __launch_bounds__(256, 8) fem_batch_kernel(FemArgs a) {  // 32 registers: full occupancy, the loads are latency-bound
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < a.nnz; p += warps) {
