@@ -827,8 +827,11 @@ static void spmv_warp_vw(const SpmvArgs &a, int grid, size_t smem, cudaStream_t 
 #endif
 constexpr int kEllCols = NPCG_ELL_COLS;  // systems per block (blockIdx.y picks the group)
 
+#ifndef NPCG_ELL_MINB
+#define NPCG_ELL_MINB 2
+#endif
 template <int E, bool VB, int OP>
-__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_ell_kernel(SpmvArgs a) {
+__global__ void __launch_bounds__(kSpmvThreads, NPCG_ELL_MINB) spmv_ell_kernel(SpmvArgs a) {
     constexpr int TEAMS = kSpmvThreads / 32;
     __shared__ double red[TEAMS * kSpmvThreads];  // reused by the tail's final pass
     __shared__ unsigned char s_act[kMaxBatch];
