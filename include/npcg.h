@@ -83,13 +83,22 @@ typedef struct {
 } npcg_pattern_info;
 int npcg_pattern_get_info(const npcg_pattern *p, npcg_pattern_info *info);
 
+/* The line-wavefront schedule of a factor pattern (built on first use;
+ * pattern.h LineSched): grid lines, warps (32 lines each), wavefront steps,
+ * and the CTAs per system (1, 2 or 4) a solve of `batch` systems launches
+ * with. All zero when the pattern does not qualify and the triangular solves
+ * run the level-set kernels. Any output may be NULL. */
+int npcg_pattern_line_info(const npcg_pattern *p, int32_t *lines, int32_t *warps, int32_t *steps,
+                           int32_t *cluster, int batch);
+
 /* Device views owned by the pattern (int32). Any may be NULL. */
 int npcg_pattern_device_arrays(const npcg_pattern *p, const int32_t **row_ptr,
                                const int32_t **col_idx, const int32_t **diag_pos,
                                const int32_t **pair, const int32_t **lower_slot);
 
 /* Exact value-symmetry test on device for B systems (sparse.py:137-147):
- * writes ok[b] = 1 when vals[p] == vals[pair[p]] bitwise for every p. */
+ * writes ok[b] = 1 when vals[p] == vals[pair[p]] for every p (IEEE
+ * equality like np.array_equal: -0.0 == 0.0, NaN never equal). */
 int npcg_check_symmetric_values(const npcg_pattern *p, int B, const double *vals,
                                 int vals_batched, int32_t *ok_host, void *stream);
 
@@ -150,7 +159,9 @@ typedef struct {
     int32_t absolute;             /* SolveOptions.absolute */
     int32_t check_every;          /* host polls convergence every k passes (0 = auto) */
     int32_t profile;              /* 1: time every kernel launch with CUDA events */
-    int32_t reserved;
+    int32_t history;              /* 1: keep ||r_k|| per system on the device (grown on
+                                     demand) for npcg_solver_history; implied when
+                                     report->history is given */
 } npcg_solve_opts;
 
 /* kernel classes reported by a profiled solve */
@@ -200,6 +211,12 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int A_batched,
                    const double *S, int S_batched, const double *D, int D_batched,
                    const double *b, double *x, const double *x0,
                    const npcg_solve_opts *opts, npcg_solve_report *report, void *stream);
+
+/* SolveReport.history (pcg.py:113,145) of the last npcg_pcg_solve on `s`:
+ * out[b*ld + k] = ||r_k|| for k < min(cols, max iterations + 1), host memory.
+ * The device buffer grows with the iterations actually run, so callers can
+ * size `out` from report->iterations instead of B x (max_iter + 1). */
+int npcg_solver_history(const npcg_solver *s, double *out, int64_t ld, int64_t cols, void *stream);
 
 /* ---- P1 FEM assembly (input side) --------------
  * Replaces pcgkit.fem.full_stiffness_and_mass / assemble's matrix part

@@ -53,6 +53,7 @@ def _kernels():
         lib.oracle_forward_unit.argtypes = [I, P, P, P, P, P]
         lib.oracle_backward_unit_t.argtypes = [I, P, P, P, P]
         lib.oracle_ldlt_apply_inverse.argtypes = [I, P, P, P, P, P, P]
+        lib.oracle_segment_sum_sorted.argtypes = [I, I, P, P, P]
         _lib = lib
     return _lib
 
@@ -274,7 +275,21 @@ def _mlp(params, prefix, x, layers):
 
 
 def _segment_sum(x, seg, n):
-    """Canonical-order segment sum (autodiff.py:221-243)."""
+    """Canonical-order segment sum (autodiff.py:221-243). CSR-ordered
+    segments (non-decreasing seg, the GNN's case) go through the C loop in
+    kernels.c, which sorts each segment's addends in the same lexicographic
+    order and sums them like np.add.reduceat; anything else takes the
+    lexsort restatement below."""
+    out = np.zeros((n, x.shape[1]))
+    if x.shape[0] and x.shape[1] and np.all(seg[1:] >= seg[:-1]):
+        xc = np.ascontiguousarray(x, dtype=np.float64)
+        sc = np.ascontiguousarray(seg, dtype=np.int64)
+        _kernels().oracle_segment_sum_sorted(x.shape[0], x.shape[1], _p(xc), _p(sc), _p(out))
+        return out
+    return _segment_sum_lexsort(x, seg, n)
+
+
+def _segment_sum_lexsort(x, seg, n):
     out = np.zeros((n, x.shape[1]))
     if x.shape[0]:
         keys = tuple(x[:, c] for c in range(x.shape[1] - 1, -1, -1)) + (seg,)

@@ -58,7 +58,7 @@ class SolveOpts(ctypes.Structure):
     _fields_ = [("n_thresholds", ctypes.c_int32), ("thresholds", ctypes.c_double * MAX_THRESHOLDS),
                 ("max_iter", ctypes.c_int64), ("absolute", ctypes.c_int32),
                 ("check_every", ctypes.c_int32), ("profile", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("history", ctypes.c_int32)]
 
 
 PROF_SLOTS = 8
@@ -99,6 +99,8 @@ SIGNATURES = {
     "npcg_solver_destroy": (I32, [P]),
     "npcg_pcg_solve": (I32, [P, P, I32, P, I32, P, I32, P, P, P, ctypes.POINTER(SolveOpts),
                              ctypes.POINTER(SolveReportC), P]),
+    "npcg_solver_history": (I32, [P, P, I64, I64, P]),
+    "npcg_pattern_line_info": (I32, [P, P, P, P, P, I32]),
     "npcg_launch_count": (I64, []),
     "npcg_debug_line_trace": (I32, [P, I32]),
     "npcg_fem_plan_create": (I32, [I64, I64, P, ctypes.POINTER(P)]),

@@ -6,7 +6,9 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -18,7 +20,13 @@
 
 using namespace npcg;
 
-struct npcg_pattern : public npcg::Pattern {};
+struct npcg_pattern : public npcg::Pattern {
+    // npcg_ldlt_apply_inverse workspaces by batch width (schedule packing,
+    // scratch vectors): built once, reused by every later call; the mutex
+    // serialises calls that share one
+    std::mutex apply_mu;
+    std::map<int, std::shared_ptr<npcg_solver>> apply_cache;
+};
 
 namespace {
 
@@ -134,14 +142,22 @@ struct npcg_solver {
     double *Dl = nullptr;  // diag in line order ([b][nslot] or [nslot])
     size_t Dl_cap = 0;
     int *xpend = nullptr;
-    int *h_active = nullptr;  // pinned
+    double *ones = nullptr;   // identity preconditioner: D = 1 (per solver: no shared state between threads)
+    long long *kmax = nullptr;  // largest k of the batch at the last poll
+    struct Poll {
+        int active;
+        int pad;
+        long long kmax;
+    };
+    Poll *h_poll = nullptr;  // pinned
+    long long history_len = 0;  // entries per system valid after the last solve
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
                         alpha, beta, rel, final_rel, history, active_count, drift_count, ctl, partial,
-                        S_fwd, S_bwd, xpend, Dl, XL, BL, ecol, eperm, evals};
+                        S_fwd, S_bwd, xpend, Dl, XL, BL, ecol, eperm, evals, ones, kmax};
         for (void *p : ptrs)
             if (p) cudaFree(p);
-        if (h_active) cudaFreeHost(h_active);
+        if (h_poll) cudaFreeHost(h_poll);
     }
 };
 
@@ -259,6 +275,18 @@ int npcg_pattern_get_info(const npcg_pattern *pc, npcg_pattern_info *info) {
         info->window = std::max(s->fwd.window, s->bwd.window);
         info->max_level_width = std::max(s->fwd.maxw, s->bwd.maxw);
     }
+    return NPCG_OK;
+}
+
+int npcg_pattern_line_info(const npcg_pattern *pc, int32_t *lines, int32_t *warps, int32_t *steps, int32_t *cluster,
+                           int batch) {
+    if (!pc) return fail(NPCG_ERR_ARGUMENT, "NULL pattern");
+    npcg_pattern *p = const_cast<npcg_pattern *>(pc);
+    LineSched *ls = p->line_schedule();
+    if (lines) *lines = ls ? ls->lines : 0;
+    if (warps) *warps = ls ? ls->fwd.warps : 0;
+    if (steps) *steps = ls ? ls->steps : 0;
+    if (cluster) *cluster = ls ? line_config_for(ls->fwd, false, std::max(batch, 1)) / 256 : 0;
     return NPCG_OK;
 }
 
@@ -428,7 +456,13 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     if (s->ls) part = std::max<size_t>(part, (size_t)((s->ls->nslot + kSpmvThreads - 1) / kSpmvThreads) * B);
     s->partial_cap = part;
     NPCG_CUDA(dalloc(&s->partial, part));
-    NPCG_CUDA(cudaMallocHost((void **)&s->h_active, sizeof(int)));
+    NPCG_CUDA(dalloc(&s->kmax, 1));
+    NPCG_CUDA(cudaMallocHost((void **)&s->h_poll, sizeof(npcg_solver::Poll)));
+    if (s->identity) {
+        NPCG_CUDA(dalloc(&s->ones, A->n));
+        std::vector<double> h(A->n, 1.0);
+        if (A->n) NPCG_CUDA(cudaMemcpy(s->ones, h.data(), (size_t)A->n * 8, cudaMemcpyHostToDevice));
+    }
     if (!s->ls) {  // level-kernel outputs start unsolved (sentinel), see trsv.cu
         launch_fill_sentinel((long long)nB, s->Y, 0);
         launch_fill_sentinel((long long)nB, s->Z, 0);
@@ -582,10 +616,20 @@ int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int s
     if (!F || B < 1 || B > kMaxBatch) return fail(NPCG_ERR_ARGUMENT, "bad argument");
     if (!F->factor_ok) return fail(NPCG_ERR_DATA_FORMAT, "pattern cannot carry a factor");
     if (F->n == 0) return NPCG_OK;
-    // a throw-away solver supplies the schedule, scratch and counters
-    npcg_solver *s = nullptr;
-    if (int rc = npcg_solver_create(F, F, B, &s)) return rc;
-    std::unique_ptr<npcg_solver> guard(s);
+    // a cached solver (per pattern and batch width) supplies the schedule,
+    // scratch and counters
+    npcg_pattern *Fm = const_cast<npcg_pattern *>(F);
+    std::lock_guard<std::mutex> lock(Fm->apply_mu);
+    std::shared_ptr<npcg_solver> &slot = Fm->apply_cache[B];
+    if (!slot) {
+        npcg_solver *made = nullptr;
+        if (int rc = npcg_solver_create(F, F, B, &made)) {
+            Fm->apply_cache.erase(B);
+            return rc;
+        }
+        slot.reset(made, [](npcg_solver *p) { npcg_solver_destroy(p); });
+    }
+    npcg_solver *s = slot.get();
     cudaStream_t st = (cudaStream_t)stream;
     if (int rc = stage_factor(s, S, sb, D, db, st)) return rc;
     if (s->ls) {  // through line order: r -> R, Y, Z -> z
@@ -629,31 +673,30 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     cudaStream_t st = (cudaStream_t)stream;
     const bool identity = s->identity != nullptr;
     // identity preconditioner: S unused, D = 1
-    static double *ones = nullptr;
-    static size_t ones_n = 0;
     if (identity) {
-        if (ones_n < (size_t)n) {
-            if (ones) cudaFree(ones);
-            NPCG_CUDA(dalloc(&ones, n));
-            std::vector<double> h(n, 1.0);
-            NPCG_CUDA(cudaMemcpy(ones, h.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
-            ones_n = n;
-        }
-        S = ones;  // never read: identity pattern has no off-diagonal entries
+        S = s->ones;  // never read: identity pattern has no off-diagonal entries
         sb = 0;
-        D = ones;
+        D = s->ones;
         db = 0;
     }
-    // history buffer
-    const long long cap = rep->history ? std::max<long long>(rep->history_cap, 1) : 1;
-    if (cap > s->history_cap || !s->history) {
+    // history: [B][cap] on the device, grown on demand as iterations advance
+    // (a history can reach max_iter + 1 entries, pcg.py:113,145, but rarely
+    // does: it is not preallocated at that size)
+    const bool want_hist = o->history != 0 || rep->history != nullptr;
+    const long long hist_full = o->max_iter + 1;
+    long long cap = want_hist ? std::min<long long>(hist_full, 1024) : 1;
+    if (!s->history || s->history_cap < cap) {
         if (s->history) cudaFree(s->history);
         s->history = nullptr;
+        s->history_cap = 0;
         NPCG_CUDA(dalloc(&s->history, (size_t)cap * B));
         s->history_cap = cap;
+    } else {
+        cap = want_hist ? std::min(hist_full, s->history_cap) : 1;
     }
+    s->history_len = 0;
     SolveState sst = make_state(s, o);
-    sst.history_cap = rep->history ? cap : 1;
+    sst.history_cap = cap;
     if (n == 0) {
         for (int b = 0; b < B; ++b) {
             rep->status[b] = NPCG_STATUS_CONVERGED;
@@ -793,8 +836,17 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         return cudaGetLastError();
     };
 
+    // the kernels carry the state by value: refresh every copy after the
+    // history buffer moved
+    auto set_state = [&]() {
+        apdot.st = drift.st = sst;
+        fw.v.st = fw.l.st = sst;
+        bw.v.st = bw.l.st = sst;
+    };
     int check = o->check_every > 0 ? o->check_every : 8;
-    const long long max_passes = 2 * o->max_iter + 8;
+    // a pass advances k by at most one; an iteration whose drift check
+    // restarts takes three passes (iterate, restart, re-init)
+    const long long max_passes = 3 * o->max_iter + 16;
     long long passes = 0;
     for (;;) {
         for (int q = 0; q < check; ++q) {
@@ -805,12 +857,30 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
             NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
         }
         passes += check;
-        note_launch(); count_active_kernel<<<1, 256, 0, st>>>(sst, B);
-        NPCG_CUDA(cudaMemcpyAsync(s->h_active, s->active_count, 4, cudaMemcpyDeviceToHost, st));
+        const bool last = passes >= max_passes;
+        note_launch(); count_active_kernel<<<1, 256, 0, st>>>(sst, B, s->kmax, last ? 1 : 0);
+        NPCG_CUDA(cudaMemcpyAsync(&s->h_poll->active, s->active_count, 4, cudaMemcpyDeviceToHost, st));
+        NPCG_CUDA(cudaMemcpyAsync(&s->h_poll->kmax, s->kmax, 8, cudaMemcpyDeviceToHost, st));
         NPCG_CUDA(cudaStreamSynchronize(st));
         harvest();
-        if (*s->h_active == 0 || passes >= max_passes) break;
+        if (s->h_poll->active == 0 || last) break;
         if (check < 64) check *= 2;
+        // the next `check` passes write history entries up to kmax + check
+        const long long need = std::min(hist_full, s->h_poll->kmax + check + 2);
+        if (want_hist && need > cap) {
+            const long long ncap = std::min(hist_full, std::max(2 * cap, need));
+            double *nh = nullptr;
+            NPCG_CUDA(dalloc(&nh, (size_t)ncap * B));
+            NPCG_CUDA(cudaMemcpy2DAsync(nh, (size_t)ncap * 8, s->history, (size_t)cap * 8, (size_t)cap * 8, B,
+                                        cudaMemcpyDeviceToDevice, st));
+            NPCG_CUDA(cudaStreamSynchronize(st));
+            cudaFree(s->history);
+            s->history = nh;
+            s->history_cap = cap = ncap;
+            sst.history = nh;
+            sst.history_cap = ncap;
+            set_state();
+        }
     }
     for (Ev &e : pool) {
         cudaEventDestroy(e.a);
@@ -829,7 +899,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     bool any_max = false;
     for (int b = 0; b < B; ++b) any_max |= status[b] == ST_MAXITER || status[b] == ST_ACTIVE;
     if (any_max) {
-        // columns still ACTIVE after the pass budget count as max-iter
+        // columns still ACTIVE after the pass budget were turned into MAXITER
         SpmvArgs fin = spl;
         fin.op = SPMV_RESID_FINAL;
         fin.X = xv;
@@ -859,12 +929,24 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
                 itto[(size_t)b * T + t] >= 0 ? (double)(tto[(size_t)b * T + t] - t0) * 1e-9 : -1.0;
         }
     }
+    s->history_len = want_hist ? std::min<long long>(kmax + 1, cap) : 0;
     if (rep->history) {
-        const long long w = std::min<long long>(kmax + 1, cap);
+        const long long w = std::min<long long>(s->history_len, rep->history_cap);
         NPCG_CUDA(cudaMemcpy2DAsync(rep->history, (size_t)rep->history_cap * 8, s->history, (size_t)cap * 8,
                                     (size_t)w * 8, B, cudaMemcpyDeviceToHost, st));
         NPCG_CUDA(cudaStreamSynchronize(st));
     }
+    return NPCG_OK;
+}
+
+int npcg_solver_history(const npcg_solver *s, double *out, int64_t ld, int64_t cols, void *stream) {
+    if (!s || !out || ld < cols || cols < 0) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    const long long w = std::min<long long>(cols, s->history_len);
+    if (w <= 0) return NPCG_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    NPCG_CUDA(cudaMemcpy2DAsync(out, (size_t)ld * 8, s->history, (size_t)s->history_cap * 8, (size_t)w * 8, s->B,
+                                cudaMemcpyDeviceToHost, st));
+    NPCG_CUDA(cudaStreamSynchronize(st));
     return NPCG_OK;
 }
 

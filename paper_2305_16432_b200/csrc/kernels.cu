@@ -678,14 +678,26 @@ cudaError_t launch_from_line(int nslot, int B, const int *rowof, const double *s
     return cudaGetLastError();
 }
 
-__global__ void count_active_kernel(SolveState st, int B) {
+// active columns and the largest iteration count (the host grows the history
+// buffer from it); `finish` turns columns still ACTIVE after the pass budget
+// into MAXITER so the final residual pass covers them (pcg.py:171-172)
+__global__ void count_active_kernel(SolveState st, int B, long long *kmax, int finish) {
     __shared__ int s;
-    if (threadIdx.x == 0) s = 0;
+    __shared__ unsigned long long km;
+    if (threadIdx.x == 0) s = 0, km = 0;
     __syncthreads();
-    for (int b = threadIdx.x; b < B; b += blockDim.x)
-        if (st.status[b] == ST_ACTIVE) atomicAdd(&s, 1);
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        if (st.status[b] == ST_ACTIVE) {
+            if (finish) st.status[b] = ST_MAXITER;
+            else atomicAdd(&s, 1);
+        }
+        atomicMax(&km, (unsigned long long)st.k[b]);
+    }
     __syncthreads();
-    if (threadIdx.x == 0) *st.active_count = s;
+    if (threadIdx.x == 0) {
+        *st.active_count = s;
+        *kmax = (long long)km;
+    }
 }
 
 // S[p] from strict-lower values in A.strict_lower() order (symmetric fill).
@@ -710,7 +722,8 @@ __global__ void factor_to_lower_kernel(int nnz_lower, int B, const int *lower_sl
     }
 }
 
-// ok[b] &= vals[p] == vals[pair[p]] bitwise (sparse.py:137-147).
+// ok[b] &= vals[p] == vals[pair[p]] (sparse.py:137-147: np.array_equal on
+// values, so -0.0 matches 0.0 and a NaN never matches).
 __global__ void symmetric_check_kernel(long long nnz, int B, int vb, const int *pair, const double *vals,
                                        int *ok) {
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nnz * B;
@@ -720,7 +733,7 @@ __global__ void symmetric_check_kernel(long long nnz, int B, int vb, const int *
         const int pp = pair[p];
         const double u = vb ? vals[q] : vals[p];
         const double v = vb ? vals[(size_t)pp * B + b] : vals[pp];
-        if (__double_as_longlong(u) != __double_as_longlong(v)) ok[b] = 0;
+        if (!(u == v)) ok[b] = 0;
     }
 }
 

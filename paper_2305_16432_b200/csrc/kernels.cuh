@@ -53,7 +53,7 @@ __global__ void init_state_kernel(SolveState st, int B, long long hist_cap_init)
 __global__ void normb_kernel(int n, int B, const double *v, SolveState st, double *partial, Ctl *ctl);
 __global__ void init_x_kernel(long long nB, int B, const double *x0, double *x, SolveState st);
 __global__ void pupd_kernel(long long nB, int B, double *z, double *p, double *x, SolveState st, int rearm);
-__global__ void count_active_kernel(SolveState st, int B);
+__global__ void count_active_kernel(SolveState st, int B, long long *kmax, int finish);
 __global__ void factor_from_lower_kernel(int nnz_lower, int B, int lb, const int *lower_slot,
                                          const int *pair, const double *lower, double *S);
 __global__ void factor_to_lower_kernel(int nnz_lower, int B, const int *lower_slot, const double *S,

@@ -128,8 +128,10 @@ __device__ __forceinline__ void line_epilogue(const LineArgs &a, int b, double t
 constexpr int kTraceEvents = 16, kTraceBatches = 2048;
 __device__ long long g_line_trace[kTraceEvents][kTraceBatches];
 
+__host__ __device__ constexpr int line_cta_warps(int C) { return C == 1 ? kLineMaxWarps : kLineMaxWarpsCluster; }
+
 template <bool UPPER, bool PCG, bool SB, int G, int C>
-__global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(LineArgs a) {
+__global__ void __launch_bounds__(32 * line_cta_warps(C), 1) trsv_line_kernel(LineArgs a) {
     constexpr int STEPS = kTileSteps * G;
     static_assert(2 * STEPS <= 32, "a stage pair's ring slots are checked by one warp");
     constexpr int NV = line_vectors(UPPER, PCG);
@@ -137,10 +139,12 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
     __shared__ double s_red[kLineMaxWarps];
     __shared__ double s_cta[4];
     constexpr int NS = line_stages(G);
-    const int W = a.warps, WL = W / C, R = a.ring;
+    // WL warps per CTA; the last CTA of a cluster may hold idle warps (w >= W)
+    const int W = a.warps, WL = (W + C - 1) / C, R = a.ring;
     const int wl = threadIdx.x >> 5, t = threadIdx.x & 31;
     const int rank = C > 1 ? (int)cluster_rank() : 0, b = blockIdx.x / C;
     const int w = rank * WL + wl;  // warp of the direction's schedule
+    const bool idle = w >= W;
     // what this system needs from this launch (uniform over the cluster)
     int op = TOP_SOLVE;
     if (PCG) {
@@ -149,7 +153,14 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
         op = !UPPER ? (ph == PH_ITER ? TOP_UPDATE : (ph == PH_INIT ? TOP_SOLVE : TOP_SKIP))
                     : ((ph == PH_ITER || ph == PH_INIT) ? TOP_SOLVE : TOP_SKIP);
         if (op == TOP_SKIP) {
-            if (UPPER && rank == 0 && threadIdx.x == 0) line_epilogue(a, b, 0.0);  // pflag / restart bookkeeping
+            // every thread of the cluster has read status / phase before the
+            // epilogue changes them (PH_RESTART -> PH_INIT), else a late
+            // reader would take the solve path and wait on warps that left
+            if (UPPER) {
+                if (C > 1) cluster_sync_all();
+                else __syncthreads();
+                if (rank == 0 && threadIdx.x == 0) line_epilogue(a, b, 0.0);  // pflag / restart bookkeeping
+            }
             return;
         }
     }
@@ -160,7 +171,7 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
     char *stage = sm + m.stage0 + (size_t)wl * NS * m.stage_bytes;
     for (int i = threadIdx.x; i < WL * R; i += blockDim.x) ring[i] = sentinel();
     const int4 *meta = reinterpret_cast<const int4 *>(a.meta);
-    const int4 me = meta[w];
+    const int4 me = idle ? make_int4(0, 0, 0, 0) : meta[w];
     if (t == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], 1);
         fence_mbar_init();
@@ -174,7 +185,7 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
     // [max(C0_right - 2, C0), min(C1_right - 1, C1)) to the right warp; every
     // value is read once and re-armed by its reader
     int P0 = 0, P1 = 0, Q0 = 0, Q1 = 0;
-    if (w > 0) {
+    if (w > 0 && !idle) {
         const int4 pm = meta[w - 1];
         P0 = pm.x;
         P1 = pm.x + kTileSteps * pm.y;
@@ -184,7 +195,7 @@ __global__ void __launch_bounds__(32 * kLineMaxWarps / C, 1) trsv_line_kernel(Li
         Q0 = max(qm.x - 2, C0);
         Q1 = min(qm.x + kTileSteps * qm.y - 1, C1);
     }
-    const bool cons = w > 0 && t == 0, prod = w + 1 < W && t == 31;
+    const bool cons = !idle && w > 0 && t == 0, prod = !idle && w + 1 < W && t == 31;
     double *rin = ring + wl * R;  // my incoming ring (local)
     // my outgoing ring: the right warp's incoming ring, in its CTA
     const int wr = w + 1 < W ? w + 1 : w;
@@ -422,10 +433,19 @@ int line_config_for(const LineDir &L, bool upper, int B) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (optin <= 0) optin = 227 * 1024;
     const size_t cap = (size_t)optin - 1024;  // static shared memory
-    // CTAs per system: split over two SMs while the batch leaves them free
+    // CTAs per system: split over two SMs while the batch leaves them free;
+    // more than 16 warps (lines > 512) always take a cluster, of 2 CTAs up to
+    // 20 warps and 4 beyond (the last CTA may hold idle warps)
+    auto fits = [&](int c) { return c >= 1 && (L.warps + c - 1) / c <= line_cta_warps(c) && (c == 1 || L.warps >= c); };
     int C = (L.warps % 2 == 0 && 2 * B <= sms) ? 2 : 1;
-    if (const char *env = std::getenv("NPCG_LINE_CLUSTER")) C = (std::atoi(env) == 2 && L.warps % 2 == 0) ? 2 : 1;
-    const int WL = L.warps / C;
+    if (L.warps > kLineMaxWarps) C = (L.warps <= 2 * kLineMaxWarpsCluster && 2 * B <= sms) ? 2 : 4;
+    if (const char *env = std::getenv("NPCG_LINE_CLUSTER")) {
+        const int c = std::atoi(env);
+        if ((c == 1 || c == 2 || c == 4) && fits(c)) C = c;
+    }
+    if (!fits(C)) C = fits(4) ? 4 : 0;
+    if (!C) return 0;
+    const int WL = (L.warps + C - 1) / C;
     if (const char *env = std::getenv("NPCG_LINE_CFG")) {
         const int c = std::atoi(env), G = c / 16, NS = c % 16;
         if (G >= 1 && G <= 4 && NS == line_stages(G) && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
@@ -440,7 +460,8 @@ int line_config_for(const LineDir &L, bool upper, int B) {
 template <bool UPPER, bool PCG, bool SB, int G, int C>
 static cudaError_t launch_line_t(const LineArgs &a, cudaStream_t s) {
     auto kern = trsv_line_kernel<UPPER, PCG, SB, G, C>;
-    const size_t smem = line_smem(a.warps / C, a.ring, G, a.stages, UPPER, PCG);
+    const int WL = (a.warps + C - 1) / C;
+    const size_t smem = line_smem(WL, a.ring, G, a.stages, UPPER, PCG);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -450,7 +471,7 @@ static cudaError_t launch_line_t(const LineArgs &a, cudaStream_t s) {
     note_launch();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.B * C);
-    cfg.blockDim = dim3(32 * (a.warps / C));
+    cfg.blockDim = dim3(32 * WL);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -475,9 +496,16 @@ static cudaError_t launch_line_gc(const LineArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s) {
-    if (a.group < 1 || a.group > 4 || a.stages != line_stages(a.group) || a.warps < 1 || a.warps > kLineMaxWarps || a.warps % a.cluster) return cudaErrorInvalidValue;
+    if (a.group < 1 || a.group > 4 || a.stages != line_stages(a.group) || a.warps < 1 ||
+        (a.cluster != 1 && a.cluster != 2 && a.cluster != 4) ||
+        (a.warps + a.cluster - 1) / a.cluster > line_cta_warps(a.cluster))
+        return cudaErrorInvalidValue;
     const int key = a.cluster * 16 + a.group;
     switch (key) {
+        case 64 + 1: return launch_line_gc<1, 4>(a, s);
+        case 64 + 2: return launch_line_gc<2, 4>(a, s);
+        case 64 + 3: return launch_line_gc<3, 4>(a, s);
+        case 64 + 4: return launch_line_gc<4, 4>(a, s);
         case 16 + 1: return launch_line_gc<1, 1>(a, s);
         case 16 + 2: return launch_line_gc<2, 1>(a, s);
         case 16 + 3: return launch_line_gc<3, 1>(a, s);

@@ -155,6 +155,8 @@ def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True, profile
         return X, reps
     torch = _torch()
     n = A.n
+    if fac is not None and fac[5] not in (1, batch):
+        raise DimensionMismatchError("batched factor does not match the batch")
     cuts = [batch * i // k for i in range(k + 1)]
     caller = torch.cuda.current_stream()
     streams = _side_streams(k)
@@ -241,6 +243,7 @@ def _pcg_device_one(A, Bm, fac, opts, batch, values=None, with_history=True, pro
     o.absolute = int(opts.absolute)
     o.check_every = 0
     o.profile = int(profile)
+    o.history = int(with_history)
     kms = np.zeros(_native.PROF_SLOTS, dtype=np.float64)
     kn = np.zeros(_native.PROF_SLOTS, dtype=np.int64)
     x0 = None if opts.x0 is None else to_device(opts.x0).view(n, 1).expand(n, B).contiguous()
@@ -251,16 +254,14 @@ def _pcg_device_one(A, Bm, fac, opts, batch, values=None, with_history=True, pro
     sec_to = np.zeros((B, T), dtype=np.float64)
     final = np.zeros(B, dtype=np.float64)
     bd = np.zeros(B, dtype=np.int64)
-    cap = max_iter + 1 if with_history else 0
-    hist = np.zeros((B, cap), dtype=np.float64) if with_history else None
     rep = _native.SolveReportC()
     rep.status = status.ctypes.data
     rep.iterations = iters.ctypes.data
     rep.iterations_to = it_to.ctypes.data
     rep.seconds_to = sec_to.ctypes.data
     rep.final_relative_residual = final.ctypes.data
-    rep.history = hist.ctypes.data if with_history else None
-    rep.history_cap = cap
+    rep.history = None  # fetched below, sized by the iterations actually run
+    rep.history_cap = 0
     rep.breakdown_iteration = bd.ctypes.data
     rep.kernel_ms = kms.ctypes.data
     rep.kernel_launches = kn.ctypes.data
@@ -268,6 +269,10 @@ def _pcg_device_one(A, Bm, fac, opts, batch, values=None, with_history=True, pro
         solver, _native.ptr(vals), vb, _native.ptr(S), int(sb), _native.ptr(D), int(db),
         _native.ptr(Bm), _native.ptr(X), _native.ptr(x0), ctypes.byref(o), ctypes.byref(rep),
         _native.stream_handle()))
+    if with_history:
+        cap = int(iters.max()) + 1 if B else 1
+        hist = np.zeros((B, cap), dtype=np.float64)
+        _native.check(lib.npcg_solver_history(solver, hist.ctypes.data, cap, cap, _native.stream_handle()))
     prof = dict(passes=int(rep.passes), iterations=iters.copy(),
                 kernel_ms={k: float(kms[i]) for i, k in enumerate(_native.PROF_NAMES)},
                 kernel_launches={k: int(kn[i]) for i, k in enumerate(_native.PROF_NAMES)})
@@ -279,7 +284,7 @@ def _pcg_device_one(A, Bm, fac, opts, batch, values=None, with_history=True, pro
             if it_to[b, i] >= 0:
                 itd[t] = int(it_to[b, i])
                 sd[t] = float(sec_to[b, i])
-        h = hist[b, : min(k + 1, cap)].tolist() if with_history else []
+        h = hist[b, : k + 1].tolist() if with_history else []
         reports.append(SolveReport(opts.thresholds, itd, sd, float(final[b]),
                                    bool(status[b] == _native.STATUS_CONVERGED), h, k, int(status[b])))
     return X, reports, prof

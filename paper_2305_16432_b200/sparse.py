@@ -227,8 +227,9 @@ class SparseMatrixCsr:
         return np.count_nonzero(self.row_indices() == self.col_idx) == self.n
 
     def is_symmetric(self):
-        """Exact (bitwise) value symmetry, checked on the device (once: the
-        values are immutable, like the device copy they are checked on)."""
+        """Exact value symmetry (sparse.py:137-147, np.array_equal semantics),
+        checked on the device (once: the values are immutable, like the
+        device copy they are checked on)."""
         if self._sym is None:
             pat = self.device_pattern()
             ok = (ctypes.c_int32 * 1)()

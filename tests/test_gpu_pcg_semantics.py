@@ -300,3 +300,34 @@ def test_deterministic_bitwise(gpu):
     x2, r2 = pcg.pcg_solve(A, b, P2)
     np.testing.assert_array_equal(x1, x2)
     assert r1.history == r2.history
+
+
+@pytest.mark.parametrize("k", [12, 40])
+def test_non_finite_runs_to_max_iter(gpu, k):
+    """SURVEY Appendix A.3 (pcg.py:136-140): an overflowing factor makes
+    p'Ap inf / NaN; `pAp <= 0.0` is then False, so no BreakdownError -- the
+    NaN propagates, the loop runs to max_iter and converged is False, with a
+    NaN final residual. Checked against the oracle (the reference's own
+    semantics); k = 40 takes the line-wavefront path, k = 12 the level path
+    or the line path depending on the pattern."""
+    from paper_2305_16432_b200 import inputs
+    prob = inputs.heat_2d(k=k, cfg=13)
+    A, b = prob.A, prob.rhs[:, 0]
+    low = A.strict_lower()
+    vals = np.where(np.arange(low.nnz) % 2 == 0, 1e300, -1e300)
+    P = gnn.assemble_preconditioner(vals, A)
+    oF = port.Factor(A.n, port.Csr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    with np.errstate(all="ignore"):
+        ox, orep = port.pcg_solve(port.Csr(A.n, A.row_ptr, A.col_idx, A.values), b, oF,
+                                  thresholds=(1e-8,), max_iter=25)
+    x, rep = pcg.pcg_solve(A, b, P, pcg.SolveOptions(thresholds=(1e-8,), max_iter=25))
+    assert orep.breakdown is None and not orep.converged and orep.iterations == 25
+    assert not rep.converged and rep.iterations == 25
+    assert rep.status == orep_status_maxiter()
+    assert np.isnan(rep.final_relative_residual) == np.isnan(orep.final_relative_residual)
+    assert len(rep.history) == 26
+
+
+def orep_status_maxiter():
+    from paper_2305_16432_b200 import _native
+    return _native.STATUS_MAXITER
