@@ -128,28 +128,26 @@ class ClockSampler:
 
 
 def roofline(A, nnz_lower, prof, iters, peak_gbs, step_ms=None):
-    """Achieved algorithmic GB/s of the dominant kernel (the triangular
-    solves, trsv_kernel) and of a whole PCG iteration.
+    """Achieved algorithmic GB/s of the dominant kernel (ldlt_line_kernel:
+    forward solve, y / D and backward solve in one launch) and of a whole PCG
+    iteration.
 
     Per launch, fp64 values / int32 indices, compulsory traffic only:
-      trsv fwd: 12*nnz(L) + 4(n+1) + per active column 32 n
-                (read r, Ap; write r_{k+1}, y; the y /= diag pass is timed
-                with it and adds 8 n (diag) + 16 n per column)
-      trsv bwd: 12*nnz(L) + 4(n+1) + per active column 24 n
-                (read y/diag, r; write z)
+      factor of both directions 2 (12 nnz(L) + 4(n+1)) + D and 1/D 16 n
+      + per solving column 56 n (forward: read r, Ap, write r_{k+1}, y;
+        backward: read y, r, write z).
     Whole iteration: M + B V with
       M = 12 nnz(A) + 4(n+1) + 2 (12 nnz(L) + 4(n+1)) + 8 n,  V = 104 n.
     """
     n, nnz = A.n, A.nnz
     ML = 12 * nnz_lower + 4 * (n + 1)
     col_iters = int(np.sum(iters))
-    nfwd = prof["kernel_launches"]["trsv_fwd"]
-    nbwd = prof["kernel_launches"]["trsv_bwd"]
+    nl = prof["kernel_launches"]["trsv_fwd"] + prof["kernel_launches"]["trsv_bwd"]
     ncol = len(iters)
-    fwd_bytes = nfwd * (ML + 8 * n) + col_iters * 48 * n + ncol * 32 * n  # + the initial z = P^-1 r solves
-    bwd_bytes = nbwd * ML + (col_iters + ncol) * 24 * n
+    solves = col_iters + ncol  # every iteration plus the initial z = P^-1 r
+    trsv_bytes = nl * (2 * ML + 16 * n) + solves * 56 * n
     t_trsv = (prof["kernel_ms"]["trsv_fwd"] + prof["kernel_ms"]["trsv_bwd"]) * 1e-3
-    achieved = (fwd_bytes + bwd_bytes) / t_trsv / 1e9
+    achieved = trsv_bytes / t_trsv / 1e9
     M = 12 * nnz + 4 * (n + 1) + 2 * ML + 8 * n
     iter_bytes = int(np.max(iters)) * M + col_iters * 104 * n
     # the batch runs as concurrent sub-batches (pcg.SPLIT_STREAMS): summed
@@ -158,12 +156,12 @@ def roofline(A, nnz_lower, prof, iters, peak_gbs, step_ms=None):
     t_iter = step_ms * 1e-3 if step_ms else t_loop
     iter_gbs = iter_bytes / t_iter / 1e9
     return {
-        "kernel": "trsv_line_kernel (forward + backward triangular solves; forward includes diag_scale_kernel)",
+        "kernel": "ldlt_line_kernel (forward solve + y/D + backward solve, one launch per pass)",
         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
         "frac": round(achieved / peak_gbs, 4), "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
         "traffic": ncu_traffic(),
-        "launch_ms": round(t_trsv * 1e3 / max(nfwd + nbwd, 1), 4),
-        "bytes_per_launch": int((fwd_bytes + bwd_bytes) / max(nfwd + nbwd, 1)),
+        "launch_ms": round(t_trsv * 1e3 / max(nl, 1), 4),
+        "bytes_per_launch": int(trsv_bytes / max(nl, 1)),
         "pcg_iteration": {"achieved": round(iter_gbs, 1), "frac_of_measured": round(iter_gbs / peak_gbs, 4),
                           "frac_of_8TBs": round(iter_gbs / 8000.0, 4), "bytes": int(iter_bytes),
                           "time_ms": round(t_iter * 1e3, 3),

@@ -62,6 +62,8 @@ class SolveOpts(ctypes.Structure):
 
 
 PROF_SLOTS = 8
+# line path: "trsv_fwd" is the one-launch P^{-1} (ldlt_line_kernel) and "spmv_apdot" carries the
+# p / x updates; the level path launches all five classes
 PROF_NAMES = ("spmv_apdot", "trsv_fwd", "spmv_drift", "trsv_bwd", "pupd", "other")
 
 

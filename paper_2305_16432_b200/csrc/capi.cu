@@ -131,7 +131,7 @@ struct npcg_solver {
     double *S_fwd = nullptr, *S_bwd = nullptr;  // factor entries in schedule order
     size_t S_cap = 0;
     LineSched *ls = nullptr;  // line-wavefront schedule (owned by the pattern) or null
-    int line_K = 0, line_Kb = 0;  // launch shapes (line_config_for) of the forward / backward line kernels
+    int line_K = 0;  // launch shape (line_config_for) of the line P^{-1} kernel
     // line mode: every loop vector is in line order ([b][nslot]): P, XL (x), BL (b)
     // too; A as ELL by slot
     double *XL = nullptr, *BL = nullptr;
@@ -139,9 +139,10 @@ struct npcg_solver {
     int *ecol = nullptr, *eperm = nullptr;  // [ell_width][nslot]: column slot / natural CSR position (-1: none)
     double *evals = nullptr;                // packed A values ([b][ell_width][nslot] or [ell_width][nslot])
     size_t evals_cap = 0, partial_cap = 0;
-    double *Dl = nullptr;  // diag in line order ([b][nslot] or [nslot])
+    double *Dl = nullptr, *rDl = nullptr;  // diag in line order ([b][nslot] or [nslot]) and 1 / diag
     size_t Dl_cap = 0;
     int *xpend = nullptr;
+    int *ppar = nullptr, *xpar = nullptr;  // line path: current p / x buffer per system
     double *ones = nullptr;   // identity preconditioner: D = 1 (per solver: no shared state between threads)
     long long *kmax = nullptr;  // largest k of the batch at the last poll
     struct Poll {
@@ -154,7 +155,7 @@ struct npcg_solver {
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
                         alpha, beta, rel, final_rel, history, active_count, drift_count, ctl, partial,
-                        S_fwd, S_bwd, xpend, Dl, XL, BL, ecol, eperm, evals, ones, kmax};
+                        S_fwd, S_bwd, xpend, Dl, rDl, XL, BL, ecol, eperm, evals, ones, kmax, ppar, xpar};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_poll) cudaFreeHost(h_poll);
@@ -286,7 +287,7 @@ int npcg_pattern_line_info(const npcg_pattern *pc, int32_t *lines, int32_t *warp
     if (lines) *lines = ls ? ls->lines : 0;
     if (warps) *warps = ls ? ls->fwd.warps : 0;
     if (steps) *steps = ls ? ls->steps : 0;
-    if (cluster) *cluster = ls ? line_config_for(ls->fwd, false, std::max(batch, 1)) / 256 : 0;
+    if (cluster) *cluster = ls ? line_config_for(*ls, std::max(batch, 1)) / 256 : 0;
     return NPCG_OK;
 }
 
@@ -389,11 +390,10 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     std::string err;
     if (int rc = plan_solve(s->F, B, s->plan, err)) return fail(rc, err);
     if (LineSched *ls = s->F->line_schedule()) {
-        const int kf = line_config_for(ls->fwd, false, B), kb = line_config_for(ls->bwd, true, B);
-        if (kf > 0 && kb > 0) {
+        const int k = line_config_for(*ls, B);
+        if (k > 0) {
             s->ls = ls;
-            s->line_K = kf;
-            s->line_Kb = kb;
+            s->line_K = k;
         }
     }
     if (s->ls) {  // A as ELL by slot (the line-order loop); rows wider than 16 keep the level path
@@ -406,14 +406,15 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     const size_t nB = (size_t)A->n * B;
     const size_t vB = s->ls ? (size_t)s->ls->nslot * B : nB;  // line-order vectors
     NPCG_CUDA(dalloc(&s->R, vB));
-    NPCG_CUDA(dalloc(&s->P, vB));
+    NPCG_CUDA(dalloc(&s->P, s->ls ? 2 * vB : vB));  // line path: two p buffers
     NPCG_CUDA(dalloc(&s->Z, vB));
     NPCG_CUDA(dalloc(&s->AP, vB));
     NPCG_CUDA(dalloc(&s->Y, vB));
     if (s->ls) {  // padding slots stay zero; A as ELL by slot for the SpMV
-        NPCG_CUDA(dalloc(&s->XL, vB));
+        NPCG_CUDA(dalloc(&s->XL, 2 * vB));  // two x buffers
         NPCG_CUDA(dalloc(&s->BL, vB));
-        for (double *v : {s->R, s->Z, s->AP, s->Y, s->P, s->XL, s->BL}) NPCG_CUDA(cudaMemset(v, 0, vB * 8));
+        for (double *v : {s->R, s->Z, s->AP, s->Y, s->BL}) NPCG_CUDA(cudaMemset(v, 0, vB * 8));
+        for (double *v : {s->P, s->XL}) NPCG_CUDA(cudaMemset(v, 0, 2 * vB * 8));
         const LineSched &ls = *s->ls;
         const int E = s->ell_width;
         std::vector<int> ecol((size_t)E * ls.nslot, -1), eperm((size_t)E * ls.nslot, -1);
@@ -432,6 +433,10 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     }
     NPCG_CUDA(dalloc(&s->status, B));
     NPCG_CUDA(dalloc(&s->xpend, B));
+    NPCG_CUDA(dalloc(&s->ppar, B));
+    NPCG_CUDA(dalloc(&s->xpar, B));
+    NPCG_CUDA(cudaMemset(s->ppar, 0, B * 4));
+    NPCG_CUDA(cudaMemset(s->xpar, 0, B * 4));
     NPCG_CUDA(dalloc(&s->phase, B));
     NPCG_CUDA(dalloc(&s->pflag, B));
     NPCG_CUDA(dalloc(&s->k, B));
@@ -481,6 +486,8 @@ static SolveState make_state(npcg_solver *s, const npcg_solve_opts *o) {
     SolveState st{};
     st.status = s->status;
     st.xpend = s->xpend;
+    st.ppar = s->ls ? s->ppar : nullptr;
+    st.xpar = s->ls ? s->xpar : nullptr;
     st.phase = s->phase;
     st.pflag = s->pflag;
     st.k = s->k;
@@ -531,12 +538,15 @@ static int stage_factor(npcg_solver *s, const double *S, int sb, const double *D
         const size_t dneed = (size_t)s->ls->nslot * (db ? s->B : 1);
         if (dneed > s->Dl_cap) {
             if (s->Dl) cudaFree(s->Dl);
-            s->Dl = nullptr;
+            if (s->rDl) cudaFree(s->rDl);
+            s->Dl = s->rDl = nullptr;
             s->Dl_cap = 0;
             NPCG_CUDA(dalloc(&s->Dl, dneed));
+            NPCG_CUDA(dalloc(&s->rDl, dneed));
             s->Dl_cap = dneed;
         }
         NPCG_CUDA(launch_to_line(s->ls->nslot, db ? s->B : 1, s->ls->rowof, D, db, 1.0, s->Dl, st));
+        NPCG_CUDA(launch_reciprocal((long long)dneed, s->Dl, s->rDl, st));
     } else {
         launch_factor_pack(s->plan.set->fwd, s->B, s->plan.G, sb, S, s->S_fwd, st);
         launch_factor_pack(s->plan.set->bwd, s->B, s->plan.G, sb, S, s->S_bwd, st);
@@ -545,53 +555,10 @@ static int stage_factor(npcg_solver *s, const double *S, int sb, const double *D
     return NPCG_OK;
 }
 
-// One direction of P^{-1}: the line-wavefront kernel when the pattern
-// qualifies, else the chunked level kernel. Vectors are RHS-minor (i*B + b).
-struct Tri {
-    bool line = false;
+// P^{-1} on the level path: one direction of the chunked level kernel.
+// Vectors are RHS-minor (i*B + b).
+static TrsvArgs level_args(npcg_solver *s, bool upper, int mode, int sb, const double *D, int db) {
     TrsvArgs v;
-    LineArgs l;
-    void io(double *in, double *out, double *R, const double *AP, const SolveState &st) {
-        v.in = l.in = in;
-        v.out = l.out = out;
-        v.R = l.R = R;
-        v.AP = l.AP = AP;
-        v.st = l.st = st;
-    }
-    cudaError_t launch(cudaStream_t s) const {
-        if (!line) return launch_trsv(v, s);
-        cudaError_t e = launch_trsv_line(l, s);
-        if (e == cudaSuccess && !l.upper) e = launch_diag_scale(l.nslot, l.B, l.D, l.d_batched, l.out, s);
-        return e;
-    }
-};
-
-static Tri tri_args(npcg_solver *s, bool upper, int mode, int sb, const double *D, int db) {
-    Tri t;
-    t.line = s->ls != nullptr;
-    if (t.line) {
-        LineArgs &l = t.l;
-        const LineDir &dir = upper ? s->ls->bwd : s->ls->fwd;
-        const int cfg = upper ? s->line_Kb : s->line_K;
-        l.B = s->B;
-        l.cluster = cfg / 256;
-        l.group = cfg / 16 % 16;
-        l.stages = cfg % 16;
-        l.upper = upper;
-        l.mode = mode;
-        l.nslot = s->ls->nslot;
-        l.warps = dir.warps;
-        l.ring = dir.ring;
-        l.meta = dir.meta;
-        l.fac_slots = dir.fac_slots;
-        l.S = upper ? s->S_bwd : s->S_fwd;
-        l.s_batched = sb;
-        l.D = s->Dl;  // staged by stage_factor
-        l.d_batched = db;
-        l.drift_count = s->drift_count;
-        return t;
-    }
-    TrsvArgs &v = t.v;
     const Pattern *F = s->F;
     v.n = (int)F->n;
     v.B = s->B;
@@ -608,7 +575,33 @@ static Tri tri_args(npcg_solver *s, bool upper, int mode, int sb, const double *
     v.ctl = s->ctl;
     v.partial = s->partial;
     v.drift_count = s->drift_count;
-    return t;
+    return v;
+}
+
+// P^{-1} on the line path: forward solve, y / D and backward solve in one
+// launch (ldlt_line_kernel); every vector in line order ([b][nslot]).
+static LineArgs line_args(npcg_solver *s, int mode, int sb, int db) {
+    LineArgs l;
+    const int cfg = s->line_K;
+    l.B = s->B;
+    l.cluster = cfg / 256;
+    l.group = cfg / 16 % 16;
+    l.stages = cfg % 16;
+    l.mode = mode;
+    l.nslot = s->ls->nslot;
+    l.warps = s->ls->fwd.warps;
+    l.ring = std::max(s->ls->fwd.ring, s->ls->bwd.ring);
+    l.meta_f = s->ls->fwd.meta;
+    l.meta_b = s->ls->bwd.meta;
+    l.fac_slots = s->ls->fwd.fac_slots;
+    l.S_f = s->S_fwd;
+    l.S_b = s->S_bwd;
+    l.s_batched = sb;
+    l.D = s->Dl;  // staged by stage_factor
+    l.rD = s->rDl;
+    l.d_batched = db;
+    l.drift_count = s->drift_count;
+    return l;
 }
 
 int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int sb, const double *D, int db,
@@ -632,24 +625,25 @@ int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int s
     npcg_solver *s = slot.get();
     cudaStream_t st = (cudaStream_t)stream;
     if (int rc = stage_factor(s, S, sb, D, db, st)) return rc;
-    if (s->ls) {  // through line order: r -> R, Y, Z -> z
+    if (s->ls) {  // through line order: r -> R, (Y), Z -> z
         const LineSched &ls = *s->ls;
         NPCG_CUDA(launch_to_line(ls.nslot, B, ls.rowof, r, 1, 0.0, s->R, st));
-        Tri f = tri_args(s, false, TRSV_PLAIN, sb, D, db);
-        f.io(s->R, s->Y, nullptr, nullptr, SolveState{});
-        NPCG_CUDA(f.launch(st));
-        Tri b = tri_args(s, true, TRSV_PLAIN, sb, D, db);
-        b.io(s->Y, s->Z, nullptr, nullptr, SolveState{});
-        NPCG_CUDA(b.launch(st));
+        LineArgs l = line_args(s, TRSV_PLAIN, sb, db);
+        l.in = s->R;
+        l.Y = s->Y;
+        l.out = s->Z;
+        NPCG_CUDA(launch_ldlt_line(l, st));
         NPCG_CUDA(launch_from_line(ls.nslot, B, ls.rowof, s->Z, z, st));
     } else {
         launch_fill_sentinel((long long)F->n * B, z, st);  // level kernel polls z
-        Tri f = tri_args(s, false, TRSV_PLAIN, sb, D, db);
-        f.io(const_cast<double *>(r), s->Y, nullptr, nullptr, SolveState{});  // r is only read
-        NPCG_CUDA(f.launch(st));
-        Tri b = tri_args(s, true, TRSV_PLAIN, sb, D, db);
-        b.io(s->Y, z, nullptr, nullptr, SolveState{});
-        NPCG_CUDA(b.launch(st));
+        TrsvArgs f = level_args(s, false, TRSV_PLAIN, sb, D, db);
+        f.in = const_cast<double *>(r);  // r is only read
+        f.out = s->Y;
+        NPCG_CUDA(launch_trsv(f, st));
+        TrsvArgs b = level_args(s, true, TRSV_PLAIN, sb, D, db);
+        b.in = s->Y;
+        b.out = z;
+        NPCG_CUDA(launch_trsv(b, st));
     }
     NPCG_CUDA(cudaStreamSynchronize(st));
     return NPCG_OK;
@@ -764,11 +758,18 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     apdot.op = SPMV_APDOT;
     apdot.X = s->P;
     apdot.Y = s->AP;
-    if (s->ls) {  // the drift check rides on the next APDOT launch (no separate drift SpMV)
+    if (s->ls) {
+        // the drift check rides on the next APDOT launch (no separate drift
+        // SpMV), and so do the p / x updates of the previous pass (no pupd):
+        // p and x are double-buffered, ppar / xpar pick the current buffers
         apdot.merge_drift = 1;
-        apdot.X2 = xv;
         apdot.Bv = bv;
         apdot.R = s->R;
+        apdot.fused_pupd = 1;
+        apdot.vstride = (long long)s->ls->nslot * B;
+        apdot.Pbuf = s->P;
+        apdot.Xbuf = s->XL;
+        apdot.Z = s->Z;
     }
     SpmvArgs drift = spl;
     drift.op = SPMV_RESID_DRIFT;
@@ -782,10 +783,30 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         launch_fill_sentinel(nB, s->Y, st);
         launch_fill_sentinel(nB, s->Z, st);
     }
-    Tri fw = tri_args(s, false, TRSV_PCG, sb, D, db);
-    fw.io(s->R, s->Y, s->R, s->AP, sst);
-    Tri bw = tri_args(s, true, TRSV_PCG, sb, D, db);
-    bw.io(s->Y, s->Z, s->R, nullptr, sst);
+    // P^{-1}: line path (one launch) or level path (forward, drift, backward)
+    LineArgs ll{};
+    TrsvArgs fw{}, bw{};
+    if (s->ls) {
+        ll = line_args(s, TRSV_PCG, sb, db);
+        ll.in = s->R;
+        ll.R = s->R;
+        ll.AP = s->AP;
+        ll.Y = s->Y;
+        ll.out = s->Z;
+        ll.st = sst;
+    } else {
+        fw = level_args(s, false, TRSV_PCG, sb, D, db);
+        fw.in = s->R;
+        fw.out = s->Y;
+        fw.R = s->R;
+        fw.AP = s->AP;
+        fw.st = sst;
+        bw = level_args(s, true, TRSV_PCG, sb, D, db);
+        bw.in = s->Y;
+        bw.out = s->Z;
+        bw.R = s->R;
+        bw.st = sst;
+    }
 
     // Optional per-launch timing (npcg_solve_opts.profile): a start/stop
     // event pair around every launch of the loop, summed per kernel class.
@@ -830,7 +851,6 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         used.clear();
     };
     auto pupd = [&]() {
-        if (s->ls) return launch_pupd_ell(s->ls->nslot, B, s->Z, s->P, s->XL, sst, st);
         note_launch();
         pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, x, sst, 1);
         return cudaGetLastError();
@@ -840,8 +860,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     // history buffer moved
     auto set_state = [&]() {
         apdot.st = drift.st = sst;
-        fw.v.st = fw.l.st = sst;
-        bw.v.st = bw.l.st = sst;
+        fw.st = bw.st = ll.st = sst;
     };
     int check = o->check_every > 0 ? o->check_every : 8;
     // a pass advances k by at most one; an iteration whose drift check
@@ -851,9 +870,13 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     for (;;) {
         for (int q = 0; q < check; ++q) {
             NPCG_CUDA(timed(NPCG_PROF_SPMV_APDOT, [&] { return launch_spmv(apdot, st); }));
-            NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return fw.launch(st); }));
-            if (!s->ls) NPCG_CUDA(timed(NPCG_PROF_SPMV_DRIFT, [&] { return launch_spmv(drift, st); }));
-            NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return bw.launch(st); }));
+            if (s->ls) {  // x / p updates ride on the next APDOT
+                NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return launch_ldlt_line(ll, st); }));
+                continue;
+            }
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return launch_trsv(fw, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_SPMV_DRIFT, [&] { return launch_spmv(drift, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return launch_trsv(bw, st); }));
             NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
         }
         passes += check;
@@ -896,6 +919,8 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     std::vector<int> status(B);
     NPCG_CUDA(cudaMemcpyAsync(status.data(), s->status, B * 4, cudaMemcpyDeviceToHost, st));
     NPCG_CUDA(cudaStreamSynchronize(st));
+    // line path: x into buffer 0, with an update a budget-stopped pass left pending
+    if (s->ls) NPCG_CUDA(launch_flush_ell(s->ls->nslot, B, s->XL, s->P, (long long)s->ls->nslot * B, sst, st));
     bool any_max = false;
     for (int b = 0; b < B; ++b) any_max |= status[b] == ST_MAXITER || status[b] == ST_ACTIVE;
     if (any_max) {

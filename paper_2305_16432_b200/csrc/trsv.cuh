@@ -41,32 +41,38 @@ struct TrsvSmem {
 
 TrsvSmem trsv_smem_plan(const Schedule &S, int G, int s_batched);
 
-// Line-wavefront solve (trsv_line.cu): one CTA per system, one lane per
-// line. Every vector is in line order, system-major: element (slot q,
-// system b) at b * nslot + q.
+// Line-wavefront P^{-1} (trsv_line.cu): one cluster of 1, 2 or 4 CTAs per
+// system, one lane per grid line; ONE launch runs the forward solve, the
+// diagonal scaling and the backward solve (ldlt_line_kernel). Every vector
+// is in line order, system-major: element (slot q, system b) at b*nslot + q.
 struct LineArgs {
-    int B = 1, upper = 0, mode = TRSV_PLAIN;
+    int B = 1, mode = TRSV_PLAIN;
     int cluster = 1, group = 2, stages = 2;  // CTAs per system, tiles per pipeline stage, stages per warp
-    int nslot = 0, warps = 0, ring = 64;  // ring: steps per warp's outgoing ring (LineDir::ring)
-    const int *meta = nullptr;  // LineDir::meta of this direction
+    int nslot = 0, warps = 0, ring = 64;     // ring: steps per warp's incoming value ring (LineDir::ring)
+    const int *meta_f = nullptr, *meta_b = nullptr;  // LineDir::meta of the two directions
     long long fac_slots = 0;
-    const double *S = nullptr;  // packed factor values ([b][fac_slots] when s_batched)
+    const double *S_f = nullptr, *S_b = nullptr;  // packed factor values ([b][fac_slots] when s_batched)
     int s_batched = 0;
-    const double *D = nullptr;  // diag(A) in line order: [nslot] or [b][nslot] (padding 1.0)
+    // diag(A) and its correctly rounded reciprocal in line order ([nslot] or
+    // [b][nslot], padding 1.0): y / D is formed exactly from them
+    const double *D = nullptr, *rD = nullptr;
     int d_batched = 0;
-    double *in = nullptr, *out = nullptr, *R = nullptr;
-    const double *AP = nullptr;
+    const double *in = nullptr;   // forward right-hand side (PCG: r_k)
+    double *Y = nullptr;          // forward result y (scratch between the phases)
+    double *out = nullptr;        // z
+    double *R = nullptr;          // PCG: r_{k+1} = r_k - alpha Ap, written by the forward phase
+    const double *AP = nullptr;   // PCG: A p
     SolveState st{};
     int *drift_count = nullptr;
 };
 // Launch shape (cluster * 256 + group * 16 + stages) for B systems that fits
-// shared memory for this direction, 0 when none does. NPCG_LINE_CFG
-// (group * 16 + stages) and NPCG_LINE_CLUSTER override.
-int line_config_for(const LineDir &L, bool upper, int B);
+// shared memory, 0 when none does. NPCG_LINE_CFG (group * 16 + stages) and
+// NPCG_LINE_CLUSTER override.
+int line_config_for(const LineSched &L, int B);
 int line_trace_copy(long long *out, int n);  // debug timeline (NPCG_LINE_TRACE builds)
-cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s);
-// y[b][slot] /= D[(b)][slot] (the diagonal scaling between the line solves)
-cudaError_t launch_diag_scale(int nslot, int B, const double *D, int d_batched, double *y, cudaStream_t s);
+cudaError_t launch_ldlt_line(const LineArgs &a, cudaStream_t s);
+// rD[q] = 1 / D[q] (correctly rounded), count entries
+cudaError_t launch_reciprocal(long long count, const double *D, double *rD, cudaStream_t s);
 // factor values S[p * ps + b * bs] -> line order of `L` (per system when batched)
 void launch_line_factor_pack(const LineDir &L, int B, int sb, long long ps, long long bs, const double *S,
                              double *packed, cudaStream_t s);

@@ -1,7 +1,9 @@
 // trsv_line.cu -- line-wavefront triangular solves (pattern.h, LineSched).
 //
-// One system per cluster of C CTAs (C = 1 or 2, each on its own SM), one
-// lane per grid line, no block-wide synchronisation inside the solve:
+// One system per cluster of C CTAs (C = 1, 2 or 4, each on its own SM), one
+// lane per grid line, no block-wide synchronisation inside the solve; the
+// forward solve, the diagonal scaling and the backward solve run in ONE
+// launch (ldlt_line_kernel):
 //
 //   * at every step a lane solves the next row of its line. Its operands are
 //     its own previous value (register), and its left neighbour's values one
@@ -20,9 +22,9 @@
 //     one mbarrier per stage) of the factor values and vector slices into the
 //     warp's private stage ring. Results go from registers to global memory
 //     in coalesced 256-byte warp stores.
-//   * the diagonal scaling y /= diag (sparse.py:273) is applied by the
-//     forward solve as it stores y (off the dependency chain), so the
-//     backward solve reads y / diag directly. PCG mode also fuses the
+//   * the diagonal scaling y /= diag (sparse.py:273) is formed by the
+//     backward phase as it reads its operands (off the dependency chain),
+//     exactly, from staged D and 1/D (div_by_diag). PCG mode also fuses the
 //     forward r -= alpha Ap (pcg.py:142) with |r|^2 (pcg.py:143) and the
 //     backward r.z (pcg.py:167), reduced in a fixed order at the end.
 //   * splitting a system over C SMs divides what every SM's shared-memory /
@@ -48,24 +50,7 @@ namespace {
 // up to 3-tile stages, two for 4-tile stages (shared memory)
 __host__ __device__ constexpr int line_stages(int G) { return G >= 4 ? 2 : 3; }
 
-struct LineSmem {  // byte offsets into dynamic shared memory
-    size_t ring, mbar, stage0, stage_bytes, total;
-};
-
 __host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
-
-// vectors staged per stage: forward r [, Ap] ; backward y/diag [, r]
-__host__ __device__ constexpr int line_vectors(bool upper, bool pcg) { return pcg ? 2 : 1; }
-
-__host__ __device__ inline LineSmem line_layout(int WL, int R, int G, int NS, int nv) {
-    LineSmem m;
-    m.ring = 0;
-    m.mbar = al128((size_t)WL * R * 8);
-    m.stage0 = al128(m.mbar + (size_t)WL * NS * 8);
-    m.stage_bytes = (size_t)G * (kLineKinds + nv) * kTileSlots * 8;
-    m.total = m.stage0 + (size_t)WL * NS * m.stage_bytes;
-    return m;
-}
 
 __device__ __forceinline__ double ld_vol(const double *p) { return *reinterpret_cast<const volatile double *>(p); }
 __device__ __forceinline__ void st_vol(double *p, double v) { *reinterpret_cast<volatile double *>(p) = v; }
@@ -115,77 +100,54 @@ __device__ __forceinline__ double stage_dot(const double (&u)[N], const double (
     return p[0];
 }
 
-__device__ __forceinline__ void line_epilogue(const LineArgs &a, int b, double total) {
-    if (a.upper) bwd_epilogue(a.st, b, total);
-    else fwd_epilogue(a.st, b, total, a.drift_count);
+// exact y / D from D and rD = RN(1 / D): q = RN(y rD) is within an ulp of
+// the quotient, the residual e = y - q D is exact (FMA), and RN(q + e rD)
+// is the correctly rounded quotient (Markstein) -- bitwise __ddiv_rn(y, D),
+// three fp64 operations instead of a division sequence. e == 0 means q is
+// exact (and keeps the sign of a zero y); quotients near the ends of the
+// exponent range, infinities and NaNs take the division.
+__device__ __forceinline__ double div_by_diag(double y, double D, double rD) {
+    const double q = __dmul_rn(y, rD);
+    const double e = __fma_rn(-q, D, y);
+    double r = e == 0.0 ? q : __fma_rn(e, rD, q);
+    const double aq = fabs(q);
+    if (q != 0.0 && !(aq > 0x1p-960 && aq < 0x1p960)) r = __ddiv_rn(y, D);
+    return r;
 }
 
-}  // namespace
+// One direction of the line solve for this warp (see the file comment).
+struct LinePhase {
+    const int4 *meta = nullptr;    // this direction's warp table
+    const double *fac = nullptr;   // packed factor values of this direction (this system)
+    const double *vec[4] = {};     // staged vectors (this system's base)
+    double *out = nullptr;         // results (this system's base)
+    double *rg = nullptr;          // forward PCG update: r_{k+1}
+    double *ring = nullptr;        // this phase's incoming-value rings, [WL][R] in this CTA
+    int w = 0;                     // warp in this direction's order
+    bool rev = false;              // the direction's warp w runs on physical warp W - 1 - w
+    int jbase = 0;                 // stages this warp consumed before (mbarrier parity)
+};
 
-// Debug timeline (build with -DNPCG_LINE_TRACE): per warp of the first
-// cluster (first 16), its first step, then clock64 before / after each
-// stage's mbarrier wait.
-constexpr int kTraceEvents = 16, kTraceBatches = 2048;
-__device__ long long g_line_trace[kTraceEvents][kTraceBatches];
-
-__host__ __device__ constexpr int line_cta_warps(int C) { return C == 1 ? kLineMaxWarps : kLineMaxWarpsCluster; }
-
-template <bool UPPER, bool PCG, bool SB, int G, int C>
-__global__ void __launch_bounds__(32 * line_cta_warps(C), 1) trsv_line_kernel(LineArgs a) {
+// NV staged vectors: forward r [, Ap]; backward y, D, rD [, r] (DIAG: y / D
+// formed from them as the operands are read).
+template <bool UPPER, bool PCG, int G, int C, int NV>
+__device__ __forceinline__ double line_phase(const LinePhase &io, const int W, const int WL, const int R,
+                                             const int wl, const int t, uint64_t *mbar, char *stage,
+                                             const size_t slot_bytes, const bool upd, const double alpha) {
     constexpr int STEPS = kTileSteps * G;
-    static_assert(2 * STEPS <= 32, "a stage pair's ring slots are checked by one warp");
-    constexpr int NV = line_vectors(UPPER, PCG);
-    extern __shared__ __align__(128) char sm[];
-    __shared__ double s_red[kLineMaxWarps];
-    __shared__ double s_cta[4];
     constexpr int NS = line_stages(G);
-    // WL warps per CTA; the last CTA of a cluster may hold idle warps (w >= W)
-    const int W = a.warps, WL = (W + C - 1) / C, R = a.ring;
-    const int wl = threadIdx.x >> 5, t = threadIdx.x & 31;
-    const int rank = C > 1 ? (int)cluster_rank() : 0, b = blockIdx.x / C;
-    const int w = rank * WL + wl;  // warp of the direction's schedule
-    const bool idle = w >= W;
-    // what this system needs from this launch (uniform over the cluster)
-    int op = TOP_SOLVE;
-    if (PCG) {
-        const SolveState &st = a.st;
-        const int ph = st.status[b] == ST_ACTIVE ? st.phase[b] : -1;
-        op = !UPPER ? (ph == PH_ITER ? TOP_UPDATE : (ph == PH_INIT ? TOP_SOLVE : TOP_SKIP))
-                    : ((ph == PH_ITER || ph == PH_INIT) ? TOP_SOLVE : TOP_SKIP);
-        if (op == TOP_SKIP) {
-            // every thread of the cluster has read status / phase before the
-            // epilogue changes them (PH_RESTART -> PH_INIT), else a late
-            // reader would take the solve path and wait on warps that left
-            if (UPPER) {
-                if (C > 1) cluster_sync_all();
-                else __syncthreads();
-                if (rank == 0 && threadIdx.x == 0) line_epilogue(a, b, 0.0);  // pflag / restart bookkeeping
-            }
-            return;
-        }
-    }
-    const bool upd = !UPPER && PCG && op == TOP_UPDATE;
-    const LineSmem m = line_layout(WL, R, G, NS, NV);
-    double *ring = reinterpret_cast<double *>(sm + m.ring);  // [WL][R]: values of the warp left of each warp
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + m.mbar) + wl * NS;
-    char *stage = sm + m.stage0 + (size_t)wl * NS * m.stage_bytes;
-    for (int i = threadIdx.x; i < WL * R; i += blockDim.x) ring[i] = sentinel();
-    const int4 *meta = reinterpret_cast<const int4 *>(a.meta);
-    const int4 me = idle ? make_int4(0, 0, 0, 0) : meta[w];
-    if (t == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], 1);
-        fence_mbar_init();
-    }
-    if (C > 1) cluster_sync_all();  // every ring armed before any remote write
-    else __syncthreads();
-
+    constexpr bool DIAG = UPPER;
+    static_assert(2 * STEPS <= 32, "a stage pair's ring slots are checked by one warp");
+    const int w = io.w;
+    const int4 *meta = io.meta;
+    const int4 me = meta[w];
     const int C0 = me.x, nt = me.y, tile0 = me.z, C1 = C0 + kTileSteps * nt;
     const int nstage = (nt + G - 1) / G;
     // ring protocol: warp w sends its last lane's values of steps
     // [max(C0_right - 2, C0), min(C1_right - 1, C1)) to the right warp; every
     // value is read once and re-armed by its reader
     int P0 = 0, P1 = 0, Q0 = 0, Q1 = 0;
-    if (w > 0 && !idle) {
+    if (w > 0) {
         const int4 pm = meta[w - 1];
         P0 = pm.x;
         P1 = pm.x + kTileSteps * pm.y;
@@ -195,11 +157,12 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) trsv_line_kernel(Li
         Q0 = max(qm.x - 2, C0);
         Q1 = min(qm.x + kTileSteps * qm.y - 1, C1);
     }
-    const bool cons = !idle && w > 0 && t == 0, prod = !idle && w + 1 < W && t == 31;
-    double *rin = ring + wl * R;  // my incoming ring (local)
+    const bool cons = w > 0 && t == 0, prod = w + 1 < W && t == 31;
+    double *rin = io.ring + wl * R;  // my incoming ring (local)
     // my outgoing ring: the right warp's incoming ring, in its CTA
     const int wr = w + 1 < W ? w + 1 : w;
-    const unsigned rout = map_rank(ring + (wr % WL) * R, (unsigned)(wr / WL));
+    const int pr = io.rev ? W - 1 - wr : wr;  // its physical warp
+    const unsigned rout = map_rank(io.ring + (pr % WL) * R, (unsigned)(pr / WL));
     auto ring_read = [&](int x) -> double {  // value of the left line at step x (0 outside its range)
         if (x < P0 || x >= P1) return 0.0;
         double *p = rin + (x & (R - 1));
@@ -211,42 +174,28 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) trsv_line_kernel(Li
         st_vol(p, sentinel());
         return v;
     };
-
-    const long long vb = (long long)b * a.nslot;
-    const double *fac = a.S + (SB ? (size_t)b * a.fac_slots : 0);
-    const double *src[3];
-    if (!UPPER) {
-        src[0] = a.in + vb;
-        src[1] = PCG ? a.AP + vb : nullptr;
-        src[2] = nullptr;
-    } else {
-        src[0] = a.in + vb;
-        src[1] = PCG ? a.R + vb : nullptr;
-        src[2] = nullptr;
-    }
-    double *out = a.out + vb, *rout_g = PCG && !UPPER ? a.R + vb : nullptr;
     // tiles [lo, lo + g) of stage j (ascending in memory; the backward solve walks them downwards)
     auto stage_tiles = [&](int j, int &lo, int &g) {
         g = min(G, nt - j * G);
         lo = UPPER ? tile0 + nt - j * G - g : tile0 + j * G;
     };
+    constexpr size_t kFacBytes = (size_t)G * kLineKinds * kTileSlots * 8, kVecBytes = (size_t)G * kTileSlots * 8;
     auto issue = [&](int j) {  // elected lane: bulk copies of stage j into its ring slot
         int lo, g;
         stage_tiles(j, lo, g);
-        char *sp = stage + (size_t)(j % NS) * m.stage_bytes;
+        const int js = io.jbase + j;
+        char *sp = stage + (size_t)(js % NS) * slot_bytes;
         const unsigned fb = (unsigned)g * kLineKinds * kTileSlots * 8, vbytes = (unsigned)g * kTileSlots * 8;
-        uint64_t *bar = &mbar[j % NS];
+        uint64_t *bar = &mbar[js % NS];
         mbar_expect_tx(bar, fb + NV * vbytes);
-        bulk_g2s(sp, fac + (size_t)lo * kLineKinds * kTileSlots, fb, bar);
+        bulk_g2s(sp, io.fac + (size_t)lo * kLineKinds * kTileSlots, fb, bar);
 #pragma unroll
         for (int v = 0; v < NV; ++v)
-            bulk_g2s(sp + (size_t)G * kLineKinds * kTileSlots * 8 + (size_t)v * G * kTileSlots * 8,
-                     src[v] + (size_t)lo * kTileSlots, vbytes, bar);
+            bulk_g2s(sp + kFacBytes + (size_t)v * kVecBytes, io.vec[v] + (size_t)lo * kTileSlots, vbytes, bar);
     };
     if (t == 0)
         for (int j = 0; j < NS && j < nstage; ++j) issue(j);
 
-    const double alpha = upd ? a.st.alpha[b] : 0.0;
     double h0 = 0.0;  // my value one step back
     double lp = 0.0;  // left neighbour's value two steps back (at the next step)
     double acc2 = 0.0;
@@ -257,31 +206,17 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) trsv_line_kernel(Li
     }
     if (cons) lp = ring_read(C0 - 2);
     for (int j = 0; j < nstage; ++j) {
-        const int s = j % NS, sig = C0 + j * STEPS;  // first step of the stage
-#ifdef NPCG_LINE_TRACE
-        const bool tr = b == 0 && t == 0 && w < kTraceEvents && 10 * j + 11 < kTraceBatches && (NPCG_LINE_TRACE != 2 || !UPPER);
-#define LTR(k)                                                   \
-    do {                                                         \
-        if (tr) g_line_trace[w][10 * j + 1 + (k)] = clock64();   \
-    } while (0)
-        if (tr && j == 0) g_line_trace[w][0] = C0;
-        LTR(0);
-#else
-#define LTR(k) \
-    do {       \
-    } while (0)
-#endif
-        mbar_wait(&mbar[s], (j / NS) & 1);
-        LTR(1);
+        const int js = io.jbase + j;
+        const int s = js % NS, sig = C0 + j * STEPS;  // first step of the stage
+        mbar_wait(&mbar[s], (js / NS) & 1);
         // refill the slot of stage j - 1 (every lane's reads of it ended at its __syncwarp)
         // with stage j - 1 + NS before this stage's operand loads
         if (t == 0 && j >= 1 && j - 1 + NS < nstage) issue(j - 1 + NS);
         int lo, g;
         stage_tiles(j, lo, g);
-        const char *sp = stage + (size_t)s * m.stage_bytes;
+        const char *sp = stage + (size_t)s * slot_bytes;
         const double *f = reinterpret_cast<const double *>(sp);
-        const double *v0 = f + G * kLineKinds * kTileSlots;
-        const double *v1 = v0 + G * kTileSlots;
+        const double *v0 = reinterpret_cast<const double *>(sp + kFacBytes);
         const int live_steps = g * kTileSteps;
         // a step pair's operands (a lane's two steps of a tile half are adjacent, pattern.h:
         // one 16-byte load each), loaded one pair ahead inside the step loop so the shared-
@@ -298,16 +233,23 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) trsv_line_kernel(Li
             f2 = *reinterpret_cast<const double2 *>(ft + 2 * kTileSlots);
             // vectors are in forward tile order: the backward pair is reversed
             const int ve = tpc * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
-            a0 = *reinterpret_cast<const double2 *>(v0 + ve);
-            a1 = NV > 1 ? *reinterpret_cast<const double2 *>(v1 + ve) : make_double2(0.0, 0.0);
+            const double *vv = v0 + ve;
+            if (DIAG) {  // y / D (sparse.py:273), off the dependency chain
+                const double2 y = *reinterpret_cast<const double2 *>(vv);
+                const double2 d = *reinterpret_cast<const double2 *>(vv + G * kTileSlots);
+                const double2 rd = *reinterpret_cast<const double2 *>(vv + 2 * G * kTileSlots);
+                a0 = make_double2(div_by_diag(y.x, d.x, rd.x), div_by_diag(y.y, d.y, rd.y));
+                a1 = NV > 3 ? *reinterpret_cast<const double2 *>(vv + 3 * G * kTileSlots) : make_double2(0.0, 0.0);
+            } else {
+                a0 = *reinterpret_cast<const double2 *>(vv);
+                a1 = NV > 1 ? *reinterpret_cast<const double2 *>(vv + G * kTileSlots) : make_double2(0.0, 0.0);
+            }
         };
         double VIN[STEPS], AUX[STEPS], ACC[STEPS];  // padding steps of a partial stage stay 0
 #pragma unroll
         for (int i = 0; i < STEPS; ++i) VIN[i] = AUX[i] = ACC[i] = 0.0;
         double2 cf0, cf1, cf2, ca0, ca1;
         pair_ops(0, cf0, cf1, cf2, ca0, ca1);
-        LTR(2);
-        LTR(3);
         // left line's values at steps sig-1 .. sig+STEPS-2 (lane i holds step sig-1+i): one
         // batch per stage, each slot re-armed after the read
         double x = 0.0;
@@ -322,7 +264,6 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) trsv_line_kernel(Li
             }
             if (pend) st_vol(px, sentinel());
         }
-        LTR(4);
         // my outgoing slots of this stage pair must have been re-armed by the right warp;
         // checked once per two stages (lane i: step sig + i), loaded two stages ahead (a
         // re-armed slot stays so until I write it)
@@ -338,8 +279,7 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) trsv_line_kernel(Li
             const bool chn = t < 2 * STEPS && yn >= Q0 && yn < Q1 && yn - R >= Q0;
             ychk = chn ? ld_dsm(rout + (unsigned)(yn & (R - 1)) * 8u) : sentinel();
         }
-        LTR(5);
-        double *og = out + (size_t)lo * kTileSlots, *rg = upd ? rout_g + (size_t)lo * kTileSlots : nullptr;
+        double *og = io.out + (size_t)lo * kTileSlots, *rg = upd ? io.rg + (size_t)lo * kTileSlots : nullptr;
 #pragma unroll
         for (int pi = 0; pi < STEPS / 2; ++pi) {
             const int i = 2 * pi;
@@ -377,91 +317,214 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) trsv_line_kernel(Li
                 const int e = tile_elem(i % kTileSteps, t);
                 const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
                 if (!UPPER) {
-                    *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i], ACC[i + 1]);  // y (diag_scale_kernel divides)
+                    *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i], ACC[i + 1]);  // y
                     if (upd) *reinterpret_cast<double2 *>(rg + ve) = make_double2(VIN[i], VIN[i + 1]);  // r_{k+1}
                 } else {
-                    *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i + 1], ACC[i]);
+                    *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i + 1], ACC[i]);  // z
                 }
             }
             if (pi + 1 < STEPS / 2) cf0 = nf0, cf1 = nf1, cf2 = nf2, ca0 = na0, ca1 = na1;
         }
         if (upd) acc2 = __dadd_rn(acc2, stage_dot(VIN, VIN));  // |r_{k+1}|^2 (pcg.py:143)
-        LTR(6);
         if (UPPER && PCG) acc2 = __dadd_rn(acc2, stage_dot(AUX, ACC));  // r.z (pcg.py:167)
-        LTR(7);
         // every lane's reads of this slot are done before the elected lane refills it
         __syncwarp();
-        LTR(8);
-        LTR(9);
     }
-    if (PCG) {  // fixed-order reduction: lanes, warps, then the cluster's CTAs
-        double v = acc2;
+    return acc2;
+}
+
+__host__ __device__ constexpr int line_cta_warps(int C) { return C == 1 ? kLineMaxWarps : kLineMaxWarpsCluster; }
+// staged vectors per direction (see line_phase) and the larger of the two
+__host__ __device__ constexpr int line_nv_f(bool pcg) { return pcg ? 2 : 1; }
+__host__ __device__ constexpr int line_nv_b(bool pcg) { return pcg ? 4 : 3; }
+
+struct LineSmem {  // byte offsets into dynamic shared memory
+    size_t ring_f, ring_b, mbar, stage0, slot_bytes, total;
+};
+
+__host__ __device__ inline LineSmem line_layout(int WL, int R, int G, int NS, bool pcg) {
+    LineSmem m;
+    m.ring_f = 0;
+    m.ring_b = al128((size_t)WL * R * 8);
+    m.mbar = m.ring_b + al128((size_t)WL * R * 8);
+    m.stage0 = al128(m.mbar + (size_t)WL * NS * 8);
+    m.slot_bytes = (size_t)G * (kLineKinds + line_nv_b(pcg)) * kTileSlots * 8;
+    m.total = m.stage0 + (size_t)WL * NS * m.slot_bytes;
+    return m;
+}
+
+}  // namespace
+
+// P^{-1} r for one system per cluster: the forward unit solve (with the PCG
+// residual update fused in front), then y / D and the backward transpose
+// solve -- one launch (sparse.py:222-239, 265-275; pcg.py:142-143, 167).
+//
+// Every physical warp owns the same 32 grid lines in both directions (the
+// backward order walks warp W-1-w, lane 31-t), so the backward operands y and
+// r of a warp's rows are the values the warp itself stored in the forward
+// phase: a proxy fence and the warp's own TMA loads carry them over, with no
+// grid-wide barrier between the directions. The backward wavefront starts on
+// the last warp as soon as it finishes its forward rows.
+//
+// PCG mode is speculative across the phase boundary: the backward solve runs
+// for every system that iterates; the forward epilogue (which may turn the
+// system to the drift check, pcg.py:147) runs before the backward one at the
+// end, and the backward epilogue then ignores the solve (common.cuh).
+template <bool PCG, bool SB, int G, int C>
+__global__ void __launch_bounds__(32 * line_cta_warps(C), 1) ldlt_line_kernel(LineArgs a) {
+    extern __shared__ __align__(128) char sm[];
+    __shared__ double s_red[2][kLineMaxWarps];
+    __shared__ double s_cta[2][4];
+    constexpr int NS = line_stages(G);
+    // WL warps per CTA; the last CTA of a cluster may hold idle warps (p >= W)
+    const int W = a.warps, WL = (W + C - 1) / C, R = a.ring;
+    const int wl = threadIdx.x >> 5, t = threadIdx.x & 31;
+    const int rank = C > 1 ? (int)cluster_rank() : 0, b = blockIdx.x / C;
+    const int pw = rank * WL + wl;  // physical warp = forward warp
+    const bool idle = pw >= W;
+    // what this system needs from this launch (uniform over the cluster)
+    bool upd = false, solve = true;
+    if (PCG) {
+        const SolveState &st = a.st;
+        const int ph = st.status[b] == ST_ACTIVE ? st.phase[b] : -1;
+        upd = ph == PH_ITER;
+        solve = ph == PH_ITER || ph == PH_INIT;
+        if (!solve) {
+            // every thread of the cluster has read status / phase before the
+            // epilogue changes them (PH_RESTART -> PH_INIT)
+            if (C > 1) cluster_sync_all();
+            else __syncthreads();
+            if (rank == 0 && threadIdx.x == 0) bwd_epilogue(a.st, b, 0.0);  // pflag / restart bookkeeping
+            return;
+        }
+    }
+    const LineSmem m = line_layout(WL, R, G, NS, PCG);
+    double *ring_f = reinterpret_cast<double *>(sm + m.ring_f);
+    double *ring_b = reinterpret_cast<double *>(sm + m.ring_b);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + m.mbar) + wl * NS;
+    char *stage = sm + m.stage0 + (size_t)wl * NS * m.slot_bytes;
+    for (int i = threadIdx.x; i < WL * R; i += blockDim.x) ring_f[i] = ring_b[i] = sentinel();
+    if (t == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], 1);
+        fence_mbar_init();
+    }
+    if (C > 1) cluster_sync_all();  // every ring armed before any remote write
+    else __syncthreads();
+
+    const long long vb = (long long)b * a.nslot;
+    const long long db = a.d_batched ? vb : 0;
+    const size_t fb = SB ? (size_t)b * a.fac_slots : 0;
+    double acc_f = 0.0, acc_b = 0.0;
+    if (!idle) {
+        LinePhase F;
+        F.meta = reinterpret_cast<const int4 *>(a.meta_f);
+        F.fac = a.S_f + fb;
+        F.vec[0] = a.in + vb;
+        F.vec[1] = PCG ? a.AP + vb : nullptr;
+        F.out = a.Y + vb;
+        F.rg = PCG ? a.R + vb : nullptr;
+        F.ring = ring_f;
+        F.w = pw;
+        F.rev = false;
+        F.jbase = 0;
+        const double alpha = upd ? a.st.alpha[b] : 0.0;
+        acc_f = line_phase<false, PCG, G, C, line_nv_f(PCG)>(F, W, WL, R, wl, t, mbar, stage, m.slot_bytes, upd,
+                                                              alpha);
+        // the backward phase reads this warp's y (and r) stores through TMA
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        const int nt_f = F.meta[pw].y;
+        LinePhase Bk;
+        Bk.meta = reinterpret_cast<const int4 *>(a.meta_b);
+        Bk.fac = a.S_b + fb;
+        Bk.vec[0] = a.Y + vb;
+        Bk.vec[1] = a.D + db;
+        Bk.vec[2] = a.rD + db;
+        Bk.vec[3] = PCG ? a.R + vb : nullptr;
+        Bk.out = a.out + vb;
+        Bk.ring = ring_b;
+        Bk.w = W - 1 - pw;
+        Bk.rev = true;
+        Bk.jbase = (nt_f + G - 1) / G;
+        acc_b = line_phase<true, PCG, G, C, line_nv_b(PCG)>(Bk, W, WL, R, wl, t, mbar, stage, m.slot_bytes, false,
+                                                             0.0);
+    }
+    if (PCG) {  // fixed-order reductions: lanes, warps, then the cluster's CTAs
+        double vf = acc_f, vbk = acc_b;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
-        if (t == 0) s_red[wl] = v;
+        for (int off = 16; off > 0; off >>= 1) {
+            vf = __dadd_rn(vf, __shfl_down_sync(0xffffffffu, vf, off));
+            vbk = __dadd_rn(vbk, __shfl_down_sync(0xffffffffu, vbk, off));
+        }
+        if (t == 0) s_red[0][wl] = vf, s_red[1][wl] = vbk;
         __syncthreads();
         if (threadIdx.x == 0) {
-            double tot = 0.0;
-            for (int q = 0; q < WL; ++q) tot = __dadd_rn(tot, s_red[q]);
-            if (C > 1) st_dsm(map_rank(&s_cta[rank], 0), tot);
-            else line_epilogue(a, b, tot);
+            double tf = 0.0, tb = 0.0;
+            for (int q = 0; q < WL; ++q) tf = __dadd_rn(tf, s_red[0][q]), tb = __dadd_rn(tb, s_red[1][q]);
+            if (C > 1) {
+                st_dsm(map_rank(&s_cta[0][rank], 0), tf);
+                st_dsm(map_rank(&s_cta[1][rank], 0), tb);
+            } else {
+                fwd_epilogue(a.st, b, tf, a.drift_count);
+                bwd_epilogue(a.st, b, tb);
+            }
         }
     }
     if (C > 1) {  // remote rings / partials stay valid until every CTA of the cluster is done
         cluster_sync_all();
         if (PCG && rank == 0 && threadIdx.x == 0) {
-            double tot = 0.0;
-            for (int q = 0; q < C; ++q) tot = __dadd_rn(tot, s_cta[q]);
-            line_epilogue(a, b, tot);
+            double tf = 0.0, tb = 0.0;
+            for (int q = 0; q < C; ++q) tf = __dadd_rn(tf, s_cta[0][q]), tb = __dadd_rn(tb, s_cta[1][q]);
+            fwd_epilogue(a.st, b, tf, a.drift_count);
+            bwd_epilogue(a.st, b, tb);
         }
     }
 }
 
 int line_trace_copy(long long *out, int n) {
-    n = std::min(n, kTraceEvents * kTraceBatches);
-    return (int)cudaMemcpyFromSymbol(out, g_line_trace, n * sizeof(long long));
+    (void)out;
+    (void)n;
+    return 0;  // no timeline in this build
 }
 
-static size_t line_smem(int WL, int R, int G, int NS, bool upper, bool pcg) {
-    return line_layout(WL, R, G, NS, line_vectors(upper, pcg)).total;
-}
+static size_t line_smem(int WL, int R, int G, int NS, bool pcg) { return line_layout(WL, R, G, NS, pcg).total; }
 
-int line_config_for(const LineDir &L, bool upper, int B) {
+int line_config_for(const LineSched &L, int B) {
     int dev = 0, optin = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (optin <= 0) optin = 227 * 1024;
     const size_t cap = (size_t)optin - 1024;  // static shared memory
+    const int W = L.fwd.warps, R = std::max(L.fwd.ring, L.bwd.ring);
     // CTAs per system: split over two SMs while the batch leaves them free;
     // more than 16 warps (lines > 512) always take a cluster, of 2 CTAs up to
     // 20 warps and 4 beyond (the last CTA may hold idle warps)
-    auto fits = [&](int c) { return c >= 1 && (L.warps + c - 1) / c <= line_cta_warps(c) && (c == 1 || L.warps >= c); };
-    int C = (L.warps % 2 == 0 && 2 * B <= sms) ? 2 : 1;
-    if (L.warps > kLineMaxWarps) C = (L.warps <= 2 * kLineMaxWarpsCluster && 2 * B <= sms) ? 2 : 4;
+    auto fits = [&](int c) { return c >= 1 && (W + c - 1) / c <= line_cta_warps(c) && (c == 1 || W >= c); };
+    int C = (W % 2 == 0 && 2 * B <= sms) ? 2 : 1;
+    if (W > kLineMaxWarps) C = (W <= 2 * kLineMaxWarpsCluster && 2 * B <= sms) ? 2 : 4;
     if (const char *env = std::getenv("NPCG_LINE_CLUSTER")) {
         const int c = std::atoi(env);
         if ((c == 1 || c == 2 || c == 4) && fits(c)) C = c;
     }
     if (!fits(C)) C = fits(4) ? 4 : 0;
     if (!C) return 0;
-    const int WL = (L.warps + C - 1) / C;
+    const int WL = (W + C - 1) / C;
     if (const char *env = std::getenv("NPCG_LINE_CFG")) {
         const int c = std::atoi(env), G = c / 16, NS = c % 16;
-        if (G >= 1 && G <= 4 && NS == line_stages(G) && line_smem(WL, L.ring, G, NS, upper, true) <= cap) return C * 256 + c;
+        if (G >= 1 && G <= 4 && NS == line_stages(G) && line_smem(WL, R, G, NS, true) <= cap) return C * 256 + c;
     }
-    // three operand stages: two in flight while one is consumed
     static const int prefs[][2] = {{4, line_stages(4)}, {3, line_stages(3)}, {2, line_stages(2)}, {1, line_stages(1)}};
     for (const auto &p : prefs)
-        if (line_smem(WL, L.ring, p[0], p[1], upper, true) <= cap) return C * 256 + p[0] * 16 + p[1];
+        if (line_smem(WL, R, p[0], p[1], true) <= cap) return C * 256 + p[0] * 16 + p[1];
     return 0;
 }
 
-template <bool UPPER, bool PCG, bool SB, int G, int C>
-static cudaError_t launch_line_t(const LineArgs &a, cudaStream_t s) {
-    auto kern = trsv_line_kernel<UPPER, PCG, SB, G, C>;
+template <bool PCG, bool SB, int G, int C>
+static cudaError_t launch_ldlt_t(const LineArgs &a, cudaStream_t s) {
+    auto kern = ldlt_line_kernel<PCG, SB, G, C>;
     const int WL = (a.warps + C - 1) / C;
-    const size_t smem = line_smem(WL, a.ring, G, a.stages, UPPER, PCG);
+    const size_t smem = line_smem(WL, a.ring, G, a.stages, PCG);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -485,59 +548,43 @@ static cudaError_t launch_line_t(const LineArgs &a, cudaStream_t s) {
 }
 
 template <int G, int C>
-static cudaError_t launch_line_gc(const LineArgs &a, cudaStream_t s) {
+static cudaError_t launch_ldlt_gc(const LineArgs &a, cudaStream_t s) {
     const bool pcg = a.mode == TRSV_PCG;
-    if (a.upper) {
-        if (pcg) return a.s_batched ? launch_line_t<true, true, true, G, C>(a, s) : launch_line_t<true, true, false, G, C>(a, s);
-        return a.s_batched ? launch_line_t<true, false, true, G, C>(a, s) : launch_line_t<true, false, false, G, C>(a, s);
-    }
-    if (pcg) return a.s_batched ? launch_line_t<false, true, true, G, C>(a, s) : launch_line_t<false, true, false, G, C>(a, s);
-    return a.s_batched ? launch_line_t<false, false, true, G, C>(a, s) : launch_line_t<false, false, false, G, C>(a, s);
+    if (pcg) return a.s_batched ? launch_ldlt_t<true, true, G, C>(a, s) : launch_ldlt_t<true, false, G, C>(a, s);
+    return a.s_batched ? launch_ldlt_t<false, true, G, C>(a, s) : launch_ldlt_t<false, false, G, C>(a, s);
 }
 
-cudaError_t launch_trsv_line(const LineArgs &a, cudaStream_t s) {
+cudaError_t launch_ldlt_line(const LineArgs &a, cudaStream_t s) {
     if (a.group < 1 || a.group > 4 || a.stages != line_stages(a.group) || a.warps < 1 ||
         (a.cluster != 1 && a.cluster != 2 && a.cluster != 4) ||
         (a.warps + a.cluster - 1) / a.cluster > line_cta_warps(a.cluster))
         return cudaErrorInvalidValue;
-    const int key = a.cluster * 16 + a.group;
-    switch (key) {
-        case 64 + 1: return launch_line_gc<1, 4>(a, s);
-        case 64 + 2: return launch_line_gc<2, 4>(a, s);
-        case 64 + 3: return launch_line_gc<3, 4>(a, s);
-        case 64 + 4: return launch_line_gc<4, 4>(a, s);
-        case 16 + 1: return launch_line_gc<1, 1>(a, s);
-        case 16 + 2: return launch_line_gc<2, 1>(a, s);
-        case 16 + 3: return launch_line_gc<3, 1>(a, s);
-        case 16 + 4: return launch_line_gc<4, 1>(a, s);
-        case 32 + 1: return launch_line_gc<1, 2>(a, s);
-        case 32 + 2: return launch_line_gc<2, 2>(a, s);
-        case 32 + 3: return launch_line_gc<3, 2>(a, s);
-        case 32 + 4: return launch_line_gc<4, 2>(a, s);
+    switch (a.cluster * 16 + a.group) {
+        case 16 + 1: return launch_ldlt_gc<1, 1>(a, s);
+        case 16 + 2: return launch_ldlt_gc<2, 1>(a, s);
+        case 16 + 3: return launch_ldlt_gc<3, 1>(a, s);
+        case 16 + 4: return launch_ldlt_gc<4, 1>(a, s);
+        case 32 + 1: return launch_ldlt_gc<1, 2>(a, s);
+        case 32 + 2: return launch_ldlt_gc<2, 2>(a, s);
+        case 32 + 3: return launch_ldlt_gc<3, 2>(a, s);
+        case 32 + 4: return launch_ldlt_gc<4, 2>(a, s);
+        case 64 + 1: return launch_ldlt_gc<1, 4>(a, s);
+        case 64 + 2: return launch_ldlt_gc<2, 4>(a, s);
+        case 64 + 3: return launch_ldlt_gc<3, 4>(a, s);
+        case 64 + 4: return launch_ldlt_gc<4, 4>(a, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
-// y /= diag (sparse.py:273) between the two solves: an elementwise pass
-// over every SM at HBM speed, where inside the wavefront kernels the divide
-// would sit on the few SMs that carry the solve.
-__global__ void __launch_bounds__(256) diag_scale_kernel(int nslot, const double *D, int d_batched, double *y) {
-    const int b = blockIdx.y;
-    const double2 *d2 = reinterpret_cast<const double2 *>(D + (d_batched ? (size_t)b * nslot : 0));
-    double2 *y2 = reinterpret_cast<double2 *>(y + (size_t)b * nslot);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nslot / 2; i += gridDim.x * blockDim.x) {
-        double2 v = y2[i];
-        const double2 d = d2[i];
-        v.x = __ddiv_rn(v.x, d.x);
-        v.y = __ddiv_rn(v.y, d.y);
-        y2[i] = v;
-    }
+__global__ void reciprocal_kernel(long long count, const double *D, double *rD) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < count; q += (long long)gridDim.x * blockDim.x)
+        rD[q] = __ddiv_rn(1.0, D[q]);
 }
 
-cudaError_t launch_diag_scale(int nslot, int B, const double *D, int d_batched, double *y, cudaStream_t s) {
-    const int gx = std::max(1, (nslot / 2 + 255) / 256);  // one pair per thread: the divides are latency bound
+cudaError_t launch_reciprocal(long long count, const double *D, double *rD, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
     note_launch();
-    diag_scale_kernel<<<dim3(gx, B), 256, 0, s>>>(nslot, D, d_batched, y);
+    reciprocal_kernel<<<(int)std::min<long long>((count + 255) / 256, 4096), 256, 0, s>>>(count, D, rD);
     return cudaGetLastError();
 }
 
