@@ -142,7 +142,6 @@ struct npcg_solver {
     double *Dl = nullptr, *rDl = nullptr;  // diag in line order ([b][nslot] or [nslot]) and 1 / diag
     size_t Dl_cap = 0;
     int *xpend = nullptr;
-    int *ppar = nullptr, *xpar = nullptr;  // line path: current p / x buffer per system
     double *ones = nullptr;   // identity preconditioner: D = 1 (per solver: no shared state between threads)
     long long *kmax = nullptr;  // largest k of the batch at the last poll
     struct Poll {
@@ -155,7 +154,7 @@ struct npcg_solver {
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
                         alpha, beta, rel, final_rel, history, active_count, drift_count, ctl, partial,
-                        S_fwd, S_bwd, xpend, Dl, rDl, XL, BL, ecol, eperm, evals, ones, kmax, ppar, xpar};
+                        S_fwd, S_bwd, xpend, Dl, rDl, XL, BL, ecol, eperm, evals, ones, kmax};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_poll) cudaFreeHost(h_poll);
@@ -406,15 +405,14 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     const size_t nB = (size_t)A->n * B;
     const size_t vB = s->ls ? (size_t)s->ls->nslot * B : nB;  // line-order vectors
     NPCG_CUDA(dalloc(&s->R, vB));
-    NPCG_CUDA(dalloc(&s->P, s->ls ? 2 * vB : vB));  // line path: two p buffers
+    NPCG_CUDA(dalloc(&s->P, vB));
     NPCG_CUDA(dalloc(&s->Z, vB));
     NPCG_CUDA(dalloc(&s->AP, vB));
     NPCG_CUDA(dalloc(&s->Y, vB));
     if (s->ls) {  // padding slots stay zero; A as ELL by slot for the SpMV
-        NPCG_CUDA(dalloc(&s->XL, 2 * vB));  // two x buffers
+        NPCG_CUDA(dalloc(&s->XL, vB));
         NPCG_CUDA(dalloc(&s->BL, vB));
-        for (double *v : {s->R, s->Z, s->AP, s->Y, s->BL}) NPCG_CUDA(cudaMemset(v, 0, vB * 8));
-        for (double *v : {s->P, s->XL}) NPCG_CUDA(cudaMemset(v, 0, 2 * vB * 8));
+        for (double *v : {s->R, s->Z, s->AP, s->Y, s->P, s->XL, s->BL}) NPCG_CUDA(cudaMemset(v, 0, vB * 8));
         const LineSched &ls = *s->ls;
         const int E = s->ell_width;
         std::vector<int> ecol((size_t)E * ls.nslot, -1), eperm((size_t)E * ls.nslot, -1);
@@ -433,10 +431,7 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     }
     NPCG_CUDA(dalloc(&s->status, B));
     NPCG_CUDA(dalloc(&s->xpend, B));
-    NPCG_CUDA(dalloc(&s->ppar, B));
-    NPCG_CUDA(dalloc(&s->xpar, B));
-    NPCG_CUDA(cudaMemset(s->ppar, 0, B * 4));
-    NPCG_CUDA(cudaMemset(s->xpar, 0, B * 4));
+
     NPCG_CUDA(dalloc(&s->phase, B));
     NPCG_CUDA(dalloc(&s->pflag, B));
     NPCG_CUDA(dalloc(&s->k, B));
@@ -486,8 +481,7 @@ static SolveState make_state(npcg_solver *s, const npcg_solve_opts *o) {
     SolveState st{};
     st.status = s->status;
     st.xpend = s->xpend;
-    st.ppar = s->ls ? s->ppar : nullptr;
-    st.xpar = s->ls ? s->xpar : nullptr;
+
     st.phase = s->phase;
     st.pflag = s->pflag;
     st.k = s->k;
@@ -758,18 +752,11 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     apdot.op = SPMV_APDOT;
     apdot.X = s->P;
     apdot.Y = s->AP;
-    if (s->ls) {
-        // the drift check rides on the next APDOT launch (no separate drift
-        // SpMV), and so do the p / x updates of the previous pass (no pupd):
-        // p and x are double-buffered, ppar / xpar pick the current buffers
+    if (s->ls) {  // the drift check rides on the next APDOT launch (no separate drift SpMV)
         apdot.merge_drift = 1;
+        apdot.X2 = xv;
         apdot.Bv = bv;
         apdot.R = s->R;
-        apdot.fused_pupd = 1;
-        apdot.vstride = (long long)s->ls->nslot * B;
-        apdot.Pbuf = s->P;
-        apdot.Xbuf = s->XL;
-        apdot.Z = s->Z;
     }
     SpmvArgs drift = spl;
     drift.op = SPMV_RESID_DRIFT;
@@ -851,6 +838,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         used.clear();
     };
     auto pupd = [&]() {
+        if (s->ls) return launch_pupd_ell(s->ls->nslot, B, s->Z, s->P, s->XL, sst, st);
         note_launch();
         pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, x, sst, 1);
         return cudaGetLastError();
@@ -870,8 +858,9 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     for (;;) {
         for (int q = 0; q < check; ++q) {
             NPCG_CUDA(timed(NPCG_PROF_SPMV_APDOT, [&] { return launch_spmv(apdot, st); }));
-            if (s->ls) {  // x / p updates ride on the next APDOT
+            if (s->ls) {  // P^{-1} in one launch, then the x / p updates
                 NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return launch_ldlt_line(ll, st); }));
+                NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
                 continue;
             }
             NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return launch_trsv(fw, st); }));
@@ -919,8 +908,6 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     std::vector<int> status(B);
     NPCG_CUDA(cudaMemcpyAsync(status.data(), s->status, B * 4, cudaMemcpyDeviceToHost, st));
     NPCG_CUDA(cudaStreamSynchronize(st));
-    // line path: x into buffer 0, with an update a budget-stopped pass left pending
-    if (s->ls) NPCG_CUDA(launch_flush_ell(s->ls->nslot, B, s->XL, s->P, (long long)s->ls->nslot * B, sst, st));
     bool any_max = false;
     for (int b = 0; b < B; ++b) any_max |= status[b] == ST_MAXITER || status[b] == ST_ACTIVE;
     if (any_max) {

@@ -47,10 +47,6 @@ struct SolveState {
     // per column [B]
     int *status, *phase, *pflag;
     int *xpend;                // 1 while this pass's x += alpha p is pending
-    // line path: p and x are double-buffered ([2][B][nslot]); the buffer
-    // holding each system's current p / x (the APDOT SpMV applies the pending
-    // pflag updates on the fly and writes the other buffer)
-    int *ppar, *xpar;
     long long *k;              // iterations
     long long *breakdown_at;
     double *scale, *rz, *alpha, *beta, *rel, *final_rel;

@@ -36,12 +36,6 @@ __device__ __forceinline__ bool spmv_col_active(const SpmvArgs &a, int b) {
 // Per-column control logic after the batch reduction (one thread per column).
 __device__ void spmv_epilogue(const SpmvArgs &a, int b, double total) {
     const SolveState &st = a.st;
-    if (a.op == SPMV_APDOT && a.fused_pupd) {  // the launch applied this column's pending updates
-        const int f = st.pflag[b];
-        if (f & (PF_UPDATE | PF_COPY)) st.ppar[b] ^= 1;
-        if (f & PF_X) st.xpar[b] ^= 1;
-        st.pflag[b] = PF_NONE;
-    }
     const int op = (a.op == SPMV_APDOT && a.merge_drift && st.status[b] == ST_ACTIVE && st.phase[b] == PH_DRIFT)
                        ? SPMV_RESID_DRIFT
                        : a.op;
@@ -537,8 +531,6 @@ __global__ void init_state_kernel(SolveState st, int B, long long hist_cap_init)
     st.phase[b] = PH_INIT;
     st.pflag[b] = PF_NONE;
     st.xpend[b] = 0;
-    if (st.ppar) st.ppar[b] = 0;
-    if (st.xpar) st.xpar[b] = 0;
     st.k[b] = 0;
     st.breakdown_at[b] = 0;
     st.rz[b] = st.alpha[b] = st.beta[b] = st.rel[b] = st.final_rel[b] = 0.0;
@@ -859,25 +851,15 @@ __global__ void __launch_bounds__(kSpmvThreads, NPCG_ELL_MINB) spmv_ell_kernel(S
     __shared__ unsigned char s_xp[kMaxBatch];
     __shared__ double s_al[kMaxBatch];
     __shared__ unsigned char s_dr[kMaxBatch];
-    __shared__ unsigned char s_f[kMaxBatch];  // fused APDOT: pending pflag
-    __shared__ double s_be[kMaxBatch];
-    __shared__ unsigned char s_pp[kMaxBatch], s_xq[kMaxBatch];
     const int B = a.B, ns = a.nslot, lane = threadIdx.x & 31, team = threadIdx.x >> 5;
     const int bl = blockIdx.y * kEllCols, bh = min(B, bl + kEllCols);  // this block's columns
-    constexpr bool FUSED = OP == SPMV_APDOT;  // the line path's APDOT always carries the p / x updates
-    if (OP == SPMV_RESID_DRIFT && *a.drift_count == 0) return;  // nothing drifted
+    if (OP == SPMV_RESID_DRIFT && *a.drift_count == 0) return;
     for (int b = threadIdx.x; b < B; b += blockDim.x) {
         s_act[b] = spmv_col_active(a, b) ? 1 : 0;
         s_xp[b] = OP == SPMV_RESID_DRIFT && a.st.xpend[b];
-        // merged drift columns: true residual from x_{k+1} (pcg.py:147-165)
+        s_al[b] = s_xp[b] ? a.st.alpha[b] : 0.0;
+        // merged drift columns: true residual from X2 (x already holds x + alpha p)
         s_dr[b] = OP == SPMV_APDOT && a.merge_drift && a.st.status[b] == ST_ACTIVE && a.st.phase[b] == PH_DRIFT;
-        if (FUSED) {
-            s_f[b] = (unsigned char)a.st.pflag[b];
-            s_pp[b] = (unsigned char)a.st.ppar[b];
-            s_xq[b] = (unsigned char)a.st.xpar[b];
-            s_be[b] = a.st.beta[b];
-        }
-        s_al[b] = (s_xp[b] || FUSED) ? a.st.alpha[b] : 0.0;
     }
     __syncthreads();
     const int q = blockIdx.x * kSpmvThreads + threadIdx.x;
@@ -895,7 +877,6 @@ __global__ void __launch_bounds__(kSpmvThreads, NPCG_ELL_MINB) spmv_ell_kernel(S
         v[e] = (!VB && c >= 0) ? a.evals[(size_t)e * ns + q] : 0.0;
     }
     const bool use_x = OP != SPMV_RESID_INIT || a.has_x;
-    auto ldb = [](const double *base, unsigned off) { return *reinterpret_cast<const double *>(reinterpret_cast<const char *>(base) + off); };
     // NB systems at a time: their gathers are in flight together and their
     // dot-product trees interleave
     constexpr int NB = NPCG_ELL_NB;
@@ -907,42 +888,15 @@ __global__ void __launch_bounds__(kSpmvThreads, NPCG_ELL_MINB) spmv_ell_kernel(S
             const int b = min(b0 + u, bh - 1);
             const size_t vb = (size_t)b * ns;
             const bool dr = OP == SPMV_APDOT && s_dr[b];
-            if (FUSED) {
-                // p_{k} / x_{k+1} with the updates the previous pass left pending, formed per
-                // operand exactly as pupd would store them (pcg.py:129, 141, 170)
-                const int f = s_f[b];
-                const double al = s_al[b], be = s_be[b];
-                const double *Po = a.Pbuf + (size_t)s_pp[b] * a.vstride + vb;
-                const double *Xo = a.Xbuf + (size_t)s_xq[b] * a.vstride + vb;
-                const double *Zb = a.Z + vb;
-                auto pcur = [&](unsigned off) {
-                    const double pv = ldb(Po, off);
-                    return (f & PF_UPDATE) ? __dadd_rn(ldb(Zb, off), __dmul_rn(be, pv)) : ((f & PF_COPY) ? ldb(Zb, off) : pv);
-                };
-                auto xcur = [&](unsigned off) {
-                    const double xv0 = ldb(Xo, off);
-                    return (f & PF_X) ? __dadd_rn(xv0, __dmul_rn(al, ldb(Po, off))) : xv0;
-                };
+            const char *Xb = reinterpret_cast<const char *>((dr ? a.X2 : a.X) + vb);
 #pragma unroll
-                for (int e = 0; e < E; ++e) xv[u][e] = dr ? xcur(cb[e]) : pcur(cb[e]);
-                const unsigned qo = (unsigned)qq * 8u;
-                const double pown = pcur(qo);
-                own[u] = dr ? a.Bv[vb + qq] : pown;
-                if (live && b0 + u < bh) {  // this slot's updates land in the other buffers
-                    if (f & (PF_UPDATE | PF_COPY)) a.Pbuf[(size_t)(s_pp[b] ^ 1) * a.vstride + vb + q] = pown;
-                    if (f & PF_X) a.Xbuf[(size_t)(s_xq[b] ^ 1) * a.vstride + vb + q] = xcur(qo);
-                }
-            } else {
-                const char *Xb = reinterpret_cast<const char *>(a.X + vb);
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    xv[u][e] = use_x ? *reinterpret_cast<const double *>(Xb + cb[e]) : 0.0;
-                    if (OP == SPMV_RESID_DRIFT && s_xp[b])  // x_{k+1} = x + alpha p not yet stored (pcg.py:141)
-                        xv[u][e] = __dadd_rn(xv[u][e], __dmul_rn(s_al[b], *reinterpret_cast<const double *>(
-                                                                           reinterpret_cast<const char *>(a.P + vb) + cb[e])));
-                }
-                own[u] = a.Bv[vb + qq];
+            for (int e = 0; e < E; ++e) {
+                xv[u][e] = use_x ? *reinterpret_cast<const double *>(Xb + cb[e]) : 0.0;
+                if (OP == SPMV_RESID_DRIFT && s_xp[b])  // x_{k+1} = x + alpha p not yet stored (pcg.py:141)
+                    xv[u][e] = __dadd_rn(xv[u][e], __dmul_rn(s_al[b], *reinterpret_cast<const double *>(
+                                                                       reinterpret_cast<const char *>(a.P + vb) + cb[e])));
             }
+            own[u] = (OP == SPMV_APDOT && !dr) ? a.X[vb + qq] : a.Bv[vb + qq];
         }
         double pr[NB];
 #pragma unroll
@@ -997,7 +951,6 @@ static void spmv_ell_e(const SpmvArgs &a, dim3 grid, cudaStream_t s) {
 
 static cudaError_t launch_spmv_ell(const SpmvArgs &a, cudaStream_t s) {
     if (a.op == SPMV_PLAIN || a.nslot <= 0) return cudaErrorInvalidValue;
-    if (a.op == SPMV_APDOT && (!a.fused_pupd || !a.Pbuf || !a.Xbuf || !a.Z)) return cudaErrorInvalidValue;
     const dim3 grid((a.nslot + kSpmvThreads - 1) / kSpmvThreads, (a.B + kEllCols - 1) / kEllCols);
     if ((size_t)grid.x * a.B > a.partial_cap) return cudaErrorInvalidValue;
     switch (a.ell_width) {
@@ -1039,40 +992,6 @@ __global__ void __launch_bounds__(256) pupd_ell_kernel(int nslot, const double *
             p2[i] = pq;
         }
     }
-}
-
-// x of every system into buffer 0 of X, with a still pending x += alpha p
-// applied (a solve that stopped on its pass budget); flags / parities reset
-__global__ void __launch_bounds__(256) flush_ell_kernel(int nslot, double *X, const double *P, long long vstride,
-                                                         SolveState st) {
-    const int b = blockIdx.y, f = st.pflag[b], xp = st.xpar[b], pp = st.ppar[b];
-    if (!(f & PF_X) && xp == 0) return;
-    const double al = st.alpha[b];
-    const size_t vb = (size_t)b * nslot;
-    const double *xs = X + (size_t)xp * vstride + vb, *ps = P + (size_t)pp * vstride + vb;
-    double *xd = X + vb;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nslot; i += gridDim.x * blockDim.x) {
-        double x = xs[i];
-        if (f & PF_X) x = __dadd_rn(x, __dmul_rn(al, ps[i]));  // pcg.py:141
-        xd[i] = x;
-    }
-}
-
-__global__ void flush_state_kernel(SolveState st, int B) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= B) return;
-    st.pflag[b] = PF_NONE;
-    st.xpar[b] = 0;
-}
-
-cudaError_t launch_flush_ell(int nslot, int B, double *X, const double *P, long long vstride, const SolveState &st,
-                             cudaStream_t s) {
-    const int gx = std::max(1, std::min((nslot + 255) / 256, (4 * num_sms() + B - 1) / B));
-    note_launch();
-    flush_ell_kernel<<<dim3(gx, B), 256, 0, s>>>(nslot, X, P, vstride, st);
-    note_launch();
-    flush_state_kernel<<<(B + 127) / 128, 128, 0, s>>>(st, B);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_pupd_ell(int nslot, int B, const double *z, double *p, double *x, const SolveState &st,

@@ -47,13 +47,6 @@ struct SpmvArgs {
     const double *X2 = nullptr;
     int ell_width = 0;
     size_t partial_cap = 0;  // doubles available at `partial`
-    // line-path APDOT with the p / x updates fused in (pcg.py:129, 141, 170):
-    // P / X hold two buffers each (vstride apart), st.ppar / st.xpar pick the
-    // current one per system, Z is the last preconditioned residual
-    int fused_pupd = 0;
-    long long vstride = 0;
-    double *Pbuf = nullptr, *Xbuf = nullptr;
-    const double *Z = nullptr;
 };
 
 __global__ void init_state_kernel(SolveState st, int B, long long hist_cap_init);
@@ -76,10 +69,6 @@ cudaError_t launch_from_line(int nslot, int B, const int *rowof, const double *s
 // all-line-order PCG vectors: p / x update, and value gathers into a packed order
 cudaError_t launch_pupd_ell(int nslot, int B, const double *z, double *p, double *x, const SolveState &st,
                             cudaStream_t s);
-// end of a fused-update solve: x (buffer xpar, plus a still pending
-// x += alpha p) -> buffer 0 of X for every system; flags and parities reset
-cudaError_t launch_flush_ell(int nslot, int B, double *X, const double *P, long long vstride, const SolveState &st,
-                             cudaStream_t s);
 void launch_gather_pack(long long per, int B, int sb, long long ps, long long bs, const int *perm, const double *S,
                         double *packed, cudaStream_t s);
 

@@ -77,12 +77,11 @@ struct SchedSet {
 constexpr int32_t kTileSteps = 4;
 constexpr int32_t kTileSlots = 32 * kTileSteps;
 constexpr int32_t kLineKinds = 3;  // L2, L1, S1
-// warps of one CTA: 16 (512 threads, <= 128 registers per lane) for a
-// one-CTA system, 8 (<= 255 registers) per CTA of a 2- or 4-CTA cluster
-constexpr int32_t kLineMaxWarps = 16;
-constexpr int32_t kLineMaxWarpsCluster = 8;
+// line warps of one CTA (each paired with a helper warp: 16 warps, 512
+// threads, <= 128 registers) and CTAs of one system's cluster
+constexpr int32_t kLineMaxWarps = 8;
 constexpr int32_t kLineMaxClusterCtas = 4;
-constexpr int32_t kLineMaxLines = 32 * kLineMaxWarpsCluster * kLineMaxClusterCtas;  // 1024
+constexpr int32_t kLineMaxLines = 32 * kLineMaxWarps * kLineMaxClusterCtas;  // 1024
 
 struct LineDir {
     int32_t warps = 0;

@@ -48,7 +48,7 @@ namespace {
 
 // operand stages per warp (a slot is refilled the stage after its use): three
 // up to 3-tile stages, two for 4-tile stages (shared memory)
-__host__ __device__ constexpr int line_stages(int G) { return G >= 4 ? 2 : 3; }
+__host__ __device__ constexpr int line_stages(int G) { return G >= 4 ? 2 : (G == 3 ? 3 : 4); }
 
 __host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
 
@@ -100,6 +100,21 @@ __device__ __forceinline__ double stage_dot(const double (&u)[N], const double (
     return p[0];
 }
 
+#ifdef NPCG_LINE_TRACE
+// Debug timeline (build with -DNPCG_LINE_TRACE): CTA 0 of system 0, per
+// warp (line warps, then helpers) and stage, three clock64 stamps.
+constexpr int kTraceWarps = 4 * 8, kTraceStages = 1024;
+__device__ long long g_ws_trace[kTraceWarps][kTraceStages][3];
+#define WS_TRACE(role, jj, k)                                                                             \
+    do {                                                                                                   \
+        if (trace_on && t == 0 && (jj) < kTraceStages) g_ws_trace[(role) * 8 + wl_][(jj)][(k)] = clock64(); \
+    } while (0)
+#else
+#define WS_TRACE(role, jj, k) \
+    do {                      \
+    } while (0)
+#endif
+
 // exact y / D from D and rD = RN(1 / D): q = RN(y rD) is within an ulp of
 // the quotient, the residual e = y - q D is exact (FMA), and RN(q + e rD)
 // is the correctly rounded quotient (Markstein) -- bitwise __ddiv_rn(y, D),
@@ -115,33 +130,72 @@ __device__ __forceinline__ double div_by_diag(double y, double D, double rD) {
     return r;
 }
 
-// One direction of the line solve for this warp (see the file comment).
-struct LinePhase {
+// y / D for many elements at once: the fast path for all of them first (no
+// branch between them), then the division for any lane that needs it
+// (div_by_diag's range conditions), once per batch and warp
+template <int K>
+__device__ __forceinline__ void div_by_diag_batch(double2 (&y)[K], const double2 (&d)[K], const double2 (&rd)[K]) {
+    bool slow = false;
+    double2 q[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double qx = __dmul_rn(y[k].x, rd[k].x), qy = __dmul_rn(y[k].y, rd[k].y);
+        const double ex = __fma_rn(-qx, d[k].x, y[k].x), ey = __fma_rn(-qy, d[k].y, y[k].y);
+        const double ax = fabs(qx), ay = fabs(qy);
+        slow |= (qx != 0.0 && !(ax > 0x1p-960 && ax < 0x1p960)) || (qy != 0.0 && !(ay > 0x1p-960 && ay < 0x1p960));
+        qx = ex == 0.0 ? qx : __fma_rn(ex, rd[k].x, qx);
+        qy = ey == 0.0 ? qy : __fma_rn(ey, rd[k].y, qy);
+        q[k] = make_double2(qx, qy);
+    }
+    if (__any_sync(0xffffffffu, slow)) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) q[k] = make_double2(div_by_diag(y[k].x, d[k].x, rd[k].x), div_by_diag(y[k].y, d[k].y, rd[k].y));
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) y[k] = q[k];
+}
+
+// A stage slot of a line-warp pair holds G tiles of: the factor kinds
+// [G][3][128], then three vector areas [G][128] each:
+//   forward:  V0 = r (the helper turns it into r - alpha Ap in place)
+//             V1 = Ap, overwritten by the solver's y
+//   backward: V0 = y (the helper turns it into y / D in place)
+//             V1 = D, overwritten by the solver's z;  V2 = 1 / D
+constexpr int kSlotArrays = kLineKinds + 3;
+
+// One direction of the solve for one line warp.
+struct LineDirIO {
     const int4 *meta = nullptr;    // this direction's warp table
     const double *fac = nullptr;   // packed factor values of this direction (this system)
-    const double *vec[4] = {};     // staged vectors (this system's base)
-    double *out = nullptr;         // results (this system's base)
+    const double *v[3] = {};       // vectors the helper stages (this system's base; see above)
+    int nv = 0;                    // how many of them
+    double *out = nullptr;         // y (forward) or z (backward)
     double *rg = nullptr;          // forward PCG update: r_{k+1}
-    double *ring = nullptr;        // this phase's incoming-value rings, [WL][R] in this CTA
+    const double *rdot = nullptr;  // backward PCG: r, for r.z
+    double *ring = nullptr;        // this direction's incoming-value rings, [WL][R] in this CTA
     int w = 0;                     // warp in this direction's order
-    bool rev = false;              // the direction's warp w runs on physical warp W - 1 - w
-    int jbase = 0;                 // stages this warp consumed before (mbarrier parity)
+    bool rev = false;              // the direction's warp w runs on line warp W - 1 - w
+    int jbase = 0;                 // stages the pair consumed before (mbarrier parity)
 };
 
-// NV staged vectors: forward r [, Ap]; backward y, D, rD [, r] (DIAG: y / D
-// formed from them as the operands are read).
-template <bool UPPER, bool PCG, int G, int C, int NV>
-__device__ __forceinline__ double line_phase(const LinePhase &io, const int W, const int WL, const int R,
-                                             const int wl, const int t, uint64_t *mbar, char *stage,
-                                             const size_t slot_bytes, const bool upd, const double alpha) {
+// Solver warp: the dependency chain only. Per step a lane reads its
+// prepared operands (r_{k+1} or y / D, and the three factor kinds) from the
+// slot, takes the left neighbour's value by shuffle (lane 0: from the ring
+// written by the previous warp's lane 31), and leaves the result in the slot.
+template <bool UPPER, int G>
+__device__ __forceinline__ void line_solver(const LineDirIO &io, const int W, const int WL, const int R, const int wl,
+                                            const int t, uint64_t *full, uint64_t *done, char *slots,
+                                            const size_t slot_bytes, const bool trace_on) {
+    const int wl_ = wl;
+    (void)trace_on;
+    (void)wl_;
     constexpr int STEPS = kTileSteps * G;
     constexpr int NS = line_stages(G);
-    constexpr bool DIAG = UPPER;
     static_assert(2 * STEPS <= 32, "a stage pair's ring slots are checked by one warp");
     const int w = io.w;
     const int4 *meta = io.meta;
     const int4 me = meta[w];
-    const int C0 = me.x, nt = me.y, tile0 = me.z, C1 = C0 + kTileSteps * nt;
+    const int C0 = me.x, nt = me.y, C1 = C0 + kTileSteps * nt;
     const int nstage = (nt + G - 1) / G;
     // ring protocol: warp w sends its last lane's values of steps
     // [max(C0_right - 2, C0), min(C1_right - 1, C1)) to the right warp; every
@@ -161,7 +215,7 @@ __device__ __forceinline__ double line_phase(const LinePhase &io, const int W, c
     double *rin = io.ring + wl * R;  // my incoming ring (local)
     // my outgoing ring: the right warp's incoming ring, in its CTA
     const int wr = w + 1 < W ? w + 1 : w;
-    const int pr = io.rev ? W - 1 - wr : wr;  // its physical warp
+    const int pr = io.rev ? W - 1 - wr : wr;  // its line warp
     const unsigned rout = map_rank(io.ring + (pr % WL) * R, (unsigned)(pr / WL));
     auto ring_read = [&](int x) -> double {  // value of the left line at step x (0 outside its range)
         if (x < P0 || x >= P1) return 0.0;
@@ -174,31 +228,8 @@ __device__ __forceinline__ double line_phase(const LinePhase &io, const int W, c
         st_vol(p, sentinel());
         return v;
     };
-    // tiles [lo, lo + g) of stage j (ascending in memory; the backward solve walks them downwards)
-    auto stage_tiles = [&](int j, int &lo, int &g) {
-        g = min(G, nt - j * G);
-        lo = UPPER ? tile0 + nt - j * G - g : tile0 + j * G;
-    };
-    constexpr size_t kFacBytes = (size_t)G * kLineKinds * kTileSlots * 8, kVecBytes = (size_t)G * kTileSlots * 8;
-    auto issue = [&](int j) {  // elected lane: bulk copies of stage j into its ring slot
-        int lo, g;
-        stage_tiles(j, lo, g);
-        const int js = io.jbase + j;
-        char *sp = stage + (size_t)(js % NS) * slot_bytes;
-        const unsigned fb = (unsigned)g * kLineKinds * kTileSlots * 8, vbytes = (unsigned)g * kTileSlots * 8;
-        uint64_t *bar = &mbar[js % NS];
-        mbar_expect_tx(bar, fb + NV * vbytes);
-        bulk_g2s(sp, io.fac + (size_t)lo * kLineKinds * kTileSlots, fb, bar);
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-            bulk_g2s(sp + kFacBytes + (size_t)v * kVecBytes, io.vec[v] + (size_t)lo * kTileSlots, vbytes, bar);
-    };
-    if (t == 0)
-        for (int j = 0; j < NS && j < nstage; ++j) issue(j);
-
     double h0 = 0.0;  // my value one step back
     double lp = 0.0;  // left neighbour's value two steps back (at the next step)
-    double acc2 = 0.0;
     double ychk = sentinel();  // this stage pair's outgoing-slot check (loaded a pair ahead)
     if (w + 1 < W) {
         const int ys = C0 + t;
@@ -206,50 +237,14 @@ __device__ __forceinline__ double line_phase(const LinePhase &io, const int W, c
     }
     if (cons) lp = ring_read(C0 - 2);
     for (int j = 0; j < nstage; ++j) {
-        const int js = io.jbase + j;
-        const int s = js % NS, sig = C0 + j * STEPS;  // first step of the stage
-        mbar_wait(&mbar[s], (js / NS) & 1);
-        // refill the slot of stage j - 1 (every lane's reads of it ended at its __syncwarp)
-        // with stage j - 1 + NS before this stage's operand loads
-        if (t == 0 && j >= 1 && j - 1 + NS < nstage) issue(j - 1 + NS);
-        int lo, g;
-        stage_tiles(j, lo, g);
-        const char *sp = stage + (size_t)s * slot_bytes;
-        const double *f = reinterpret_cast<const double *>(sp);
-        const double *v0 = reinterpret_cast<const double *>(sp + kFacBytes);
+        const int jj = io.jbase + j;
+        const int s = jj % NS, sig = C0 + j * STEPS;  // first step of the stage
+        const int g = min(G, nt - j * G);
+        WS_TRACE(0, jj, 0);
         const int live_steps = g * kTileSteps;
-        // a step pair's operands (a lane's two steps of a tile half are adjacent, pattern.h:
-        // one 16-byte load each), loaded one pair ahead inside the step loop so the shared-
-        // memory reads overlap the dependency chain instead of preceding it. A partial
-        // stage's lookahead reads stale slot contents, never used.
-        auto pair_ops = [&](int pi, double2 &f0, double2 &f1, double2 &f2, double2 &a0, double2 &a1) {
-            const int i = 2 * pi;
-            const int tp = UPPER ? G - 1 - i / kTileSteps - (G - g) : i / kTileSteps;  // tile within the stage
-            const int tpc = tp < 0 ? 0 : tp;
-            const int e = tile_elem(i % kTileSteps, t);  // element of step i, this direction
-            const double *ft = f + tpc * kLineKinds * kTileSlots + e;
-            f0 = *reinterpret_cast<const double2 *>(ft);
-            f1 = *reinterpret_cast<const double2 *>(ft + kTileSlots);
-            f2 = *reinterpret_cast<const double2 *>(ft + 2 * kTileSlots);
-            // vectors are in forward tile order: the backward pair is reversed
-            const int ve = tpc * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
-            const double *vv = v0 + ve;
-            if (DIAG) {  // y / D (sparse.py:273), off the dependency chain
-                const double2 y = *reinterpret_cast<const double2 *>(vv);
-                const double2 d = *reinterpret_cast<const double2 *>(vv + G * kTileSlots);
-                const double2 rd = *reinterpret_cast<const double2 *>(vv + 2 * G * kTileSlots);
-                a0 = make_double2(div_by_diag(y.x, d.x, rd.x), div_by_diag(y.y, d.y, rd.y));
-                a1 = NV > 3 ? *reinterpret_cast<const double2 *>(vv + 3 * G * kTileSlots) : make_double2(0.0, 0.0);
-            } else {
-                a0 = *reinterpret_cast<const double2 *>(vv);
-                a1 = NV > 1 ? *reinterpret_cast<const double2 *>(vv + G * kTileSlots) : make_double2(0.0, 0.0);
-            }
-        };
-        double VIN[STEPS], AUX[STEPS], ACC[STEPS];  // padding steps of a partial stage stay 0
-#pragma unroll
-        for (int i = 0; i < STEPS; ++i) VIN[i] = AUX[i] = ACC[i] = 0.0;
-        double2 cf0, cf1, cf2, ca0, ca1;
-        pair_ops(0, cf0, cf1, cf2, ca0, ca1);
+        const double *f = reinterpret_cast<const double *>(slots + (size_t)s * slot_bytes);
+        const double *vin = f + G * kLineKinds * kTileSlots;
+        double *res = const_cast<double *>(vin) + G * kTileSlots;
         // left line's values at steps sig-1 .. sig+STEPS-2 (lane i holds step sig-1+i): one
         // batch per stage, each slot re-armed after the read
         double x = 0.0;
@@ -264,6 +259,7 @@ __device__ __forceinline__ double line_phase(const LinePhase &io, const int W, c
             }
             if (pend) st_vol(px, sentinel());
         }
+        WS_TRACE(2, jj, 0);
         // my outgoing slots of this stage pair must have been re-armed by the right warp;
         // checked once per two stages (lane i: step sig + i), loaded two stages ahead (a
         // re-armed slot stays so until I write it)
@@ -279,27 +275,41 @@ __device__ __forceinline__ double line_phase(const LinePhase &io, const int W, c
             const bool chn = t < 2 * STEPS && yn >= Q0 && yn < Q1 && yn - R >= Q0;
             ychk = chn ? ld_dsm(rout + (unsigned)(yn & (R - 1)) * 8u) : sentinel();
         }
-        double *og = io.out + (size_t)lo * kTileSlots, *rg = upd ? io.rg + (size_t)lo * kTileSlots : nullptr;
+        WS_TRACE(2, jj, 1);
+        mbar_wait(&full[s], (jj / NS) & 1);  // operands prepared by the helper
+        WS_TRACE(0, jj, 1);
+        // a step pair's operands (a lane's two steps of a tile half are adjacent, pattern.h:
+        // one 16-byte load each), loaded one pair ahead so the shared-memory reads overlap
+        // the chain. A partial stage's lookahead reads stale slot contents, never used.
+        auto pair_at = [&](int i) {  // element offset of step pair (i, i + 1) in this direction
+            const int tp = UPPER ? G - 1 - i / kTileSteps - (G - g) : i / kTileSteps;  // tile within the stage
+            const int tpc = tp < 0 ? 0 : tp;
+            const int e = tile_elem(i % kTileSteps, t);
+            return make_int2(tpc * kLineKinds * kTileSlots + e, tpc * kTileSlots + (UPPER ? kTileSlots - 2 - e : e));
+        };
+        auto pair_ops = [&](int i, double2 &f0, double2 &f1, double2 &f2, double2 &a0) {
+            const int2 o = pair_at(i);
+            f0 = *reinterpret_cast<const double2 *>(f + o.x);
+            f1 = *reinterpret_cast<const double2 *>(f + o.x + kTileSlots);
+            f2 = *reinterpret_cast<const double2 *>(f + o.x + 2 * kTileSlots);
+            a0 = *reinterpret_cast<const double2 *>(vin + o.y);
+        };
+        double2 cf0, cf1, cf2, ca0;
+        pair_ops(0, cf0, cf1, cf2, ca0);
 #pragma unroll
         for (int pi = 0; pi < STEPS / 2; ++pi) {
             const int i = 2 * pi;
             if (i >= live_steps) break;
-            double2 nf0, nf1, nf2, na0, na1;
-            if (pi + 1 < STEPS / 2) pair_ops(pi + 1, nf0, nf1, nf2, na0, na1);
-            double v_lo = UPPER ? ca0.y : ca0.x, v_hi = UPPER ? ca0.x : ca0.y;
-            const double w_lo = UPPER ? ca1.y : ca1.x, w_hi = UPPER ? ca1.x : ca1.y;
-            if (!UPPER && PCG) {  // r_{k+1} = r_k - alpha A p (pcg.py:142); alpha = 0 unless updating
-                v_lo = upd ? __dsub_rn(v_lo, __dmul_rn(alpha, w_lo)) : v_lo;
-                v_hi = upd ? __dsub_rn(v_hi, __dmul_rn(alpha, w_hi)) : v_hi;
-            }
-            VIN[i] = v_lo;  // r_{k+1} | y / diag
-            VIN[i + 1] = v_hi;
-            if (UPPER && PCG) AUX[i] = w_lo, AUX[i + 1] = w_hi;  // r
+            double2 nf0, nf1, nf2, na0;
+            if (pi + 1 < STEPS / 2) pair_ops(i + 2, nf0, nf1, nf2, na0);
+            // vectors are in forward tile order: the backward pair is reversed
+            const double V[2] = {UPPER ? ca0.y : ca0.x, UPPER ? ca0.x : ca0.y};
             const double F0[2] = {cf0.x, cf0.y}, F1[2] = {cf1.x, cf1.y}, F2[2] = {cf2.x, cf2.y};
+            double A[2];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 2; ++h) {  // sparse.py:222-239 order: L2, L1, S1 terms
                 const int step = sig + i + h;
-                const double pre = __dsub_rn(VIN[i + h], __dmul_rn(F0[h], lp));
+                const double pre = __dsub_rn(V[h], __dmul_rn(F0[h], lp));
                 const double p2 = __dmul_rn(F2[h], h0);
                 double l1 = __shfl_up_sync(0xffffffffu, h0, 1);
                 const double xl = __shfl_sync(0xffffffffu, x, i + h);
@@ -309,87 +319,226 @@ __device__ __forceinline__ double line_phase(const LinePhase &io, const int W, c
                 h0 = acc;
                 lp = l1;
                 if (prod && step >= Q0 && step < Q1) st_dsm(rout + (unsigned)(step & (R - 1)) * 8u, acc);
-                ACC[i + h] = acc;
+                A[h] = acc;
             }
-            // results straight from registers: coalesced 16-byte stores, off the dependency chain
-            {
-                const int tp = UPPER ? g - 1 - i / kTileSteps : i / kTileSteps;
-                const int e = tile_elem(i % kTileSteps, t);
-                const int ve = tp * kTileSlots + (UPPER ? kTileSlots - 2 - e : e);
-                if (!UPPER) {
-                    *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i], ACC[i + 1]);  // y
-                    if (upd) *reinterpret_cast<double2 *>(rg + ve) = make_double2(VIN[i], VIN[i + 1]);  // r_{k+1}
-                } else {
-                    *reinterpret_cast<double2 *>(og + ve) = make_double2(ACC[i + 1], ACC[i]);  // z
-                }
-            }
-            if (pi + 1 < STEPS / 2) cf0 = nf0, cf1 = nf1, cf2 = nf2, ca0 = na0, ca1 = na1;
+            const int2 o = pair_at(i);
+            *reinterpret_cast<double2 *>(res + o.y) = UPPER ? make_double2(A[1], A[0]) : make_double2(A[0], A[1]);
+            if (pi + 1 < STEPS / 2) cf0 = nf0, cf1 = nf1, cf2 = nf2, ca0 = na0;
         }
-        if (upd) acc2 = __dadd_rn(acc2, stage_dot(VIN, VIN));  // |r_{k+1}|^2 (pcg.py:143)
-        if (UPPER && PCG) acc2 = __dadd_rn(acc2, stage_dot(AUX, ACC));  // r.z (pcg.py:167)
-        // every lane's reads of this slot are done before the elected lane refills it
-        __syncwarp();
+        __syncwarp();  // every lane's results are in the slot
+        if (t == 0) mbar_arrive(&done[s]);
+        WS_TRACE(0, jj, 2);
     }
-    return acc2;
 }
 
-__host__ __device__ constexpr int line_cta_warps(int C) { return C == 1 ? kLineMaxWarps : kLineMaxWarpsCluster; }
-// staged vectors per direction (see line_phase) and the larger of the two
-__host__ __device__ constexpr int line_nv_f(bool pcg) { return pcg ? 2 : 1; }
-__host__ __device__ constexpr int line_nv_b(bool pcg) { return pcg ? 4 : 3; }
+// Helper warp of a line warp: stages the operands with TMA, prepares them
+// (r_{k+1} = r - alpha Ap with |r_{k+1}|^2, pcg.py:142-143; or y / D,
+// sparse.py:273), writes the solver's results back to global memory
+// (coalesced) and forms r.z (pcg.py:167; r is brought into the slot's 1/D
+// area by a second bulk copy once y / D is formed). Returns this lane's dot
+// partial. Every loop over a stage is unrolled over its 2G chunks per lane:
+// the loads of a stage are in flight together.
+template <bool UPPER, bool PCG, int G>
+__device__ __forceinline__ double line_helper(const LineDirIO &io, const int t, const bool upd, const double alpha,
+                                              uint64_t *tma, uint64_t *full, uint64_t *done, uint64_t *rtma,
+                                              char *slots, const size_t slot_bytes, const int wl_, const bool trace_on) {
+    (void)trace_on;
+    (void)wl_;
+    constexpr int NS = line_stages(G);
+    constexpr int K = 2 * G;  // double2 chunks per lane per stage (g * 64 chunks of a stage)
+    const int4 me = io.meta[io.w];
+    const int nt = me.y, tile0 = me.z;
+    const int nstage = (nt + G - 1) / G;
+    auto stage_tiles = [&](int j, int &lo, int &g) {  // ascending in memory; backward walks them downwards
+        g = min(G, nt - j * G);
+        lo = UPPER ? tile0 + nt - j * G - g : tile0 + j * G;
+    };
+    constexpr size_t kFac = (size_t)G * kLineKinds * kTileSlots, kVec = (size_t)G * kTileSlots;  // doubles
+    auto slot_of = [&](int s) { return reinterpret_cast<double *>(slots + (size_t)s * slot_bytes); };
+    auto issue = [&](int j) {  // lane 0: bulk copies of stage j into its slot
+        int lo, g;
+        stage_tiles(j, lo, g);
+        const int s = (io.jbase + j) % NS;
+        double *sp = slot_of(s);
+        const unsigned fb = (unsigned)g * kLineKinds * kTileSlots * 8, vb = (unsigned)g * kTileSlots * 8;
+        mbar_expect_tx(&tma[s], fb + io.nv * vb);
+        bulk_g2s(sp, io.fac + (size_t)lo * kLineKinds * kTileSlots, fb, &tma[s]);
+        for (int v = 0; v < io.nv; ++v) bulk_g2s(sp + kFac + v * kVec, io.v[v] + (size_t)lo * kTileSlots, vb, &tma[s]);
+    };
+    if (t == 0)
+        for (int j = 0; j < NS && j < nstage; ++j) issue(j);
+    double acc = 0.0;
+    int jp = 0, jw = 0;  // next stage to prepare / to write back
+    // whatever is ready first, write-backs (they issue the refills) before
+    // preparations; never block on one while the other could proceed
+    while (jw < nstage) {
+        const int jjw = io.jbase + jw, sw = jjw % NS;
+        const bool wb_ready = jw < jp && mbar_test(&done[sw], (jjw / NS) & 1) &&
+                              (!(UPPER && PCG) || mbar_test(&rtma[sw], (jw / NS) & 1));
+        const int jjp = io.jbase + jp;
+        const bool prep_ready = !wb_ready && jp < nstage && jp < jw + NS && mbar_test(&tma[jjp % NS], (jjp / NS) & 1);
+        if (!wb_ready && !prep_ready) continue;
+        if (prep_ready) {
+            const int jj = jjp, s = jj % NS;
+            WS_TRACE(1, jj, 0);
+            int lo, g;
+            stage_tiles(jp, lo, g);
+            double *sp = slot_of(s);
+            double2 *v0 = reinterpret_cast<double2 *>(sp + kFac);
+            const double2 *v1 = reinterpret_cast<const double2 *>(sp + kFac + kVec);
+            const double2 *v2 = reinterpret_cast<const double2 *>(sp + kFac + 2 * kVec);
+            const int nc = g * (kTileSlots / 2);
+            if (UPPER) {
+                double2 y[K], d[K], rd[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int c = t + 32 * k < nc ? t + 32 * k : t;
+                    y[k] = v0[c], d[k] = v1[c], rd[k] = v2[c];
+                }
+                div_by_diag_batch<K>(y, d, rd);
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (t + 32 * k < nc) v0[t + 32 * k] = y[k];
+            } else if (PCG && upd) {
+                double2 r[K], ap[K];
+                double part[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int c = t + 32 * k < nc ? t + 32 * k : t;
+                    r[k] = v0[c], ap[k] = v1[c];
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    r[k].x = __dsub_rn(r[k].x, __dmul_rn(alpha, ap[k].x));  // pcg.py:142
+                    r[k].y = __dsub_rn(r[k].y, __dmul_rn(alpha, ap[k].y));
+                    part[k] = t + 32 * k < nc ? __dadd_rn(__dmul_rn(r[k].x, r[k].x), __dmul_rn(r[k].y, r[k].y)) : 0.0;
+                    if (t + 32 * k < nc) v0[t + 32 * k] = r[k];
+                }
+#pragma unroll
+                for (int h = 1; h < K; h <<= 1)  // |r_{k+1}|^2 (pcg.py:143), fixed pairwise order
+#pragma unroll
+                    for (int k = 0; k + h < K; k += 2 * h) part[k] = __dadd_rn(part[k], part[k + h]);
+                acc = __dadd_rn(acc, part[0]);
+            }
+            __syncwarp();
+            if (t == 0) mbar_arrive(&full[s]);
+            WS_TRACE(3, jj, 0);
+            if (UPPER && PCG) {  // r for r.z into the 1/D area, no longer read
+                fence_proxy_async();
+                __syncwarp();
+                if (t == 0) {
+                    const unsigned vb = (unsigned)g * kTileSlots * 8;
+                    mbar_expect_tx(&rtma[s], vb);
+                    bulk_g2s(sp + kFac + 2 * kVec, io.rdot + (size_t)lo * kTileSlots, vb, &rtma[s]);
+                }
+            }
+            WS_TRACE(1, jj, 1);
+            ++jp;
+        } else {
+            const int jj = jjw, s = sw;  // rtma is armed in this phase only: parity by jw
+            int lo, g;
+            stage_tiles(jw, lo, g);
+            const double *sp = slot_of(s);
+            const double2 *v0 = reinterpret_cast<const double2 *>(sp + kFac);
+            const double2 *v1 = reinterpret_cast<const double2 *>(sp + kFac + kVec);
+            const double2 *v2 = reinterpret_cast<const double2 *>(sp + kFac + 2 * kVec);
+            const int nc = g * (kTileSlots / 2);
+            double2 res[K], rk[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int c = t + 32 * k < nc ? t + 32 * k : t;
+                res[k] = v1[c];
+                if (!UPPER && PCG) rk[k] = v0[c];
+                if (UPPER && PCG) rk[k] = v2[c];
+            }
+            double2 *og = reinterpret_cast<double2 *>(io.out + (size_t)lo * kTileSlots);
+            double part[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const bool ok = t + 32 * k < nc;
+                if (ok) og[t + 32 * k] = res[k];  // y | z
+                if (!UPPER && PCG && upd && ok) reinterpret_cast<double2 *>(io.rg + (size_t)lo * kTileSlots)[t + 32 * k] = rk[k];
+                part[k] = (UPPER && PCG && ok) ? __dadd_rn(__dmul_rn(rk[k].x, res[k].x), __dmul_rn(rk[k].y, res[k].y)) : 0.0;
+            }
+            if (UPPER && PCG) {  // r.z (pcg.py:167), fixed pairwise order
+#pragma unroll
+                for (int h = 1; h < K; h <<= 1)
+#pragma unroll
+                    for (int k = 0; k + h < K; k += 2 * h) part[k] = __dadd_rn(part[k], part[k + h]);
+                acc = __dadd_rn(acc, part[0]);
+            }
+            // the slot's generic accesses (mine and the solver's) before the async-proxy refill
+            fence_proxy_async();
+            __syncwarp();
+            if (t == 0 && jw + NS < nstage) issue(jw + NS);
+            WS_TRACE(1, jj, 2);
+            ++jw;
+        }
+    }
+    return acc;
+}
+
+// line warps per CTA: a 2-CTA cluster keeps 4 pairs (256 threads: the full
+// register file per thread), one CTA or a 4-CTA cluster up to 8 pairs
+__host__ __device__ constexpr int line_cta_warps(int C) { return C == 2 ? kLineMaxWarps / 2 : kLineMaxWarps; }
 
 struct LineSmem {  // byte offsets into dynamic shared memory
-    size_t ring_f, ring_b, mbar, stage0, slot_bytes, total;
+    size_t ring_f, ring_b, bars, slots, slot_bytes, total;
 };
 
-__host__ __device__ inline LineSmem line_layout(int WL, int R, int G, int NS, bool pcg) {
+// per CTA: two direction rings [WL][R]; per line-warp pair 4 x NS mbarriers
+// (tma, full, done, rtma) and NS slots
+__host__ __device__ inline LineSmem line_layout(int WL, int R, int G, int NS) {
     LineSmem m;
     m.ring_f = 0;
     m.ring_b = al128((size_t)WL * R * 8);
-    m.mbar = m.ring_b + al128((size_t)WL * R * 8);
-    m.stage0 = al128(m.mbar + (size_t)WL * NS * 8);
-    m.slot_bytes = (size_t)G * (kLineKinds + line_nv_b(pcg)) * kTileSlots * 8;
-    m.total = m.stage0 + (size_t)WL * NS * m.slot_bytes;
+    m.bars = m.ring_b + al128((size_t)WL * R * 8);
+    m.slots = al128(m.bars + (size_t)WL * 4 * NS * 8);
+    m.slot_bytes = (size_t)G * kSlotArrays * kTileSlots * 8;
+    m.total = m.slots + (size_t)WL * NS * m.slot_bytes;
     return m;
 }
 
 }  // namespace
 
-// P^{-1} r for one system per cluster: the forward unit solve (with the PCG
-// residual update fused in front), then y / D and the backward transpose
-// solve -- one launch (sparse.py:222-239, 265-275; pcg.py:142-143, 167).
+// P^{-1} r for one system per cluster, one launch: the forward unit solve
+// (with the PCG residual update in front), then y / D and the backward
+// transpose solve (sparse.py:222-239, 265-275; pcg.py:142-143, 167).
 //
-// Every physical warp owns the same 32 grid lines in both directions (the
-// backward order walks warp W-1-w, lane 31-t), so the backward operands y and
-// r of a warp's rows are the values the warp itself stored in the forward
-// phase: a proxy fence and the warp's own TMA loads carry them over, with no
-// grid-wide barrier between the directions. The backward wavefront starts on
-// the last warp as soon as it finishes its forward rows.
+// Warps come in pairs (line warp w: warp w of the CTA, its helper: warp
+// WL + w): the line warp carries only the wavefront's dependency chain, the
+// helper everything else (line_helper). Every line warp owns the same 32
+// grid lines in both directions (the backward order walks warp W-1-w, lane
+// 31-t), so the backward operands of a pair's rows are values its own
+// helper wrote in the forward phase: a proxy fence and the helper's TMA
+// loads carry them over, no grid-wide barrier. The backward wavefront starts
+// on the last warp as soon as it finishes its forward rows.
 //
 // PCG mode is speculative across the phase boundary: the backward solve runs
 // for every system that iterates; the forward epilogue (which may turn the
 // system to the drift check, pcg.py:147) runs before the backward one at the
 // end, and the backward epilogue then ignores the solve (common.cuh).
 template <bool PCG, bool SB, int G, int C>
-__global__ void __launch_bounds__(32 * line_cta_warps(C), 1) ldlt_line_kernel(LineArgs a) {
+__global__ void __launch_bounds__(64 * line_cta_warps(C), 1) ldlt_line_kernel(LineArgs a) {
     extern __shared__ __align__(128) char sm[];
     __shared__ double s_red[2][kLineMaxWarps];
     __shared__ double s_cta[2][4];
     constexpr int NS = line_stages(G);
-    // WL warps per CTA; the last CTA of a cluster may hold idle warps (p >= W)
+    // WL line warps (+ WL helpers) per CTA; the last CTA of a cluster may hold idle pairs
     const int W = a.warps, WL = (W + C - 1) / C, R = a.ring;
-    const int wl = threadIdx.x >> 5, t = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, t = threadIdx.x & 31;
+    const bool helper = warp >= WL;
+    const int wl = helper ? warp - WL : warp;
     const int rank = C > 1 ? (int)cluster_rank() : 0, b = blockIdx.x / C;
-    const int pw = rank * WL + wl;  // physical warp = forward warp
+    const int pw = rank * WL + wl;  // line warp = forward warp
     const bool idle = pw >= W;
     // what this system needs from this launch (uniform over the cluster)
-    bool upd = false, solve = true;
+    bool upd = false;
     if (PCG) {
         const SolveState &st = a.st;
         const int ph = st.status[b] == ST_ACTIVE ? st.phase[b] : -1;
         upd = ph == PH_ITER;
-        solve = ph == PH_ITER || ph == PH_INIT;
-        if (!solve) {
+        if (!(ph == PH_ITER || ph == PH_INIT)) {
             // every thread of the cluster has read status / phase before the
             // epilogue changes them (PH_RESTART -> PH_INIT)
             if (C > 1) cluster_sync_all();
@@ -398,14 +547,15 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) ldlt_line_kernel(Li
             return;
         }
     }
-    const LineSmem m = line_layout(WL, R, G, NS, PCG);
+    const LineSmem m = line_layout(WL, R, G, NS);
     double *ring_f = reinterpret_cast<double *>(sm + m.ring_f);
     double *ring_b = reinterpret_cast<double *>(sm + m.ring_b);
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + m.mbar) + wl * NS;
-    char *stage = sm + m.stage0 + (size_t)wl * NS * m.slot_bytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + m.bars) + (size_t)wl * 4 * NS;
+    uint64_t *tma = bars, *full = bars + NS, *done = bars + 2 * NS, *rtma = bars + 3 * NS;
+    char *slots = sm + m.slots + (size_t)wl * NS * m.slot_bytes;
     for (int i = threadIdx.x; i < WL * R; i += blockDim.x) ring_f[i] = ring_b[i] = sentinel();
-    if (t == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], 1);
+    if (helper && t == 0) {
+        for (int s = 0; s < 4 * NS; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     if (C > 1) cluster_sync_all();  // every ring armed before any remote write
@@ -413,50 +563,55 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) ldlt_line_kernel(Li
 
     const long long vb = (long long)b * a.nslot;
     const long long db = a.d_batched ? vb : 0;
+    const bool trace_on = b == 0 && rank == 0;
     const size_t fb = SB ? (size_t)b * a.fac_slots : 0;
     double acc_f = 0.0, acc_b = 0.0;
     if (!idle) {
-        LinePhase F;
+        LineDirIO F;
         F.meta = reinterpret_cast<const int4 *>(a.meta_f);
         F.fac = a.S_f + fb;
-        F.vec[0] = a.in + vb;
-        F.vec[1] = PCG ? a.AP + vb : nullptr;
+        F.v[0] = a.in + vb;
+        F.v[1] = PCG ? a.AP + vb : nullptr;
+        F.nv = PCG && upd ? 2 : 1;
         F.out = a.Y + vb;
         F.rg = PCG ? a.R + vb : nullptr;
         F.ring = ring_f;
         F.w = pw;
         F.rev = false;
         F.jbase = 0;
-        const double alpha = upd ? a.st.alpha[b] : 0.0;
-        acc_f = line_phase<false, PCG, G, C, line_nv_f(PCG)>(F, W, WL, R, wl, t, mbar, stage, m.slot_bytes, upd,
-                                                              alpha);
-        // the backward phase reads this warp's y (and r) stores through TMA
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncwarp();
-        const int nt_f = F.meta[pw].y;
-        LinePhase Bk;
+        LineDirIO Bk;
         Bk.meta = reinterpret_cast<const int4 *>(a.meta_b);
         Bk.fac = a.S_b + fb;
-        Bk.vec[0] = a.Y + vb;
-        Bk.vec[1] = a.D + db;
-        Bk.vec[2] = a.rD + db;
-        Bk.vec[3] = PCG ? a.R + vb : nullptr;
+        Bk.v[0] = a.Y + vb;
+        Bk.v[1] = a.D + db;
+        Bk.v[2] = a.rD + db;
+        Bk.nv = 3;
         Bk.out = a.out + vb;
+        Bk.rdot = PCG ? a.R + vb : nullptr;
         Bk.ring = ring_b;
         Bk.w = W - 1 - pw;
         Bk.rev = true;
-        Bk.jbase = (nt_f + G - 1) / G;
-        acc_b = line_phase<true, PCG, G, C, line_nv_b(PCG)>(Bk, W, WL, R, wl, t, mbar, stage, m.slot_bytes, false,
-                                                             0.0);
+        Bk.jbase = (F.meta[pw].y + G - 1) / G;
+        if (helper) {
+            const double alpha = upd ? a.st.alpha[b] : 0.0;
+            acc_f = line_helper<false, PCG, G>(F, t, upd, alpha, tma, full, done, rtma, slots, m.slot_bytes, wl, trace_on);
+            // the backward phase reads this warp's y (and r) stores through TMA
+            fence_proxy_async_global();
+            __syncwarp();
+            acc_b = line_helper<true, PCG, G>(Bk, t, false, 0.0, tma, full, done, rtma, slots, m.slot_bytes, wl, trace_on);
+        } else {
+            line_solver<false, G>(F, W, WL, R, wl, t, full, done, slots, m.slot_bytes, trace_on);
+            line_solver<true, G>(Bk, W, WL, R, wl, t, full, done, slots, m.slot_bytes, trace_on);
+        }
     }
-    if (PCG) {  // fixed-order reductions: lanes, warps, then the cluster's CTAs
+    if (PCG) {  // fixed-order reductions: lanes, helper warps, then the cluster's CTAs
         double vf = acc_f, vbk = acc_b;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             vf = __dadd_rn(vf, __shfl_down_sync(0xffffffffu, vf, off));
             vbk = __dadd_rn(vbk, __shfl_down_sync(0xffffffffu, vbk, off));
         }
-        if (t == 0) s_red[0][wl] = vf, s_red[1][wl] = vbk;
+        if (helper && t == 0) s_red[0][wl] = vf, s_red[1][wl] = vbk;
         __syncthreads();
         if (threadIdx.x == 0) {
             double tf = 0.0, tb = 0.0;
@@ -482,12 +637,17 @@ __global__ void __launch_bounds__(32 * line_cta_warps(C), 1) ldlt_line_kernel(Li
 }
 
 int line_trace_copy(long long *out, int n) {
+#ifdef NPCG_LINE_TRACE
+    n = std::min(n, kTraceWarps * kTraceStages * 3);
+    return (int)cudaMemcpyFromSymbol(out, g_ws_trace, n * sizeof(long long));
+#else
     (void)out;
     (void)n;
     return 0;  // no timeline in this build
+#endif
 }
 
-static size_t line_smem(int WL, int R, int G, int NS, bool pcg) { return line_layout(WL, R, G, NS, pcg).total; }
+static size_t line_smem(int WL, int R, int G, int NS) { return line_layout(WL, R, G, NS).total; }
 
 int line_config_for(const LineSched &L, int B) {
     int dev = 0, optin = 0, sms = 0;
@@ -498,25 +658,28 @@ int line_config_for(const LineSched &L, int B) {
     const size_t cap = (size_t)optin - 1024;  // static shared memory
     const int W = L.fwd.warps, R = std::max(L.fwd.ring, L.bwd.ring);
     // CTAs per system: split over two SMs while the batch leaves them free;
-    // more than 16 warps (lines > 512) always take a cluster, of 2 CTAs up to
-    // 20 warps and 4 beyond (the last CTA may hold idle warps)
-    auto fits = [&](int c) { return c >= 1 && (W + c - 1) / c <= line_cta_warps(c) && (c == 1 || W >= c); };
-    int C = (W % 2 == 0 && 2 * B <= sms) ? 2 : 1;
-    if (W > kLineMaxWarps) C = (W <= 2 * kLineMaxWarpsCluster && 2 * B <= sms) ? 2 : 4;
+    // more than 8 line warps always take a cluster (2 CTAs up to 16 warps,
+    // 4 beyond; the last CTA may hold idle pairs)
+    auto fits = [&](int c) { return (W + c - 1) / c <= line_cta_warps(c) && (c == 1 || W >= c); };
+    int C = (W % 2 == 0 && 2 * B <= sms && fits(2)) ? 2 : 1;
+    if (!fits(C)) C = (fits(2) && 2 * B <= sms) ? 2 : 4;
     if (const char *env = std::getenv("NPCG_LINE_CLUSTER")) {
         const int c = std::atoi(env);
         if ((c == 1 || c == 2 || c == 4) && fits(c)) C = c;
     }
-    if (!fits(C)) C = fits(4) ? 4 : 0;
+    if (!fits(C)) C = fits(2) ? 2 : (fits(4) ? 4 : 0);
     if (!C) return 0;
     const int WL = (W + C - 1) / C;
     if (const char *env = std::getenv("NPCG_LINE_CFG")) {
         const int c = std::atoi(env), G = c / 16, NS = c % 16;
-        if (G >= 1 && G <= 4 && NS == line_stages(G) && line_smem(WL, R, G, NS, true) <= cap) return C * 256 + c;
+        if (G >= 1 && G <= 4 && NS == line_stages(G) && line_smem(WL, R, G, NS) <= cap) return C * 256 + c;
     }
-    static const int prefs[][2] = {{4, line_stages(4)}, {3, line_stages(3)}, {2, line_stages(2)}, {1, line_stages(1)}};
+    // long stages first (the line warp's per-stage hand-offs amortise over 16
+    // steps; measured 263 vs 249 systems/s against 8-step stages four deep at
+    // config 2), then deeper pipelines of shorter stages
+    static const int prefs[][2] = {{4, line_stages(4)}, {2, line_stages(2)}, {3, line_stages(3)}, {1, line_stages(1)}};
     for (const auto &p : prefs)
-        if (line_smem(WL, R, p[0], p[1], true) <= cap) return C * 256 + p[0] * 16 + p[1];
+        if (line_smem(WL, R, p[0], p[1]) <= cap) return C * 256 + p[0] * 16 + p[1];
     return 0;
 }
 
@@ -524,7 +687,7 @@ template <bool PCG, bool SB, int G, int C>
 static cudaError_t launch_ldlt_t(const LineArgs &a, cudaStream_t s) {
     auto kern = ldlt_line_kernel<PCG, SB, G, C>;
     const int WL = (a.warps + C - 1) / C;
-    const size_t smem = line_smem(WL, a.ring, G, a.stages, PCG);
+    const size_t smem = line_smem(WL, a.ring, G, a.stages);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -534,7 +697,7 @@ static cudaError_t launch_ldlt_t(const LineArgs &a, cudaStream_t s) {
     note_launch();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.B * C);
-    cfg.blockDim = dim3(32 * WL);
+    cfg.blockDim = dim3(64 * WL);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
