@@ -1,27 +1,35 @@
 #!/usr/bin/env python
 """bench.py -- NeuralPCG solve path on B200 (BASELINE.json headline metric).
 
-Workload (config 2 of BASELINE.json, the config the metric is quoted on):
-2-D Poisson, 256 x 256 jittered triangulated unit square, full-boundary
-Dirichlet eliminated (n = 65,025, nnz = 453,137), 64 right-hand sides
-(GRF loads), ONE shared learned factor L' from the GNN (reference-mode
-architecture at latent 64, 5 message-passing rounds, seeded weights with
-the processor output gain cancelled) computed on RHS 0, PCG to rtol 1e-8.
+Default workload (config 2 of BASELINE.json, the config the metric is quoted
+on): 2-D Poisson, 256 x 256 jittered triangulated unit square, full-boundary
+Dirichlet eliminated (n = 65,025, nnz = 453,137), 64 right-hand sides (GRF
+loads), ONE shared learned factor L' from the GNN (reference-mode
+architecture at latent 64, 5 message-passing rounds, seeded weights with the
+processor output gain cancelled) computed on RHS 0, PCG to rtol 1e-8.
 
-A step = build_learned (GNN on the device) + one batched PCG over the 64
-right-hand sides; a unit = one right-hand side solved to rtol; metric =
-units / second (whole job, all ranks). ``value`` has inputs resident in HBM;
-``e2e`` runs the same step through the public API from pinned host buffers
-with the host<->device copies inside the timed region. L2 is flushed
-(256 MiB write) before every timed step, outside the timed interval.
+``--config 3``: 2-D implicit wave step on a jittered 512 x 512 grid (n =
+263,169, nnz = 1,838,081), 32 distinct systems per GPU, each with its own A,
+b and GNN-built L' (latent 64, 5 rounds), PCG to rtol 1e-8.
 
-Multi-GPU: one process per GPU (torchrun), each rank solves its own batch
-of 64 right-hand sides on the shared mesh (weak scaling, no collective in
-the data path; barrier + max-over-ranks timing only).
+A step = the GNN (build_learned / build_learned_batch on the device) + one
+batched PCG + (N > 1) the final gather of x, iteration counts and status to
+rank 0 over NCCL; a unit = one right-hand side (config 2) or one system
+(config 3) solved to rtol; metric = units / second (whole job, all ranks).
+``value`` has inputs resident in HBM; ``e2e`` runs the same step through the
+public API from pinned host buffers with the host<->device copies inside the
+timed region. L2 is flushed (256 MiB write) before every timed step, outside
+the timed interval.
+
+Multi-GPU: one process per GPU (torchrun); rank r solves its own shard of
+the job (config 2: its own 64 right-hand sides on the shared mesh; config 3:
+systems [32 r, 32 r + 32) of the global list) with no collective in the data
+path, then the solutions are gathered to rank 0 (paper_2305_16432_b200.dist).
 
 ``--impl reference`` times the reference's CPU implementation of the same
-path on the host cores (the oracle port, oracle/port.py: the reference has
-no compiled artefact to build), see reference_arm().
+path on the host cores (the oracle port, oracle/port.py: the reference is
+pure Python + numba, there is no compiled artefact to build), see
+reference_arm().
 """
 from __future__ import annotations
 
@@ -40,6 +48,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CFG = dict(k=256, jitter=0.2, batch=64, rtol=1e-8, width=64, h=64, n_mp=5, seed=3)
+CFG3 = dict(k=512, batch=32)
 METRIC = "systems solved to rtol 1e-8 /sec; PCG-iteration HBM GB/s vs 8 TB/s peak"
 UNIT = "systems/s"
 
@@ -50,17 +59,22 @@ def args_():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--k", type=int, default=CFG["k"], help="mesh cells per side (256 = config 2)")
-    ap.add_argument("--batch", type=int, default=CFG["batch"])
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3], help="BASELINE.json config (2: shared L', "
+                    "64 RHS; 3: 32 distinct systems per GPU)")
+    ap.add_argument("--k", type=int, default=None, help="mesh cells per side (default 256 / 512)")
+    ap.add_argument("--batch", type=int, default=None, help="RHS (config 2) or systems (config 3) per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="one profiled step, no JSON (for ncu)")
     return ap.parse_args()
 
 
-def workload(k, batch, rank=0):
+def workload(k, batch, rank=0, config=2):
     from paper_2305_16432_b200 import gnn, inputs
-    prob = inputs.poisson_2d(k=k, batch=batch, first=rank * batch)
+    if config == 3:
+        prob = inputs.wave_2d(k=k, batch=batch, first=rank * batch)
+    else:
+        prob = inputs.poisson_2d(k=k, batch=batch, first=rank * batch)
     gnn.FEATURE_WIDTH = CFG["width"]
     hyper = gnn.GnnHyperParams(l=1, h=CFG["h"], n_mp=CFG["n_mp"], l_mp=1, h_mp=CFG["h"])
     model = gnn.create_model(hyper, seed=CFG["seed"])
@@ -70,17 +84,35 @@ def workload(k, batch, rank=0):
     return prob, model
 
 
-def config_dict(prob, k, batch, world):
+def config_dict(prob, k, batch, world, config=2):
     A = prob.A
-    return {
-        "workload": f"cfg2 poisson-2d {k}x{k} jittered P1, Dirichlet-eliminated (n={A.n}, nnz={A.nnz}), "
-                    f"{batch} GRF right-hand sides per GPU, one shared L' from the GNN "
-                    f"(latent {CFG['width']}, {CFG['n_mp']} rounds) per step, PCG rtol {CFG['rtol']}",
-        "n": A.n, "nnz": A.nnz, "rhs_per_gpu": batch, "gnn": f"reference-mode F={CFG['width']} h={CFG['h']} "
-        f"n_mp={CFG['n_mp']}, create_model(seed={CFG['seed']}) with processor output layers x10",
-        "l2": "flushed (256 MiB write) before every timed step",
-        "parallelism": f"batch-parallel x{world} (weak)",
-    }
+    gnn_desc = (f"reference-mode F={CFG['width']} h={CFG['h']} n_mp={CFG['n_mp']}, "
+                f"create_model(seed={CFG['seed']}) with processor output layers x10")
+    common = {"n": A.n, "nnz": A.nnz, "gnn": gnn_desc, "l2": "flushed (256 MiB write) before every timed step",
+              "parallelism": f"batch-parallel x{world} (weak), final NCCL gather to rank 0 when N > 1"}
+    if config == 3:
+        return {"workload": f"cfg3 wave-2d {k}x{k} jittered P1, A = M + dt^2 K_c (c = exp(GRF)), no Dirichlet "
+                            f"(n={A.n}, nnz={A.nnz}), {batch} distinct systems per GPU, each with its own L' "
+                            f"from the GNN (latent {CFG['width']}, {CFG['n_mp']} rounds), PCG rtol {CFG['rtol']}",
+                "systems_per_gpu": batch, **common}
+    return {"workload": f"cfg2 poisson-2d {k}x{k} jittered P1, Dirichlet-eliminated (n={A.n}, nnz={A.nnz}), "
+                        f"{batch} GRF right-hand sides per GPU, one shared L' from the GNN "
+                        f"(latent {CFG['width']}, {CFG['n_mp']} rounds) per step, PCG rtol {CFG['rtol']}",
+            "rhs_per_gpu": batch, **common}
+
+
+def gnn_flops(n, m, B, width=None, h=None, n_mp=None):
+    """FLOPs of one GNN forward (gnn.py:227-263; l = l_mp = 1, multiply-add = 2)
+    for B systems: encoders 1 -> h -> F, per round the aggregation (m F
+    multiply-adds) and the node (2F -> h_mp -> F) and edge (3F -> h_mp -> F)
+    MLPs, the edge decoder F -> h -> 1."""
+    F = width or CFG["width"]
+    h = h or CFG["h"]
+    R = n_mp or CFG["n_mp"]
+    enc = (n + m) * 2 * (h + h * F)
+    rnd = m * 2 * F + n * 2 * (2 * F * h + h * F) + m * 2 * (3 * F * h + h * F)
+    dec = m * 2 * (F * h + h)
+    return B * (enc + R * rnd + dec)
 
 
 # ---------------------------------------------------------------------------
@@ -127,7 +159,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def roofline(A, nnz_lower, prof, iters, peak_gbs, step_ms=None):
+def roofline(A, nnz_lower, prof, iters, peak_gbs, step_ms=None, distinct=False, pcg_ms=None):
     """Achieved algorithmic GB/s of the dominant kernel (ldlt_line_kernel:
     forward solve, y / D and backward solve in one launch) and of a whole PCG
     iteration.
@@ -145,15 +177,19 @@ def roofline(A, nnz_lower, prof, iters, peak_gbs, step_ms=None):
     nl = prof["kernel_launches"]["trsv_fwd"] + prof["kernel_launches"]["trsv_bwd"]
     ncol = len(iters)
     solves = col_iters + ncol  # every iteration plus the initial z = P^-1 r
-    trsv_bytes = nl * (2 * ML + 16 * n) + solves * 56 * n
+    if distinct:  # config 3: a factor (and D, 1/D) per system, read by each solve
+        trsv_bytes = solves * (2 * ML + 16 * n + 56 * n)
+    else:
+        trsv_bytes = nl * (2 * ML + 16 * n) + solves * 56 * n
     t_trsv = (prof["kernel_ms"]["trsv_fwd"] + prof["kernel_ms"]["trsv_bwd"]) * 1e-3
     achieved = trsv_bytes / t_trsv / 1e9
     M = 12 * nnz + 4 * (n + 1) + 2 * ML + 8 * n
-    iter_bytes = int(np.max(iters)) * M + col_iters * 104 * n
+    iter_bytes = (col_iters * (M + 104 * n)) if distinct else (int(np.max(iters)) * M + col_iters * 104 * n)
     # the batch runs as concurrent sub-batches (pcg.SPLIT_STREAMS): summed
-    # kernel time overstates the loop, the timed step (GNN included) does not
+    # kernel time overstates the loop, the timed step (GNN included) or the
+    # timed PCG call does not
     t_loop = sum(prof["kernel_ms"].values()) * 1e-3
-    t_iter = step_ms * 1e-3 if step_ms else t_loop
+    t_iter = step_ms * 1e-3 if step_ms else (pcg_ms * 1e-3 if pcg_ms else t_loop)
     iter_gbs = iter_bytes / t_iter / 1e9
     return {
         "kernel": "ldlt_line_kernel (forward solve + y/D + backward solve, one launch per pass)",
@@ -165,7 +201,8 @@ def roofline(A, nnz_lower, prof, iters, peak_gbs, step_ms=None):
         "pcg_iteration": {"achieved": round(iter_gbs, 1), "frac_of_measured": round(iter_gbs / peak_gbs, 4),
                           "frac_of_8TBs": round(iter_gbs / 8000.0, 4), "bytes": int(iter_bytes),
                           "time_ms": round(t_iter * 1e3, 3),
-                          "time_from": "timed step (GNN + whole batched solve)" if step_ms else "summed kernel time",
+                          "time_from": "timed step (GNN + whole batched solve)" if step_ms else
+                          ("timed PCG call" if pcg_ms else "summed kernel time"),
                           "summed_kernel_ms": round(t_loop * 1e3, 3), "streams": prof.get("streams", 1)},
         "kernel_ms": {k: round(v, 3) for k, v in prof["kernel_ms"].items()},
         "kernel_share": {k: round(v / max(sum(prof["kernel_ms"].values()), 1e-9), 4)
@@ -213,57 +250,110 @@ def _cpu_solve(j):
     return time.perf_counter() - t, rep.iterations, rep.converged
 
 
-def cpu_reference(prob, model, steps, warmup, cores=None):
-    """Reference path (oracle port of pcgkit: numpy GNN + sequential C
-    SpMV / SpTRSV, fp64) on the host: the GNN once with all BLAS threads,
-    then rounds of `cores` right-hand sides in parallel (one process per
-    core, single-threaded each -- the reference solve is sequential).
-    Step time = t_gnn + ceil(B / cores) * t_round, i.e. the full 64-RHS step
-    extrapolated from the measured round. Returns (value, info)."""
+def _cpu_system(j):
+    """Config 3 unit: build_learned + pcg_solve of system j (own A, b, L')."""
+    from oracle import port
+    prob, params, hp = _CPU["prob"], _CPU["params"], _CPU["hp"]
+    A = prob.A
+    t = time.perf_counter()
+    oA = port.Csr(A.n, A.row_ptr, A.col_idx, np.ascontiguousarray(prob.values[:, j]))
+    F = port.build_learned(hp, params, oA, prob.rhs[:, j])
+    x, rep = port.pcg_solve(oA, prob.rhs[:, j], F, thresholds=(CFG["rtol"],))
+    return time.perf_counter() - t, rep.iterations, rep.converged
+
+
+def _hyper():
+    from oracle import port
+    return port.Hyper(l=1, h=CFG["h"], n_mp=CFG["n_mp"], l_mp=1, h_mp=CFG["h"], width=CFG["width"])
+
+
+def cpu_reference(prob, model, steps, warmup, config=2, full_steps=True, cores=None):
+    """The reference path (oracle port of pcgkit: numpy GNN + sequential C
+    SpMV / SpTRSV, fp64) on the host cores, one process per core with one
+    BLAS thread each (the reference solve is sequential).
+
+    Config 2, full_steps: every timed step is the whole job -- the GNN once
+    (all BLAS threads) and all B right-hand sides solved in parallel --
+    measured wall clock. full_steps=False (the bounded cpu_baseline sample
+    of our arm's line): the GNN once and ONE round of `cores` right-hand
+    sides, step = t_gnn + ceil(B / cores) * t_round.
+    Config 3 (a unit is a whole system, GNN included): every step solves
+    `cores` systems in parallel (full_steps) or one system with all
+    threads (the bounded sample). Returns (value, cores, step_s, info)."""
     import multiprocessing as mp
     from oracle import port
     cores = cores or len(os.sched_getaffinity(0))
-    A = port.Csr(prob.A.n, prob.A.row_ptr, prob.A.col_idx, prob.A.values)
-    hp = port.Hyper(l=1, h=CFG["h"], n_mp=CFG["n_mp"], l_mp=1, h_mp=CFG["h"], width=CFG["width"])
-    t = time.perf_counter()
-    F = port.build_learned(hp, model.params, A, prob.rhs[:, 0])
-    t_gnn = time.perf_counter() - t
-    _CPU.update(A=A, F=F, rhs=prob.rhs)
-    B = prob.rhs.shape[1]
-    per_round = min(cores, B)
     ctx = mp.get_context("fork")
-    rounds = []
-    its = []
-    with ctx.Pool(per_round, initializer=_cpu_worker_init) as pool:
-        for s in range(warmup + steps):
-            cols = [(s * per_round + j) % B for j in range(per_round)]
+    B = prob.rhs.shape[1]
+    if config == 3:
+        _CPU.update(prob=prob, params=model.params, hp=_hyper())
+        if not full_steps:
             t = time.perf_counter()
-            res = pool.map(_cpu_solve, cols)
-            dt = time.perf_counter() - t
-            if s >= warmup:
-                rounds.append(dt)
-                its.extend(r[1] for r in res)
-    step_s = [t_gnn + math.ceil(B / per_round) * r for r in rounds]
-    value = B / statistics.mean(step_s)
-    info = {"t_gnn_s": round(t_gnn, 3), "t_round_s": round(statistics.mean(rounds), 3),
+            dt, it, conv = _cpu_system(0)
+            wall = time.perf_counter() - t
+            return 1.0 / wall, cores, [wall], {"systems_per_step": 1, "iterations_mean": float(it),
+                                                "threads": "all BLAS threads for the GNN"}
+        per = min(cores, B)
+        step_s, its = [], []
+        with ctx.Pool(per, initializer=_cpu_worker_init) as pool:
+            for s in range(warmup + steps):
+                cols = [(s * per + j) % B for j in range(per)]
+                t = time.perf_counter()
+                res = pool.map(_cpu_system, cols)
+                if s >= warmup:
+                    step_s.append(time.perf_counter() - t)
+                    its.extend(r[1] for r in res)
+        return per / statistics.mean(step_s), cores, step_s, {"systems_per_step": per,
+                                                              "iterations_mean": float(np.mean(its))}
+    A = port.Csr(prob.A.n, prob.A.row_ptr, prob.A.col_idx, prob.A.values)
+    hp = _hyper()
+    per_round = min(cores, B)
+    step_s, its, gnn_s, round_s = [], [], [], []
+    _CPU.update(A=A, rhs=prob.rhs)
+    for s in range(warmup + steps):
+        t = time.perf_counter()
+        F = port.build_learned(hp, model.params, A, prob.rhs[:, 0])
+        tg = time.perf_counter() - t
+        _CPU["F"] = F  # the workers, forked below, inherit the step's factor
+        cols = list(range(B)) if full_steps else [(s * per_round + j) % B for j in range(per_round)]
+        with ctx.Pool(per_round, initializer=_cpu_worker_init) as pool:
+            res = pool.map(_cpu_solve, cols, chunksize=1)
+        dt = time.perf_counter() - t
+        if s >= warmup:
+            gnn_s.append(tg)
+            round_s.append(dt - tg)
+            its.extend(r[1] for r in res)
+            step_s.append(dt if full_steps else tg + math.ceil(B / per_round) * (dt - tg))
+    info = {"t_gnn_s": round(statistics.mean(gnn_s), 3), "t_solves_s": round(statistics.mean(round_s), 3),
             "rhs_per_round": per_round, "iterations_mean": float(np.mean(its)) if its else None}
-    return value, cores, step_s, info
+    return B / statistics.mean(step_s), cores, step_s, info
+
+
+def _sizes(a):
+    k = a.k or (CFG3["k"] if a.config == 3 else CFG["k"])
+    batch = a.batch or (CFG3["batch"] if a.config == 3 else CFG["batch"])
+    return k, batch
 
 
 def reference_arm(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    prob, model = workload(a.k, a.batch)
-    value, cores, step_s, info = cpu_reference(prob, model, a.steps, a.warmup)
-    sample = (f"oracle port of the reference (numpy GNN + sequential C kernels, fp64): GNN once "
-              f"({info['t_gnn_s']} s, all BLAS threads) + {a.steps} timed rounds of {info['rhs_per_round']} "
-              f"RHS solved in parallel (1 process/core); step = GNN + ceil({a.batch}/{info['rhs_per_round']}) rounds")
+    k, batch = _sizes(a)
+    prob, model = workload(k, batch, config=a.config)
+    value, cores, step_s, info = cpu_reference(prob, model, a.steps, a.warmup, config=a.config, full_steps=True)
+    if a.config == 3:
+        sample = (f"oracle port of the reference (numpy GNN + sequential C kernels, fp64), one process per core: "
+                  f"each timed step solves {info['systems_per_step']} whole systems (GNN + PCG each) in parallel")
+    else:
+        sample = (f"oracle port of the reference (numpy GNN + sequential C kernels, fp64): every timed step is the "
+                  f"whole job -- the GNN once (all BLAS threads) then all {batch} right-hand sides solved on "
+                  f"{info['rhs_per_round']} processes (one per core); wall clock per step")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(statistics.mean(step_s) * 1e3, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(prob, a.k, a.batch, 1),
+            "config": config_dict(prob, k, batch, 1, a.config),
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": sample, **info},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -290,17 +380,31 @@ def main():
     torch.cuda.set_device(local)
 
     from paper_2305_16432_b200 import _native, gnn, pcg, sparse
-    prob, model = workload(a.k, a.batch, rank)
+    from paper_2305_16432_b200.dist import gather_solutions
+    cfg3 = a.config == 3
+    k, B = _sizes(a)
+    prob, model = workload(k, B, rank, config=a.config)
     A = prob.A
-    B = a.batch
     opts = pcg.SolveOptions(thresholds=(CFG["rtol"],))
     rhs_dev = torch.from_numpy(prob.rhs).cuda()
+    vals_dev = torch.from_numpy(prob.values).cuda() if cfg3 else None
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB
 
-    def step(profile=False):
-        P = gnn.build_learned(model, A, rhs_dev[:, 0])
-        X, reps = pcg.pcg_solve_batch(A, rhs_dev, P, opts, profile=profile)
+    def build(Am, rhs, vals):
+        if cfg3:
+            return gnn.build_learned_batch(model, Am, rhs, values=vals)
+        return gnn.build_learned(model, Am, rhs[:, 0])
+
+    def finish(X, reps):
+        # the job's result: every rank's solutions gathered to rank 0
+        if world > 1:
+            gather_solutions(X, [r.iterations for r in reps], [r.status for r in reps], B * world)
         return X, reps
+
+    def step(profile=False):
+        P = build(A, rhs_dev, vals_dev)
+        X, reps = pcg.pcg_solve_batch(A, rhs_dev, P, opts, values=vals_dev, profile=profile)
+        return finish(X, reps)
 
     def barrier():
         torch.cuda.synchronize()
@@ -308,18 +412,11 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
+    def reduce(x, op):
         if world == 1:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
     if a.profile_only:
@@ -347,59 +444,85 @@ def main():
     barrier()
     clk = clocks.stop() if clocks else None
     launches = lib.npcg_launch_count() - launches0
-    ms = max_over_ranks(statistics.mean(times))
+    ms = reduce(statistics.mean(times), dist.ReduceOp.MAX if world > 1 else None)
     value = B * world / (ms * 1e-3)
     iters = np.array([r.iterations for r in reps_all])
     converged = all(r.converged for r in reps_all)
 
-    # roofline: one profiled step (per-launch CUDA events, same stream)
+    # one profiled step: the GNN and the PCG timed apart (CUDA events on the
+    # solve stream), every PCG launch timed (roofline)
     flush.fill_(1.0)
     barrier()
-    P = gnn.build_learned(model, A, rhs_dev[:, 0])
-    pcg.pcg_solve_batch(A, rhs_dev, P, opts, profile=True)
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    P = build(A, rhs_dev, vals_dev)
+    g1.record()
+    g1.synchronize()
+    gnn_ms = g0.elapsed_time(g1)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record()
+    pcg.pcg_solve_batch(A, rhs_dev, P, opts, values=vals_dev, profile=True)
+    p1.record()
+    p1.synchronize()
+    pcg_ms = p0.elapsed_time(p1)
     prof = dict(pcg.LAST_PROFILE)
     nnz_lower = (A.nnz - A.n) // 2
-    roof = roofline(A, nnz_lower, prof, prof["iterations"], peak_hbm(), step_ms=ms)
+    roof = roofline(A, nnz_lower, prof, prof["iterations"], peak_hbm(), step_ms=None if cfg3 else ms,
+                    distinct=cfg3, pcg_ms=pcg_ms if cfg3 else None)
+    gflop = gnn_flops(A.n, A.nnz, B if cfg3 else 1) / 1e9
+    fp32_spec = 148 * 128 * 2 * 1.965e9 / 1e12
+    gnn_line = {"ms": round(gnn_ms, 3), "gflop": round(gflop, 1), "tflops": round(gflop / gnn_ms, 2),
+                "fp32_fma_spec_tflops": round(fp32_spec, 1), "frac_of_fp32_spec": round(gflop / gnn_ms / fp32_spec, 4),
+                "pcg_ms": round(pcg_ms, 3), "share_of_step": round(gnn_ms / (gnn_ms + pcg_ms), 4)}
 
     # e2e through the public API from pinned host buffers
     e2e = None
     if not a.no_e2e:
-        vals_pin = torch.from_numpy(A.values.copy()).pin_memory()
+        vals_pin = torch.from_numpy((prob.values if cfg3 else A.values).copy()).pin_memory()
         rhs_pin = torch.from_numpy(prob.rhs.copy()).pin_memory()
         b0_pin = torch.from_numpy(prob.rhs[:, 0].copy()).pin_memory()
         e2e_t = []
-        for s in range(a.warmup + a.steps):
+        for s_ in range(a.warmup + a.steps):
             flush.fill_(1.0)
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            Ah = sparse.SparseMatrixCsr(A.n, A.row_ptr, A.col_idx, vals_pin.numpy())
-            Ph = gnn.build_learned(model, Ah, b0_pin)
-            Xh, reps_h = pcg.pcg_solve_batch(Ah, rhs_pin, Ph, opts)  # host in -> host out
+            if cfg3:  # host values -> device (one copy), host rhs -> the API
+                vd = vals_pin.cuda(non_blocking=True)
+                Ph = gnn.build_learned_batch(model, A, rhs_pin, values=vd)
+                Xh, reps_h = pcg.pcg_solve_batch(A, rhs_pin, Ph, opts, values=vd)  # host rhs in -> host x out
+            else:
+                Ah = sparse.SparseMatrixCsr(A.n, A.row_ptr, A.col_idx, vals_pin.numpy())
+                Ph = gnn.build_learned(model, Ah, b0_pin)
+                Xh, reps_h = pcg.pcg_solve_batch(Ah, rhs_pin, Ph, opts)  # host in -> host out
             e1.record()
             e1.synchronize()
-            if s >= a.warmup:
+            if s_ >= a.warmup:
                 e2e_t.append(e0.elapsed_time(e1))
-        e2e_ms = max_over_ranks(statistics.mean(e2e_t))
+        e2e_ms = reduce(statistics.mean(e2e_t), dist.ReduceOp.MAX if world > 1 else None)
+        nv = prob.values.size if cfg3 else A.nnz
         e2e = {"value": round(B * world / (e2e_ms * 1e-3), 3), "unit": UNIT,
-               "h2d_bytes_per_step": int(A.nnz * 8 + A.n * B * 8 + A.n * 8),
+               "h2d_bytes_per_step": int(nv * 8 + A.n * B * 8 + (0 if cfg3 else A.n * 8)),
                "d2h_bytes_per_step": int(A.n * B * 8 + B * (int(iters.max()) + 1) * 8),
                "ms_per_step": round(e2e_ms, 3)}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        v, cores, step_s, info = cpu_reference(prob, model, steps=1, warmup=0)
-        cpu = {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"GNN once + one round of {info['rhs_per_round']} RHS on {cores} cores, "
-                         f"step extrapolated to {B} RHS", **info}
-    total_launches = int(sum_over_ranks(launches))
+        v, cores, step_s, info = cpu_reference(prob, model, steps=1, warmup=0, config=a.config, full_steps=False)
+        if cfg3:
+            sample = "one whole system (GNN with all BLAS threads + PCG), wall clock"
+        else:
+            sample = (f"GNN once + one round of {info['rhs_per_round']} RHS on {cores} processes, "
+                      f"step = t_gnn + ceil({B}/{info['rhs_per_round']}) * t_round")
+        cpu = {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "port", "sample": sample, **info}
+    total_launches = int(reduce(launches, dist.ReduceOp.SUM if world > 1 else None))
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded jittered mesh + GRF loads; seeded GNN weights)",
-                "config": config_dict(prob, a.k, B, world), "roofline": roof, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": total_launches, "clocks": clk,
+                "data": "synthetic (seeded jittered mesh + GRF loads / coefficients; seeded GNN weights)",
+                "config": config_dict(prob, k, B, world, a.config), "roofline": roof, "gnn": gnn_line,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": total_launches, "clocks": clk,
                 "iterations": {"min": int(iters.min()), "max": int(iters.max()), "mean": float(iters.mean())},
                 "all_converged": converged, "gnn_dtype": "f32", "pcg_dtype": "f64"}
         print(json.dumps(line), flush=True)

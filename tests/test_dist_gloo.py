@@ -64,3 +64,59 @@ def test_rank_streams_are_disjoint_and_reproducible():
     np.testing.assert_array_equal(c.rhs[:, :3], a.rhs)
     np.testing.assert_array_equal(c.rhs[:, 3:], b.rhs)  # rank 1's batch = streams 3..5
     assert not np.allclose(a.rhs, b.rhs)
+
+
+def _gather_worker(rank, world, port, total, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    from paper_2305_16432_b200 import _native
+    from paper_2305_16432_b200.dist import gather_solutions, shard
+    n = 7
+    lo, hi = shard(total, world, rank)
+    cols = np.arange(lo, hi)
+    # stand-in for this rank's solves: column j of the global batch is j * 100 + row
+    X = torch.from_numpy(np.stack([j * 100.0 + np.arange(n) for j in cols], axis=1).reshape(n, hi - lo))
+    its = cols + 10
+    status = np.where(cols % 3 == 2, _native.STATUS_MAXITER, _native.STATUS_CONVERGED)
+    g = gather_solutions(X, its, status, total)
+    if rank == 0:
+        out["X"] = g.X.numpy().copy()
+        out["its"] = g.iterations.copy()
+        out["status"] = g.status.copy()
+        out["conv"] = g.converged.copy()
+    else:
+        out[f"none{rank}"] = g is None
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [5, 6])
+def test_fixed_job_split_and_gather_order(total):
+    """A fixed job of `total` systems split over two ranks (uneven for 5):
+    rank 0 receives every column in global order with its iteration count
+    and status; the other rank receives nothing."""
+    from paper_2305_16432_b200 import _native
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gather_worker, args=(2, _free_port(), total, out), nprocs=2, join=True)
+    X = out["X"]
+    assert X.shape == (7, total)
+    for j in range(total):
+        np.testing.assert_array_equal(X[:, j], j * 100.0 + np.arange(7))
+    np.testing.assert_array_equal(out["its"], np.arange(total) + 10)
+    want = np.where(np.arange(total) % 3 == 2, _native.STATUS_MAXITER, _native.STATUS_CONVERGED)
+    np.testing.assert_array_equal(out["status"], want)
+    np.testing.assert_array_equal(out["conv"], want == _native.STATUS_CONVERGED)
+    assert out["none1"]
+
+
+def test_shard_covers_the_job():
+    from paper_2305_16432_b200.dist import shard
+    for total in (0, 1, 7, 32, 256, 257):
+        for world in (1, 2, 3, 8):
+            rs = [shard(total, world, r) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == total
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert max(h - l for l, h in rs) - min(h - l for l, h in rs) <= 1
+    with pytest.raises(ValueError):
+        shard(4, 2, 2)
