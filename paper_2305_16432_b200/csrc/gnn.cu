@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "gnn.cuh"
@@ -390,6 +391,19 @@ __global__ void diag_kernel(int n, int B, const int *dp, const double *A, int ab
     }
 }
 
+// tcgen05 edge update (gnn_tc.cu), F = H = 64; NPCG_GNN_TC=0 keeps the FFMA tiles
+cudaError_t launch_mp_edge_tc(int n, long long m, int B, const int *src, const int *col, const float *W1,
+                              const float *b1, const float *W2, const float *b2, float *e, const float *v,
+                              cudaStream_t s);
+static bool gnn_tc_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *env = std::getenv("NPCG_GNN_TC");
+        on = env ? std::atoi(env) != 0 : 1;
+    }
+    return on != 0;
+}
+
 // ---------------------------------------------------------------------------
 template <int F, int H, int TE>
 static cudaError_t run_rounds(const GnnDev &g, const Pattern &A, int B, float *e, float *v, float *v2,
@@ -412,6 +426,12 @@ static cudaError_t run_rounds(const GnnDev &g, const Pattern &A, int B, float *e
             n, m, B, A.rp, A.col, A.src, w + g.mp_node[r][0].w, w + g.mp_node[r][0].b, w + g.mp_node[r][1].w,
             w + g.mp_node[r][1].b, e, v, v2);
         std::swap(v, v2);
+        if (F == 64 && H == 64 && gnn_tc_enabled()) {
+            cudaError_t c = launch_mp_edge_tc(n, m, B, A.src, A.col, w + g.mp_edge[r][0].w, w + g.mp_edge[r][0].b,
+                                              w + g.mp_edge[r][1].w, w + g.mp_edge[r][1].b, e, v, s);
+            if (c != cudaSuccess) return c;
+            continue;
+        }
         note_launch(); mp_kernel<F, H, TE, false><<<ge, kGnnThreads, smem_edge, s>>>(
             n, m, B, A.rp, A.col, A.src, w + g.mp_edge[r][0].w, w + g.mp_edge[r][0].b, w + g.mp_edge[r][1].w,
             w + g.mp_edge[r][1].b, e, v, nullptr);

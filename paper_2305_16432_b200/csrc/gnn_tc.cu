@@ -1,0 +1,306 @@
+// gnn_tc.cu -- the GNN's edge update on the 5th-generation tensor cores
+// (tcgen05, sm_100a): e' = MLP([e | v_src | v_dst]) for latent F = 64,
+// hidden H = 64 (gnn.py:249-258 over autodiff.py:113-137).
+//
+// fp32 accuracy from TF32 tensor cores ("3xTF32"): every fp32 operand x is
+// split into x_hi = tf32(x) and x_lo = tf32(x - x_hi); a product is
+// a_hi b_hi + (a_hi b_lo + a_lo b_hi), the dropped a_lo b_lo term being
+// below fp32 rounding. The big and the correction terms accumulate in
+// separate TMEM columns and are added on the CUDA cores in the epilogue:
+// accumulated into one tensor-core sum the small terms lose their low bits
+// (measured: 1.4e-5 vs 2e-6 normwise error of M at config 2; separate
+// accumulators restore fp32-FMA accuracy). The reference computes in fp64;
+// L' parity (1e-5 normwise) is held by tests/test_gpu_parity.py.
+//
+// One persistent CTA per SM, 4 warps (128 threads = 128 edges of a tile,
+// thread t owns row t). Shared memory (1024-byte aligned, every operand in
+// the canonical K-major 128-byte-swizzle layout: 8-row groups 1024 B apart,
+// a row's 16-byte chunk j stored at chunk j ^ (row % 8)):
+//   W1^T hi / lo [64 x 192]  48 KB each  (B operand of layer 1)
+//   W2^T hi / lo [64 x 64]   16 KB each  (B operand of layer 2)
+//   two A buffers of one 32-wide K chunk, hi + lo [128 x 32] each (32 KB)
+// Per tile of 128 edges: the six K chunks of X = [e | v_src | v_dst] are
+// gathered, split and stored while the previous chunk's MMAs run
+// (double-buffered, completion via tcgen05.commit -> mbarrier); layer 1
+// accumulates H = X W1 in TMEM columns [0, 64) (big) and [64, 128)
+// (corrections); the epilogue adds them and b1, applies ReLU, splits H and
+// stores it as layer 2's A operand (both buffers); layer 2 accumulates
+// E = H W2 in columns [128, 192) / [192, 256); the final epilogue adds b2
+// and writes e in place.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gnn.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace npcg {
+
+namespace {
+
+constexpr int kTcRows = 128;            // edges per tile = UMMA M
+constexpr int kTcF = 64, kTcH = 64;     // latent width, processor hidden width
+constexpr int kTcK1 = 3 * kTcF;         // layer-1 fan-in
+constexpr int kAtomBytes = kTcRows * 128;  // one 32-wide K chunk of 128 rows (16 KB)
+
+// byte offsets in dynamic shared memory
+constexpr int kW1Hi = 0;
+constexpr int kW1Lo = kW1Hi + kTcH * kTcK1 * 4;  // 48 KB
+constexpr int kW2Hi = kW1Lo + kTcH * kTcK1 * 4;
+constexpr int kW2Lo = kW2Hi + kTcF * kTcH * 4;   // 16 KB
+constexpr int kABuf = kW2Lo + kTcF * kTcH * 4;   // 2 x (hi, lo) x 16 KB
+constexpr int kSmemTc = kABuf + 2 * 2 * kAtomBytes + 1024;  // + alignment slack
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// offset of (row r, 16-byte chunk j) in a [rows x 32 fp32] swizzled K-major block
+__device__ __forceinline__ uint32_t sw128(int r, int j) {
+    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
+}
+
+// smem matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;            // leading byte offset (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset
+    d |= (uint64_t)1 << 46;            // descriptor version (sm100)
+    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor: D fp32, A / B tf32, both K-major, M = 128, N = 64
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcH >> 3) << 17) |
+                            ((uint32_t)(kTcRows >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit(void *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 16 consecutive TMEM columns of this warp's 32 lanes -> 16 registers per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// store 32 consecutive fp32 values (one K chunk of one row) split hi / lo
+__device__ __forceinline__ void store_split(char *hi, char *lo, int r, const float4 (&x)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float4 h, l;
+        h.x = tf32_rna(x[j].x), l.x = tf32_rna(x[j].x - h.x);
+        h.y = tf32_rna(x[j].y), l.y = tf32_rna(x[j].y - h.y);
+        h.z = tf32_rna(x[j].z), l.z = tf32_rna(x[j].z - h.z);
+        h.w = tf32_rna(x[j].w), l.w = tf32_rna(x[j].w - h.w);
+        *reinterpret_cast<float4 *>(hi + sw128(r, j)) = h;
+        *reinterpret_cast<float4 *>(lo + sw128(r, j)) = l;
+    }
+}
+
+}  // namespace
+
+// e <- MLP_edge([e | v_src | v_dst]) for B systems (e [b][m][F], v [b][n][F]).
+__global__ void __launch_bounds__(128, 1) mp_edge_tc_kernel(int n, long long m, int B, const int *src, const int *col,
+                                                            const float *W1, const float *b1, const float *W2,
+                                                            const float *b2, float *e, const float *v) {
+    extern __shared__ __align__(1024) char smem_raw[];
+    char *sm = reinterpret_cast<char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t bar[3];  // A buffer 0 / 1 consumed, layer 2 done
+    __shared__ uint32_t s_tmem;
+    __shared__ float sb1[kTcH], sb2[kTcF];
+    const int t = threadIdx.x, warp = t >> 5;
+    // weights, transposed to [out][in] (the MMA's K-major B), split hi / lo
+    for (int q = t; q < kTcH * kTcK1; q += blockDim.x) {
+        const int o = q / kTcK1, i = q % kTcK1;  // W1 is [in][out]
+        const float w = W1[(size_t)i * kTcH + o], h = tf32_rna(w);
+        const uint32_t off = (uint32_t)(i / 32) * (kTcH * 128) + (uint32_t)((o >> 3) * 1024 + (o & 7) * 128 +
+                                                                          ((((i % 32) >> 2) ^ (o & 7)) << 4) + (i & 3) * 4);
+        *reinterpret_cast<float *>(sm + kW1Hi + off) = h;
+        *reinterpret_cast<float *>(sm + kW1Lo + off) = tf32_rna(w - h);
+    }
+    for (int q = t; q < kTcF * kTcH; q += blockDim.x) {
+        const int o = q / kTcH, i = q % kTcH;  // W2 is [in = H][out = F]
+        const float w = W2[(size_t)i * kTcF + o], h = tf32_rna(w);
+        const uint32_t off = (uint32_t)(i / 32) * (kTcF * 128) + (uint32_t)((o >> 3) * 1024 + (o & 7) * 128 +
+                                                                          ((((i % 32) >> 2) ^ (o & 7)) << 4) + (i & 3) * 4);
+        *reinterpret_cast<float *>(sm + kW2Hi + off) = h;
+        *reinterpret_cast<float *>(sm + kW2Lo + off) = tf32_rna(w - h);
+    }
+    for (int q = t; q < kTcH; q += blockDim.x) sb1[q] = b1[q];
+    for (int q = t; q < kTcF; q += blockDim.x) sb2[q] = b2[q];
+    if (t == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_proxy_async();  // weights (generic stores) -> tensor-core reads
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's TMEM lanes
+    const uint32_t a_base = smem_u32(sm + kABuf);
+    const uint32_t w1h = smem_u32(sm + kW1Hi), w1l = smem_u32(sm + kW1Lo);
+    const uint32_t w2h = smem_u32(sm + kW2Hi), w2l = smem_u32(sm + kW2Lo);
+    // A buffer u: hi at a_base + u * 2 * kAtomBytes, lo right after
+    auto abuf = [&](int u, int lo) { return sm + kABuf + (u * 2 + lo) * kAtomBytes; };
+    uint32_t use[2] = {0, 0}, ph2 = 0;  // completed-use counts (mbarrier parity)
+    const long long tiles_per = (m + kTcRows - 1) / kTcRows, tiles = tiles_per * B;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int b = (int)(tile / tiles_per);
+        const long long edge = (tile % tiles_per) * kTcRows + t;
+        const bool live = edge < m;
+        const float *eb = e + ((size_t)b * m) * kTcF;
+        const float *vb = v + ((size_t)b * n) * kTcF;
+        const float *xrow[3];
+        xrow[0] = eb + (size_t)(live ? edge : 0) * kTcF;
+        xrow[1] = vb + (size_t)(live ? src[edge] : 0) * kTcF;
+        xrow[2] = vb + (size_t)(live ? col[edge] : 0) * kTcF;
+        // ---- layer 1: six K chunks of 32, double-buffered ----
+        for (int c = 0; c < kTcK1 / 32; ++c) {
+            const int u = c & 1;
+            float4 x[8];
+            const float4 *p = reinterpret_cast<const float4 *>(xrow[c >> 1] + (c & 1) * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = live ? p[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (use[u] > 0) mbar_wait(&bar[u], (use[u] - 1) & 1);  // the MMAs that last read this buffer are done
+            store_split(abuf(u, 0), abuf(u, 1), t, x);
+            fence_proxy_async();
+            __syncthreads();
+            if (t == 0) {
+                tc_fence_after();
+                const uint32_t ah = a_base + (uint32_t)(u * 2) * kAtomBytes, al = ah + kAtomBytes;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t ko = (uint32_t)k * 32;
+                    const uint32_t bo = (uint32_t)c * (kTcH * 128) + ko;
+                    mma_tf32(tmem, sw128_desc(ah + ko), sw128_desc(w1h + bo), (c | k) != 0);
+                    mma_tf32(tmem + 64, sw128_desc(ah + ko), sw128_desc(w1l + bo), (c | k) != 0);
+                    mma_tf32(tmem + 64, sw128_desc(al + ko), sw128_desc(w1h + bo), 1);
+                }
+                mma_commit(&bar[u]);
+            }
+            ++use[u];
+        }
+        // every layer-1 MMA done (the last commit of each buffer)
+        mbar_wait(&bar[0], (use[0] - 1) & 1);
+        mbar_wait(&bar[1], (use[1] - 1) & 1);
+        tc_fence_after();
+        // ---- epilogue 1: H = relu(X W1 + b1) -> layer 2's A operand (K = 64: both buffers) ----
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float hv[16], hc[16];
+            tmem_ld16(tl + (uint32_t)(q * 16), hv);
+            tmem_ld16(tl + (uint32_t)(64 + q * 16), hc);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) hv[i] += hc[i];
+            float4 x[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                x[j] = make_float4(fmaxf(hv[4 * j] + sb1[q * 16 + 4 * j], 0.f), fmaxf(hv[4 * j + 1] + sb1[q * 16 + 4 * j + 1], 0.f),
+                                   fmaxf(hv[4 * j + 2] + sb1[q * 16 + 4 * j + 2], 0.f),
+                                   fmaxf(hv[4 * j + 3] + sb1[q * 16 + 4 * j + 3], 0.f));
+            const int u = q >> 1;  // hidden features 0..31 -> buffer 0, 32..63 -> buffer 1
+            char *hi = abuf(u, 0), *lo = abuf(u, 1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int jj = (q & 1) * 4 + j;  // 16-byte chunk within the 32-wide row
+                float4 h, l;
+                h.x = tf32_rna(x[j].x), l.x = tf32_rna(x[j].x - h.x);
+                h.y = tf32_rna(x[j].y), l.y = tf32_rna(x[j].y - h.y);
+                h.z = tf32_rna(x[j].z), l.z = tf32_rna(x[j].z - h.z);
+                h.w = tf32_rna(x[j].w), l.w = tf32_rna(x[j].w - h.w);
+                *reinterpret_cast<float4 *>(hi + sw128(t, jj)) = h;
+                *reinterpret_cast<float4 *>(lo + sw128(t, jj)) = l;
+            }
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        __syncthreads();
+        if (t == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int u = k >> 2;
+                const uint32_t ah = a_base + (uint32_t)(u * 2) * kAtomBytes + (uint32_t)(k & 3) * 32, al = ah + kAtomBytes;
+                const uint32_t bo = (uint32_t)u * (kTcF * 128) + (uint32_t)(k & 3) * 32;
+                mma_tf32(tmem + 128, sw128_desc(ah), sw128_desc(w2h + bo), k != 0);
+                mma_tf32(tmem + 192, sw128_desc(ah), sw128_desc(w2l + bo), k != 0);
+                mma_tf32(tmem + 192, sw128_desc(al), sw128_desc(w2h + bo), 1);
+            }
+            mma_commit(&bar[2]);
+        }
+        mbar_wait(&bar[2], ph2 & 1);
+        ++ph2;
+        // layer 2 read both A buffers: the next tile's chunk loads wait on this too
+        tc_fence_after();
+        // ---- epilogue 2: e = H W2 + b2, in place ----
+        float *eo = e + ((size_t)b * m + (size_t)(live ? edge : 0)) * kTcF;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float ov[16], oc[16];
+            tmem_ld16(tl + (uint32_t)(128 + q * 16), ov);
+            tmem_ld16(tl + (uint32_t)(192 + q * 16), oc);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) ov[i] += oc[i];
+            if (live) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    reinterpret_cast<float4 *>(eo)[q * 4 + j] =
+                        make_float4(ov[4 * j] + sb2[q * 16 + 4 * j], ov[4 * j + 1] + sb2[q * 16 + 4 * j + 1],
+                                    ov[4 * j + 2] + sb2[q * 16 + 4 * j + 2], ov[4 * j + 3] + sb2[q * 16 + 4 * j + 3]);
+            }
+        }
+        tc_fence_before();
+        __syncthreads();  // TMEM reads done before the next tile's MMAs overwrite it
+    }
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+size_t mp_edge_tc_smem() { return (size_t)kSmemTc; }
+
+cudaError_t launch_mp_edge_tc(int n, long long m, int B, const int *src, const int *col, const float *W1,
+                              const float *b1, const float *W2, const float *b2, float *e, const float *v,
+                              cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t c = cudaFuncSetAttribute(mp_edge_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTc);
+        if (c != cudaSuccess) return c;
+        configured = true;
+    }
+    const long long tiles = (m + kTcRows - 1) / kTcRows * B;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(tiles, num_sms()));
+    note_launch();
+    mp_edge_tc_kernel<<<grid, 128, kSmemTc, s>>>(n, m, B, src, col, W1, b1, W2, b2, e, v);
+    return cudaGetLastError();
+}
+
+}  // namespace npcg

@@ -48,7 +48,10 @@ namespace {
 
 // operand stages per warp (a slot is refilled the stage after its use): three
 // up to 3-tile stages, two for 4-tile stages (shared memory)
-__host__ __device__ constexpr int line_stages(int G) { return G >= 4 ? 2 : (G == 3 ? 3 : 4); }
+// (tiles per stage, stages in flight) combinations the kernel is built for
+__host__ __device__ constexpr bool line_shape_ok(int G, int NS) {
+    return (G == 4 && NS == 2) || (G == 2 && (NS == 3 || NS == 4)) || (G == 1 && NS == 4);
+}
 
 __host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
 
@@ -182,7 +185,7 @@ struct LineDirIO {
 // prepared operands (r_{k+1} or y / D, and the three factor kinds) from the
 // slot, takes the left neighbour's value by shuffle (lane 0: from the ring
 // written by the previous warp's lane 31), and leaves the result in the slot.
-template <bool UPPER, int G>
+template <bool UPPER, int G, int NS>
 __device__ __forceinline__ void line_solver(const LineDirIO &io, const int W, const int WL, const int R, const int wl,
                                             const int t, uint64_t *full, uint64_t *done, char *slots,
                                             const size_t slot_bytes, const bool trace_on) {
@@ -190,7 +193,6 @@ __device__ __forceinline__ void line_solver(const LineDirIO &io, const int W, co
     (void)trace_on;
     (void)wl_;
     constexpr int STEPS = kTileSteps * G;
-    constexpr int NS = line_stages(G);
     static_assert(2 * STEPS <= 32, "a stage pair's ring slots are checked by one warp");
     const int w = io.w;
     const int4 *meta = io.meta;
@@ -338,13 +340,12 @@ __device__ __forceinline__ void line_solver(const LineDirIO &io, const int W, co
 // area by a second bulk copy once y / D is formed). Returns this lane's dot
 // partial. Every loop over a stage is unrolled over its 2G chunks per lane:
 // the loads of a stage are in flight together.
-template <bool UPPER, bool PCG, int G>
+template <bool UPPER, bool PCG, int G, int NS>
 __device__ __forceinline__ double line_helper(const LineDirIO &io, const int t, const bool upd, const double alpha,
                                               uint64_t *tma, uint64_t *full, uint64_t *done, uint64_t *rtma,
                                               char *slots, const size_t slot_bytes, const int wl_, const bool trace_on) {
     (void)trace_on;
     (void)wl_;
-    constexpr int NS = line_stages(G);
     constexpr int K = 2 * G;  // double2 chunks per lane per stage (g * 64 chunks of a stage)
     const int4 me = io.meta[io.w];
     const int nt = me.y, tile0 = me.z;
@@ -518,12 +519,11 @@ __host__ __device__ inline LineSmem line_layout(int WL, int R, int G, int NS) {
 // for every system that iterates; the forward epilogue (which may turn the
 // system to the drift check, pcg.py:147) runs before the backward one at the
 // end, and the backward epilogue then ignores the solve (common.cuh).
-template <bool PCG, bool SB, int G, int C>
+template <bool PCG, bool SB, int G, int NS, int C>
 __global__ void __launch_bounds__(64 * line_cta_warps(C), 1) ldlt_line_kernel(LineArgs a) {
     extern __shared__ __align__(128) char sm[];
     __shared__ double s_red[2][kLineMaxWarps];
     __shared__ double s_cta[2][4];
-    constexpr int NS = line_stages(G);
     // WL line warps (+ WL helpers) per CTA; the last CTA of a cluster may hold idle pairs
     const int W = a.warps, WL = (W + C - 1) / C, R = a.ring;
     const int warp = threadIdx.x >> 5, t = threadIdx.x & 31;
@@ -594,14 +594,14 @@ __global__ void __launch_bounds__(64 * line_cta_warps(C), 1) ldlt_line_kernel(Li
         Bk.jbase = (F.meta[pw].y + G - 1) / G;
         if (helper) {
             const double alpha = upd ? a.st.alpha[b] : 0.0;
-            acc_f = line_helper<false, PCG, G>(F, t, upd, alpha, tma, full, done, rtma, slots, m.slot_bytes, wl, trace_on);
+            acc_f = line_helper<false, PCG, G, NS>(F, t, upd, alpha, tma, full, done, rtma, slots, m.slot_bytes, wl, trace_on);
             // the backward phase reads this warp's y (and r) stores through TMA
             fence_proxy_async_global();
             __syncwarp();
-            acc_b = line_helper<true, PCG, G>(Bk, t, false, 0.0, tma, full, done, rtma, slots, m.slot_bytes, wl, trace_on);
+            acc_b = line_helper<true, PCG, G, NS>(Bk, t, false, 0.0, tma, full, done, rtma, slots, m.slot_bytes, wl, trace_on);
         } else {
-            line_solver<false, G>(F, W, WL, R, wl, t, full, done, slots, m.slot_bytes, trace_on);
-            line_solver<true, G>(Bk, W, WL, R, wl, t, full, done, slots, m.slot_bytes, trace_on);
+            line_solver<false, G, NS>(F, W, WL, R, wl, t, full, done, slots, m.slot_bytes, trace_on);
+            line_solver<true, G, NS>(Bk, W, WL, R, wl, t, full, done, slots, m.slot_bytes, trace_on);
         }
     }
     if (PCG) {  // fixed-order reductions: lanes, helper warps, then the cluster's CTAs
@@ -672,22 +672,22 @@ int line_config_for(const LineSched &L, int B) {
     const int WL = (W + C - 1) / C;
     if (const char *env = std::getenv("NPCG_LINE_CFG")) {
         const int c = std::atoi(env), G = c / 16, NS = c % 16;
-        if (G >= 1 && G <= 4 && NS == line_stages(G) && line_smem(WL, R, G, NS) <= cap) return C * 256 + c;
+        if (line_shape_ok(G, NS) && line_smem(WL, R, G, NS) <= cap) return C * 256 + c;
     }
     // long stages first (the line warp's per-stage hand-offs amortise over 16
     // steps; measured 263 vs 249 systems/s against 8-step stages four deep at
     // config 2), then deeper pipelines of shorter stages
-    static const int prefs[][2] = {{4, line_stages(4)}, {2, line_stages(2)}, {3, line_stages(3)}, {1, line_stages(1)}};
+    static const int prefs[][2] = {{4, 2}, {2, 4}, {2, 3}, {1, 4}};
     for (const auto &p : prefs)
         if (line_smem(WL, R, p[0], p[1]) <= cap) return C * 256 + p[0] * 16 + p[1];
     return 0;
 }
 
-template <bool PCG, bool SB, int G, int C>
+template <bool PCG, bool SB, int G, int NS, int C>
 static cudaError_t launch_ldlt_t(const LineArgs &a, cudaStream_t s) {
-    auto kern = ldlt_line_kernel<PCG, SB, G, C>;
+    auto kern = ldlt_line_kernel<PCG, SB, G, NS, C>;
     const int WL = (a.warps + C - 1) / C;
-    const size_t smem = line_smem(WL, a.ring, G, a.stages);
+    const size_t smem = line_smem(WL, a.ring, G, NS);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -710,32 +710,32 @@ static cudaError_t launch_ldlt_t(const LineArgs &a, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <int G, int C>
+template <int G, int NS, int C>
 static cudaError_t launch_ldlt_gc(const LineArgs &a, cudaStream_t s) {
     const bool pcg = a.mode == TRSV_PCG;
-    if (pcg) return a.s_batched ? launch_ldlt_t<true, true, G, C>(a, s) : launch_ldlt_t<true, false, G, C>(a, s);
-    return a.s_batched ? launch_ldlt_t<false, true, G, C>(a, s) : launch_ldlt_t<false, false, G, C>(a, s);
+    if (pcg) return a.s_batched ? launch_ldlt_t<true, true, G, NS, C>(a, s) : launch_ldlt_t<true, false, G, NS, C>(a, s);
+    return a.s_batched ? launch_ldlt_t<false, true, G, NS, C>(a, s) : launch_ldlt_t<false, false, G, NS, C>(a, s);
+}
+
+template <int C>
+static cudaError_t launch_ldlt_c(const LineArgs &a, cudaStream_t s) {
+    switch (a.group * 16 + a.stages) {
+        case 4 * 16 + 2: return launch_ldlt_gc<4, 2, C>(a, s);
+        case 2 * 16 + 4: return launch_ldlt_gc<2, 4, C>(a, s);
+        case 2 * 16 + 3: return launch_ldlt_gc<2, 3, C>(a, s);
+        case 1 * 16 + 4: return launch_ldlt_gc<1, 4, C>(a, s);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t launch_ldlt_line(const LineArgs &a, cudaStream_t s) {
-    if (a.group < 1 || a.group > 4 || a.stages != line_stages(a.group) || a.warps < 1 ||
-        (a.cluster != 1 && a.cluster != 2 && a.cluster != 4) ||
+    if (!line_shape_ok(a.group, a.stages) || a.warps < 1 || (a.cluster != 1 && a.cluster != 2 && a.cluster != 4) ||
         (a.warps + a.cluster - 1) / a.cluster > line_cta_warps(a.cluster))
         return cudaErrorInvalidValue;
-    switch (a.cluster * 16 + a.group) {
-        case 16 + 1: return launch_ldlt_gc<1, 1>(a, s);
-        case 16 + 2: return launch_ldlt_gc<2, 1>(a, s);
-        case 16 + 3: return launch_ldlt_gc<3, 1>(a, s);
-        case 16 + 4: return launch_ldlt_gc<4, 1>(a, s);
-        case 32 + 1: return launch_ldlt_gc<1, 2>(a, s);
-        case 32 + 2: return launch_ldlt_gc<2, 2>(a, s);
-        case 32 + 3: return launch_ldlt_gc<3, 2>(a, s);
-        case 32 + 4: return launch_ldlt_gc<4, 2>(a, s);
-        case 64 + 1: return launch_ldlt_gc<1, 4>(a, s);
-        case 64 + 2: return launch_ldlt_gc<2, 4>(a, s);
-        case 64 + 3: return launch_ldlt_gc<3, 4>(a, s);
-        case 64 + 4: return launch_ldlt_gc<4, 4>(a, s);
-        default: return cudaErrorInvalidValue;
+    switch (a.cluster) {
+        case 1: return launch_ldlt_c<1>(a, s);
+        case 2: return launch_ldlt_c<2>(a, s);
+        default: return launch_ldlt_c<4>(a, s);
     }
 }
 
