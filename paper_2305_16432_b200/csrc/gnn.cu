@@ -395,6 +395,9 @@ __global__ void diag_kernel(int n, int B, const int *dp, const double *A, int ab
 cudaError_t launch_mp_edge_tc(int n, long long m, int B, const int *src, const int *col, const float *W1,
                               const float *b1, const float *W2, const float *b2, float *e, const float *v,
                               cudaStream_t s);
+cudaError_t launch_mp_node_tc(int n, long long m, int B, const int *rp, const int *col, const float *W1,
+                              const float *b1, const float *W2, const float *b2, const float *e, const float *v,
+                              float *v_out, cudaStream_t s);
 static bool gnn_tc_enabled() {
     static int on = -1;
     if (on < 0) {
@@ -420,13 +423,20 @@ static cudaError_t run_rounds(const GnnDev &g, const Pattern &A, int B, float *e
     const long long tn = ((long long)n + TE - 1) / TE * B, te = (m + TE - 1) / TE * B;
     const int gn = (int)std::max<long long>(1, std::min<long long>(tn, (long long)std::max(occ_n, 1) * num_sms()));
     const int ge = (int)std::max<long long>(1, std::min<long long>(te, (long long)std::max(occ_e, 1) * num_sms()));
+    const bool tc = F == 64 && H == 64 && gnn_tc_enabled();
     for (int r = 0; r < g.d.n_mp; ++r) {
         const float *w = g.w;
-        note_launch(); mp_kernel<F, H, TE, true><<<gn, kGnnThreads, smem_node, s>>>(
-            n, m, B, A.rp, A.col, A.src, w + g.mp_node[r][0].w, w + g.mp_node[r][0].b, w + g.mp_node[r][1].w,
-            w + g.mp_node[r][1].b, e, v, v2);
+        if (tc) {
+            cudaError_t c = launch_mp_node_tc(n, m, B, A.rp, A.col, w + g.mp_node[r][0].w, w + g.mp_node[r][0].b,
+                                              w + g.mp_node[r][1].w, w + g.mp_node[r][1].b, e, v, v2, s);
+            if (c != cudaSuccess) return c;
+        } else {
+            note_launch(); mp_kernel<F, H, TE, true><<<gn, kGnnThreads, smem_node, s>>>(
+                n, m, B, A.rp, A.col, A.src, w + g.mp_node[r][0].w, w + g.mp_node[r][0].b, w + g.mp_node[r][1].w,
+                w + g.mp_node[r][1].b, e, v, v2);
+        }
         std::swap(v, v2);
-        if (F == 64 && H == 64 && gnn_tc_enabled()) {
+        if (tc) {
             cudaError_t c = launch_mp_edge_tc(n, m, B, A.src, A.col, w + g.mp_edge[r][0].w, w + g.mp_edge[r][0].b,
                                               w + g.mp_edge[r][1].w, w + g.mp_edge[r][1].b, e, v, s);
             if (c != cudaSuccess) return c;

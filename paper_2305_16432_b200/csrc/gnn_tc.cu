@@ -1,32 +1,40 @@
-// gnn_tc.cu -- the GNN's edge update on the 5th-generation tensor cores
-// (tcgen05, sm_100a): e' = MLP([e | v_src | v_dst]) for latent F = 64,
-// hidden H = 64 (gnn.py:249-258 over autodiff.py:113-137).
+// gnn_tc.cu -- the GNN's message-passing MLPs on the 5th-generation tensor
+// cores (tcgen05, sm_100a) for latent F = 64, hidden H = 64 (gnn.py:249-258
+// over autodiff.py:113-137, 174-243):
+//   node update  v' = MLP([v | agg]),  agg_i = sum_{p in row i} e_p * v_col(p)
+//   edge update  e' = MLP([e | v_src | v_dst])
 //
 // fp32 accuracy from TF32 tensor cores ("3xTF32"): every fp32 operand x is
 // split into x_hi = tf32(x) and x_lo = tf32(x - x_hi); a product is
 // a_hi b_hi + (a_hi b_lo + a_lo b_hi), the dropped a_lo b_lo term being
-// below fp32 rounding. The big and the correction terms accumulate in
-// separate TMEM columns and are added on the CUDA cores in the epilogue:
-// accumulated into one tensor-core sum the small terms lose their low bits
-// (measured: 1.4e-5 vs 2e-6 normwise error of M at config 2; separate
-// accumulators restore fp32-FMA accuracy). The reference computes in fp64;
-// L' parity (1e-5 normwise) is held by tests/test_gpu_parity.py.
+// below fp32 rounding. The tensor core's own accumulation loses low bits
+// (it does not round to nearest), so nothing long accumulates inside it:
+// every 32-wide K chunk's big terms get a fresh TMEM accumulator, the
+// correction terms one of their own, and the epilogue adds them on the
+// CUDA cores in fixed order with fp32 round-to-nearest. Measured normwise
+// error of the edge outputs M against the fp64 oracle at config 2: one
+// tensor-core accumulator 1.4e-5, big / correction split 1.1e-5 with both
+// MLPs on the tensor cores, per-chunk accumulators (this) -- see DESIGN.md;
+// the FFMA tiles give 2e-6. L' parity (1e-5 normwise) is held by
+// tests/test_gpu_parity.py and tests/test_gpu_fullsize.py.
 //
-// One persistent CTA per SM, 4 warps (128 threads = 128 edges of a tile,
-// thread t owns row t). Shared memory (1024-byte aligned, every operand in
-// the canonical K-major 128-byte-swizzle layout: 8-row groups 1024 B apart,
-// a row's 16-byte chunk j stored at chunk j ^ (row % 8)):
-//   W1^T hi / lo [64 x 192]  48 KB each  (B operand of layer 1)
-//   W2^T hi / lo [64 x 64]   16 KB each  (B operand of layer 2)
+// One persistent CTA per SM, 4 warps (128 threads = the 128 rows -- edges or
+// nodes -- of a tile, thread t owns row t). Shared memory (1024-byte
+// aligned, every operand in the canonical K-major 128-byte-swizzle layout:
+// 8-row groups 1024 B apart, a row's 16-byte chunk j stored at chunk
+// j ^ (row % 8)):
+//   W1^T hi / lo [64 x K1]  (K1 = 192 edge / 128 node; B operand of layer 1)
+//   W2^T hi / lo [64 x 64]  16 KB each  (B operand of layer 2)
 //   two A buffers of one 32-wide K chunk, hi + lo [128 x 32] each (32 KB)
-// Per tile of 128 edges: the six K chunks of X = [e | v_src | v_dst] are
+// Per tile: the K chunks of X ([e | v_src | v_dst], or [v | agg] with agg
+// formed by the row's thread from its CSR row in stored order) are
 // gathered, split and stored while the previous chunk's MMAs run
 // (double-buffered, completion via tcgen05.commit -> mbarrier); layer 1
-// accumulates H = X W1 in TMEM columns [0, 64) (big) and [64, 128)
-// (corrections); the epilogue adds them and b1, applies ReLU, splits H and
-// stores it as layer 2's A operand (both buffers); layer 2 accumulates
-// E = H W2 in columns [128, 192) / [192, 256); the final epilogue adds b2
-// and writes e in place.
+// accumulates chunk c's big terms in TMEM columns [64 c, 64 c + 64) and all
+// corrections in [448, 512); the epilogue sums them with b1, applies ReLU,
+// splits H and stores it as layer 2's A operand (both buffers); layer 2
+// accumulates in columns [0, 128) (two chunks) and [128, 192); the final
+// epilogue adds b2 and writes e in place (edge) or v_out (node).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -41,16 +49,20 @@ namespace {
 
 constexpr int kTcRows = 128;            // edges per tile = UMMA M
 constexpr int kTcF = 64, kTcH = 64;     // latent width, processor hidden width
-constexpr int kTcK1 = 3 * kTcF;         // layer-1 fan-in
+template <bool NODE>
+constexpr int tc_k1() { return NODE ? 2 * kTcF : 3 * kTcF; }  // layer-1 fan-in
 constexpr int kAtomBytes = kTcRows * 128;  // one 32-wide K chunk of 128 rows (16 KB)
 
 // byte offsets in dynamic shared memory
-constexpr int kW1Hi = 0;
-constexpr int kW1Lo = kW1Hi + kTcH * kTcK1 * 4;  // 48 KB
-constexpr int kW2Hi = kW1Lo + kTcH * kTcK1 * 4;
-constexpr int kW2Lo = kW2Hi + kTcF * kTcH * 4;   // 16 KB
-constexpr int kABuf = kW2Lo + kTcF * kTcH * 4;   // 2 x (hi, lo) x 16 KB
-constexpr int kSmemTc = kABuf + 2 * 2 * kAtomBytes + 1024;  // + alignment slack
+template <bool NODE>
+struct TcSmem {
+    static constexpr int W1Hi = 0;
+    static constexpr int W1Lo = W1Hi + kTcH * tc_k1<NODE>() * 4;
+    static constexpr int W2Hi = W1Lo + kTcH * tc_k1<NODE>() * 4;
+    static constexpr int W2Lo = W2Hi + kTcF * kTcH * 4;
+    static constexpr int ABuf = W2Lo + kTcF * kTcH * 4;      // 2 x (hi, lo) x 16 KB
+    static constexpr int Total = ABuf + 2 * 2 * kAtomBytes + 1024;  // + alignment slack
+};
 
 __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;
@@ -123,10 +135,16 @@ __device__ __forceinline__ void store_split(char *hi, char *lo, int r, const flo
 
 }  // namespace
 
-// e <- MLP_edge([e | v_src | v_dst]) for B systems (e [b][m][F], v [b][n][F]).
-__global__ void __launch_bounds__(128, 1) mp_edge_tc_kernel(int n, long long m, int B, const int *src, const int *col,
-                                                            const float *W1, const float *b1, const float *W2,
-                                                            const float *b2, float *e, const float *v) {
+// EDGE: e <- MLP_edge([e | v_src | v_dst]); NODE: v_out <- MLP_node([v | agg]),
+// for B systems (e [b][m][F], v / v_out [b][n][F]).
+template <bool NODE>
+__global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B, const int *rp, const int *src,
+                                                       const int *col, const float *W1, const float *b1,
+                                                       const float *W2, const float *b2, float *e, const float *v,
+                                                       float *v_out) {
+    constexpr int kTcK1 = tc_k1<NODE>();
+    using L = TcSmem<NODE>;
+    constexpr int kW1Hi = L::W1Hi, kW1Lo = L::W1Lo, kW2Hi = L::W2Hi, kW2Lo = L::W2Lo, kABuf = L::ABuf;
     extern __shared__ __align__(1024) char smem_raw[];
     char *sm = reinterpret_cast<char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     __shared__ uint64_t bar[3];  // A buffer 0 / 1 consumed, layer 2 done
@@ -157,7 +175,7 @@ __global__ void __launch_bounds__(128, 1) mp_edge_tc_kernel(int n, long long m, 
         fence_mbar_init();
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     fence_proxy_async();  // weights (generic stores) -> tensor-core reads
@@ -172,26 +190,63 @@ __global__ void __launch_bounds__(128, 1) mp_edge_tc_kernel(int n, long long m, 
     // A buffer u: hi at a_base + u * 2 * kAtomBytes, lo right after
     auto abuf = [&](int u, int lo) { return sm + kABuf + (u * 2 + lo) * kAtomBytes; };
     uint32_t use[2] = {0, 0}, ph2 = 0;  // completed-use counts (mbarrier parity)
-    const long long tiles_per = (m + kTcRows - 1) / kTcRows, tiles = tiles_per * B;
+    const long long items = NODE ? (long long)n : m;
+    const long long tiles_per = (items + kTcRows - 1) / kTcRows, tiles = tiles_per * B;
     for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int b = (int)(tile / tiles_per);
-        const long long edge = (tile % tiles_per) * kTcRows + t;
-        const bool live = edge < m;
+        const long long item = (tile % tiles_per) * kTcRows + t;
+        const bool live = item < items;
+        const long long it = live ? item : 0;
         const float *eb = e + ((size_t)b * m) * kTcF;
         const float *vb = v + ((size_t)b * n) * kTcF;
         const float *xrow[3];
-        xrow[0] = eb + (size_t)(live ? edge : 0) * kTcF;
-        xrow[1] = vb + (size_t)(live ? src[edge] : 0) * kTcF;
-        xrow[2] = vb + (size_t)(live ? col[edge] : 0) * kTcF;
-        // ---- layer 1: six K chunks of 32, double-buffered ----
+        int p0 = 0, p1 = 0;
+        if (NODE) {
+            xrow[0] = vb + (size_t)it * kTcF;
+            p0 = live ? rp[it] : 0;
+            p1 = live ? rp[it + 1] : 0;
+        } else {
+            xrow[0] = eb + (size_t)it * kTcF;
+            xrow[1] = vb + (size_t)(live ? src[it] : 0) * kTcF;
+            xrow[2] = vb + (size_t)(live ? col[it] : 0) * kTcF;
+        }
+        // chunk c of this row's input: 32 consecutive features
+        auto load_chunk = [&](int c, float4 (&x)[8]) {
+            if (!NODE || c < 2) {
+                const float4 *p = reinterpret_cast<const float4 *>(xrow[c >> 1] + (c & 1) * 32);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) x[j] = live ? p[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {  // agg_i = sum_p e_p * v_col(p), CSR order (autodiff.py:174, 209, 221-243)
+                const int f0 = (c & 1) * 32;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) x[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 2
+                for (int p = p0; p < p1; ++p) {
+                    const float4 *ep = reinterpret_cast<const float4 *>(eb + (size_t)p * kTcF + f0);
+                    const float4 *vp = reinterpret_cast<const float4 *>(vb + (size_t)col[p] * kTcF + f0);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 a = ep[j], q = vp[j];
+                        x[j].x = fmaf(a.x, q.x, x[j].x);
+                        x[j].y = fmaf(a.y, q.y, x[j].y);
+                        x[j].z = fmaf(a.z, q.z, x[j].z);
+                        x[j].w = fmaf(a.w, q.w, x[j].w);
+                    }
+                }
+            }
+        };
+        // ---- layer 1: K chunks of 32, double-buffered, loads one chunk ahead ----
+        float4 xa[8];
+        load_chunk(0, xa);
+#pragma unroll 1
         for (int c = 0; c < kTcK1 / 32; ++c) {
             const int u = c & 1;
-            float4 x[8];
-            const float4 *p = reinterpret_cast<const float4 *>(xrow[c >> 1] + (c & 1) * 32);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = live ? p[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 xb[8];
+            if (c + 1 < kTcK1 / 32) load_chunk(c + 1, xb);
             if (use[u] > 0) mbar_wait(&bar[u], (use[u] - 1) & 1);  // the MMAs that last read this buffer are done
-            store_split(abuf(u, 0), abuf(u, 1), t, x);
+            store_split(abuf(u, 0), abuf(u, 1), t, xa);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xa[j] = xb[j];
             fence_proxy_async();
             __syncthreads();
             if (t == 0) {
@@ -201,9 +256,9 @@ __global__ void __launch_bounds__(128, 1) mp_edge_tc_kernel(int n, long long m, 
                 for (int k = 0; k < 4; ++k) {
                     const uint32_t ko = (uint32_t)k * 32;
                     const uint32_t bo = (uint32_t)c * (kTcH * 128) + ko;
-                    mma_tf32(tmem, sw128_desc(ah + ko), sw128_desc(w1h + bo), (c | k) != 0);
-                    mma_tf32(tmem + 64, sw128_desc(ah + ko), sw128_desc(w1l + bo), (c | k) != 0);
-                    mma_tf32(tmem + 64, sw128_desc(al + ko), sw128_desc(w1h + bo), 1);
+                    mma_tf32(tmem + 64 * c, sw128_desc(ah + ko), sw128_desc(w1h + bo), k != 0);
+                    mma_tf32(tmem + 448, sw128_desc(ah + ko), sw128_desc(w1l + bo), (c | k) != 0);
+                    mma_tf32(tmem + 448, sw128_desc(al + ko), sw128_desc(w1h + bo), 1);
                 }
                 mma_commit(&bar[u]);
             }
@@ -218,7 +273,13 @@ __global__ void __launch_bounds__(128, 1) mp_edge_tc_kernel(int n, long long m, 
         for (int q = 0; q < 4; ++q) {
             float hv[16], hc[16];
             tmem_ld16(tl + (uint32_t)(q * 16), hv);
-            tmem_ld16(tl + (uint32_t)(64 + q * 16), hc);
+#pragma unroll
+            for (int c = 1; c < kTcK1 / 32; ++c) {
+                tmem_ld16(tl + (uint32_t)(64 * c + q * 16), hc);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) hv[i] += hc[i];
+            }
+            tmem_ld16(tl + (uint32_t)(448 + q * 16), hc);
 #pragma unroll
             for (int i = 0; i < 16; ++i) hv[i] += hc[i];
             float4 x[4];
@@ -251,9 +312,9 @@ __global__ void __launch_bounds__(128, 1) mp_edge_tc_kernel(int n, long long m, 
                 const int u = k >> 2;
                 const uint32_t ah = a_base + (uint32_t)(u * 2) * kAtomBytes + (uint32_t)(k & 3) * 32, al = ah + kAtomBytes;
                 const uint32_t bo = (uint32_t)u * (kTcF * 128) + (uint32_t)(k & 3) * 32;
-                mma_tf32(tmem + 128, sw128_desc(ah), sw128_desc(w2h + bo), k != 0);
-                mma_tf32(tmem + 192, sw128_desc(ah), sw128_desc(w2l + bo), k != 0);
-                mma_tf32(tmem + 192, sw128_desc(al), sw128_desc(w2h + bo), 1);
+                mma_tf32(tmem + 64 * u, sw128_desc(ah), sw128_desc(w2h + bo), (k & 3) != 0);
+                mma_tf32(tmem + 128, sw128_desc(ah), sw128_desc(w2l + bo), k != 0);
+                mma_tf32(tmem + 128, sw128_desc(al), sw128_desc(w2h + bo), 1);
             }
             mma_commit(&bar[2]);
         }
@@ -261,13 +322,16 @@ __global__ void __launch_bounds__(128, 1) mp_edge_tc_kernel(int n, long long m, 
         ++ph2;
         // layer 2 read both A buffers: the next tile's chunk loads wait on this too
         tc_fence_after();
-        // ---- epilogue 2: e = H W2 + b2, in place ----
-        float *eo = e + ((size_t)b * m + (size_t)(live ? edge : 0)) * kTcF;
+        // ---- epilogue 2: e = H W2 + b2 in place | v_out = H W2 + b2 ----
+        float *eo = NODE ? v_out + ((size_t)b * n + (size_t)it) * kTcF : e + ((size_t)b * m + (size_t)it) * kTcF;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             float ov[16], oc[16];
-            tmem_ld16(tl + (uint32_t)(128 + q * 16), ov);
-            tmem_ld16(tl + (uint32_t)(192 + q * 16), oc);
+            tmem_ld16(tl + (uint32_t)(q * 16), ov);
+            tmem_ld16(tl + (uint32_t)(64 + q * 16), oc);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) ov[i] += oc[i];
+            tmem_ld16(tl + (uint32_t)(128 + q * 16), oc);
 #pragma unroll
             for (int i = 0; i < 16; ++i) ov[i] += oc[i];
             if (live) {
@@ -282,25 +346,38 @@ __global__ void __launch_bounds__(128, 1) mp_edge_tc_kernel(int n, long long m, 
         __syncthreads();  // TMEM reads done before the next tile's MMAs overwrite it
     }
     tc_fence_after();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-size_t mp_edge_tc_smem() { return (size_t)kSmemTc; }
+template <bool NODE>
+static cudaError_t launch_mp_tc_t(int n, long long m, int B, const int *rp, const int *src, const int *col,
+                                  const float *W1, const float *b1, const float *W2, const float *b2, float *e,
+                                  const float *v, float *v_out, cudaStream_t s) {
+    static bool configured = false;
+    const int smem = TcSmem<NODE>::Total;
+    if (!configured) {
+        cudaError_t c = cudaFuncSetAttribute(mp_tc_kernel<NODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (c != cudaSuccess) return c;
+        configured = true;
+    }
+    const long long items = NODE ? (long long)n : m;
+    const long long tiles = (items + kTcRows - 1) / kTcRows * B;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(tiles, num_sms()));
+    note_launch();
+    mp_tc_kernel<NODE><<<grid, 128, smem, s>>>(n, m, B, rp, src, col, W1, b1, W2, b2, e, v, v_out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_mp_edge_tc(int n, long long m, int B, const int *src, const int *col, const float *W1,
                               const float *b1, const float *W2, const float *b2, float *e, const float *v,
                               cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t c = cudaFuncSetAttribute(mp_edge_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTc);
-        if (c != cudaSuccess) return c;
-        configured = true;
-    }
-    const long long tiles = (m + kTcRows - 1) / kTcRows * B;
-    const int grid = (int)std::max<long long>(1, std::min<long long>(tiles, num_sms()));
-    note_launch();
-    mp_edge_tc_kernel<<<grid, 128, kSmemTc, s>>>(n, m, B, src, col, W1, b1, W2, b2, e, v);
-    return cudaGetLastError();
+    return launch_mp_tc_t<false>(n, m, B, nullptr, src, col, W1, b1, W2, b2, e, v, nullptr, s);
+}
+
+cudaError_t launch_mp_node_tc(int n, long long m, int B, const int *rp, const int *col, const float *W1,
+                              const float *b1, const float *W2, const float *b2, const float *e, const float *v,
+                              float *v_out, cudaStream_t s) {
+    return launch_mp_tc_t<true>(n, m, B, rp, nullptr, col, W1, b1, W2, b2, const_cast<float *>(e), v, v_out, s);
 }
 
 }  // namespace npcg
