@@ -135,6 +135,13 @@ typedef struct {
     int32_t n_mp;         /* message-passing rounds */
     int32_t normalize;    /* GnnHyperParams.normalize */
     int32_t with_x0_head; /* node_dec present in the weight blob */
+    /* BASELINE.json north_star extensions (0 = the reference network):
+     * node inputs (b_i, boundary flag), edge inputs (A_ij, d_1..d_dim, |d|),
+     * LayerNorm (gain, shift; appended to the blob after all layers, in the
+     * order node_enc, edge_enc, mp0.node, mp0.edge, ...) after every encoder
+     * and processor MLP, and the factor P = L L^T with L_ii = exp(M_ii). */
+    int32_t north_star;
+    int32_t dim;          /* mesh dimension of the edge geometry (2 or 3) */
 } npcg_gnn_desc;
 int npcg_gnn_create(const npcg_gnn_desc *desc, const double *weights_host,
                     int64_t n_weights, npcg_gnn **out);
@@ -150,6 +157,18 @@ int npcg_gnn_build_factor(const npcg_gnn *g, const npcg_pattern *A, int B,
                           const double *A_vals, int A_batched, const double *rhs,
                           double *S, double *D, double *edge_out, double *x0_out,
                           int64_t *pivot, void *stream);
+
+/* build_learned(model, A, b, mesh) in north_star mode (no reference
+ * function: the extension of gnn.py:314-318 BASELINE.json names). pos
+ * [n][dim] and boundary [n] (0 / 1) are device arrays shared by the batch
+ * (one mesh). Writes the factor in the solver's unit-lower LDL^T form:
+ * S = L diag(L)^-1 on the symmetric pattern, D = diag(L)^2, so
+ * P = L L^T = (I + S) D (I + S)^T. NPCG_ERR_INVALID_FACTOR when L has
+ * non-finite entries. */
+int npcg_gnn_build_factor_mesh(const npcg_gnn *g, const npcg_pattern *A, int B,
+                               const double *A_vals, int A_batched, const double *rhs,
+                               const double *pos, const double *boundary,
+                               double *S, double *D, double *edge_out, int64_t *pivot, void *stream);
 
 /* ---- PCG (pcg.py:75-176) ---------------------------------------------------- */
 typedef struct {

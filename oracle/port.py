@@ -200,10 +200,25 @@ def graph_from_system(A, b):
 
 
 class Hyper:
+    """mode "reference": pcgkit's network (gnn.py:106-147). mode
+    "north_star": BASELINE.json's extensions -- node inputs (b_i, boundary
+    flag), edge inputs (A_ij, d_1..d_dim, |d|) with d = x_dst - x_src,
+    LayerNorm after every encoder / processor MLP, and a factor L with an
+    exponentiated diagonal, P = L L^T (no reference code pins these: this
+    restatement is their only oracle -- "parity unpinned")."""
+
     def __init__(self, l=1, h=16, n_mp=5, l_mp=1, h_mp=16, with_x0_head=False,
-                 normalize=True, width=16):
+                 normalize=True, width=16, mode="reference", dim=2):
         self.l, self.h, self.n_mp, self.l_mp, self.h_mp = l, h, n_mp, l_mp, h_mp
         self.with_x0_head, self.normalize, self.width = with_x0_head, normalize, width
+        self.mode, self.dim = mode, dim
+
+    @property
+    def north_star(self):
+        return self.mode == "north_star"
+
+
+LN_EPS = 1e-5
 
 
 def layer_specs(hp):
@@ -216,8 +231,9 @@ def layer_specs(hp):
             out.append((f"{prefix}.{k}", dims[k], dims[k + 1]))
 
     F = hp.width
-    stack("node_enc", 1, hp.h, hp.l, F)
-    stack("edge_enc", 1, hp.h, hp.l, F)
+    ns = getattr(hp, "north_star", False)
+    stack("node_enc", 2 if ns else 1, hp.h, hp.l, F)
+    stack("edge_enc", 2 + hp.dim if ns else 1, hp.h, hp.l, F)
     for r in range(hp.n_mp):
         stack(f"mp{r}.node", 2 * F, hp.h_mp, hp.l_mp, F)
         stack(f"mp{r}.edge", 3 * F, hp.h_mp, hp.l_mp, F)
@@ -237,7 +253,20 @@ def create_params(hp, seed=0):
             s *= 0.1
         params[name + ".w"] = rng.standard_normal((fi, fo)) * s
         params[name + ".b"] = np.zeros(fo)
+    for stack_name in ln_stacks(hp):  # LayerNorm gain / shift, no RNG draws
+        params[stack_name + ".ln.g"] = np.ones(hp.width)
+        params[stack_name + ".ln.b"] = np.zeros(hp.width)
     return params
+
+
+def ln_stacks(hp):
+    """Stacks followed by a LayerNorm (north_star mode): encoders and processors."""
+    if not getattr(hp, "north_star", False):
+        return []
+    out = ["node_enc", "edge_enc"]
+    for r in range(hp.n_mp):
+        out += [f"mp{r}.node", f"mp{r}.edge"]
+    return out
 
 
 def load_checkpoint(path):
@@ -300,19 +329,56 @@ def _segment_sum_lexsort(x, seg, n):
     return out
 
 
+def _layer_norm(params, prefix, x):
+    """LayerNorm over the feature axis (population variance, eps LN_EPS),
+    then gain and shift: the north_star MLPs' output normalisation."""
+    mu = x.mean(axis=1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=1, keepdims=True)
+    return (x - mu) / np.sqrt(var + LN_EPS) * params[prefix + ".ln.g"] + params[prefix + ".ln.b"]
+
+
+def _mlp_ln(params, prefix, x, layers, ln):
+    y = _mlp(params, prefix, x, layers)
+    return _layer_norm(params, prefix, y) if ln else y
+
+
+def north_star_inputs(g, b, A, pos, boundary):
+    """Node inputs (b_i, boundary flag) and edge inputs (A_ij, d, |d|) with
+    d = pos[dst] - pos[src], every column standardised per graph with the
+    reference's sorted statistics (gnn.py:42-51)."""
+    b = np.asarray(b, dtype=np.float64)
+    pos = np.asarray(pos, dtype=np.float64)
+    flag = np.asarray(boundary, dtype=np.float64)
+    node = np.stack([b, flag], axis=1)
+    d = pos[g.dst] - pos[g.src]
+    dist = np.sqrt(np.sum(d * d, axis=1))
+    edge = np.concatenate([A.values[:, None], d, dist[:, None]], axis=1)
+
+    def standardise(x):
+        cols = []
+        for c in range(x.shape[1]):
+            mu, sd = sorted_stats(x[:, c])
+            cols.append((x[:, c] - mu) / sd)
+        return np.stack(cols, axis=1)
+
+    return standardise(node), standardise(edge)
+
+
 def gnn_run(hp, params, g):
-    """Returns (edge scalars M[m], node scalars x0[n] or None)."""
+    """Returns (edge scalars M[m], node scalars x0[n] or None). In north_star
+    mode g carries the standardised mesh inputs (north_star_inputs)."""
+    ln = getattr(hp, "north_star", False)
     node_in, edge_in = g.node_in, g.edge_in
-    if hp.normalize:
+    if not ln and hp.normalize:
         node_in = (node_in - g.node_stats[0]) / g.node_stats[1]
         edge_in = (edge_in - g.edge_stats[0]) / g.edge_stats[1]
-    v = _mlp(params, "node_enc", node_in, hp.l)
-    e = _mlp(params, "edge_enc", edge_in, hp.l)
+    v = _mlp_ln(params, "node_enc", node_in, hp.l, ln)
+    e = _mlp_ln(params, "edge_enc", edge_in, hp.l, ln)
     for r in range(hp.n_mp):
         agg = _segment_sum(e * v[g.dst], g.src, g.n)
-        v = _mlp(params, f"mp{r}.node", np.concatenate((v, agg), axis=1), hp.l_mp)
-        e = _mlp(params, f"mp{r}.edge",
-                 np.concatenate((e, v[g.src], v[g.dst]), axis=1), hp.l_mp)
+        v = _mlp_ln(params, f"mp{r}.node", np.concatenate((v, agg), axis=1), hp.l_mp, ln)
+        e = _mlp_ln(params, f"mp{r}.edge",
+                    np.concatenate((e, v[g.src], v[g.dst]), axis=1), hp.l_mp, ln)
     M = _mlp(params, "edge_dec", e, hp.l).reshape(-1)
     x0 = _mlp(params, "node_dec", v, hp.l).reshape(-1) if hp.with_x0_head else None
     return M, x0
@@ -331,8 +397,28 @@ def assemble(lower_values, A):
     return Factor(A.n, Csr(A.n, pat.row_ptr, pat.col_idx, lower_values), d.copy())
 
 
-def build_learned(hp, params, A, b):
+def assemble_exp(M, g, A):
+    """north_star factor P = L L^T: L_ii = exp(M_ii) (the self-loop outputs),
+    L_ij = (M_ij + M_ji) / 2 below the diagonal. Returned in the unit-lower
+    LDL^T form the solver applies, U = L diag(L)^-1 and D = diag(L)^2, so
+    P = U D U^T exactly in real arithmetic."""
+    lower = symmetrize(M, g)
+    diag_slots = np.flatnonzero(g.src == g.dst)
+    d = np.exp(M[diag_slots])  # one per row, in row order (CSR)
+    pat = strict_lower(A)
+    rows = pat.rows()
+    U = lower / d[pat.col_idx]
+    if not (np.all(np.isfinite(U)) and np.all(np.isfinite(d)) and np.all(d > 0.0)):
+        raise ValueError("factor values must be finite with a positive diagonal")
+    return Factor(A.n, Csr(A.n, pat.row_ptr, pat.col_idx, U), d * d)
+
+
+def build_learned(hp, params, A, b, mesh=None):
     g = graph_from_system(A, b)
+    if getattr(hp, "north_star", False):
+        g.node_in, g.edge_in = north_star_inputs(g, b, A, *mesh)
+        M, _ = gnn_run(hp, params, g)
+        return assemble_exp(M, g, A)
     M, _ = gnn_run(hp, params, g)
     return assemble(symmetrize(M, g), A)
 

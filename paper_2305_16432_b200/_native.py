@@ -51,7 +51,8 @@ class PatternInfo(ctypes.Structure):
 class GnnDesc(ctypes.Structure):
     _fields_ = [("width", ctypes.c_int32), ("h", ctypes.c_int32), ("l", ctypes.c_int32),
                 ("h_mp", ctypes.c_int32), ("l_mp", ctypes.c_int32), ("n_mp", ctypes.c_int32),
-                ("normalize", ctypes.c_int32), ("with_x0_head", ctypes.c_int32)]
+                ("normalize", ctypes.c_int32), ("with_x0_head", ctypes.c_int32),
+                ("north_star", ctypes.c_int32), ("dim", ctypes.c_int32)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -97,6 +98,7 @@ SIGNATURES = {
     "npcg_gnn_create": (I32, [ctypes.POINTER(GnnDesc), P, I64, ctypes.POINTER(P)]),
     "npcg_gnn_destroy": (I32, [P]),
     "npcg_gnn_build_factor": (I32, [P, P, I32, P, I32, P, P, P, P, P, ctypes.POINTER(I64), P]),
+    "npcg_gnn_build_factor_mesh": (I32, [P, P, I32, P, I32, P, P, P, P, P, P, ctypes.POINTER(I64), P]),
     "npcg_solver_create": (I32, [P, P, I32, ctypes.POINTER(P)]),
     "npcg_solver_destroy": (I32, [P]),
     "npcg_pcg_solve": (I32, [P, P, I32, P, I32, P, I32, P, P, P, ctypes.POINTER(SolveOpts),

@@ -991,11 +991,32 @@ int npcg_gnn_build_factor(const npcg_gnn *g, const npcg_pattern *A, int B, const
                           const double *rhs, double *S, double *D, double *edge_out, double *x0_out, int64_t *pivot,
                           void *stream) {
     if (!g || !A || !A_vals || !rhs || !S || !D || B < 1 || B > kMaxBatch) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    if (g->d.north_star) return fail(NPCG_ERR_ARGUMENT, "north_star weights: use npcg_gnn_build_factor_mesh");
     if (!A->full_diag) return fail(NPCG_ERR_DATA_FORMAT, "matrix is missing explicit diagonal entries");
     if (!A->symmetric) return fail(NPCG_ERR_DATA_FORMAT, "matrix values are not symmetric");
     int64_t piv = -1;
     std::string err;
     const int rc = gnn_build(*g, *A, B, A_vals, ab, rhs, S, D, edge_out, x0_out, &piv, (cudaStream_t)stream, err);
+    if (pivot) *pivot = piv;
+    if (rc) return fail(rc, err);
+    return NPCG_OK;
+}
+
+int npcg_gnn_build_factor_mesh(const npcg_gnn *g, const npcg_pattern *A, int B, const double *A_vals, int ab,
+                               const double *rhs, const double *pos, const double *boundary, double *S, double *D,
+                               double *edge_out, int64_t *pivot, void *stream) {
+    if (!g || !A || !A_vals || !rhs || !S || !D || !pos || !boundary || B < 1 || B > kMaxBatch)
+        return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    if (!g->d.north_star) return fail(NPCG_ERR_ARGUMENT, "reference weights: use npcg_gnn_build_factor");
+    if (!A->full_diag) return fail(NPCG_ERR_DATA_FORMAT, "matrix is missing explicit diagonal entries");
+    if (!A->symmetric) return fail(NPCG_ERR_DATA_FORMAT, "matrix values are not symmetric");
+    GnnMesh mesh;
+    mesh.pos = pos;
+    mesh.boundary = boundary;
+    int64_t piv = -1;
+    std::string err;
+    const int rc = gnn_build(*g, *A, B, A_vals, ab, rhs, S, D, edge_out, nullptr, &piv, (cudaStream_t)stream, err,
+                             &mesh);
     if (pivot) *pivot = piv;
     if (rc) return fail(rc, err);
     return NPCG_OK;

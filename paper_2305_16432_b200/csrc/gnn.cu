@@ -46,9 +46,11 @@ std::string gnn_init(GnnDev &g, const npcg_gnn_desc &d, const double *weights, i
         L.b = off;
         off += fo;
     };
-    layer(g.node_enc[0], 1, d.h);
+    if (d.north_star && d.dim != 2 && d.dim != 3) return "north_star mode needs dim 2 or 3";
+    const int node_in = d.north_star ? 2 : 1, edge_in = d.north_star ? 2 + d.dim : 1;
+    layer(g.node_enc[0], node_in, d.h);
     layer(g.node_enc[1], d.h, F);
-    layer(g.edge_enc[0], 1, d.h);
+    layer(g.edge_enc[0], edge_in, d.h);
     layer(g.edge_enc[1], d.h, F);
     for (int r = 0; r < d.n_mp; ++r) {
         layer(g.mp_node[r][0], 2 * F, hm);
@@ -61,6 +63,14 @@ std::string gnn_init(GnnDev &g, const npcg_gnn_desc &d, const double *weights, i
     if (d.with_x0_head) {
         layer(g.node_dec[0], F, d.h);
         layer(g.node_dec[1], d.h, 1);
+    }
+    if (d.north_star) {  // LayerNorm gain / shift per stack, after every layer
+        layer(g.ln_node_enc, 1, F);
+        layer(g.ln_edge_enc, 1, F);
+        for (int r = 0; r < d.n_mp; ++r) {
+            layer(g.ln_mp_node[r], 1, F);
+            layer(g.ln_mp_edge[r], 1, F);
+        }
     }
     if (off != n_weights) return "weight blob length does not match the hyper-parameters";
     std::vector<float> h(off);
@@ -121,37 +131,98 @@ __global__ void colstat_final_kernel(long long count, int B, int nblk, const dou
 }
 
 // ---------------------------------------------------------------------------
-// encoders: scalar input -> h -> F  (gnn.py:247-248)
-// items are (system b, index i); input x[i*xs + b*xb]; out[(b*count + i)*F]
+// LayerNorm over a row of F features (north_star): population variance,
+// eps 1e-5, then gain and shift (oracle/port.py _layer_norm)
 // ---------------------------------------------------------------------------
+constexpr float kLnEps = 1e-5f;
+
 template <int F>
-__global__ void __launch_bounds__(kGnnThreads) encode_kernel(long long count, int B, const double *x, int xb,
-                                                             const double *mean, const double *sd, int normalize,
+__device__ __forceinline__ void layer_norm_row(float (&x)[F], const float *g, const float *b) {
+    float mu = 0.f;
+#pragma unroll
+    for (int f = 0; f < F; ++f) mu += x[f];
+    mu /= (float)F;
+    float var = 0.f;
+#pragma unroll
+    for (int f = 0; f < F; ++f) var = fmaf(x[f] - mu, x[f] - mu, var);
+    var /= (float)F;
+    const float rs = 1.0f / sqrtf(var + kLnEps);
+#pragma unroll
+    for (int f = 0; f < F; ++f) x[f] = fmaf((x[f] - mu) * rs, g[f], b[f]);
+}
+
+// in-place LayerNorm of rows [rows][F] (the FFMA processor path)
+template <int F>
+__global__ void __launch_bounds__(kGnnThreads) ln_rows_kernel(long long rows, float *x, const float *g,
+                                                              const float *b) {
+    __shared__ float sg[F], sb[F];
+    for (int q = threadIdx.x; q < F; q += blockDim.x) sg[q] = g[q], sb[q] = b[q];
+    __syncthreads();
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += (long long)gridDim.x * blockDim.x) {
+        float v[F];
+        float4 *p = reinterpret_cast<float4 *>(x + (size_t)r * F);
+#pragma unroll
+        for (int f4 = 0; f4 < F / 4; ++f4) {
+            const float4 t = p[f4];
+            v[4 * f4] = t.x, v[4 * f4 + 1] = t.y, v[4 * f4 + 2] = t.z, v[4 * f4 + 3] = t.w;
+        }
+        layer_norm_row<F>(v, sg, sb);
+#pragma unroll
+        for (int f4 = 0; f4 < F / 4; ++f4) p[f4] = make_float4(v[4 * f4], v[4 * f4 + 1], v[4 * f4 + 2], v[4 * f4 + 3]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// encoders: WIN inputs -> h -> F  (gnn.py:247-248; north_star: more inputs
+// and a LayerNorm). Items are (system b, index i); input feature k of item
+// i is x[k][i*B + b] (batched) or x[k][i] (shared), standardised with its
+// per-system statistics; out[(b*count + i)*F]
+// ---------------------------------------------------------------------------
+constexpr int kMaxEncIn = 5;
+struct EncIn {
+    const double *x[kMaxEncIn];
+    int xb[kMaxEncIn];
+    const double *mean[kMaxEncIn], *sd[kMaxEncIn];  // [B] each
+};
+
+template <int F, int WIN>
+__global__ void __launch_bounds__(kGnnThreads) encode_kernel(long long count, int B, EncIn in, int normalize,
                                                              const float *W1, const float *b1, const float *W2,
-                                                             const float *b2, int h, float *out) {
-    __shared__ float sW1[kMaxHidden], sb1[kMaxHidden];
+                                                             const float *b2, int h, const float *ln_g,
+                                                             const float *ln_b, float *out) {
+    __shared__ float sW1[WIN * kMaxHidden], sb1[kMaxHidden];
     __shared__ __align__(16) float sW2[kMaxHidden * F];
     __shared__ __align__(16) float sb2[F];
-    for (int k = threadIdx.x; k < h; k += blockDim.x) {
-        sW1[k] = W1[k];
-        sb1[k] = b1[k];
-    }
+    __shared__ float sg[F], sb[F];
+    for (int k = threadIdx.x; k < WIN * h; k += blockDim.x) sW1[k] = W1[k];
+    for (int k = threadIdx.x; k < h; k += blockDim.x) sb1[k] = b1[k];
     for (int k = threadIdx.x; k < h * F; k += blockDim.x) sW2[k] = W2[k];
-    for (int k = threadIdx.x; k < F; k += blockDim.x) sb2[k] = b2[k];
+    for (int k = threadIdx.x; k < F; k += blockDim.x) {
+        sb2[k] = b2[k];
+        sg[k] = ln_g ? ln_g[k] : 1.f;
+        sb[k] = ln_b ? ln_b[k] : 0.f;
+    }
     __syncthreads();
     const long long total = count * B;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
          q += (long long)gridDim.x * blockDim.x) {
         const int b = (int)(q / count);
         const long long i = q % count;
-        double xv = xb ? x[(size_t)i * B + b] : x[i];
-        if (normalize) xv = (xv - mean[b]) / sd[b];
-        const float xf = (float)xv;
+        float xf[WIN];
+#pragma unroll
+        for (int k = 0; k < WIN; ++k) {
+            double xv = in.xb[k] ? in.x[k][(size_t)i * B + b] : in.x[k][i];
+            if (normalize) xv = (xv - in.mean[k][b]) / in.sd[k][b];
+            xf[k] = (float)xv;
+        }
         float acc[F];
 #pragma unroll
         for (int f = 0; f < F; ++f) acc[f] = sb2[f];
         for (int k = 0; k < h; ++k) {
-            const float hk = fmaxf(fmaf(xf, sW1[k], sb1[k]), 0.0f);
+            float a = sb1[k];
+#pragma unroll
+            for (int c = 0; c < WIN; ++c) a = fmaf(xf[c], sW1[c * h + k], a);
+            const float hk = fmaxf(a, 0.0f);
             const float4 *w4 = reinterpret_cast<const float4 *>(sW2 + k * F);
 #pragma unroll
             for (int f4 = 0; f4 < F / 4; ++f4) {
@@ -162,9 +233,25 @@ __global__ void __launch_bounds__(kGnnThreads) encode_kernel(long long count, in
                 acc[4 * f4 + 3] = fmaf(hk, w.w, acc[4 * f4 + 3]);
             }
         }
+        if (ln_g) layer_norm_row<F>(acc, sg, sb);
         float4 *o4 = reinterpret_cast<float4 *>(out + ((size_t)b * count + i) * F);
 #pragma unroll
         for (int f4 = 0; f4 < F / 4; ++f4) o4[f4] = make_float4(acc[4 * f4], acc[4 * f4 + 1], acc[4 * f4 + 2], acc[4 * f4 + 3]);
+    }
+}
+
+// north_star edge geometry: geo[k][p] = pos[col p][k] - pos[src p][k] (k < dim), geo[dim][p] = |d|
+__global__ void edge_geometry_kernel(long long m, int dim, const int *src, const int *col, const double *pos,
+                                     double *geo) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < m; p += (long long)gridDim.x * blockDim.x) {
+        const int i = src[p], j = col[p];
+        double s2 = 0.0;
+        for (int k = 0; k < dim; ++k) {
+            const double d = pos[(size_t)j * dim + k] - pos[(size_t)i * dim + k];
+            geo[(size_t)k * m + p] = d;
+            s2 = fma(d, d, s2);
+        }
+        geo[(size_t)dim * m + p] = sqrt(s2);
     }
 }
 
@@ -393,11 +480,11 @@ __global__ void diag_kernel(int n, int B, const int *dp, const double *A, int ab
 
 // tcgen05 edge update (gnn_tc.cu), F = H = 64; NPCG_GNN_TC=0 keeps the FFMA tiles
 cudaError_t launch_mp_edge_tc(int n, long long m, int B, const int *src, const int *col, const float *W1,
-                              const float *b1, const float *W2, const float *b2, float *e, const float *v,
-                              cudaStream_t s);
+                              const float *b1, const float *W2, const float *b2, const float *ln_g,
+                              const float *ln_b, float *e, const float *v, cudaStream_t s);
 cudaError_t launch_mp_node_tc(int n, long long m, int B, const int *rp, const int *col, const float *W1,
-                              const float *b1, const float *W2, const float *b2, const float *e, const float *v,
-                              float *v_out, cudaStream_t s);
+                              const float *b1, const float *W2, const float *b2, const float *ln_g,
+                              const float *ln_b, const float *e, const float *v, float *v_out, cudaStream_t s);
 static bool gnn_tc_enabled() {
     static int on = -1;
     if (on < 0) {
@@ -405,6 +492,37 @@ static bool gnn_tc_enabled() {
         on = env ? std::atoi(env) != 0 : 1;
     }
     return on != 0;
+}
+
+// north_star factor P = L L^T with L_ii = exp(M_ii), L_ij = (M_ij + M_ji) / 2
+// (i > j), in the solver's unit-lower form: S_p = L_ij / L_jj on both slots of
+// the pair, D_i = L_ii^2 (oracle/port.py assemble_exp).
+__global__ void exp_diag_kernel(int n, int B, const int *dp, const double *M, double *D, double *d, int *nonfinite) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < (long long)n * B;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(q / B), b = (int)(q % B);
+        const double li = exp(M[(size_t)dp[i] * B + b]);
+        d[q] = li;
+        D[q] = li * li;
+        if (!(isfinite(li) && li > 0.0 && isfinite(li * li))) *nonfinite = 1;
+    }
+}
+
+__global__ void exp_factor_kernel(long long nnz, int B, const int *pair, const int *src, const int *col,
+                                  const double *M, const double *d, double *S, int *nonfinite) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nnz * B;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long p = q / B;
+        const int b = (int)(q % B);
+        double s = 0.0;
+        const int r = src[p], c = col[p];
+        if (r != c) {
+            const double l = 0.5 * (M[q] + M[(size_t)pair[p] * B + b]);
+            s = l / d[(size_t)(r < c ? r : c) * B + b];
+            if (!isfinite(s)) *nonfinite = 1;
+        }
+        S[q] = s;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -424,39 +542,59 @@ static cudaError_t run_rounds(const GnnDev &g, const Pattern &A, int B, float *e
     const int gn = (int)std::max<long long>(1, std::min<long long>(tn, (long long)std::max(occ_n, 1) * num_sms()));
     const int ge = (int)std::max<long long>(1, std::min<long long>(te, (long long)std::max(occ_e, 1) * num_sms()));
     const bool tc = F == 64 && H == 64 && gnn_tc_enabled();
+    const bool ln = g.d.north_star != 0;
+    const float *w = g.w;
+    auto ln_rows = [&](long long rows, float *x, const LayerOff &L) {
+        if (!ln || tc) return cudaSuccess;  // the tensor-core kernels normalise in their epilogue
+        const int grid = (int)std::max<long long>(1, std::min<long long>((rows + kGnnThreads - 1) / kGnnThreads, 8 * num_sms()));
+        note_launch();
+        ln_rows_kernel<F><<<grid, kGnnThreads, 0, s>>>(rows, x, w + L.w, w + L.b);
+        return cudaGetLastError();
+    };
     for (int r = 0; r < g.d.n_mp; ++r) {
-        const float *w = g.w;
+        const float *lng_n = ln ? w + g.ln_mp_node[r].w : nullptr, *lnb_n = ln ? w + g.ln_mp_node[r].b : nullptr;
+        const float *lng_e = ln ? w + g.ln_mp_edge[r].w : nullptr, *lnb_e = ln ? w + g.ln_mp_edge[r].b : nullptr;
         if (tc) {
             cudaError_t c = launch_mp_node_tc(n, m, B, A.rp, A.col, w + g.mp_node[r][0].w, w + g.mp_node[r][0].b,
-                                              w + g.mp_node[r][1].w, w + g.mp_node[r][1].b, e, v, v2, s);
+                                              w + g.mp_node[r][1].w, w + g.mp_node[r][1].b, lng_n, lnb_n, e, v, v2, s);
             if (c != cudaSuccess) return c;
         } else {
             note_launch(); mp_kernel<F, H, TE, true><<<gn, kGnnThreads, smem_node, s>>>(
                 n, m, B, A.rp, A.col, A.src, w + g.mp_node[r][0].w, w + g.mp_node[r][0].b, w + g.mp_node[r][1].w,
                 w + g.mp_node[r][1].b, e, v, v2);
+            if (cudaError_t c = ln_rows((long long)n * B, v2, g.ln_mp_node[r])) return c;
         }
         std::swap(v, v2);
         if (tc) {
             cudaError_t c = launch_mp_edge_tc(n, m, B, A.src, A.col, w + g.mp_edge[r][0].w, w + g.mp_edge[r][0].b,
-                                              w + g.mp_edge[r][1].w, w + g.mp_edge[r][1].b, e, v, s);
+                                              w + g.mp_edge[r][1].w, w + g.mp_edge[r][1].b, lng_e, lnb_e, e, v, s);
             if (c != cudaSuccess) return c;
             continue;
         }
         note_launch(); mp_kernel<F, H, TE, false><<<ge, kGnnThreads, smem_edge, s>>>(
             n, m, B, A.rp, A.col, A.src, w + g.mp_edge[r][0].w, w + g.mp_edge[r][0].b, w + g.mp_edge[r][1].w,
             w + g.mp_edge[r][1].b, e, v, nullptr);
+        if (cudaError_t c = ln_rows(m * B, e, g.ln_mp_edge[r])) return c;
     }
     *v_final = v;
     return cudaGetLastError();
 }
 
 template <int F>
-static cudaError_t encode(const GnnDev &g, long long count, int B, const double *x, int xb, const double *mean,
-                          const double *sd, const LayerOff *L, float *out, cudaStream_t s) {
+static cudaError_t encode(const GnnDev &g, long long count, int B, int win, const EncIn &in, const LayerOff *L,
+                          const LayerOff *ln, float *out, cudaStream_t s) {
     const long long total = count * B;
     const int grid = (int)std::max<long long>(1, std::min<long long>((total + kGnnThreads - 1) / kGnnThreads, 8 * num_sms()));
-    note_launch(); encode_kernel<F><<<grid, kGnnThreads, 0, s>>>(count, B, x, xb, mean, sd, g.d.normalize, g.w + L[0].w,
-                                                   g.w + L[0].b, g.w + L[1].w, g.w + L[1].b, g.d.h, out);
+    const float *w = g.w;
+    const float *lg = ln ? w + ln->w : nullptr, *lb = ln ? w + ln->b : nullptr;
+    note_launch();
+    switch (win) {
+        case 1: encode_kernel<F, 1><<<grid, kGnnThreads, 0, s>>>(count, B, in, g.d.normalize, w + L[0].w, w + L[0].b, w + L[1].w, w + L[1].b, g.d.h, lg, lb, out); break;
+        case 2: encode_kernel<F, 2><<<grid, kGnnThreads, 0, s>>>(count, B, in, g.d.normalize, w + L[0].w, w + L[0].b, w + L[1].w, w + L[1].b, g.d.h, lg, lb, out); break;
+        case 4: encode_kernel<F, 4><<<grid, kGnnThreads, 0, s>>>(count, B, in, g.d.normalize, w + L[0].w, w + L[0].b, w + L[1].w, w + L[1].b, g.d.h, lg, lb, out); break;
+        case 5: encode_kernel<F, 5><<<grid, kGnnThreads, 0, s>>>(count, B, in, g.d.normalize, w + L[0].w, w + L[0].b, w + L[1].w, w + L[1].b, g.d.h, lg, lb, out); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
@@ -483,7 +621,12 @@ static cudaError_t stats(long long count, int B, const double *x, double *mean, 
 template <int F>
 static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_vals, int ab, const double *rhs,
                    double *S, double *D, double *edge_out, double *x0_out, int64_t *pivot, cudaStream_t s,
-                   std::string &err) {
+                   std::string &err, const GnnMesh *mesh) {
+    const bool ns = g.d.north_star != 0;
+    if (ns && (!mesh || !mesh->pos || !mesh->boundary)) {
+        err = "north_star mode needs the mesh (positions, boundary flags)";
+        return NPCG_ERR_ARGUMENT;
+    }
     const int n = (int)A.n;
     const long long m = A.nnz;
     float *e = nullptr, *v = nullptr, *v2 = nullptr;
@@ -500,22 +643,55 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
               ck(cudaMallocAsync((void **)&v, sizeof(float) * std::max<long long>((long long)n * F * B, 1), s)) &&
               ck(cudaMallocAsync((void **)&v2, sizeof(float) * std::max<long long>((long long)n * F * B, 1), s)) &&
               ck(cudaMallocAsync((void **)&M, sizeof(double) * std::max<long long>(m * B, 1), s)) &&
-              ck(cudaMallocAsync((void **)&st, sizeof(double) * (4 * B + 2 * num_sms() * (size_t)B + 8), s)) &&
+              ck(cudaMallocAsync((void **)&st, sizeof(double) * (16 * B + 2 * num_sms() * (size_t)B + 8), s)) &&
               ck(cudaMallocAsync((void **)&flags, sizeof(int) * 4, s));
+    double *geo = nullptr, *dl = nullptr;  // north_star: edge geometry [dim+1][m], diag(L) [n][B]
+    if (ok && ns)
+        ok = ck(cudaMallocAsync((void **)&geo, sizeof(double) * std::max<long long>((long long)(g.d.dim + 1) * m, 1), s)) &&
+             ck(cudaMallocAsync((void **)&dl, sizeof(double) * std::max<long long>((long long)n * B, 1), s));
     int h_flags[4] = {n, 0, 0, 0};  // bad_row, nonfinite diag, nonfinite L'
     if (ok) {
-        double *mb = st, *sb = st + B, *ma = st + 2 * B, *sa = st + 3 * B, *partial = st + 4 * B;
+        // per-system mean / sd of every input feature: slots [k][B] in st
+        double *partial = st + 16 * B;
+        auto mean_of = [&](int k) { return st + (size_t)(2 * k) * B; };
+        auto sd_of = [&](int k) { return st + (size_t)(2 * k + 1) * B; };
         ok = ck(cudaMemcpyAsync(flags, h_flags, sizeof(h_flags), cudaMemcpyHostToDevice, s));
-        if (ok && g.d.normalize) {
-            ok = ck(stats(n, B, rhs, mb, sb, partial, s)) && ck(stats(m, Bs, A_vals, ma, sa, partial, s));
-            if (ok && Bs != B) {  // shared A: broadcast its statistics to every system
-                for (int b = 1; b < B && ok; ++b)
-                    ok = ck(cudaMemcpyAsync(ma + b, ma, 8, cudaMemcpyDeviceToDevice, s)) &&
-                         ck(cudaMemcpyAsync(sa + b, sa, 8, cudaMemcpyDeviceToDevice, s));
+        // feature k: (data, batched, count) -> statistics slot k (gnn.py:42-51, 239-245)
+        auto feature_stats = [&](int k, const double *x, int xb, long long count) {
+            if (!ok || !g.d.normalize) return;
+            const int cols = xb ? B : 1;
+            ok = ck(stats(count, cols, x, mean_of(k), sd_of(k), partial, s));
+            for (int b = 1; b < B && ok && !xb; ++b)  // shared feature: broadcast to every system
+                ok = ck(cudaMemcpyAsync(mean_of(k) + b, mean_of(k), 8, cudaMemcpyDeviceToDevice, s)) &&
+                     ck(cudaMemcpyAsync(sd_of(k) + b, sd_of(k), 8, cudaMemcpyDeviceToDevice, s));
+        };
+        EncIn nin{}, ein{};
+        int nwin = 1, ewin = 1;
+        nin.x[0] = rhs, nin.xb[0] = 1;
+        ein.x[0] = A_vals, ein.xb[0] = ab;
+        feature_stats(0, rhs, 1, n);
+        feature_stats(1, A_vals, ab, m);
+        nin.mean[0] = mean_of(0), nin.sd[0] = sd_of(0);
+        ein.mean[0] = mean_of(1), ein.sd[0] = sd_of(1);
+        if (ok && ns) {  // (b, boundary flag); (A, d_1..d_dim, |d|), d = pos[dst] - pos[src]
+            const int dim = g.d.dim;
+            note_launch();
+            edge_geometry_kernel<<<(int)std::min<long long>((m + 255) / 256, 8 * num_sms()), 256, 0, s>>>(
+                m, dim, A.src, A.col, mesh->pos, geo);
+            ok = ck(cudaGetLastError());
+            nwin = 2;
+            nin.x[1] = mesh->boundary, nin.xb[1] = 0;
+            feature_stats(2, mesh->boundary, 0, n);
+            nin.mean[1] = mean_of(2), nin.sd[1] = sd_of(2);
+            ewin = 2 + dim;
+            for (int k = 0; k <= dim; ++k) {
+                ein.x[1 + k] = geo + (size_t)k * m, ein.xb[1 + k] = 0;
+                feature_stats(3 + k, geo + (size_t)k * m, 0, m);
+                ein.mean[1 + k] = mean_of(3 + k), ein.sd[1 + k] = sd_of(3 + k);
             }
         }
-        if (ok) ok = ck(encode<F>(g, n, B, rhs, 1, mb, sb, g.node_enc, v, s));
-        if (ok) ok = ck(encode<F>(g, m, B, A_vals, ab, ma, sa, g.edge_enc, e, s));
+        if (ok) ok = ck(encode<F>(g, n, B, nwin, nin, g.node_enc, ns ? &g.ln_node_enc : nullptr, v, s));
+        if (ok) ok = ck(encode<F>(g, m, B, ewin, ein, g.edge_enc, ns ? &g.ln_edge_enc : nullptr, e, s));
         if (ok) {
             const int hm = g.d.h_mp;
             cudaError_t c = cudaErrorInvalidValue;
@@ -529,11 +705,17 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
         double *Mout = edge_out ? edge_out : M;
         if (ok) ok = ck(decode<F>(g, m, B, e, g.edge_dec, Mout, s));
         if (ok && x0_out && g.d.with_x0_head) ok = ck(decode<F>(g, n, B, vfin, g.node_dec, x0_out, s));
-        if (ok) {
+        if (ok && !ns) {
             const int grid = (int)std::min<long long>((m * B + 255) / 256 + 1, 8192);
             note_launch(); symm_kernel<<<grid, 256, 0, s>>>(m, B, A.pair, A.src, A.col, Mout, S, flags + 2);
             note_launch(); diag_kernel<<<(int)std::min<long long>(((long long)n * B + 255) / 256 + 1, 8192), 256, 0, s>>>(
                 n, B, A.dp, A_vals, ab, D, flags, flags + 1);
+            ok = ck(cudaGetLastError());
+        } else if (ok) {  // P = L L^T, exp on the diagonal
+            note_launch(); exp_diag_kernel<<<(int)std::min<long long>(((long long)n * B + 255) / 256 + 1, 8192), 256, 0, s>>>(
+                n, B, A.dp, Mout, D, dl, flags + 1);
+            const int grid = (int)std::min<long long>((m * B + 255) / 256 + 1, 8192);
+            note_launch(); exp_factor_kernel<<<grid, 256, 0, s>>>(m, B, A.pair, A.src, A.col, Mout, dl, S, flags + 2);
             ok = ck(cudaGetLastError());
         }
         if (ok) ok = ck(cudaMemcpyAsync(h_flags, flags, sizeof(h_flags), cudaMemcpyDeviceToHost, s)) &&
@@ -545,6 +727,8 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
     cudaFreeAsync(M, s);
     cudaFreeAsync(st, s);
     cudaFreeAsync(flags, s);
+    if (geo) cudaFreeAsync(geo, s);
+    if (dl) cudaFreeAsync(dl, s);
     if (!ok) return NPCG_ERR_CUDA;
     if (h_flags[0] < n) {
         *pivot = h_flags[0];
@@ -563,9 +747,10 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
 }
 
 int gnn_build(const GnnDev &g, const Pattern &A, int B, const double *A_vals, int ab, const double *rhs, double *S,
-              double *D, double *edge_out, double *x0_out, int64_t *pivot, cudaStream_t s, std::string &err) {
-    if (g.d.width == 16) return build_F<16>(g, A, B, A_vals, ab, rhs, S, D, edge_out, x0_out, pivot, s, err);
-    return build_F<64>(g, A, B, A_vals, ab, rhs, S, D, edge_out, x0_out, pivot, s, err);
+              double *D, double *edge_out, double *x0_out, int64_t *pivot, cudaStream_t s, std::string &err,
+              const GnnMesh *mesh) {
+    if (g.d.width == 16) return build_F<16>(g, A, B, A_vals, ab, rhs, S, D, edge_out, x0_out, pivot, s, err, mesh);
+    return build_F<64>(g, A, B, A_vals, ab, rhs, S, D, edge_out, x0_out, pivot, s, err, mesh);
 }
 
 }  // namespace npcg

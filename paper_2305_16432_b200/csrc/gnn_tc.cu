@@ -140,8 +140,8 @@ __device__ __forceinline__ void store_split(char *hi, char *lo, int r, const flo
 template <bool NODE>
 __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B, const int *rp, const int *src,
                                                        const int *col, const float *W1, const float *b1,
-                                                       const float *W2, const float *b2, float *e, const float *v,
-                                                       float *v_out) {
+                                                       const float *W2, const float *b2, const float *ln_g,
+                                                       const float *ln_b, float *e, const float *v, float *v_out) {
     constexpr int kTcK1 = tc_k1<NODE>();
     using L = TcSmem<NODE>;
     constexpr int kW1Hi = L::W1Hi, kW1Lo = L::W1Lo, kW2Hi = L::W2Hi, kW2Lo = L::W2Lo, kABuf = L::ABuf;
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
     char *sm = reinterpret_cast<char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     __shared__ uint64_t bar[3];  // A buffer 0 / 1 consumed, layer 2 done
     __shared__ uint32_t s_tmem;
-    __shared__ float sb1[kTcH], sb2[kTcF];
+    __shared__ float sb1[kTcH], sb2[kTcF], sg[kTcF], sl[kTcF];
     const int t = threadIdx.x, warp = t >> 5;
     // weights, transposed to [out][in] (the MMA's K-major B), split hi / lo
     for (int q = t; q < kTcH * kTcK1; q += blockDim.x) {
@@ -169,7 +169,11 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
         *reinterpret_cast<float *>(sm + kW2Lo + off) = tf32_rna(w - h);
     }
     for (int q = t; q < kTcH; q += blockDim.x) sb1[q] = b1[q];
-    for (int q = t; q < kTcF; q += blockDim.x) sb2[q] = b2[q];
+    for (int q = t; q < kTcF; q += blockDim.x) {
+        sb2[q] = b2[q];
+        sg[q] = ln_g ? ln_g[q] : 1.f;
+        sl[q] = ln_b ? ln_b[q] : 0.f;
+    }
     if (t == 0) {
         for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
@@ -324,6 +328,7 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
         tc_fence_after();
         // ---- epilogue 2: e = H W2 + b2 in place | v_out = H W2 + b2 ----
         float *eo = NODE ? v_out + ((size_t)b * n + (size_t)it) * kTcF : e + ((size_t)b * m + (size_t)it) * kTcF;
+        float out[kTcF];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             float ov[16], oc[16];
@@ -333,14 +338,25 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
             for (int i = 0; i < 16; ++i) ov[i] += oc[i];
             tmem_ld16(tl + (uint32_t)(128 + q * 16), oc);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) ov[i] += oc[i];
-            if (live) {
+            for (int i = 0; i < 16; ++i) out[q * 16 + i] = (ov[i] + oc[i]) + sb2[q * 16 + i];
+        }
+        if (ln_g) {  // north_star LayerNorm over the row (gnn.cu layer_norm_row)
+            float mu = 0.f;
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    reinterpret_cast<float4 *>(eo)[q * 4 + j] =
-                        make_float4(ov[4 * j] + sb2[q * 16 + 4 * j], ov[4 * j + 1] + sb2[q * 16 + 4 * j + 1],
-                                    ov[4 * j + 2] + sb2[q * 16 + 4 * j + 2], ov[4 * j + 3] + sb2[q * 16 + 4 * j + 3]);
-            }
+            for (int f = 0; f < kTcF; ++f) mu += out[f];
+            mu /= (float)kTcF;
+            float var = 0.f;
+#pragma unroll
+            for (int f = 0; f < kTcF; ++f) var = fmaf(out[f] - mu, out[f] - mu, var);
+            var /= (float)kTcF;
+            const float rs = 1.0f / sqrtf(var + 1e-5f);
+#pragma unroll
+            for (int f = 0; f < kTcF; ++f) out[f] = fmaf((out[f] - mu) * rs, sg[f], sl[f]);
+        }
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < kTcF / 4; ++j)
+                reinterpret_cast<float4 *>(eo)[j] = make_float4(out[4 * j], out[4 * j + 1], out[4 * j + 2], out[4 * j + 3]);
         }
         tc_fence_before();
         __syncthreads();  // TMEM reads done before the next tile's MMAs overwrite it
@@ -351,8 +367,9 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
 
 template <bool NODE>
 static cudaError_t launch_mp_tc_t(int n, long long m, int B, const int *rp, const int *src, const int *col,
-                                  const float *W1, const float *b1, const float *W2, const float *b2, float *e,
-                                  const float *v, float *v_out, cudaStream_t s) {
+                                  const float *W1, const float *b1, const float *W2, const float *b2,
+                                  const float *ln_g, const float *ln_b, float *e, const float *v, float *v_out,
+                                  cudaStream_t s) {
     static bool configured = false;
     const int smem = TcSmem<NODE>::Total;
     if (!configured) {
@@ -364,20 +381,21 @@ static cudaError_t launch_mp_tc_t(int n, long long m, int B, const int *rp, cons
     const long long tiles = (items + kTcRows - 1) / kTcRows * B;
     const int grid = (int)std::max<long long>(1, std::min<long long>(tiles, num_sms()));
     note_launch();
-    mp_tc_kernel<NODE><<<grid, 128, smem, s>>>(n, m, B, rp, src, col, W1, b1, W2, b2, e, v, v_out);
+    mp_tc_kernel<NODE><<<grid, 128, smem, s>>>(n, m, B, rp, src, col, W1, b1, W2, b2, ln_g, ln_b, e, v, v_out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_mp_edge_tc(int n, long long m, int B, const int *src, const int *col, const float *W1,
-                              const float *b1, const float *W2, const float *b2, float *e, const float *v,
-                              cudaStream_t s) {
-    return launch_mp_tc_t<false>(n, m, B, nullptr, src, col, W1, b1, W2, b2, e, v, nullptr, s);
+                              const float *b1, const float *W2, const float *b2, const float *ln_g,
+                              const float *ln_b, float *e, const float *v, cudaStream_t s) {
+    return launch_mp_tc_t<false>(n, m, B, nullptr, src, col, W1, b1, W2, b2, ln_g, ln_b, e, v, nullptr, s);
 }
 
 cudaError_t launch_mp_node_tc(int n, long long m, int B, const int *rp, const int *col, const float *W1,
-                              const float *b1, const float *W2, const float *b2, const float *e, const float *v,
-                              float *v_out, cudaStream_t s) {
-    return launch_mp_tc_t<true>(n, m, B, rp, nullptr, col, W1, b1, W2, b2, const_cast<float *>(e), v, v_out, s);
+                              const float *b1, const float *W2, const float *b2, const float *ln_g,
+                              const float *ln_b, const float *e, const float *v, float *v_out, cudaStream_t s) {
+    return launch_mp_tc_t<true>(n, m, B, rp, nullptr, col, W1, b1, W2, b2, ln_g, ln_b, const_cast<float *>(e), v,
+                                v_out, s);
 }
 
 }  // namespace npcg

@@ -91,6 +91,12 @@ def _check_graph_system(A: SparseMatrixCsr):
 
 @dataclass(frozen=True)
 class GnnHyperParams:
+    """gnn.py:106-122, plus ``mode``: "reference" (pcgkit's network) or
+    "north_star" -- BASELINE.json's extensions, which no reference code
+    pins (the numpy restatement in oracle/port.py is their oracle): node
+    inputs (b_i, boundary flag), edge inputs (A_ij, d_1..d_dim, |d|) from the
+    mesh, a LayerNorm after every encoder and processor MLP, and the factor
+    P = L L^T with L_ii = exp(M_ii) (``dim``: 2 or 3)."""
     l: int = 1
     h: int = 16
     n_mp: int = 5
@@ -98,10 +104,20 @@ class GnnHyperParams:
     h_mp: int = 16
     with_x0_head: bool = False
     normalize: bool = True
+    mode: str = "reference"
+    dim: int = 2
 
     def __post_init__(self):
         if min(self.l, self.h, self.n_mp, self.l_mp, self.h_mp) < 1:
             raise DimensionMismatchError("all architecture sizes must be >= 1")
+        if self.mode not in ("reference", "north_star"):
+            raise DimensionMismatchError(f"unknown GNN mode {self.mode!r}")
+        if self.dim not in (2, 3):
+            raise DimensionMismatchError("dim must be 2 or 3")
+
+    @property
+    def north_star(self) -> bool:
+        return self.mode == "north_star"
 
 
 def _mlp_dims(in_dim, hidden, layers, out_dim):
@@ -118,8 +134,8 @@ def _layer_specs(hyper: GnnHyperParams, width: int | None = None) -> list:
         for k, (fi, fo) in enumerate(_mlp_dims(i, h, l, o)):
             specs.append((f"{prefix}.{k}", fi, fo))
 
-    stack("node_enc", 1, hyper.h, hyper.l, f)
-    stack("edge_enc", 1, hyper.h, hyper.l, f)
+    stack("node_enc", 2 if hyper.north_star else 1, hyper.h, hyper.l, f)
+    stack("edge_enc", 2 + hyper.dim if hyper.north_star else 1, hyper.h, hyper.l, f)
     for r in range(hyper.n_mp):
         stack(f"mp{r}.node", 2 * f, hyper.h_mp, hyper.l_mp, f)
         stack(f"mp{r}.edge", 3 * f, hyper.h_mp, hyper.l_mp, f)
@@ -127,6 +143,17 @@ def _layer_specs(hyper: GnnHyperParams, width: int | None = None) -> list:
     if hyper.with_x0_head:
         stack("node_dec", f, hyper.h, hyper.l, 1)
     return specs
+
+
+def _ln_stacks(hyper: GnnHyperParams) -> list:
+    """Stacks followed by a LayerNorm in north_star mode (gain ".ln.g",
+    shift ".ln.b", latent width each), in device-blob order."""
+    if not hyper.north_star:
+        return []
+    out = ["node_enc", "edge_enc"]
+    for r in range(hyper.n_mp):
+        out += [f"mp{r}.node", f"mp{r}.edge"]
+    return out
 
 
 class GnnModel:
@@ -156,6 +183,9 @@ class GnnModel:
         for name, fi, fo in _layer_specs(self.hyper, self.width):
             parts.append(np.asarray(self.params[name + ".w"], dtype=np.float64).reshape(-1))
             parts.append(np.asarray(self.params[name + ".b"], dtype=np.float64).reshape(-1))
+        for name in _ln_stacks(self.hyper):
+            parts.append(np.asarray(self.params[name + ".ln.g"], dtype=np.float64).reshape(-1))
+            parts.append(np.asarray(self.params[name + ".ln.b"], dtype=np.float64).reshape(-1))
         return np.ascontiguousarray(np.concatenate(parts))
 
     def device(self):
@@ -167,7 +197,7 @@ class GnnModel:
             return self._dev[1]
         hp = self.hyper
         d = _native.GnnDesc(self.width, hp.h, hp.l, hp.h_mp, hp.l_mp, hp.n_mp, int(hp.normalize),
-                            int(hp.with_x0_head))
+                            int(hp.with_x0_head), int(hp.north_star), hp.dim)
         lib = _native.lib()
         h = ctypes.c_void_p()
         _native.check(lib.npcg_gnn_create(ctypes.byref(d), blob.ctypes.data, len(blob), ctypes.byref(h)))
@@ -202,6 +232,9 @@ def create_model(hyper: GnnHyperParams = GnnHyperParams(), seed: int = 0) -> Gnn
             scale *= 0.1
         params[name + ".w"] = rng.standard_normal((fi, fo)) * scale
         params[name + ".b"] = np.zeros(fo)
+    for name in _ln_stacks(hyper):  # LayerNorm: unit gain, zero shift (no RNG draws)
+        params[name + ".ln.g"] = np.ones(FEATURE_WIDTH)
+        params[name + ".ln.b"] = np.zeros(FEATURE_WIDTH)
     return GnnModel(hyper, params)
 
 
@@ -210,6 +243,10 @@ def _validate_params(model: GnnModel, width: int | None = None) -> None:
     for name, fi, fo in _layer_specs(model.hyper, width):
         expected[name + ".w"] = (fi, fo)
         expected[name + ".b"] = (fo,)
+    f = FEATURE_WIDTH if width is None else width
+    for name in _ln_stacks(model.hyper):
+        expected[name + ".ln.g"] = (f,)
+        expected[name + ".ln.b"] = (f,)
     got = {k: np.shape(v) for k, v in model.params.items()}
     if got != expected:
         missing = sorted(set(expected) - set(got))
@@ -228,7 +265,22 @@ def _validate_params(model: GnnModel, width: int | None = None) -> None:
 # ---------------------------------------------------------------------------
 
 
-def _gnn_device(model: GnnModel, A: SparseMatrixCsr, rhs, values=None, want_edges=False, want_x0=False):
+def _mesh_device(model: GnnModel, A: SparseMatrixCsr, mesh):
+    """(positions, boundary) of A's rows as device fp64 arrays."""
+    torch = _torch()
+    if mesh is None:
+        raise DimensionMismatchError("north_star mode needs mesh=(positions (n, dim), boundary (n,))")
+    pos, bnd = mesh
+    pos = to_device(np.ascontiguousarray(np.asarray(pos, dtype=np.float64)) if not is_device(pos) else pos)
+    bnd = to_device(np.ascontiguousarray(np.asarray(bnd, dtype=np.float64)) if not is_device(bnd) else bnd,
+                    dtype=torch.float64)
+    if tuple(pos.shape) != (A.n, model.hyper.dim) or tuple(bnd.shape) != (A.n,):
+        raise DimensionMismatchError(f"mesh must give ({A.n}, {model.hyper.dim}) positions and ({A.n},) flags")
+    return pos.contiguous(), bnd.contiguous()
+
+
+def _gnn_device(model: GnnModel, A: SparseMatrixCsr, rhs, values=None, want_edges=False, want_x0=False,
+                mesh=None):
     """Runs npcg_gnn_build_factor. rhs (n, B) on device; values (nnz, B) or
     None (shared A). Returns (S, D, B, batched_vals, edge_out, x0_out)."""
     torch = _torch()
@@ -246,10 +298,17 @@ def _gnn_device(model: GnnModel, A: SparseMatrixCsr, rhs, values=None, want_edge
     X0 = (torch.empty((max(n, 1), B), dtype=torch.float64, device="cuda")
           if want_x0 and model.hyper.with_x0_head else None)
     piv = ctypes.c_int64(-1)
-    rc = _native.lib().npcg_gnn_build_factor(handle.h, pat.handle, B, _native.ptr(vals), vb,
-                                             _native.ptr(rhs), _native.ptr(S), _native.ptr(D),
-                                             _native.ptr(E), _native.ptr(X0), ctypes.byref(piv),
-                                             _native.stream_handle())
+    if model.hyper.north_star:
+        pos, bnd = _mesh_device(model, A, mesh)
+        rc = _native.lib().npcg_gnn_build_factor_mesh(handle.h, pat.handle, B, _native.ptr(vals), vb,
+                                                      _native.ptr(rhs), _native.ptr(pos), _native.ptr(bnd),
+                                                      _native.ptr(S), _native.ptr(D), _native.ptr(E),
+                                                      ctypes.byref(piv), _native.stream_handle())
+    else:
+        rc = _native.lib().npcg_gnn_build_factor(handle.h, pat.handle, B, _native.ptr(vals), vb,
+                                                 _native.ptr(rhs), _native.ptr(S), _native.ptr(D),
+                                                 _native.ptr(E), _native.ptr(X0), ctypes.byref(piv),
+                                                 _native.stream_handle())
     _native.check(rc, pivot=int(piv.value))
     return pat, S, D, E, X0
 
@@ -295,18 +354,22 @@ def assemble_preconditioner(lower_values, A: SparseMatrixCsr) -> FactorPrecondit
     return FactorPreconditioner("learned", lf)
 
 
-def build_learned(model: GnnModel, A: SparseMatrixCsr, b) -> FactorPreconditioner:
+def build_learned(model: GnnModel, A: SparseMatrixCsr, b, mesh=None) -> FactorPreconditioner:
     """graph -> forward -> symmetrize -> assemble, end to end on the device
-    (gnn.py:314-318). ``b`` may be numpy or a CUDA tensor."""
+    (gnn.py:314-318). ``b`` may be numpy or a CUDA tensor. ``mesh`` =
+    (positions (n, dim), boundary flags (n,)) of A's rows: required by the
+    north_star mode (BASELINE.json's build(mesh, A, b, weights)), ignored by
+    the reference network."""
     if tuple(b.shape) != (A.n,):
         raise DimensionMismatchError(f"b has shape {tuple(b.shape)}, expected ({A.n},)")
-    return build_learned_batch(model, A, to_device(b).view(A.n, 1))
+    return build_learned_batch(model, A, to_device(b).view(A.n, 1), mesh=mesh)
 
 
-def build_learned_batch(model: GnnModel, A: SparseMatrixCsr, rhs, values=None) -> FactorPreconditioner:
+def build_learned_batch(model: GnnModel, A: SparseMatrixCsr, rhs, values=None, mesh=None) -> FactorPreconditioner:
     """B factors at once: rhs (n, B); ``values`` (nnz, B) for B distinct
-    matrices on A's pattern (None: all share A). Returns one batched
-    FactorPreconditioner (batch = B)."""
+    matrices on A's pattern (None: all share A); ``mesh`` shared by the
+    batch (north_star mode). Returns one batched FactorPreconditioner
+    (batch = B)."""
     rhs = to_device(rhs)
     if rhs.dim() != 2 or rhs.shape[0] != A.n:
         raise DimensionMismatchError("rhs must be (n, B)")
@@ -317,7 +380,7 @@ def build_learned_batch(model: GnnModel, A: SparseMatrixCsr, rhs, values=None) -
         _check_values_symmetric(A, None)
     else:
         _check_values_symmetric(A, values)
-    pat, S, D, _, _ = _gnn_device(model, A, rhs, values=values)
+    pat, S, D, _, _ = _gnn_device(model, A, rhs, values=values, mesh=mesh)
     lp = _lower_pattern(A)
     sb = B > 1
     Sv = S.view(-1) if sb else S[:, 0].contiguous()
@@ -368,13 +431,21 @@ def predict_x0(model: GnnModel, graph: GraphData) -> np.ndarray:
 
 
 def save_model(path, model: GnnModel) -> None:
+    """Reference checkpoints (format_version 1) are byte-identical to
+    pcgkit's; north_star models write format_version 2 (their hyper-
+    parameters add "mode" and "dim")."""
     _validate_params(model, model.width)
-    hyper = json.dumps({
+    hyper = {
         "l": model.hyper.l, "h": model.hyper.h, "n_mp": model.hyper.n_mp,
         "l_mp": model.hyper.l_mp, "h_mp": model.hyper.h_mp,
         "with_x0_head": model.hyper.with_x0_head, "normalize": model.hyper.normalize,
-    }, sort_keys=True)
-    chunks = [f'{{"format_version": {CHECKPOINT_VERSION}, "hyper": {hyper}, "tensors": {{']
+    }
+    version = CHECKPOINT_VERSION
+    if model.hyper.north_star:
+        hyper.update(mode=model.hyper.mode, dim=model.hyper.dim)
+        version = 2
+    hyper = json.dumps(hyper, sort_keys=True)
+    chunks = [f'{{"format_version": {version}, "hyper": {hyper}, "tensors": {{']
     for k, (name, arr) in enumerate(sorted(model.params.items())):
         data = ", ".join(format(x, ".17g") for x in np.asarray(arr).ravel())
         chunks.append(f'{", " if k else ""}{json.dumps(name)}: '
@@ -390,8 +461,11 @@ def load_model(path) -> GnnModel:
             doc = json.load(fh)
     except (OSError, json.JSONDecodeError) as exc:
         raise DataFormatError(f"cannot read checkpoint {path}: {exc}") from exc
-    if doc.get("format_version") != CHECKPOINT_VERSION:
+    version = doc.get("format_version")
+    if version not in (CHECKPOINT_VERSION, 2):
         raise DataFormatError("unsupported checkpoint format version")
+    if version == CHECKPOINT_VERSION and ("mode" in doc.get("hyper", {}) or "dim" in doc.get("hyper", {})):
+        raise DataFormatError("format_version 1 checkpoints carry the reference network only")
     try:
         hyper = GnnHyperParams(**doc["hyper"])
         params = {name: np.array(rec["data"], dtype=np.float64).reshape(rec["shape"])

@@ -154,6 +154,18 @@ class Problem:
     rtol: float
     max_iter: int | None
     meta: dict
+    # north_star GNN inputs for the rows of A: positions (n, dim) and the
+    # boundary flag (domain boundary, or next to an eliminated Dirichlet node)
+    geometry: tuple | None = None
+
+
+def _free_geometry(mesh, full_pattern: SparseMatrixCsr, free: np.ndarray):
+    """Positions of the free rows and their flag: adjacent to a Dirichlet
+    (eliminated) node through the assembled pattern."""
+    rows = full_pattern.row_indices()
+    touch = np.zeros(full_pattern.n, dtype=bool)
+    np.logical_or.at(touch, rows, mesh.boundary[full_pattern.col_idx])
+    return np.ascontiguousarray(mesh.vertices[free]), touch[free]
 
 
 def heat_2d(k=32, jitter=0.2, dt=1e-2, alpha=1.0, cfg=1, batch=1) -> Problem:
@@ -178,7 +190,8 @@ def heat_2d(k=32, jitter=0.2, dt=1e-2, alpha=1.0, cfg=1, batch=1) -> Problem:
     if values is not None:
         A0 = A0.with_values(values[:, 0].copy())
     return Problem("heat2d", A0, np.stack(rhs, axis=1), values, 1e-8, 2000,
-                   {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg})
+                   {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg},
+                   (np.ascontiguousarray(mesh.vertices), mesh.boundary.copy()))
 
 
 def poisson_2d(k=256, jitter=0.2, batch=64, cfg=2, first=0) -> Problem:
@@ -201,7 +214,8 @@ def poisson_2d(k=256, jitter=0.2, batch=64, cfg=2, first=0) -> Problem:
     for j, rng in enumerate(rngs):
         f = grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3))
         rhs[:, j] = _host_spmv(Mm, f)[free]
-    return Problem("poisson2d", A, rhs, None, 1e-8, None, {"k": k, "jitter": jitter, "cfg": cfg})
+    return Problem("poisson2d", A, rhs, None, 1e-8, None, {"k": k, "jitter": jitter, "cfg": cfg},
+                   _free_geometry(mesh, asm.matrix(Kv), free))
 
 
 def wave_2d(k=512, jitter=0.2, dt=1e-3, sigma=0.5, batch=32, cfg=3, first=0) -> Problem:
@@ -223,7 +237,8 @@ def wave_2d(k=512, jitter=0.2, dt=1e-3, sigma=0.5, batch=32, cfg=3, first=0) -> 
         vals[:, j] = Mv + (dt * dt) * Kc
         rhs[:, j] = _host_spmv(Mm, grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3)))
     A = asm.matrix(np.ascontiguousarray(vals[:, 0]))
-    return Problem("wave2d", A, rhs, vals, 1e-8, None, {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg})
+    return Problem("wave2d", A, rhs, vals, 1e-8, None, {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg},
+                   (np.ascontiguousarray(mesh.vertices), mesh.boundary.copy()))
 
 
 # ---------------------------------------------------------------------------
@@ -307,7 +322,8 @@ def poisson_3d(k=64, jitter=0.15, batch=128, cfg=4, first=0) -> Problem:
     for j, rng in enumerate(rngs):
         f = grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3))
         rhs[:, j] = _host_spmv(Mm, f)[free]
-    return Problem("poisson3d", A, rhs, None, 1e-8, None, {"k": k, "jitter": jitter, "cfg": cfg})
+    return Problem("poisson3d", A, rhs, None, 1e-8, None, {"k": k, "jitter": jitter, "cfg": cfg},
+                   _free_geometry(mesh, asm.matrix(Kv), free))
 
 
 def heat_3d(k=128, jitter=0.15, dt=1e-3, sigma=1.0, batch=8, cfg=5, first=0) -> Problem:
@@ -328,7 +344,8 @@ def heat_3d(k=128, jitter=0.15, dt=1e-3, sigma=1.0, batch=8, cfg=5, first=0) -> 
         vals[:, j] = Mv + dt * asm.values(K * kap[:, None, None])
         rhs[:, j] = _host_spmv(Mm, grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3)))
     A = asm.matrix(np.ascontiguousarray(vals[:, 0]))
-    return Problem("heat3d", A, rhs, vals, 1e-10, None, {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg})
+    return Problem("heat3d", A, rhs, vals, 1e-10, None, {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg},
+                   (np.ascontiguousarray(mesh.vertices), mesh.boundary.copy()))
 
 
 def _host_spmv(A: SparseMatrixCsr, x):

@@ -63,5 +63,5 @@ def test_pattern_validation_errors_before_touching_the_device():
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(_native.SolveOpts) == 4 + 4 + 16 * 8 + 8 + 4 * 4
     assert ctypes.sizeof(_native.SolveReportC) == 11 * 8
-    assert ctypes.sizeof(_native.GnnDesc) == 8 * 4
+    assert ctypes.sizeof(_native.GnnDesc) == 10 * 4  # + north_star, dim
     assert ctypes.sizeof(_native.PatternInfo) == 3 * 8 + 9 * 4 + 4
