@@ -131,6 +131,9 @@ struct npcg_solver {
     double *S_fwd = nullptr, *S_bwd = nullptr;  // factor entries in schedule order
     size_t S_cap = 0;
     LineSched *ls = nullptr;  // line-wavefront schedule (owned by the pattern) or null
+    LevelSched *lv = nullptr;  // global level sets for the level-synchronous kernel, or null
+    unsigned *gbar = nullptr;  // its grid barrier words
+    double *lpartial = nullptr;  // its per-block partial sums [grid][B]
     int line_K = 0;  // launch shape (line_config_for) of the line P^{-1} kernel
     // line mode: every loop vector is in line order ([b][nslot]): P, XL (x), BL (b)
     // too; A as ELL by slot
@@ -154,7 +157,7 @@ struct npcg_solver {
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
                         alpha, beta, rel, final_rel, history, active_count, drift_count, ctl, partial,
-                        S_fwd, S_bwd, xpend, Dl, rDl, XL, BL, ecol, eperm, evals, ones, kmax};
+                        S_fwd, S_bwd, xpend, Dl, rDl, XL, BL, ecol, eperm, evals, ones, kmax, gbar, lpartial};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_poll) cudaFreeHost(h_poll);
@@ -395,6 +398,18 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
             s->line_K = k;
         }
     }
+    // without a line schedule: level-synchronous solves when the batch gives
+    // every level enough rows x columns (NPCG_LEVELSYNC=0/1 forces)
+    if (!s->ls) {
+        bool use = (long long)A->n * B >= (1ll << 20);
+        if (const char *env = std::getenv("NPCG_LEVELSYNC")) use = std::atoi(env) != 0;
+        if (use) s->lv = s->F->level_schedule();
+        if (s->lv) {
+            NPCG_CUDA(dalloc(&s->gbar, 2));
+            NPCG_CUDA(cudaMemset(s->gbar, 0, 8));
+            NPCG_CUDA(dalloc(&s->lpartial, (size_t)std::max(1, level_sync_grid(B)) * B));
+        }
+    }
     if (s->ls) {  // A as ELL by slot (the line-order loop); rows wider than 16 keep the level path
         const LineSched &ls = *s->ls;
         int width = 0;
@@ -511,6 +526,8 @@ static int stage_factor(npcg_solver *s, const double *S, int sb, const double *D
     size_t need;
     if (s->ls) {
         need = (size_t)std::max(s->ls->fwd.fac_slots, s->ls->bwd.fac_slots) * (sb ? s->B : 1);
+    } else if (s->lv) {
+        need = (size_t)std::max<int64_t>(std::max(s->lv->fwd.entries, s->lv->bwd.entries), 1) * (sb ? s->B : 1);
     } else {
         const Schedule &f = s->plan.set->fwd, &b = s->plan.set->bwd;
         const size_t cols = sb ? (size_t)s->plan.groups * s->plan.G : 1;
@@ -541,6 +558,9 @@ static int stage_factor(npcg_solver *s, const double *S, int sb, const double *D
         }
         NPCG_CUDA(launch_to_line(s->ls->nslot, db ? s->B : 1, s->ls->rowof, D, db, 1.0, s->Dl, st));
         NPCG_CUDA(launch_reciprocal((long long)dneed, s->Dl, s->rDl, st));
+    } else if (s->lv) {
+        launch_level_factor_pack(s->lv->fwd.entries, s->B, sb, s->lv->fwd.sperm, S, s->S_fwd, st);
+        launch_level_factor_pack(s->lv->bwd.entries, s->B, sb, s->lv->bwd.sperm, S, s->S_bwd, st);
     } else {
         launch_factor_pack(s->plan.set->fwd, s->B, s->plan.G, sb, S, s->S_fwd, st);
         launch_factor_pack(s->plan.set->bwd, s->B, s->plan.G, sb, S, s->S_bwd, st);
@@ -568,6 +588,27 @@ static TrsvArgs level_args(npcg_solver *s, bool upper, int mode, int sb, const d
     v.d_batched = db;
     v.ctl = s->ctl;
     v.partial = s->partial;
+    v.drift_count = s->drift_count;
+    return v;
+}
+
+static LevelSyncArgs level_sync_args(npcg_solver *s, bool upper, int mode, int sb, const double *D, int db) {
+    LevelSyncArgs v;
+    const LevelDir &L = upper ? s->lv->bwd : s->lv->fwd;
+    v.B = s->B;
+    v.upper = upper;
+    v.mode = mode;
+    v.nlev = L.nlev;
+    v.lvl_ptr = L.lvl_ptr;
+    v.rows = L.rows;
+    v.eptr = L.eptr;
+    v.ecol = L.ecol;
+    v.S = upper ? s->S_bwd : s->S_fwd;
+    v.s_batched = sb;
+    v.D = D;
+    v.d_batched = db;
+    v.partial = s->lpartial;
+    v.bar = s->gbar;
     v.drift_count = s->drift_count;
     return v;
 }
@@ -628,6 +669,15 @@ int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int s
         l.out = s->Z;
         NPCG_CUDA(launch_ldlt_line(l, st));
         NPCG_CUDA(launch_from_line(ls.nslot, B, ls.rowof, s->Z, z, st));
+    } else if (s->lv) {
+        LevelSyncArgs f = level_sync_args(s, false, TRSV_PLAIN, sb, D, db);
+        f.in = r;
+        f.out = s->Y;
+        NPCG_CUDA(launch_level_sync(f, st));
+        LevelSyncArgs b = level_sync_args(s, true, TRSV_PLAIN, sb, D, db);
+        b.in = s->Y;
+        b.out = z;
+        NPCG_CUDA(launch_level_sync(b, st));
     } else {
         launch_fill_sentinel((long long)F->n * B, z, st);  // level kernel polls z
         TrsvArgs f = level_args(s, false, TRSV_PLAIN, sb, D, db);
@@ -773,6 +823,20 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     // P^{-1}: line path (one launch) or level path (forward, drift, backward)
     LineArgs ll{};
     TrsvArgs fw{}, bw{};
+    LevelSyncArgs fwl{}, bwl{};
+    if (s->lv) {
+        fwl = level_sync_args(s, false, TRSV_PCG, sb, D, db);
+        fwl.in = s->R;
+        fwl.out = s->Y;
+        fwl.R = s->R;
+        fwl.AP = s->AP;
+        fwl.st = sst;
+        bwl = level_sync_args(s, true, TRSV_PCG, sb, D, db);
+        bwl.in = s->Y;
+        bwl.out = s->Z;
+        bwl.R = s->R;
+        bwl.st = sst;
+    }
     if (s->ls) {
         ll = line_args(s, TRSV_PCG, sb, db);
         ll.in = s->R;
@@ -848,7 +912,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     // history buffer moved
     auto set_state = [&]() {
         apdot.st = drift.st = sst;
-        fw.st = bw.st = ll.st = sst;
+        fw.st = bw.st = ll.st = fwl.st = bwl.st = sst;
     };
     int check = o->check_every > 0 ? o->check_every : 8;
     // a pass advances k by at most one; an iteration whose drift check
@@ -863,9 +927,9 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
                 NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
                 continue;
             }
-            NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return launch_trsv(fw, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return s->lv ? launch_level_sync(fwl, st) : launch_trsv(fw, st); }));
             NPCG_CUDA(timed(NPCG_PROF_SPMV_DRIFT, [&] { return launch_spmv(drift, st); }));
-            NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return launch_trsv(bw, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return s->lv ? launch_level_sync(bwl, st) : launch_trsv(bw, st); }));
             NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
         }
         passes += check;

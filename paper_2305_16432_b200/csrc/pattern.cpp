@@ -361,6 +361,68 @@ static bool build_line_sched(const Pattern &P, LineSched &LS) {
     return LS.rowof && LS.slot;
 }
 
+LevelSched::~LevelSched() {
+    for (LevelDir *d : {&fwd, &bwd})
+        for (int32_t *p : {d->lvl_ptr, d->rows, d->eptr, d->ecol, d->sperm})
+            if (p) cudaFree(p);
+}
+
+static bool build_level_dir(const Pattern &P, bool upper, LevelDir &D) {
+    const int32_t n = (int32_t)P.n;
+    const auto &rp = P.h_rp, &col = P.h_col, &dp = P.h_dp;
+    std::vector<int32_t> lvl(n, 0);
+    int32_t nlev = n ? 1 : 0;
+    for (int32_t t = 0; t < n; ++t) {  // processing order: ascending rows forward, descending backward
+        const int32_t i = upper ? n - 1 - t : t;
+        int32_t l = 0;
+        const int32_t p0 = upper ? dp[i] + 1 : rp[i], p1 = upper ? rp[i + 1] : dp[i];
+        for (int32_t p = p0; p < p1; ++p) l = std::max(l, lvl[col[p]] + 1);
+        lvl[i] = l;
+        nlev = std::max(nlev, l + 1);
+    }
+    std::vector<int32_t> lvl_ptr(nlev + 1, 0);
+    for (int32_t i = 0; i < n; ++i) lvl_ptr[lvl[i] + 1]++;
+    int32_t max_rows = 0;
+    for (int32_t L = 0; L < nlev; ++L) {
+        max_rows = std::max(max_rows, lvl_ptr[L + 1]);
+        lvl_ptr[L + 1] += lvl_ptr[L];
+    }
+    std::vector<int32_t> rows(n), fill(lvl_ptr.begin(), lvl_ptr.end() - 1);
+    for (int32_t t = 0; t < n; ++t) {
+        const int32_t i = upper ? n - 1 - t : t;
+        rows[fill[lvl[i]]++] = i;
+    }
+    std::vector<int32_t> eptr(n + 1, 0), ecol, sperm;
+    for (int32_t k = 0; k < n; ++k) {
+        const int32_t i = rows[k];
+        if (upper)  // the column scatter's order: descending columns (sparse.py:236-239)
+            for (int32_t p = rp[i + 1] - 1; p > dp[i]; --p) ecol.push_back(col[p]), sperm.push_back(p);
+        else
+            for (int32_t p = rp[i]; p < dp[i]; ++p) ecol.push_back(col[p]), sperm.push_back(p);
+        eptr[k + 1] = (int32_t)ecol.size();
+    }
+    D.nlev = nlev;
+    D.max_rows = max_rows;
+    D.entries = (int64_t)ecol.size();
+    D.lvl_ptr = upload(lvl_ptr);
+    D.rows = upload(rows);
+    D.eptr = upload(eptr);
+    D.ecol = upload(ecol);
+    D.sperm = upload(sperm);
+    return D.lvl_ptr && D.rows && D.eptr && D.ecol && D.sperm;
+}
+
+LevelSched *Pattern::level_schedule() {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!factor_ok) return nullptr;
+    if (!levels) {
+        auto L = std::make_unique<LevelSched>();
+        if (!build_level_dir(*this, false, L->fwd) || !build_level_dir(*this, true, L->bwd)) return nullptr;
+        levels = std::move(L);
+    }
+    return levels.get();
+}
+
 LineSched *Pattern::line_schedule() {
     std::lock_guard<std::mutex> lock(mu);
     if (!factor_ok) return nullptr;

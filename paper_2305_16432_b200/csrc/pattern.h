@@ -103,6 +103,26 @@ struct LineSched {
     ~LineSched();
 };
 
+// Global level sets of the two triangular solves (trsv_level.cu): rows in
+// level order, each row's dependencies in the reference's summation order
+// (sparse.py:222-239: ascending columns forward, the column scatter's
+// descending order backward). The level-synchronous kernel walks the levels
+// with one grid-wide barrier each; used for patterns without a line
+// schedule (3-D meshes) when the batch gives every level enough work.
+struct LevelDir {
+    int32_t nlev = 0, max_rows = 0;
+    int64_t entries = 0;
+    int32_t *lvl_ptr = nullptr;  // [nlev + 1] into rows
+    int32_t *rows = nullptr;     // [n] rows in level order
+    int32_t *eptr = nullptr;     // [n + 1] dependency range of the k-th row in level order
+    int32_t *ecol = nullptr;     // [entries] dependency row
+    int32_t *sperm = nullptr;    // [entries] CSR position of the factor value
+};
+struct LevelSched {
+    LevelDir fwd, bwd;
+    ~LevelSched();
+};
+
 struct Pattern {
     int64_t n = 0, nnz = 0, nnz_lower = 0;
     bool full_diag = false, symmetric = false, factor_ok = false;
@@ -112,12 +132,15 @@ struct Pattern {
     int32_t *src = nullptr;        // [nnz] row of each stored entry (edge source, gnn.py:83)
     std::map<int32_t, std::unique_ptr<SchedSet>> scheds;  // by chunk rows
     std::unique_ptr<LineSched> lines;                      // built on first use
+    std::unique_ptr<LevelSched> levels;                    // built on first use
     std::mutex mu;
     ~Pattern();
     // Schedule for `chunk_rows` (built on first use); nullptr + err on failure.
     SchedSet *schedule(int32_t chunk_rows, std::string &err);
     // Line schedule, or nullptr when the pattern does not qualify.
     LineSched *line_schedule();
+    // Global level sets (nullptr without a factor analysis or on allocation failure).
+    LevelSched *level_schedule();
 };
 
 // Rows per chunk for a solve over B columns in groups of G (heuristic,

@@ -76,6 +76,31 @@ cudaError_t launch_reciprocal(long long count, const double *D, double *rD, cuda
 // factor values S[p * ps + b * bs] -> line order of `L` (per system when batched)
 void launch_line_factor_pack(const LineDir &L, int B, int sb, long long ps, long long bs, const double *S,
                              double *packed, cudaStream_t s);
+// Level-synchronous solve (trsv_level.cu): one cooperative launch per
+// direction, a grid barrier per level; vectors RHS-minor (i * B + b),
+// factor values packed in the direction's entry order ([e][B] when batched).
+struct LevelSyncArgs {
+    int B = 1, upper = 0, mode = TRSV_PLAIN, grid = 0;
+    int nlev = 0;
+    const int *lvl_ptr = nullptr, *rows = nullptr, *eptr = nullptr, *ecol = nullptr;
+    const double *S = nullptr;
+    int s_batched = 0;
+    const double *D = nullptr;  // diag(A) [i * B + b] or [i]
+    int d_batched = 0;
+    const double *in = nullptr;  // forward: r ; backward: y
+    double *out = nullptr;       // forward: y ; backward: z
+    double *R = nullptr;         // PCG: r (forward writes r_{k+1}, backward reads it for r.z)
+    const double *AP = nullptr;
+    SolveState st{};
+    double *partial = nullptr;   // [grid][B]
+    unsigned *bar = nullptr;     // [2] zero-initialised barrier words
+    int *drift_count = nullptr;
+};
+int level_sync_grid(int B);
+cudaError_t launch_level_sync(const LevelSyncArgs &a, cudaStream_t s);
+// packed[e * B + b] = S[perm[e] * B + b] (batched) | packed[e] = S[perm[e]]
+void launch_level_factor_pack(long long entries, int B, int sb, const int *perm, const double *S, double *packed,
+                              cudaStream_t s);
 cudaError_t launch_trsv(const TrsvArgs &a, cudaStream_t s);
 // factor values (CSR order, symmetric S) -> packed level order of `sched`
 void launch_factor_pack(const Schedule &sched, int B, int G, int s_batched, const double *S, double *packed,

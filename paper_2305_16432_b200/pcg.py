@@ -146,8 +146,22 @@ def _side_streams(k):
     return mine[:k]
 
 
+def _has_line_schedule(A, fac):
+    """Whether the factor pattern's solves take the line wavefront (2-D
+    meshes); the others run grid-synchronous level kernels, which use the
+    whole GPU per launch and gain nothing from a stream split."""
+    if fac is None:
+        return True  # identity preconditioner: keep the split
+    pat = fac[0]
+    lines = ctypes.c_int32()
+    _native.check(_native.lib().npcg_pattern_line_info(pat.handle, ctypes.byref(lines), None, None, None, 1))
+    return lines.value > 0
+
+
 def _pcg_device(A, Bm, fac, opts, batch, values=None, with_history=True, profile=False):
     k = SPLIT_STREAMS if batch >= SPLIT_MIN_BATCH and SPLIT_STREAMS > 1 else 1
+    if k > 1 and not _has_line_schedule(A, fac):
+        k = 1
     if k == 1:
         X, reps, prof = _pcg_device_one(A, Bm, fac, opts, batch, values, with_history, profile)
         LAST_PROFILE.clear()

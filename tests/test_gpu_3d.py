@@ -76,3 +76,71 @@ def test_heat_3d_distinct_systems(gpu):
         assert rep.converged and orep.converged
         assert abs(rep.iterations - orep.iterations) <= 1, (s, rep.iterations, orep.iterations)
         assert rel(X[:, s], ox) <= X_TOL
+
+
+# ---- level-synchronous solves (trsv_level.cu): forced on at test sizes ----
+
+
+@pytest.fixture
+def levelsync(monkeypatch):
+    monkeypatch.setenv("NPCG_LEVELSYNC", "1")
+
+
+def test_level_sync_apply_inverse_bitwise(gpu, levelsync):
+    import torch
+    A = inputs.poisson_3d(k=9, batch=1).A
+    rng = np.random.default_rng(11)
+    low = A.strict_lower()
+    vals = rng.uniform(-0.2, 0.2, size=low.nnz)
+    F = sparse.LowerFactor(A.n, sparse.SparseMatrixCsr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    oF = port.Factor(A.n, port.Csr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    r = rng.standard_normal(A.n)
+    np.testing.assert_array_equal(sparse.ldlt_apply_inverse(F, r), oF.apply_inverse(r))
+    # a batch of 40 right-hand sides through the device entry point
+    R = rng.standard_normal((A.n, 40))
+    P = gnn.assemble_preconditioner(vals, A)
+    Z = P.apply_inverse(torch.from_numpy(R).cuda()).cpu().numpy()
+    for j in (0, 17, 39):
+        np.testing.assert_array_equal(Z[:, j], oF.apply_inverse(R[:, j]))
+
+
+def test_level_sync_shared_factor_batch(gpu, levelsync):
+    """Config-4 shape through the level-synchronous kernels."""
+    prob = inputs.poisson_3d(k=9, batch=24)
+    A = prob.A
+    oA = port.Csr(A.n, A.row_ptr, A.col_idx, A.values)
+    model, ohp = perturbed_model(0)
+    P = gnn.build_learned(model, A, prob.rhs[:, 0])
+    oF = port.build_learned(ohp, model.params, oA, prob.rhs[:, 0])
+    thr = (1e-8,)
+    X, reps = pcg.pcg_solve_batch(A, prob.rhs, P, pcg.SolveOptions(thresholds=thr, max_iter=3000))
+    for s in (0, 7, 23):
+        ox, orep = port.pcg_solve(oA, prob.rhs[:, s], oF, thresholds=thr, max_iter=3000)
+        assert reps[s].converged and orep.converged
+        assert abs(reps[s].iterations - orep.iterations) <= 1, (s, reps[s].iterations, orep.iterations)
+        assert rel(X[:, s], ox) <= X_TOL
+    # decoupled from the GNN: the oracle's own L', the first residual norms agree
+    # up to the dot products' summation order
+    Po = gnn.assemble_preconditioner(oF.lower.values, A)
+    X2, reps2 = pcg.pcg_solve_batch(A, prob.rhs, Po, pcg.SolveOptions(thresholds=thr, max_iter=3000))
+    ox, orep = port.pcg_solve(oA, prob.rhs[:, 5], oF, thresholds=thr, max_iter=3000)
+    np.testing.assert_allclose(np.array(reps2[5].history)[:4], np.array(orep.history)[:4], rtol=1e-9)
+    assert abs(reps2[5].iterations - orep.iterations) <= 1
+
+
+def test_level_sync_distinct_systems(gpu, levelsync):
+    """Config-5 shape (per-system A and L', rtol 1e-10) through the
+    level-synchronous kernels."""
+    prob = inputs.heat_3d(k=7, batch=5)
+    A, vals = prob.A, prob.values
+    model, ohp = perturbed_model(1)
+    P = gnn.build_learned_batch(model, A, prob.rhs, values=vals)
+    thr = (1e-10,)
+    X, reps = pcg.pcg_solve_batch(A, prob.rhs, P, pcg.SolveOptions(thresholds=thr, max_iter=3000), values=vals)
+    for s, rep in enumerate(reps):
+        oA = port.Csr(A.n, A.row_ptr, A.col_idx, np.ascontiguousarray(vals[:, s]))
+        oF = port.build_learned(ohp, model.params, oA, prob.rhs[:, s])
+        ox, orep = port.pcg_solve(oA, prob.rhs[:, s], oF, thresholds=thr, max_iter=3000)
+        assert rep.converged and orep.converged
+        assert abs(rep.iterations - orep.iterations) <= 1, (s, rep.iterations, orep.iterations)
+        assert rel(X[:, s], ox) <= X_TOL
