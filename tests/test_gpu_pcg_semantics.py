@@ -331,3 +331,21 @@ def test_non_finite_runs_to_max_iter(gpu, k):
 def orep_status_maxiter():
     from paper_2305_16432_b200 import _native
     return _native.STATUS_MAXITER
+
+
+def test_reference_dataset_solves_on_device(gpu):
+    """A dataset written by the reference (tests/golden/dataset_heat_small,
+    fem.py:417-448): each pattern group solved as one batch on the device
+    reproduces the stored x (the reference's own 1e-12 solves)."""
+    import os
+    from paper_2305_16432_b200 import datasets
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "dataset_heat_small")
+    _, trajs = datasets.load_dataset(gold)
+    tuples = [t for traj in trajs for t in traj.tuples]
+    for group in datasets.group_by_pattern(tuples):
+        A, values, rhs, x_ref = datasets.stack_tuples(group)
+        P = preconditioners.build_jacobi(A) if values.shape[1] == 1 else None
+        X, reps = pcg.pcg_solve_batch(A, rhs, P, pcg.SolveOptions(thresholds=(1e-12,)), values=values)
+        for j, rep in enumerate(reps):
+            assert rep.converged
+            assert np.linalg.norm(X[:, j] - x_ref[:, j]) <= 1e-9 * np.linalg.norm(x_ref[:, j])
