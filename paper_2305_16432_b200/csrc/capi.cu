@@ -134,6 +134,8 @@ struct npcg_solver {
     LevelSched *lv = nullptr;  // global level sets for the level-synchronous kernel, or null
     unsigned *gbar = nullptr;  // its grid barrier words
     double *lpartial = nullptr;  // its per-block partial sums [grid][B]
+    unsigned *lflags = nullptr;  // dependency-flag mode: [n][level_flag_groups(B)], or null (barrier per level)
+    unsigned lepoch = 0;         // epoch of the last level launch
     int line_K = 0;  // launch shape (line_config_for) of the line P^{-1} kernel
     // line mode: every loop vector is in line order ([b][nslot]): P, XL (x), BL (b)
     // too; A as ELL by slot
@@ -157,7 +159,7 @@ struct npcg_solver {
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
                         alpha, beta, rel, final_rel, history, active_count, drift_count, ctl, partial,
-                        S_fwd, S_bwd, xpend, Dl, rDl, XL, BL, ecol, eperm, evals, ones, kmax, gbar, lpartial};
+                        S_fwd, S_bwd, xpend, Dl, rDl, XL, BL, ecol, eperm, evals, ones, kmax, gbar, lpartial, lflags};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_poll) cudaFreeHost(h_poll);
@@ -408,6 +410,14 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
             NPCG_CUDA(dalloc(&s->gbar, 2));
             NPCG_CUDA(cudaMemset(s->gbar, 0, 8));
             NPCG_CUDA(dalloc(&s->lpartial, (size_t)std::max(1, level_sync_grid(B)) * B));
+            // dependency flags instead of a grid barrier per level (NPCG_LEVELFLAGS=0: barriers)
+            bool flags = true;
+            if (const char *env = std::getenv("NPCG_LEVELFLAGS")) flags = std::atoi(env) != 0;
+            if (flags) {
+                const size_t words = (size_t)A->n * level_flag_groups(B);
+                NPCG_CUDA(dalloc(&s->lflags, words));
+                NPCG_CUDA(cudaMemset(s->lflags, 0, words * sizeof(unsigned)));
+            }
         }
     }
     if (s->ls) {  // A as ELL by slot (the line-order loop); rows wider than 16 keep the level path
@@ -592,6 +602,19 @@ static TrsvArgs level_args(npcg_solver *s, bool upper, int mode, int sb, const d
     return v;
 }
 
+// one level launch; flag mode takes the next epoch (flags cleared before it wraps)
+static cudaError_t level_launch(npcg_solver *s, LevelSyncArgs &a, cudaStream_t st) {
+    if (a.flags) {
+        if (s->lepoch == ~0u) {
+            const cudaError_t e = cudaMemsetAsync(s->lflags, 0, (size_t)s->F->n * level_flag_groups(s->B) * sizeof(unsigned), st);
+            if (e != cudaSuccess) return e;
+            s->lepoch = 0;
+        }
+        a.epoch = ++s->lepoch;
+    }
+    return launch_level_sync(a, st);
+}
+
 static LevelSyncArgs level_sync_args(npcg_solver *s, bool upper, int mode, int sb, const double *D, int db) {
     LevelSyncArgs v;
     const LevelDir &L = upper ? s->lv->bwd : s->lv->fwd;
@@ -609,6 +632,8 @@ static LevelSyncArgs level_sync_args(npcg_solver *s, bool upper, int mode, int s
     v.d_batched = db;
     v.partial = s->lpartial;
     v.bar = s->gbar;
+    v.flags = s->lflags;
+    v.max_rows = L.max_rows;
     v.drift_count = s->drift_count;
     return v;
 }
@@ -673,11 +698,11 @@ int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int s
         LevelSyncArgs f = level_sync_args(s, false, TRSV_PLAIN, sb, D, db);
         f.in = r;
         f.out = s->Y;
-        NPCG_CUDA(launch_level_sync(f, st));
+        NPCG_CUDA(level_launch(s, f, st));
         LevelSyncArgs b = level_sync_args(s, true, TRSV_PLAIN, sb, D, db);
         b.in = s->Y;
         b.out = z;
-        NPCG_CUDA(launch_level_sync(b, st));
+        NPCG_CUDA(level_launch(s, b, st));
     } else {
         launch_fill_sentinel((long long)F->n * B, z, st);  // level kernel polls z
         TrsvArgs f = level_args(s, false, TRSV_PLAIN, sb, D, db);
@@ -927,9 +952,9 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
                 NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
                 continue;
             }
-            NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return s->lv ? launch_level_sync(fwl, st) : launch_trsv(fw, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return s->lv ? level_launch(s, fwl, st) : launch_trsv(fw, st); }));
             NPCG_CUDA(timed(NPCG_PROF_SPMV_DRIFT, [&] { return launch_spmv(drift, st); }));
-            NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return s->lv ? launch_level_sync(bwl, st) : launch_trsv(bw, st); }));
+            NPCG_CUDA(timed(NPCG_PROF_TRSV_BWD, [&] { return s->lv ? level_launch(s, bwl, st) : launch_trsv(bw, st); }));
             NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
         }
         passes += check;

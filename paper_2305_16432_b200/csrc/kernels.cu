@@ -9,6 +9,7 @@
 // sparse.py:213-239; only dot products / norms (reductions) differ in
 // order from numpy's BLAS ddot. Reductions are fixed-order (no float
 // atomics), so the path is run-to-run deterministic.
+#include <cstdlib>
 #include <atomic>
 
 #include "kernels.cuh"
@@ -118,6 +119,18 @@ struct VecT<2> {
     static __device__ __forceinline__ void get(type v, double *o) {
         o[0] = v.x;
         o[1] = v.y;
+    }
+};
+template <>
+struct VecT<4> {  // two 16-byte loads
+    struct type {
+        double2 lo, hi;
+    };
+    static __device__ __forceinline__ void get(const type &v, double *o) {
+        o[0] = v.lo.x;
+        o[1] = v.lo.y;
+        o[2] = v.hi.x;
+        o[3] = v.hi.y;
     }
 };
 
@@ -1027,10 +1040,15 @@ cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s) {
     if (a.ecol) return launch_spmv_ell(a, s);
     // 16-byte column pairs when every row of every operand stays 16-byte aligned
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
-    const int VW = (a.B % 2 == 0 && al16(a.X) && al16(a.Y) && al16(a.Bv) && al16(a.R) && al16(a.P) &&
-                    (!a.vb || al16(a.vals)))
-                       ? 2
-                       : 1;
+    const bool even16 = a.B % 2 == 0 && al16(a.X) && al16(a.Y) && al16(a.Bv) && al16(a.R) && al16(a.P) &&
+                        (!a.vb || al16(a.vals));
+    // four columns per lane (one pass over the rows) for wide shared-matrix
+    // batches: twice the gathers in flight per row (NPCG_SPMV_VW4=0 disables)
+    static const bool vw4_on = [] {
+        const char *env = std::getenv("NPCG_SPMV_VW4");
+        return !env || std::atoi(env) != 0;
+    }();
+    const int VW = (even16 && vw4_on && a.B % 4 == 0 && a.B >= 128 && !a.vb && a.op != SPMV_RESID_DRIFT) ? 4 : even16 ? 2 : 1;
     const int TL = team_lanes((a.B + VW - 1) / VW);
     const int teams = kSpmvThreads / TL;
     long long need = (a.n + teams - 1) / teams;
@@ -1039,7 +1057,14 @@ cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s) {
     else grid = (int)std::min<long long>(std::max<long long>(need, 1), (long long)kReduceBlocksPerSm * num_sms());
     size_t smem = a.op == SPMV_PLAIN ? 0 : (size_t)teams * a.B * sizeof(double);
     smem = std::max(smem, (size_t)kSpmvThreads * sizeof(double));
-    if (TL == 32 && (long long)a.n * a.B < (1ll << 31)) {
+    if (VW == 4 && (long long)a.n * a.B < (1ll << 31)) {
+        switch (a.op) {  // the drift op keeps two columns per lane (register pressure)
+            case SPMV_PLAIN: spmv_warp_t<4, false, SPMV_PLAIN>(a, grid, smem, s); break;
+            case SPMV_APDOT: spmv_warp_t<4, false, SPMV_APDOT>(a, grid, smem, s); break;
+            case SPMV_RESID_INIT: spmv_warp_t<4, false, SPMV_RESID_INIT>(a, grid, smem, s); break;
+            default: spmv_warp_t<4, false, SPMV_RESID_FINAL>(a, grid, smem, s); break;
+        }
+    } else if (TL == 32 && (long long)a.n * a.B < (1ll << 31)) {
         if (VW == 2) spmv_warp_vw<2>(a, grid, smem, s);
         else spmv_warp_vw<1>(a, grid, smem, s);
     } else if (VW == 2) {

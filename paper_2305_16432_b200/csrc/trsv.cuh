@@ -95,7 +95,16 @@ struct LevelSyncArgs {
     double *partial = nullptr;   // [grid][B]
     unsigned *bar = nullptr;     // [2] zero-initialised barrier words
     int *drift_count = nullptr;
+    // dependency-flag mode (no barrier between levels): flags[row * nflag +
+    // f] >= epoch once row's column group f is final in this launch;
+    // zero-initialised, epoch strictly increasing across launches
+    unsigned *flags = nullptr;
+    unsigned epoch = 0;
+    int max_rows = 0;   // widest level (flag-mode grid sizing)
+    int sleep_ns = 20;  // flag poll back-off
 };
+// flag words per row: one per warp of 32 columns (B % 32 == 0), else one per column
+inline int level_flag_groups(int B) { return B % 32 == 0 ? B / 32 : B; }
 int level_sync_grid(int B);
 cudaError_t launch_level_sync(const LevelSyncArgs &a, cudaStream_t s);
 // packed[e * B + b] = S[perm[e] * B + b] (batched) | packed[e] = S[perm[e]]

@@ -144,3 +144,80 @@ def test_level_sync_distinct_systems(gpu, levelsync):
         assert rep.converged and orep.converged
         assert abs(rep.iterations - orep.iterations) <= 1, (s, rep.iterations, orep.iterations)
         assert rel(X[:, s], ox) <= X_TOL
+
+
+# ---- the walk variants (trsv_level.cu): dependency flags (warp per row for
+# B a multiple of 32 dividing into <= 8 warps, thread per column otherwise)
+# and the barrier-per-level walk; every one bitwise the oracle's solves ----
+
+
+@pytest.mark.parametrize("flags", ["1", "0"])
+@pytest.mark.parametrize("B", [1, 5, 32, 64, 96, 128, 256])
+def test_level_walk_apply_inverse_bitwise(gpu, levelsync, monkeypatch, B, flags):
+    import torch
+    monkeypatch.setenv("NPCG_LEVELFLAGS", flags)
+    A = inputs.poisson_3d(k=7, batch=1).A
+    rng = np.random.default_rng(100 + B)
+    low = A.strict_lower()
+    vals = rng.uniform(-0.2, 0.2, size=low.nnz)
+    oF = port.Factor(A.n, port.Csr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    R = rng.standard_normal((A.n, B))
+    P = gnn.assemble_preconditioner(vals, A)
+    Z = P.apply_inverse(torch.from_numpy(R).cuda()).cpu().numpy()
+    for j in sorted({0, B // 2, B - 1}):
+        np.testing.assert_array_equal(Z[:, j], oF.apply_inverse(R[:, j]))
+
+
+@pytest.mark.parametrize("B", [32, 128])
+def test_level_walk_pcg_flags_vs_barrier(gpu, levelsync, monkeypatch, B):
+    """Shared factor, B columns: the flag walk and the barrier walk solve the
+    same systems (their dot products sum in different fixed orders)."""
+    prob = inputs.poisson_3d(k=8, batch=B)
+    A = prob.A
+    rng = np.random.default_rng(B)
+    vals = rng.uniform(-0.15, 0.0, size=A.strict_lower().nnz)
+    thr = (1e-8,)
+    out = {}
+    for flags in ("1", "0"):
+        monkeypatch.setenv("NPCG_LEVELFLAGS", flags)
+        P = gnn.assemble_preconditioner(vals, A)
+        out[flags] = pcg.pcg_solve_batch(A, prob.rhs, P, pcg.SolveOptions(thresholds=thr, max_iter=3000))
+    (X1, r1), (X0, r0) = out["1"], out["0"]
+    for s in range(B):
+        assert r1[s].converged and r0[s].converged
+        assert abs(r1[s].iterations - r0[s].iterations) <= 1, (s, r1[s].iterations, r0[s].iterations)
+        assert rel(X1[:, s], X0[:, s]) <= X_TOL
+    oA = port.Csr(A.n, A.row_ptr, A.col_idx, A.values)
+    low = A.strict_lower()
+    oF = port.Factor(A.n, port.Csr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    ox, orep = port.pcg_solve(oA, prob.rhs[:, B - 1], oF, thresholds=thr, max_iter=3000)
+    assert abs(r1[B - 1].iterations - orep.iterations) <= 1
+    assert rel(X1[:, B - 1], ox) <= X_TOL
+
+
+def test_level_walk_distinct_systems_warp_rows(gpu, levelsync, monkeypatch):
+    """Per-system A and L' at B = 64 (warp per row, two columns per lane,
+    factor values [entry][B]): the flag walk against the barrier walk on every
+    column, and against the oracle on systems 0-4 (the conditioning the batch-5
+    test above pins)."""
+    prob = inputs.heat_3d(k=7, batch=64)
+    A, vals = prob.A, prob.values
+    model, ohp = perturbed_model(1)
+    thr = (1e-10,)
+    out = {}
+    for flags in ("1", "0"):
+        monkeypatch.setenv("NPCG_LEVELFLAGS", flags)
+        P = gnn.build_learned_batch(model, A, prob.rhs, values=vals)
+        out[flags] = pcg.pcg_solve_batch(A, prob.rhs, P, pcg.SolveOptions(thresholds=thr, max_iter=3000), values=vals)
+    (X, reps), (X0, reps0) = out["1"], out["0"]
+    for s in range(64):
+        assert reps[s].converged and reps0[s].converged
+        assert abs(reps[s].iterations - reps0[s].iterations) <= 1, (s, reps[s].iterations, reps0[s].iterations)
+        assert rel(X[:, s], X0[:, s]) <= X_TOL
+    for s in (0, 2, 4):
+        oA = port.Csr(A.n, A.row_ptr, A.col_idx, np.ascontiguousarray(vals[:, s]))
+        oF = port.build_learned(ohp, model.params, oA, prob.rhs[:, s])
+        ox, orep = port.pcg_solve(oA, prob.rhs[:, s], oF, thresholds=thr, max_iter=3000)
+        assert orep.converged
+        assert abs(reps[s].iterations - orep.iterations) <= 1, (s, reps[s].iterations, orep.iterations)
+        assert rel(X[:, s], ox) <= X_TOL

@@ -31,7 +31,7 @@ def test_spmv_batched_bitwise(gpu):
     prob = _heat(20)
     A = prob.A
     rng = np.random.default_rng(1)
-    for B in (1, 3, 8, 32, 64, 100):
+    for B in (1, 3, 8, 32, 64, 100, 128, 200, 256):  # 128+: four columns per lane
         X = rng.standard_normal((A.n, B))
         Y = sparse.spmv_device(A, torch.from_numpy(X).cuda(), B=B).cpu().numpy()
         for b in range(B):

@@ -44,6 +44,30 @@ def run(cfg, k, batch, gain, steps):
         return gnn.build_learned_batch(model, A, rhs, values=vals)
 
     P = build()
+    if os.environ.get("PROFILE_ONLY"):  # one solve, for ncu
+        opts1 = pcg.SolveOptions(thresholds=(prob.rtol,), max_iter=int(os.environ.get("PROFILE_ITERS", "3")))
+        pcg.pcg_solve_batch(A, rhs, P, opts1, values=vals)
+        torch.cuda.synchronize()
+        return
+    if os.environ.get("SWEEP"):  # "label:VAR=v,VAR=v;label:..." -> PCG time per setting
+        for item in os.environ["SWEEP"].split(";"):
+            label, _, kv = item.partition(":")
+            for pair in filter(None, kv.split(",")):
+                key, _, v = pair.partition("=")
+                os.environ[key] = v
+            pcg.pcg_solve_batch(A, rhs, P, opts, values=vals)
+            ms = []
+            for _ in range(steps):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                X, reps = pcg.pcg_solve_batch(A, rhs, P, opts, values=vals)
+                e1.record()
+                e1.synchronize()
+                ms.append(e0.elapsed_time(e1))
+            print(json.dumps({"sweep": label, "cfg": cfg, "batch": int(rhs.shape[1]), "pcg_ms": round(float(np.mean(ms)), 3),
+                              "converged": bool(all(r.converged for r in reps))}), flush=True)
+        return
     X, reps = pcg.pcg_solve_batch(A, rhs, P, opts, values=vals)  # warm-up
     times, g_ms, p_ms = [], [], []
     for _ in range(steps):
