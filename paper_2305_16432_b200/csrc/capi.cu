@@ -137,6 +137,7 @@ struct npcg_solver {
     unsigned *lflags = nullptr;  // dependency-flag mode: [n][level_flag_groups(B)], or null (barrier per level)
     unsigned lepoch = 0;         // epoch of the last level launch
     int line_K = 0;  // launch shape (line_config_for) of the line P^{-1} kernel
+    int line_KS = 0; // the same with several systems per cluster (shared factor only; 0: none)
     // line mode: every loop vector is in line order ([b][nslot]): P, XL (x), BL (b)
     // too; A as ELL by slot
     double *XL = nullptr, *BL = nullptr;
@@ -291,7 +292,7 @@ int npcg_pattern_line_info(const npcg_pattern *pc, int32_t *lines, int32_t *warp
     if (lines) *lines = ls ? ls->lines : 0;
     if (warps) *warps = ls ? ls->fwd.warps : 0;
     if (steps) *steps = ls ? ls->steps : 0;
-    if (cluster) *cluster = ls ? line_config_for(*ls, std::max(batch, 1)) / 256 : 0;
+    if (cluster) *cluster = ls ? line_cfg_cluster(line_config_for(*ls, std::max(batch, 1))) : 0;
     return NPCG_OK;
 }
 
@@ -398,6 +399,18 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
         if (k > 0) {
             s->ls = ls;
             s->line_K = k;
+            // shared-factor batches may carry kr right-hand sides per cluster
+            // (interleaved dependency chains, NPCG_LINE_KR = 2 / 4). Off by
+            // default: at config 2 one right-hand side per 2-CTA cluster
+            // already covers 128 SMs and the per-launch latency decides
+            // (measured 123 us per 64 right-hand sides against 147 us with
+            // kr = 2 on 4-CTA clusters); it pays when the batch exceeds the SMs.
+            int kr = 1;
+            if (const char *env = std::getenv("NPCG_LINE_KR")) kr = std::atoi(env);
+            while (kr > 1 && !s->line_KS) {
+                s->line_KS = line_config_for(*ls, B, kr);
+                kr /= 2;
+            }
         }
     }
     // without a line schedule: level-synchronous solves when the batch gives
@@ -642,9 +655,10 @@ static LevelSyncArgs level_sync_args(npcg_solver *s, bool upper, int mode, int s
 // launch (ldlt_line_kernel); every vector in line order ([b][nslot]).
 static LineArgs line_args(npcg_solver *s, int mode, int sb, int db) {
     LineArgs l;
-    const int cfg = s->line_K;
+    const int cfg = (!sb && s->line_KS) ? s->line_KS : s->line_K;
     l.B = s->B;
-    l.cluster = cfg / 256;
+    l.kr = std::max(1, cfg >> 16);
+    l.cluster = line_cfg_cluster(cfg);
     l.group = cfg / 16 % 16;
     l.stages = cfg % 16;
     l.mode = mode;

@@ -47,7 +47,8 @@ TrsvSmem trsv_smem_plan(const Schedule &S, int G, int s_batched);
 // is in line order, system-major: element (slot q, system b) at b*nslot + q.
 struct LineArgs {
     int B = 1, mode = TRSV_PLAIN;
-    int cluster = 1, group = 2, stages = 2;  // CTAs per system, tiles per pipeline stage, stages per warp
+    int cluster = 1, group = 2, stages = 2;  // CTAs per cluster, tiles per pipeline stage, stages per warp
+    int kr = 1;  // systems per cluster (1, 2 or 4; more than one needs a shared factor and B % kr == 0)
     int nslot = 0, warps = 0, ring = 64;     // ring: steps per warp's incoming value ring (LineDir::ring)
     const int *meta_f = nullptr, *meta_b = nullptr;  // LineDir::meta of the two directions
     long long fac_slots = 0;
@@ -64,13 +65,54 @@ struct LineArgs {
     const double *AP = nullptr;   // PCG: A p
     SolveState st{};
     int *drift_count = nullptr;
+    long long *trace = nullptr;  // debug timeline buffer (set by launch_ldlt_line)
 };
-// Launch shape (cluster * 256 + group * 16 + stages) for B systems that fits
-// shared memory, 0 when none does. NPCG_LINE_CFG (group * 16 + stages) and
-// NPCG_LINE_CLUSTER override.
-int line_config_for(const LineSched &L, int B);
+// ---- launch geometry shared by trsv_line.cu and the kernel instances ----
+// operand stages per warp (a slot is refilled the stage after its use): three
+// up to 3-tile stages, two for 4-tile stages (shared memory)
+// (tiles per stage, stages in flight) combinations the kernel is built for
+__host__ __device__ constexpr bool line_shape_ok(int G, int NS) {
+    return (G == 4 && NS == 2) || (G == 2 && (NS == 3 || NS == 4)) || (G == 1 && NS == 4);
+}
+
+__host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
+__host__ __device__ constexpr int slot_arrays(int KR) { return kLineKinds + 3 * KR; }  // arrays of a stage slot
+constexpr int kLineMaxKR = 4;
+// line warps per CTA: a 2-CTA cluster keeps 4 pairs (256 threads: the full
+// register file per thread), one CTA or a 4-CTA cluster up to 8 pairs
+__host__ __device__ constexpr int line_cta_warps(int C) { return C == 2 ? kLineMaxWarps / 2 : kLineMaxWarps; }
+struct LineSmem {  // byte offsets into dynamic shared memory
+    size_t ring_f, ring_b, bars, slots, slot_bytes, total;
+};
+
+// per CTA: two direction rings [WL][R][KR]; per line-warp pair 4 x NS mbarriers
+// (tma, full, done, rtma) and NS slots
+__host__ __device__ inline LineSmem line_layout(int WL, int R, int G, int NS, int KR) {
+    LineSmem m;
+    m.ring_f = 0;
+    m.ring_b = al128((size_t)WL * R * KR * 8);
+    m.bars = m.ring_b + al128((size_t)WL * R * KR * 8);
+    m.slots = al128(m.bars + (size_t)WL * 4 * NS * 8);
+    m.slot_bytes = (size_t)G * slot_arrays(KR) * kTileSlots * 8;
+    m.total = m.slots + (size_t)WL * NS * m.slot_bytes;
+    return m;
+}
+inline size_t line_smem_bytes(int WL, int R, int G, int NS, int KR) { return line_layout(WL, R, G, NS, KR).total; }
+constexpr int kLineTraceWarps = 4 * 8, kLineTraceStages = 1024;  // debug timeline (NPCG_LINE_TRACE builds)
+// Launch shape (kr << 16 | cluster * 256 + group * 16 + stages) for B systems,
+// kr of them per cluster, that fits shared memory; 0 when none does.
+// NPCG_LINE_CFG (group * 16 + stages) and NPCG_LINE_CLUSTER override.
+int line_config_for(const LineSched &L, int B, int KR = 1);
+inline int line_cfg_cluster(int cfg) { return (cfg >> 8) & 0xff; }
 int line_trace_copy(long long *out, int n);  // debug timeline (NPCG_LINE_TRACE builds)
 cudaError_t launch_ldlt_line(const LineArgs &a, cudaStream_t s);
+// the instances behind it: k<systems per cluster><p: PCG mode, n: plain> (trsv_line_k*.cu)
+cudaError_t launch_ldlt_k1p(const LineArgs &a, cudaStream_t s);
+cudaError_t launch_ldlt_k1n(const LineArgs &a, cudaStream_t s);
+cudaError_t launch_ldlt_k2p(const LineArgs &a, cudaStream_t s);
+cudaError_t launch_ldlt_k2n(const LineArgs &a, cudaStream_t s);
+cudaError_t launch_ldlt_k4p(const LineArgs &a, cudaStream_t s);
+cudaError_t launch_ldlt_k4n(const LineArgs &a, cudaStream_t s);
 // rD[q] = 1 / D[q] (correctly rounded), count entries
 cudaError_t launch_reciprocal(long long count, const double *D, double *rD, cudaStream_t s);
 // factor values S[p * ps + b * bs] -> line order of `L` (per system when batched)

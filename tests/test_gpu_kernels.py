@@ -96,6 +96,60 @@ def test_apply_inverse_paths_bitwise(gpu, monkeypatch, path, k):
         np.testing.assert_array_equal(Z[:, b], oF.apply_inverse(R[:, b]))
 
 
+@pytest.mark.parametrize("kr,k,B", [(2, 64, 8), (4, 64, 8), (2, 96, 6), (4, 200, 4), (2, 256, 4)])
+def test_apply_inverse_several_rhs_per_cluster_bitwise(gpu, monkeypatch, kr, k, B):
+    """NPCG_LINE_KR right-hand sides per cluster (shared factor: one staged
+    factor, interleaved dependency chains in the line warp) give the
+    reference's bits for every column."""
+    import torch
+    monkeypatch.setenv("NPCG_LINE_KR", str(kr))
+    prob = _heat(k)
+    A = prob.A
+    rng = np.random.default_rng(40 + kr)
+    low = A.strict_lower()
+    vals = rng.uniform(-0.4, 0.4, size=low.nnz)
+    R = rng.standard_normal((A.n, B))
+    pat = A.device_pattern(factor=True)
+    import paper_2305_16432_b200._native as nat
+    S = torch.zeros((A.nnz,), dtype=torch.float64, device="cuda")
+    low_d = torch.from_numpy(vals).cuda().contiguous()
+    nat.check(nat.lib().npcg_factor_from_lower(pat.handle, 1, nat.ptr(low_d), 0, nat.ptr(S), nat.stream_handle()))
+    D = torch.from_numpy(A.diagonal()).cuda()
+    Z = sparse.apply_inverse_device(pat, S, False, D, False, torch.from_numpy(R).cuda(), B).cpu().numpy()
+    oF = port.Factor(A.n, port.Csr(A.n, low.row_ptr, low.col_idx, vals), A.diagonal())
+    for b in range(B):
+        np.testing.assert_array_equal(Z[:, b], oF.apply_inverse(R[:, b]))
+
+
+def test_pcg_several_rhs_per_cluster_same_iterates(gpu, monkeypatch):
+    """A shared-factor batch solved with 1, 2 and 4 right-hand sides per
+    cluster: same iteration counts and bitwise equal solutions (same launch
+    shape otherwise), including columns that converge at different passes."""
+    import torch
+    from paper_2305_16432_b200 import gnn, pcg
+    outs = []
+    for kr in ("1", "2", "4"):
+        monkeypatch.setenv("NPCG_LINE_KR", kr)
+        # the same stage length for every kr (the shared-memory budget would pick longer
+        # stages for kr = 1): dot products then accumulate in the same order
+        monkeypatch.setenv("NPCG_LINE_CFG", str(1 * 16 + 4))
+        prob = inputs.poisson_2d(k=96, batch=8)  # 95 lines: one CTA per cluster for every kr
+        A = prob.A
+        rng = np.random.default_rng(7)
+        P = gnn.assemble_preconditioner(rng.uniform(-0.2, 0.2, A.strict_lower().nnz), A)
+        rhs = prob.rhs.copy()
+        rhs[:, 3] = 0.0  # a zero right-hand side inside the batch
+        rhs[:, 5] *= 1e-3
+        X, reps = pcg.pcg_solve_batch(A, torch.from_numpy(rhs).cuda(), P,
+                                      pcg.SolveOptions(thresholds=(1e-4, 1e-10), max_iter=2000))
+        outs.append((X.cpu().numpy(), [r.iterations for r in reps], [r.converged for r in reps]))
+    assert all(outs[0][2])
+    assert len(set(outs[0][1])) > 1  # columns finish at different passes
+    for X, its, conv in outs[1:]:
+        assert its == outs[0][1] and conv == outs[0][2]
+        np.testing.assert_array_equal(X, outs[0][0])
+
+
 def test_apply_inverse_wide_grid_bitwise(gpu):
     """A 513 x 513 grid (511 lines: 16 warps, a 2-CTA cluster per system,
     one-tile stages): bitwise equal to the reference's solve."""
