@@ -250,6 +250,12 @@ int npcg_solver_history(const npcg_solver *s, double *out, int64_t ld, int64_t c
 typedef struct npcg_fem_plan npcg_fem_plan;
 int npcg_fem_plan_create(int64_t n_vertices, int64_t n_triangles, const int64_t *triangles_host,
                          npcg_fem_plan **out);
+/* The same for P1 elements with `verts_per_elem` vertices: 3 (triangles, 2-D
+ * vertices) or 4 (positively oriented tetrahedra, 3-D vertices: configs 4 / 5;
+ * pcgkit has no 3-D element, the host definition is inputs.tet_blocks:
+ * K_ij = |T| grad l_i . grad l_j, M_ij = |T| (1 + d_ij) / 20). */
+int npcg_fem_plan_create_p1(int64_t n_vertices, int64_t n_elements, int verts_per_elem, const int64_t *elements_host,
+                            npcg_fem_plan **out);
 int npcg_fem_plan_destroy(npcg_fem_plan *p);
 /* The assembled CSR pattern: *nnz always; row_ptr [n_vertices + 1] and
  * col_idx [nnz] (host, int64, nullable) the reference's layout. */
@@ -258,13 +264,21 @@ int npcg_fem_plan_pattern(const npcg_fem_plan *p, int64_t *nnz, int64_t *row_ptr
 #define NPCG_FEM_K          0  /* sum of (coef_e * K_e)                    */
 #define NPCG_FEM_M          1  /* sum of M_e                                */
 #define NPCG_FEM_M_PLUS_SK  2  /* (sum M_e) + scale * (sum coef_e K_e)      */
-/* Device assembly of B systems: vertices [n_vertices][2][VB] (VB = B when
+/* Device assembly of B systems: vertices [n_vertices][dim][VB] (dim = 2 for
+ * triangles, 3 for tetrahedra; VB = B when
  * vertices_batched, else 1), coef [nt][CB] nullable (CB = B when
  * coef_batched), values out [nnz][B]. bad_dev (device int, nullable) is set
  * to 1 when a triangle is degenerate or clockwise (fem.py raises there). */
 int npcg_fem_assemble(const npcg_fem_plan *p, int B, const double *vertices, int vertices_batched,
                       const double *coef, int coef_batched, int mode, double scale, double *values,
                       int *bad_dev, void *stream);
+/* Restriction of assembled values to a sub-pattern -- the Dirichlet
+ * elimination of fem.py:209-215 (SparseMatrixCsr.submatrix, sparse.py:155-163)
+ * on the device: dst[q] = src[sel[q]] for q < count (sel: device int32, the
+ * kept slots in order), or rows of a column-minor (count, B) array when
+ * `batched`. */
+int npcg_gather_values(int64_t count, int B, int batched, const int32_t *sel, const double *src, double *dst,
+                       void *stream);
 
 #ifdef __cplusplus
 }

@@ -108,6 +108,8 @@ SIGNATURES = {
     "npcg_launch_count": (I64, []),
     "npcg_debug_line_trace": (I32, [P, I32]),
     "npcg_fem_plan_create": (I32, [I64, I64, P, ctypes.POINTER(P)]),
+    "npcg_fem_plan_create_p1": (I32, [I64, I64, I32, P, ctypes.POINTER(P)]),
+    "npcg_gather_values": (I32, [I64, I32, I32, P, P, P, P]),
     "npcg_fem_plan_destroy": (I32, [P]),
     "npcg_fem_plan_pattern": (I32, [P, ctypes.POINTER(I64), P, P]),
     "npcg_fem_assemble": (I32, [P, I32, P, I32, P, I32, I32, ctypes.c_double, P, P, P]),

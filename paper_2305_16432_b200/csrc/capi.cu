@@ -1129,6 +1129,24 @@ int npcg_gnn_build_factor_mesh(const npcg_gnn *g, const npcg_pattern *A, int B, 
 
 extern "C" int64_t npcg_launch_count(void) { return (int64_t)launch_count(); }
 
+// Restriction of assembled values to a sub-pattern (Dirichlet elimination,
+// fem.py:209-215 / SparseMatrixCsr.submatrix): dst[q (* B + b)] = src[sel[q] (* B + b)].
+extern "C" int npcg_gather_values(int64_t count, int B, int batched, const int32_t *sel, const double *src, double *dst,
+                                  void *stream) {
+    if (count < 0 || B < 1 || (count && (!sel || !src || !dst))) return fail(NPCG_ERR_ARGUMENT, "bad argument");
+    if (count == 0) return NPCG_OK;
+    // launch_gather_pack writes packed[b][e] = S[perm[e] * ps + b * bs]; with the
+    // column index fastest on both sides one "system" of count * B entries does it
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!batched || B == 1) {
+        launch_gather_pack(count, 1, 0, 1, 0, sel, src, dst, s);
+    } else {
+        launch_gather_rows(count, B, sel, src, dst, s);
+    }
+    NPCG_CUDA(cudaGetLastError());
+    return NPCG_OK;
+}
+
 // Diagnostics: the line-solve timeline of CTA 0 (clock64 per batch and event,
 // [16][2048]); all zeros unless the library was built with -DNPCG_LINE_TRACE.
 extern "C" int npcg_debug_line_trace(long long *out, int n) { return line_trace_copy(out, n); }
@@ -1136,25 +1154,31 @@ extern "C" int npcg_debug_line_trace(long long *out, int n) { return line_trace_
 // ---- P1 FEM assembly (fem.cu) ---------------------------------------------
 struct npcg_fem_plan {
     long long nv = 0, nt = 0, nnz = 0;
+    int nper = 3;  // vertices per element
     std::vector<long long> row_ptr, col;
     int *d_starts = nullptr, *d_order = nullptr, *d_tri = nullptr;
     double *d_kq = nullptr, *d_ms = nullptr, *d_mq = nullptr;  // shared-mesh scratch (fem_prep_kernel)
 };
 
 extern "C" int npcg_fem_plan_create(int64_t nv, int64_t nt, const int64_t *tri, npcg_fem_plan **out) {
+    return npcg_fem_plan_create_p1(nv, nt, 3, tri, out);
+}
+
+extern "C" int npcg_fem_plan_create_p1(int64_t nv, int64_t nt, int nper, const int64_t *tri, npcg_fem_plan **out) {
     if (!out || !tri) return fail(NPCG_ERR_ARGUMENT, "null argument");
     *out = nullptr;
     FemPlanHost h;
-    const std::string err = fem_plan_build(nv, nt, reinterpret_cast<const long long *>(tri), h);
+    const std::string err = fem_plan_build(nv, nt, nper, reinterpret_cast<const long long *>(tri), h);
     if (!err.empty()) return fail(NPCG_ERR_DATA_FORMAT, err);
     std::unique_ptr<npcg_fem_plan> p(new npcg_fem_plan);
     p->nv = nv;
     p->nt = nt;
+    p->nper = nper;
     p->nnz = (long long)h.col.size();
     p->row_ptr = h.row_ptr;
     p->col.assign(h.col.begin(), h.col.end());
-    std::vector<int> t32(3 * nt);
-    for (long long q = 0; q < 3 * nt; ++q) t32[q] = (int)tri[q];
+    std::vector<int> t32((size_t)nper * nt);
+    for (long long q = 0; q < nper * nt; ++q) t32[q] = (int)tri[q];
     NPCG_CUDA(dalloc(&p->d_starts, h.starts.size()));
     NPCG_CUDA(dalloc(&p->d_order, h.order.size()));
     NPCG_CUDA(dalloc(&p->d_tri, t32.size()));
@@ -1216,6 +1240,7 @@ extern "C" int npcg_fem_assemble(const npcg_fem_plan *p, int B, const double *ve
     a.ms = p->d_ms;
     a.mq = p->d_mq;
     a.nt = (int)p->nt;
+    a.nper2 = p->nper * p->nper;
     NPCG_CUDA(launch_fem_assemble(a, flag, s));
     return NPCG_OK;
 }

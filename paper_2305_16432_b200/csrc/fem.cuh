@@ -11,10 +11,11 @@ enum FemMode : int { FEM_K = 0, FEM_M = 1, FEM_M_PLUS_SK = 2 };  // include/npcg
 
 struct FemArgs {
     int nnz = 0, B = 1, nt = 0;
+    int nper2 = 9;                // block entries per element: 9 (triangles) or 16 (tetrahedra)
     const int *starts = nullptr;  // [nnz + 1] runs of triplet ids per CSR slot
-    const int *order = nullptr;   // [9 nt] triplet ids in lexsort order
-    const int *tri = nullptr;     // [nt][3]
-    const double *V = nullptr;    // vertices [nv][2][vb]
+    const int *order = nullptr;   // [nper2 nt] triplet ids in lexsort order
+    const int *tri = nullptr;     // [nt][3] or [nt][4]
+    const double *V = nullptr;    // vertices [nv][dim][vb], dim = 2 or 3
     int vb = 1;                   // B when every system has its own vertices, else 1
     const double *coef = nullptr; // per-element stiffness coefficient [nt][cb] (nullable)
     int cb = 1;
@@ -31,8 +32,8 @@ struct FemPlanHost {
     std::vector<long long> row_ptr;
 };
 
-// stable (row, col) lexsort of the 9 nt triplets (fem.py:116-134); "" or an error
-std::string fem_plan_build(long long nv, long long nt, const long long *tri, FemPlanHost &h);
+// stable (row, col) lexsort of the nper^2 nt triplets (fem.py:116-134); "" or an error
+std::string fem_plan_build(long long nv, long long nt, int nper, const long long *elems, FemPlanHost &h);
 cudaError_t launch_fem_assemble(const FemArgs &a, int *bad, cudaStream_t s);
 
 }  // namespace npcg

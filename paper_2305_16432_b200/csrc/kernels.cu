@@ -1036,6 +1036,22 @@ void launch_gather_pack(long long per, int B, int sb, long long ps, long long bs
                                                                                              S, packed);
 }
 
+// dst[q * B + b] = src[sel[q] * B + b]: rows of a column-minor (count, B) array
+__global__ void gather_rows_kernel(long long count, int B, const int *sel, const double *src, double *dst) {
+    const long long total = count * B;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const long long q = t / B;
+        dst[t] = src[(long long)sel[q] * B + (t - q * B)];
+    }
+}
+
+void launch_gather_rows(long long count, int B, const int *sel, const double *src, double *dst, cudaStream_t s) {
+    const long long total = count * B;
+    if (total <= 0) return;
+    note_launch();
+    gather_rows_kernel<<<(int)std::min<long long>((total + 255) / 256, 16384), 256, 0, s>>>(count, B, sel, src, dst);
+}
+
 cudaError_t launch_spmv(const SpmvArgs &a, cudaStream_t s) {
     if (a.ecol) return launch_spmv_ell(a, s);
     // 16-byte column pairs when every row of every operand stays 16-byte aligned

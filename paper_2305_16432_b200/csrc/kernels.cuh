@@ -69,6 +69,7 @@ cudaError_t launch_from_line(int nslot, int B, const int *rowof, const double *s
 // all-line-order PCG vectors: p / x update, and value gathers into a packed order
 cudaError_t launch_pupd_ell(int nslot, int B, const double *z, double *p, double *x, const SolveState &st,
                             cudaStream_t s);
+void launch_gather_rows(long long count, int B, const int *sel, const double *src, double *dst, cudaStream_t s);
 void launch_gather_pack(long long per, int B, int sb, long long ps, long long bs, const int *perm, const double *S,
                         double *packed, cudaStream_t s);
 

@@ -363,25 +363,31 @@ def _host_spmv(A: SparseMatrixCsr, x):
 
 class DeviceAssembler:
     """P1 assembly on the device (libnpcg ``npcg_fem_assemble``, csrc/fem.cu):
-    the same triangle topology as :class:`Assembler`, any number of vertex
-    sets / per-element coefficients per call, values bit-identical to
-    ``Assembler.values(element_blocks(...))`` (fem.py:42-69, 116-134).
+    the same element topology as :class:`Assembler` -- triangles (nt, 3) with
+    2-D vertices or tetrahedra (nt, 4) with 3-D vertices -- any number of
+    vertex sets / per-element coefficients per call, values bit-identical to
+    ``Assembler.values(element_blocks(...))`` (fem.py:42-69, 116-134) and to
+    ``Assembler.values(tet_blocks(...))``.
 
     ``values(vertices, coef=None, mode="K" | "M" | "M+sK", scale=1.0)``:
-    vertices (nv, 2) or (nv, 2, B); coef None, (nt,) or (nt, B); returns a
+    vertices (nv, dim) or (nv, dim, B); coef None, (nt,) or (nt, B); returns a
     device float64 tensor (nnz,) or (nnz, B). Raises ValueError on a
-    degenerate / clockwise triangle like element_blocks."""
+    degenerate / negatively oriented element like element_blocks / tet_blocks."""
 
     MODES = {"K": 0, "M": 1, "M+sK": 2}
 
-    def __init__(self, n_vertices: int, triangles: np.ndarray):
+    def __init__(self, n_vertices: int, elements: np.ndarray):
         import ctypes
 
         from . import _native
         self._lib = _native.lib()
-        tri = np.ascontiguousarray(triangles, dtype=np.int64)
+        tri = np.ascontiguousarray(elements, dtype=np.int64)
+        if tri.ndim != 2 or tri.shape[1] not in (3, 4):
+            raise ValueError("elements must be (nt, 3) triangles or (nt, 4) tetrahedra")
+        self.dim = tri.shape[1] - 1
         h = ctypes.c_void_p()
-        _native.check(self._lib.npcg_fem_plan_create(int(n_vertices), len(tri), tri.ctypes.data, ctypes.byref(h)))
+        _native.check(self._lib.npcg_fem_plan_create_p1(int(n_vertices), len(tri), tri.shape[1], tri.ctypes.data,
+                                                        ctypes.byref(h)))
         self._h = h
         nnz = ctypes.c_int64()
         _native.check(self._lib.npcg_fem_plan_pattern(h, ctypes.byref(nnz), None, None))
@@ -404,8 +410,8 @@ class DeviceAssembler:
         if mode not in self.MODES:
             raise ValueError(f"mode must be one of {sorted(self.MODES)}")
         V = torch.as_tensor(vertices, dtype=torch.float64, device="cuda").contiguous()
-        if V.dim() not in (2, 3) or V.shape[0] != self.n or V.shape[1] != 2:
-            raise ValueError("vertices must be (n_vertices, 2) or (n_vertices, 2, B)")
+        if V.dim() not in (2, 3) or V.shape[0] != self.n or V.shape[1] != self.dim:
+            raise ValueError(f"vertices must be (n_vertices, {self.dim}) or (n_vertices, {self.dim}, B)")
         B = V.shape[2] if V.dim() == 3 else 1
         C = None
         if coef is not None:
@@ -424,5 +430,26 @@ class DeviceAssembler:
             self._h, B, _native.ptr(V), int(V.dim() == 3), _native.ptr(C), int(C is not None and C.dim() == 2),
             self.MODES[mode], float(scale), _native.ptr(out), _native.ptr(bad), _native.stream_handle()))
         if check and int(bad.item()):
-            raise ValueError("degenerate or clockwise triangle (reduce the jitter)")
+            raise ValueError("degenerate or inverted element (reduce the jitter)")
+        return out
+
+
+class DeviceRestriction(Restriction):
+    """:class:`Restriction` whose value gather runs on the device
+    (``npcg_gather_values``): the Dirichlet elimination of fem.py:209-215
+    applied to device-assembled values without a host round trip.
+    ``values(full)`` takes a device tensor (nnz_full,) or (nnz_full, B)."""
+
+    def values(self, values_full):
+        import torch
+
+        from . import _native
+        if not hasattr(self, "_sel_dev"):
+            self._sel_dev = torch.from_numpy(self.sel.astype(np.int32)).cuda()
+        src = values_full.contiguous()
+        batched = src.dim() == 2
+        B = src.shape[1] if batched else 1
+        out = torch.empty((len(self.sel), B) if batched else (len(self.sel),), dtype=torch.float64, device=src.device)
+        _native.check(_native.lib().npcg_gather_values(len(self.sel), B, int(batched), _native.ptr(self._sel_dev),
+                                                       _native.ptr(src), _native.ptr(out), _native.stream_handle()))
         return out
