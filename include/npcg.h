@@ -280,6 +280,37 @@ int npcg_fem_assemble(const npcg_fem_plan *p, int B, const double *vertices, int
 int npcg_gather_values(int64_t count, int B, int batched, const int32_t *sel, const double *src, double *dst,
                        void *stream);
 
+/* ---- training step --------------------------------
+ * Replaces, for one (A, b, x) tuple, train.tuple_loss + ad.backward
+ * (train.py:189-205; loss_data / apply_learned_factor train.py:104-150; the
+ * tape rules autodiff.py:113-253) and train.adam_step (train.py:164-185), in
+ * fp64 like the reference, with a hand-written reverse pass; the reference
+ * network only (l == l_mp == 1, no north_star extensions).
+ *
+ * npcg_trainer_create: weights in the checkpoint layout of npcg_gnn_create
+ * (host); Adam moments start at zero.
+ * npcg_trainer_tuple_grad: node_in [n] / edge_in [nnz] are the network inputs
+ * AFTER the optional standardisation (gnn.py:239-245; the Python mirror forms
+ * them with the reference's sorted statistics), A_vals [nnz], b, x [n]: all
+ * device fp64. *loss_host receives the tuple loss; the parameter gradient is
+ * ADDED to grad_accum [n_weights] (device; the caller sums a minibatch in
+ * tuple-index order, train.py:208-226). Synchronises `stream`.
+ * npcg_trainer_adam_step: one Adam update with g = grad * grad_scale (the
+ * minibatch mean); *nonfinite = 1 and no update when g has a non-finite entry
+ * (NonFiniteGradientError, train.py:175-176). */
+typedef struct npcg_trainer npcg_trainer;
+int npcg_trainer_create(const npcg_gnn_desc *desc, const double *weights_host, int64_t n_weights,
+                        npcg_trainer **out);
+int npcg_trainer_destroy(npcg_trainer *t);
+int npcg_trainer_get_weights(const npcg_trainer *t, double *weights_host);
+int npcg_trainer_set_weights(npcg_trainer *t, const double *weights_host, int reset_moments);
+int npcg_trainer_tuple_grad(npcg_trainer *t, const npcg_pattern *A, const double *A_vals,
+                            const double *node_in, const double *edge_in, const double *b, const double *x,
+                            double x0_aux_weight, double *loss_host, double *grad_accum, void *stream);
+int npcg_trainer_adam_step(npcg_trainer *t, const double *grad, double grad_scale, int64_t step,
+                           double learning_rate, double beta1, double beta2, double eps, int32_t *nonfinite,
+                           void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -110,6 +110,13 @@ SIGNATURES = {
     "npcg_fem_plan_create": (I32, [I64, I64, P, ctypes.POINTER(P)]),
     "npcg_fem_plan_create_p1": (I32, [I64, I64, I32, P, ctypes.POINTER(P)]),
     "npcg_gather_values": (I32, [I64, I32, I32, P, P, P, P]),
+    "npcg_trainer_create": (I32, [P, P, I64, ctypes.POINTER(P)]),
+    "npcg_trainer_destroy": (I32, [P]),
+    "npcg_trainer_get_weights": (I32, [P, P]),
+    "npcg_trainer_set_weights": (I32, [P, P, I32]),
+    "npcg_trainer_tuple_grad": (I32, [P, P, P, P, P, P, P, ctypes.c_double, P, P, P]),
+    "npcg_trainer_adam_step": (I32, [P, P, ctypes.c_double, I64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, P, P]),
     "npcg_fem_plan_destroy": (I32, [P]),
     "npcg_fem_plan_pattern": (I32, [P, ctypes.POINTER(I64), P, P]),
     "npcg_fem_assemble": (I32, [P, I32, P, I32, P, I32, I32, ctypes.c_double, P, P, P]),

@@ -14,6 +14,7 @@
 
 #include "../../include/npcg.h"
 #include "fem.cuh"
+#include "train.cuh"
 #include "gnn.cuh"
 #include "kernels.cuh"
 #include "pattern.h"
@@ -1128,6 +1129,63 @@ int npcg_gnn_build_factor_mesh(const npcg_gnn *g, const npcg_pattern *A, int B, 
 }  // extern "C"
 
 extern "C" int64_t npcg_launch_count(void) { return (int64_t)launch_count(); }
+
+// ---------------------------------------------------------------------------
+// Training step (train.cu): train.py:164-226 on the device
+struct npcg_trainer {
+    TrainNet net;
+};
+
+extern "C" int npcg_trainer_create(const npcg_gnn_desc *desc, const double *weights, int64_t n_weights,
+                                   npcg_trainer **out) {
+    if (!desc || !weights || !out) return fail(NPCG_ERR_ARGUMENT, "null argument");
+    *out = nullptr;
+    std::unique_ptr<npcg_trainer> t(new npcg_trainer);
+    const std::string err = t->net.init(*desc, weights, n_weights);
+    if (!err.empty()) return fail(NPCG_ERR_DIMENSION, err);
+    *out = t.release();
+    return NPCG_OK;
+}
+
+extern "C" int npcg_trainer_destroy(npcg_trainer *t) {
+    delete t;
+    return NPCG_OK;
+}
+
+extern "C" int npcg_trainer_get_weights(const npcg_trainer *t, double *weights_host) {
+    if (!t || !weights_host) return fail(NPCG_ERR_ARGUMENT, "null argument");
+    NPCG_CUDA(cudaMemcpy(weights_host, t->net.weights_dev(), (size_t)t->net.n_weights() * sizeof(double),
+                         cudaMemcpyDeviceToHost));
+    return NPCG_OK;
+}
+
+extern "C" int npcg_trainer_set_weights(npcg_trainer *t, const double *weights_host, int reset_moments) {
+    if (!t || !weights_host) return fail(NPCG_ERR_ARGUMENT, "null argument");
+    if (t->net.set_weights(weights_host, reset_moments)) return fail(NPCG_ERR_CUDA, "cudaMemcpy failed");
+    return NPCG_OK;
+}
+
+extern "C" int npcg_trainer_tuple_grad(npcg_trainer *t, const npcg_pattern *A, const double *A_vals,
+                                       const double *node_in, const double *edge_in, const double *b, const double *x,
+                                       double x0_aux_weight, double *loss_host, double *grad_accum, void *stream) {
+    if (!t || !A || !A_vals || !node_in || !edge_in || !b || !x || !loss_host || !grad_accum)
+        return fail(NPCG_ERR_ARGUMENT, "null argument");
+    std::string err;
+    const int rc = t->net.tuple_grad(*A, A_vals, node_in, edge_in, b, x, x0_aux_weight, loss_host, grad_accum,
+                                     (cudaStream_t)stream, err);
+    return rc == NPCG_OK ? NPCG_OK : fail(rc, err);
+}
+
+extern "C" int npcg_trainer_adam_step(npcg_trainer *t, const double *grad, double grad_scale, int64_t step,
+                                      double learning_rate, double beta1, double beta2, double eps, int32_t *nonfinite,
+                                      void *stream) {
+    if (!t || !grad || !nonfinite) return fail(NPCG_ERR_ARGUMENT, "null argument");
+    if (step < 1) return fail(NPCG_ERR_DIMENSION, "Adam step index starts at 1");
+    int nf = 0;
+    const int rc = t->net.adam(grad, grad_scale, step, learning_rate, beta1, beta2, eps, &nf, (cudaStream_t)stream);
+    *nonfinite = nf;
+    return rc == NPCG_OK ? NPCG_OK : fail(rc, "CUDA failure in the Adam step");
+}
 
 // Restriction of assembled values to a sub-pattern (Dirichlet elimination,
 // fem.py:209-215 / SparseMatrixCsr.submatrix): dst[q (* B + b)] = src[sel[q] (* B + b)].
