@@ -72,7 +72,7 @@ struct LineArgs {
 // up to 3-tile stages, two for 4-tile stages (shared memory)
 // (tiles per stage, stages in flight) combinations the kernel is built for
 __host__ __device__ constexpr bool line_shape_ok(int G, int NS) {
-    return (G == 4 && NS == 2) || (G == 2 && (NS == 3 || NS == 4)) || (G == 1 && NS == 4);
+    return (G == 4 && NS == 2) || (G == 3 && NS == 3) || (G == 2 && (NS == 3 || NS == 4)) || (G == 1 && NS == 4);
 }
 
 __host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }

@@ -82,11 +82,12 @@ int line_config_for(const LineSched &L, int B, int KR) {
     const int W = L.fwd.warps, R = std::max(L.fwd.ring, L.bwd.ring);
     const int NC = B / KR;  // clusters
     auto fits = [&](int c) { return (W + c - 1) / c <= line_cta_warps(c) && (c == 1 || W >= c); };
-    // shapes in order of preference: long stages first (the line warp's
-    // per-stage hand-offs amortise over 16 steps; measured 263 vs 249
-    // systems/s against 8-step stages four deep at config 2), then deeper
-    // pipelines of shorter stages
-    static const int prefs[][2] = {{4, 2}, {2, 4}, {2, 3}, {1, 4}};
+    // shapes in order of preference: 12-step stages three deep first (the
+    // helper's write-back -> refill -> prepare chain of a slot has two stages
+    // of slack instead of one: 116 vs 124 us per launch at config 2 against
+    // 16-step stages two deep; 8-step stages four deep: 128 us), then what
+    // fits
+    static const int prefs[][2] = {{3, 3}, {4, 2}, {2, 4}, {2, 3}, {1, 4}};
     auto shape_for = [&](int c) {
         const int WL = (W + c - 1) / c;
         if (const char *env = std::getenv("NPCG_LINE_CFG")) {

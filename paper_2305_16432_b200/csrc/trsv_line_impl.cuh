@@ -520,29 +520,38 @@ __device__ __forceinline__ void line_helper(const LineDirIO &io, const int t, co
             stage_tiles(jw, lo, g);
             const double *sp = slot_of(s);
             const int nc = g * (kTileSlots / 2);
+            // everything the write-back needs leaves the slot first, so the refill (the head of
+            // the slot's done -> refill -> prepare chain) is issued before the global stores
+            double2 res[KR][K], rk[KR][K];
 #pragma unroll
             for (int c = 0; c < KR; ++c) {
                 const double2 *v0 = reinterpret_cast<const double2 *>(sp + kFac + 3 * c * kVec);
                 const double2 *v1 = reinterpret_cast<const double2 *>(sp + kFac + (3 * c + 1) * kVec);
                 const double2 *v2 = reinterpret_cast<const double2 *>(sp + kFac + (3 * c + 2) * kVec);
-                if (!rhs.act[c]) continue;
-                double2 res[K], rk[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const int q = t + 32 * k < nc ? t + 32 * k : t;
-                    res[k] = v1[q];
-                    if (!UPPER && PCG) rk[k] = v0[q];
-                    if (UPPER && PCG) rk[k] = v2[q];
+                    res[c][k] = v1[q];
+                    if (!UPPER && PCG) rk[c][k] = v0[q];
+                    if (UPPER && PCG) rk[c][k] = v2[q];
                 }
+            }
+            // the slot's generic accesses (mine and the solver's) before the async-proxy refill
+            fence_proxy_async();
+            __syncwarp();
+            if (t == 0 && jw + NS < nstage) issue(jw + NS);
+#pragma unroll
+            for (int c = 0; c < KR; ++c) {
+                if (!rhs.act[c]) continue;
                 double2 *og = reinterpret_cast<double2 *>(io.out + c * io.sys + (size_t)lo * kTileSlots);
                 double part[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const bool ok = t + 32 * k < nc;
-                    if (ok) og[t + 32 * k] = res[k];  // y | z
+                    if (ok) og[t + 32 * k] = res[c][k];  // y | z
                     if (!UPPER && PCG && rhs.upd[c] && ok)
-                        reinterpret_cast<double2 *>(io.rg + c * io.sys + (size_t)lo * kTileSlots)[t + 32 * k] = rk[k];
-                    part[k] = (UPPER && PCG && ok) ? __dadd_rn(__dmul_rn(rk[k].x, res[k].x), __dmul_rn(rk[k].y, res[k].y)) : 0.0;
+                        reinterpret_cast<double2 *>(io.rg + c * io.sys + (size_t)lo * kTileSlots)[t + 32 * k] = rk[c][k];
+                    part[k] = (UPPER && PCG && ok) ? __dadd_rn(__dmul_rn(rk[c][k].x, res[c][k].x), __dmul_rn(rk[c][k].y, res[c][k].y)) : 0.0;
                 }
                 if (UPPER && PCG) {  // r.z (pcg.py:167), fixed pairwise order
 #pragma unroll
@@ -552,10 +561,6 @@ __device__ __forceinline__ void line_helper(const LineDirIO &io, const int t, co
                     acc[c] = __dadd_rn(acc[c], part[0]);
                 }
             }
-            // the slot's generic accesses (mine and the solver's) before the async-proxy refill
-            fence_proxy_async();
-            __syncwarp();
-            if (t == 0 && jw + NS < nstage) issue(jw + NS);
             WS_TRACE(1, jj, 2);
             ++jw;
         }
@@ -792,6 +797,7 @@ template <bool PCG, int KR, int C>
 static cudaError_t launch_ldlt_c(const LineArgs &a, cudaStream_t s) {
     switch (a.group * 16 + a.stages) {
         case 4 * 16 + 2: return launch_ldlt_gc<PCG, KR, 4, 2, C>(a, s);
+        case 3 * 16 + 3: return launch_ldlt_gc<PCG, KR, 3, 3, C>(a, s);
         case 2 * 16 + 4: return launch_ldlt_gc<PCG, KR, 2, 4, C>(a, s);
         case 2 * 16 + 3: return launch_ldlt_gc<PCG, KR, 2, 3, C>(a, s);
         case 1 * 16 + 4: return launch_ldlt_gc<PCG, KR, 1, 4, C>(a, s);
