@@ -65,6 +65,7 @@ def args_():
     ap.add_argument("--batch", type=int, default=None, help="RHS (config 2) or systems (config 3) per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-context", action="store_true", help="skip the Jacobi / Gauss-Seidel context solves")
     ap.add_argument("--profile-only", action="store_true", help="one profiled step, no JSON (for ncu)")
     return ap.parse_args()
 
@@ -506,6 +507,28 @@ def main():
                "d2h_bytes_per_step": int(A.n * B * 8 + B * (int(iters.max()) + 1) * 8),
                "ms_per_step": round(e2e_ms, 3)}
 
+    # context (not the metric): the same batch with the classic preconditioners of the
+    # reference (preconditioners.py:70-85) on the same kernels -- the seeded, untrained
+    # weights above are not a trained preconditioner, so iteration counts are read against these
+    context = None
+    if rank == 0 and world == 1 and not cfg3 and not a.no_context:
+        from paper_2305_16432_b200 import preconditioners
+        context = {"note": "seeded (untrained) GNN weights; classic preconditioners on the same device kernels, "
+                           "one timed batched solve each after one warm-up"}
+        for kind in ("jacobi", "gauss_seidel"):
+            Pc = preconditioners.build(kind, A)
+            pcg.pcg_solve_batch(A, rhs_dev, Pc, opts)
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record()
+            _, reps_c = pcg.pcg_solve_batch(A, rhs_dev, Pc, opts)
+            c1.record()
+            c1.synchronize()
+            it_c = np.array([r.iterations for r in reps_c])
+            context[kind] = {"iterations_mean": float(it_c.mean()), "ms": round(c0.elapsed_time(c1), 3),
+                             "systems_per_s": round(B / (c0.elapsed_time(c1) * 1e-3), 1),
+                             "all_converged": all(r.converged for r in reps_c)}
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         v, cores, step_s, info = cpu_reference(prob, model, steps=1, warmup=0, config=a.config, full_steps=False)
@@ -522,7 +545,7 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded jittered mesh + GRF loads / coefficients; seeded GNN weights)",
                 "config": config_dict(prob, k, B, world, a.config), "roofline": roof, "gnn": gnn_line,
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": total_launches, "clocks": clk,
+                "cpu_baseline": cpu, "e2e": e2e, "context": context, "gpu_launches": total_launches, "clocks": clk,
                 "iterations": {"min": int(iters.min()), "max": int(iters.max()), "mean": float(iters.mean())},
                 "all_converged": converged, "gnn_dtype": "f32", "pcg_dtype": "f64"}
         print(json.dumps(line), flush=True)
