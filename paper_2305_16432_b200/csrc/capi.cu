@@ -15,11 +15,21 @@
 #include "../../include/npcg.h"
 #include "fem.cuh"
 #include "train.cuh"
+
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges show up under Nsight tools, no-ops otherwise
 #include "gnn.cuh"
 #include "kernels.cuh"
 #include "pattern.h"
 
 using namespace npcg;
+
+namespace {
+// NVTX range over an entry point (the reference has no tracing; SURVEY.md section 5 lists it)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 struct npcg_pattern : public npcg::Pattern {
     // npcg_ldlt_apply_inverse workspaces by batch width (schedule packing,
@@ -329,6 +339,7 @@ int npcg_check_symmetric_values(const npcg_pattern *p, int B, const double *vals
 
 // ---------------------------------------------------------------------------
 int npcg_spmv(const npcg_pattern *A, int B, const double *vals, int vb, const double *x, double *y, void *stream) {
+    NvtxRange nvtx_range("npcg_spmv");
     if (!A || B < 1 || B > kMaxBatch) return fail(NPCG_ERR_ARGUMENT, "bad pattern or batch");
     if (A->n == 0) return NPCG_OK;
     SpmvArgs a;
@@ -681,6 +692,7 @@ static LineArgs line_args(npcg_solver *s, int mode, int sb, int db) {
 
 int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int sb, const double *D, int db,
                             const double *r, double *z, void *stream) {
+    NvtxRange nvtx_range("npcg_ldlt_apply_inverse");
     if (!F || B < 1 || B > kMaxBatch) return fail(NPCG_ERR_ARGUMENT, "bad argument");
     if (!F->factor_ok) return fail(NPCG_ERR_DATA_FORMAT, "pattern cannot carry a factor");
     if (F->n == 0) return NPCG_OK;
@@ -736,6 +748,7 @@ int npcg_ldlt_apply_inverse(const npcg_pattern *F, int B, const double *S, int s
 int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S, int sb, const double *D, int db,
                    const double *bvec, double *x, const double *x0, const npcg_solve_opts *o,
                    npcg_solve_report *rep, void *stream) {
+    NvtxRange nvtx_range("npcg_pcg_solve");
     if (!s || !o || !rep || !bvec || !x) return fail(NPCG_ERR_ARGUMENT, "NULL argument");
     if (o->n_thresholds < 1 || o->n_thresholds > kMaxThresholds)
         return fail(NPCG_ERR_DIMENSION, "at least one threshold required");
@@ -1094,6 +1107,7 @@ int npcg_gnn_destroy(npcg_gnn *g) {
 int npcg_gnn_build_factor(const npcg_gnn *g, const npcg_pattern *A, int B, const double *A_vals, int ab,
                           const double *rhs, double *S, double *D, double *edge_out, double *x0_out, int64_t *pivot,
                           void *stream) {
+    NvtxRange nvtx_range("npcg_gnn_build_factor");
     if (!g || !A || !A_vals || !rhs || !S || !D || B < 1 || B > kMaxBatch) return fail(NPCG_ERR_ARGUMENT, "bad argument");
     if (g->d.north_star) return fail(NPCG_ERR_ARGUMENT, "north_star weights: use npcg_gnn_build_factor_mesh");
     if (!A->full_diag) return fail(NPCG_ERR_DATA_FORMAT, "matrix is missing explicit diagonal entries");
@@ -1109,6 +1123,7 @@ int npcg_gnn_build_factor(const npcg_gnn *g, const npcg_pattern *A, int B, const
 int npcg_gnn_build_factor_mesh(const npcg_gnn *g, const npcg_pattern *A, int B, const double *A_vals, int ab,
                                const double *rhs, const double *pos, const double *boundary, double *S, double *D,
                                double *edge_out, int64_t *pivot, void *stream) {
+    NvtxRange nvtx_range("npcg_gnn_build_factor_mesh");
     if (!g || !A || !A_vals || !rhs || !S || !D || !pos || !boundary || B < 1 || B > kMaxBatch)
         return fail(NPCG_ERR_ARGUMENT, "bad argument");
     if (!g->d.north_star) return fail(NPCG_ERR_ARGUMENT, "reference weights: use npcg_gnn_build_factor");
@@ -1168,6 +1183,7 @@ extern "C" int npcg_trainer_set_weights(npcg_trainer *t, const double *weights_h
 extern "C" int npcg_trainer_tuple_grad(npcg_trainer *t, const npcg_pattern *A, const double *A_vals,
                                        const double *node_in, const double *edge_in, const double *b, const double *x,
                                        double x0_aux_weight, double *loss_host, double *grad_accum, void *stream) {
+    NvtxRange nvtx_range("npcg_trainer_tuple_grad");
     if (!t || !A || !A_vals || !node_in || !edge_in || !b || !x || !loss_host || !grad_accum)
         return fail(NPCG_ERR_ARGUMENT, "null argument");
     std::string err;
@@ -1272,6 +1288,7 @@ extern "C" int npcg_fem_plan_pattern(const npcg_fem_plan *p, int64_t *nnz, int64
 
 extern "C" int npcg_fem_assemble(const npcg_fem_plan *p, int B, const double *vertices, int vb, const double *coef,
                                  int cb, int mode, double scale, double *values, int *bad, void *stream) {
+    NvtxRange nvtx_range("npcg_fem_assemble");
     if (!p || B < 1 || !vertices || !values) return fail(NPCG_ERR_ARGUMENT, "bad argument");
     if (mode != NPCG_FEM_K && mode != NPCG_FEM_M && mode != NPCG_FEM_M_PLUS_SK) return fail(NPCG_ERR_ARGUMENT, "bad mode");
     cudaStream_t s = (cudaStream_t)stream;

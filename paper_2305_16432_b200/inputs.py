@@ -157,6 +157,9 @@ class Problem:
     # north_star GNN inputs for the rows of A: positions (n, dim) and the
     # boundary flag (domain boundary, or next to an eliminated Dirichlet node)
     geometry: tuple | None = None
+    # what DeviceAssembler needs to form `values` on the device instead of uploading them:
+    # {"elements", "vertices", "coef" (n_elements, B), "mode", "scale"} (distinct-system configs)
+    assembly: dict | None = None
 
 
 def _free_geometry(mesh, full_pattern: SparseMatrixCsr, free: np.ndarray):
@@ -231,14 +234,18 @@ def wave_2d(k=512, jitter=0.2, dt=1e-3, sigma=0.5, batch=32, cfg=3, first=0) -> 
     cent = mesh.vertices[mesh.triangles].mean(axis=1)
     vals = np.empty((len(asm.col_idx), batch))
     rhs = np.empty((len(mesh.vertices), batch))
+    coef = np.empty((len(mesh.triangles), batch))
     for j, rng in enumerate(rngs):
         c = np.exp(sigma * grf_2d(cent, rng, rng.uniform(0.05, 0.3)))
         Kc = asm.values(K * c[:, None, None])
         vals[:, j] = Mv + (dt * dt) * Kc
+        coef[:, j] = c
         rhs[:, j] = _host_spmv(Mm, grf_2d(mesh.vertices, rng, rng.uniform(0.05, 0.3)))
     A = asm.matrix(np.ascontiguousarray(vals[:, 0]))
     return Problem("wave2d", A, rhs, vals, 1e-8, None, {"k": k, "jitter": jitter, "dt": dt, "cfg": cfg},
-                   (np.ascontiguousarray(mesh.vertices), mesh.boundary.copy()))
+                   (np.ascontiguousarray(mesh.vertices), mesh.boundary.copy()),
+                   {"elements": mesh.triangles, "vertices": mesh.vertices, "coef": coef, "mode": "M+sK",
+                    "scale": dt * dt})
 
 
 # ---------------------------------------------------------------------------
