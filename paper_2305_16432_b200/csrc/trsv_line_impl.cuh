@@ -3,6 +3,7 @@
 // (PCG, systems per cluster) pair so the instances compile in parallel.
 #pragma once
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "ptx.cuh"
@@ -327,47 +328,69 @@ __device__ __forceinline__ void line_solver(const LineDirIO &io, const int W, co
 #pragma unroll
             for (int c = 0; c < KR; ++c) a0[c] = *reinterpret_cast<const double2 *>(vin + 3 * c * kVec + o.y);
         };
-        double2 cf0, cf1, cf2, ca0[KR];
-        pair_ops(0, cf0, cf1, cf2, ca0);
+        // The steps of a stage, specialised on what the stage needs besides the chain:
+        // FULL: all G tiles live (no per-pair bound check); SEND 0: nothing goes to the right
+        // warp, 1: every step does and the ring slots of the stage do not wrap (one base
+        // address, immediate offsets), 2: checked per step.
+        auto run = [&](auto full_c, auto send_c) {
+            constexpr bool FULL = decltype(full_c)::value;
+            constexpr int SEND = decltype(send_c)::value;
+            double *obase = out_slot(sig);
+            double2 cf0, cf1, cf2, ca0[KR];
+            pair_ops(0, cf0, cf1, cf2, ca0);
 #pragma unroll
-        for (int pi = 0; pi < STEPS / 2; ++pi) {
-            const int i = 2 * pi;
-            if (i >= live_steps) break;
-            double2 nf0, nf1, nf2, na0[KR];
-            if (pi + 1 < STEPS / 2) pair_ops(i + 2, nf0, nf1, nf2, na0);
-            const double F0[2] = {cf0.x, cf0.y}, F1[2] = {cf1.x, cf1.y}, F2[2] = {cf2.x, cf2.y};
-            double A[KR][2];
+            for (int pi = 0; pi < STEPS / 2; ++pi) {
+                const int i = 2 * pi;
+                if (!FULL && i >= live_steps) break;
+                double2 nf0, nf1, nf2, na0[KR];
+                if (pi + 1 < STEPS / 2) pair_ops(i + 2, nf0, nf1, nf2, na0);
+                const double F0[2] = {cf0.x, cf0.y}, F1[2] = {cf1.x, cf1.y}, F2[2] = {cf2.x, cf2.y};
+                double A[KR][2];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {  // sparse.py:222-239 order: L2, L1, S1 terms
-                const int step = sig + i + h;
-                const bool send = prod && step >= Q0 && step < Q1;
+                for (int h = 0; h < 2; ++h) {  // sparse.py:222-239 order: L2, L1, S1 terms
+                    const int step = sig + i + h;
+                    const bool send = SEND == 2 && prod && step >= Q0 && step < Q1;
 #pragma unroll
-                for (int c = 0; c < KR; ++c) {
-                    // vectors are in forward tile order: the backward pair is reversed
-                    const double V = (h == 0) == UPPER ? ca0[c].y : ca0[c].x;
-                    const double pre = __dsub_rn(V, __dmul_rn(F0[h], lp[c]));
-                    const double p2 = __dmul_rn(F2[h], h0[c]);
-                    double l1 = __shfl_up_sync(0xffffffffu, h0[c], 1);
-                    const double xl = __shfl_sync(0xffffffffu, x[c], i + h);
-                    if (t == 0) l1 = xl;
-                    double acc = __dsub_rn(pre, __dmul_rn(F1[h], l1));
-                    acc = __dsub_rn(acc, p2);
-                    h0[c] = acc;
-                    lp[c] = l1;
-                    if (send) st_gen(out_slot(step) + c, acc);
-                    A[c][h] = acc;
+                    for (int c = 0; c < KR; ++c) {
+                        // vectors are in forward tile order: the backward pair is reversed
+                        const double V = (h == 0) == UPPER ? ca0[c].y : ca0[c].x;
+                        const double pre = __dsub_rn(V, __dmul_rn(F0[h], lp[c]));
+                        const double p2 = __dmul_rn(F2[h], h0[c]);
+                        double l1 = __shfl_up_sync(0xffffffffu, h0[c], 1);
+                        const double xl = __shfl_sync(0xffffffffu, x[c], i + h);
+                        if (t == 0) l1 = xl;
+                        double acc = __dsub_rn(pre, __dmul_rn(F1[h], l1));
+                        acc = __dsub_rn(acc, p2);
+                        h0[c] = acc;
+                        lp[c] = l1;
+                        if (SEND == 1) {
+                            if (t == 31) st_gen(obase + (i + h) * KR + c, acc);
+                        } else if (send) {
+                            st_gen(out_slot(step) + c, acc);
+                        }
+                        A[c][h] = acc;
+                    }
+                }
+                const int2 o = pair_at(i);
+#pragma unroll
+                for (int c = 0; c < KR; ++c)
+                    *reinterpret_cast<double2 *>(vin + (3 * c + 1) * kVec + o.y) =
+                        UPPER ? make_double2(A[c][1], A[c][0]) : make_double2(A[c][0], A[c][1]);
+                if (pi + 1 < STEPS / 2) {
+                    cf0 = nf0, cf1 = nf1, cf2 = nf2;
+#pragma unroll
+                    for (int c = 0; c < KR; ++c) ca0[c] = na0[c];
                 }
             }
-            const int2 o = pair_at(i);
-#pragma unroll
-            for (int c = 0; c < KR; ++c)
-                *reinterpret_cast<double2 *>(vin + (3 * c + 1) * kVec + o.y) =
-                    UPPER ? make_double2(A[c][1], A[c][0]) : make_double2(A[c][0], A[c][1]);
-            if (pi + 1 < STEPS / 2) {
-                cf0 = nf0, cf1 = nf1, cf2 = nf2;
-#pragma unroll
-                for (int c = 0; c < KR; ++c) ca0[c] = na0[c];
-            }
+        };
+        {
+            const int last = sig + live_steps - 1;
+            const bool right = w + 1 < W;
+            const bool none = !right || last < Q0 || sig >= Q1;
+            const bool all = right && sig >= Q0 && last < Q1 && (sig & (R - 1)) + live_steps <= R;
+            if (g == G && all) run(std::true_type{}, std::integral_constant<int, 1>{});
+            else if (g == G && none) run(std::true_type{}, std::integral_constant<int, 0>{});
+            else run(std::false_type{}, std::integral_constant<int, 2>{});
         }
         __syncwarp();  // every lane's results are in the slot
         if (t == 0) mbar_arrive(&done[s]);
