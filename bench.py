@@ -63,11 +63,21 @@ def args_():
                     "64 RHS; 3: 32 distinct systems per GPU)")
     ap.add_argument("--k", type=int, default=None, help="mesh cells per side (default 256 / 512)")
     ap.add_argument("--batch", type=int, default=None, help="RHS (config 2) or systems (config 3) per GPU")
+    ap.add_argument("--weights", default="trained", choices=["trained", "seeded"],
+                    help="config 2 GNN weights: the committed trained checkpoint (default) or the seeded "
+                         "create_model draws with the processor gain cancelled (round 1 / early round 2 lines)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-context", action="store_true", help="skip the Jacobi / Gauss-Seidel context solves")
     ap.add_argument("--profile-only", action="store_true", help="one profiled step, no JSON (for ncu)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    global WEIGHTS
+    WEIGHTS = a.weights
+    return a
+
+
+WEIGHTS = "trained"  # --weights: "trained" (config 2: the committed checkpoint) or "seeded"
+TRAINED_WEIGHTS = os.path.join(ROOT, "paper_2305_16432_b200", "weights", "poisson2d_latent64_mp5.json")
 
 
 def workload(k, batch, rank=0, config=2):
@@ -77,6 +87,13 @@ def workload(k, batch, rank=0, config=2):
     else:
         prob = inputs.poisson_2d(k=k, batch=batch, first=rank * batch)
     gnn.FEATURE_WIDTH = CFG["width"]
+    if config == 2 and WEIGHTS == "trained":
+        # trained on 24^2 .. 48^2 Poisson tuples by the device training step
+        # (tools/train_bench_weights.py, log in profiles/r2_train_bench_weights.log)
+        model = gnn.load_model(TRAINED_WEIGHTS)
+        hp = model.hyper
+        assert (hp.h, hp.n_mp, hp.h_mp, model.width) == (CFG["h"], CFG["n_mp"], CFG["h"], CFG["width"])
+        return prob, model
     hyper = gnn.GnnHyperParams(l=1, h=CFG["h"], n_mp=CFG["n_mp"], l_mp=1, h_mp=CFG["h"])
     model = gnn.create_model(hyper, seed=CFG["seed"])
     for r in range(hyper.n_mp):  # cancel the 0.1 init gain: a non-trivial L'
@@ -87,8 +104,13 @@ def workload(k, batch, rank=0, config=2):
 
 def config_dict(prob, k, batch, world, config=2):
     A = prob.A
-    gnn_desc = (f"reference-mode F={CFG['width']} h={CFG['h']} n_mp={CFG['n_mp']}, "
-                f"create_model(seed={CFG['seed']}) with processor output layers x10")
+    if config == 2 and WEIGHTS == "trained":
+        gnn_desc = (f"reference-mode F={CFG['width']} h={CFG['h']} n_mp={CFG['n_mp']}, trained checkpoint "
+                    f"weights/poisson2d_latent64_mp5.json (data loss, Adam, 24^2..48^2 Poisson tuples, device "
+                    f"training step)")
+    else:
+        gnn_desc = (f"reference-mode F={CFG['width']} h={CFG['h']} n_mp={CFG['n_mp']}, "
+                    f"create_model(seed={CFG['seed']}) with processor output layers x10")
     common = {"n": A.n, "nnz": A.nnz, "gnn": gnn_desc, "l2": "flushed (256 MiB write) before every timed step",
               "parallelism": f"batch-parallel x{world} (weak), final NCCL gather to rank 0 when N > 1"}
     if config == 3:
@@ -203,7 +225,7 @@ def roofline(A, nnz_lower, prof, iters, peak_gbs, step_ms=None, distinct=False, 
                           "frac_of_8TBs": round(iter_gbs / 8000.0, 4), "bytes": int(iter_bytes),
                           "time_ms": round(t_iter * 1e3, 3),
                           "time_from": "timed step (GNN + whole batched solve)" if step_ms else
-                          ("timed PCG call" if pcg_ms else "summed kernel time"),
+                          ("timed PCG call (unprofiled, CUDA events)" if pcg_ms else "summed kernel time"),
                           "summed_kernel_ms": round(t_loop * 1e3, 3), "streams": prof.get("streams", 1)},
         "kernel_ms": {k: round(v, 3) for k, v in prof["kernel_ms"].items()},
         "kernel_share": {k: round(v / max(sum(prof["kernel_ms"].values()), 1e-9), 4)
@@ -350,7 +372,7 @@ def reference_arm(a):
         sample = (f"oracle port of the reference (numpy GNN + sequential C kernels, fp64): every timed step is the "
                   f"whole job -- the GNN once (all BLAS threads) then all {batch} right-hand sides solved on "
                   f"{info['rhs_per_round']} processes (one per core); wall clock per step")
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+    line = {"impl": "reference", "weights": WEIGHTS if a.config == 2 else "seeded", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(statistics.mean(step_s) * 1e3, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -383,6 +405,8 @@ def main():
     from paper_2305_16432_b200 import _native, gnn, pcg, sparse
     from paper_2305_16432_b200.dist import gather_solutions
     cfg3 = a.config == 3
+    if (cfg3 or WEIGHTS == "seeded") and "NPCG_STREAMS" not in os.environ:
+        pcg.SPLIT_STREAMS = 2  # long solves (~1100+ iterations): two concurrent sub-batches gain 6-12 %
     k, B = _sizes(a)
     prob, model = workload(k, B, rank, config=a.config)
     A = prob.A
@@ -467,14 +491,27 @@ def main():
     p1.synchronize()
     pcg_ms = p0.elapsed_time(p1)
     prof = dict(pcg.LAST_PROFILE)
+    # the PCG call alone, unprofiled (no per-launch events): the loop time of the iteration roofline
+    flush.fill_(1.0)
+    barrier()
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record()
+    pcg.pcg_solve_batch(A, rhs_dev, P, opts, values=vals_dev)
+    q1.record()
+    q1.synchronize()
+    pcg_plain_ms = q0.elapsed_time(q1)
     nnz_lower = (A.nnz - A.n) // 2
-    roof = roofline(A, nnz_lower, prof, prof["iterations"], peak_hbm(), step_ms=None if cfg3 else ms,
-                    distinct=cfg3, pcg_ms=pcg_ms if cfg3 else None)
+    roof = roofline(A, nnz_lower, prof, prof["iterations"], peak_hbm(), step_ms=None, distinct=cfg3,
+                    pcg_ms=pcg_plain_ms)
+    if not cfg3:  # the same bytes over the whole timed step (GNN included), as earlier lines reported it
+        it = roof["pcg_iteration"]
+        it["frac_of_measured_whole_step"] = round(it["bytes"] / (ms * 1e-3) / 1e9 / peak_hbm(), 4)
     gflop = gnn_flops(A.n, A.nnz, B if cfg3 else 1) / 1e9
     fp32_spec = 148 * 128 * 2 * 1.965e9 / 1e12
     gnn_line = {"ms": round(gnn_ms, 3), "gflop": round(gflop, 1), "tflops": round(gflop / gnn_ms, 2),
                 "fp32_fma_spec_tflops": round(fp32_spec, 1), "frac_of_fp32_spec": round(gflop / gnn_ms / fp32_spec, 4),
-                "pcg_ms": round(pcg_ms, 3), "share_of_step": round(gnn_ms / (gnn_ms + pcg_ms), 4)}
+                "pcg_ms": round(pcg_plain_ms, 3), "pcg_profiled_ms": round(pcg_ms, 3),
+                "share_of_step": round(gnn_ms / (gnn_ms + pcg_plain_ms), 4)}
 
     # e2e through the public API from pinned host buffers
     e2e = None
@@ -549,6 +586,9 @@ def main():
         from paper_2305_16432_b200 import preconditioners
         context = {"note": "seeded (untrained) GNN weights; classic preconditioners on the same device kernels, "
                            "one timed batched solve each after one warm-up"}
+        if WEIGHTS == "trained":
+            context["note"] = ("the benchmark's L' comes from the trained checkpoint; classic preconditioners on the "
+                               "same device kernels, one timed batched solve each after one warm-up")
         for kind in ("jacobi", "gauss_seidel"):
             Pc = preconditioners.build(kind, A)
             pcg.pcg_solve_batch(A, rhs_dev, Pc, opts)
@@ -574,7 +614,8 @@ def main():
         cpu = {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "port", "sample": sample, **info}
     total_launches = int(reduce(launches, dist.ReduceOp.SUM if world > 1 else None))
     if rank == 0:
-        line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        line = {"metric": METRIC, "weights": WEIGHTS if a.config == 2 else "seeded", "value": round(value, 3),
+                "unit": UNIT, "n_gpus": world,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded jittered mesh + GRF loads / coefficients; seeded GNN weights)",

@@ -166,7 +166,8 @@ struct npcg_solver {
         int pad;
         long long kmax;
     };
-    Poll *h_poll = nullptr;  // pinned
+    Poll *h_poll = nullptr;  // pinned, two slots (polls alternate)
+    cudaEvent_t poll_ev[2] = {nullptr, nullptr};
     long long history_len = 0;  // entries per system valid after the last solve
     ~npcg_solver() {
         void *ptrs[] = {R, P, Z, AP, Y, status, phase, pflag, k, bd, iter_to, t_to, t_start, scale, rz,
@@ -175,6 +176,8 @@ struct npcg_solver {
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_poll) cudaFreeHost(h_poll);
+        for (cudaEvent_t e : poll_ev)
+            if (e) cudaEventDestroy(e);
     }
 };
 
@@ -507,7 +510,8 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     s->partial_cap = part;
     NPCG_CUDA(dalloc(&s->partial, part));
     NPCG_CUDA(dalloc(&s->kmax, 1));
-    NPCG_CUDA(cudaMallocHost((void **)&s->h_poll, sizeof(npcg_solver::Poll)));
+    NPCG_CUDA(cudaMallocHost((void **)&s->h_poll, 2 * sizeof(npcg_solver::Poll)));
+    for (cudaEvent_t &e : s->poll_ev) NPCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (s->identity) {
         NPCG_CUDA(dalloc(&s->ones, A->n));
         std::vector<double> h(A->n, 1.0);
@@ -967,12 +971,16 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         apdot.st = drift.st = sst;
         fw.st = bw.st = ll.st = fwl.st = bwl.st = sst;
     };
-    int check = o->check_every > 0 ? o->check_every : 8;
+    // Passes are enqueued in chunks of `check`; every chunk ends with a poll (active columns,
+    // largest iteration count) copied to pinned memory and an event. The host waits for poll
+    // k only after chunk k + 1 is enqueued, so the device never idles on the host; after the
+    // last column converges at most one more chunk runs (every kernel takes its skip path).
+    const int check = o->check_every > 0 ? o->check_every : 8;
     // a pass advances k by at most one; an iteration whose drift check
     // restarts takes three passes (iterate, restart, re-init)
     const long long max_passes = 3 * o->max_iter + 16;
     long long passes = 0;
-    for (;;) {
+    auto enqueue_chunk = [&]() -> int {
         for (int q = 0; q < check; ++q) {
             NPCG_CUDA(timed(NPCG_PROF_SPMV_APDOT, [&] { return launch_spmv(apdot, st); }));
             if (s->ls) {  // P^{-1} in one launch, then the x / p updates
@@ -986,17 +994,34 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
             NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
         }
         passes += check;
-        const bool last = passes >= max_passes;
+        return NPCG_OK;
+    };
+    auto enqueue_poll = [&](int slot, bool last) -> int {
         note_launch(); count_active_kernel<<<1, 256, 0, st>>>(sst, B, s->kmax, last ? 1 : 0);
-        NPCG_CUDA(cudaMemcpyAsync(&s->h_poll->active, s->active_count, 4, cudaMemcpyDeviceToHost, st));
-        NPCG_CUDA(cudaMemcpyAsync(&s->h_poll->kmax, s->kmax, 8, cudaMemcpyDeviceToHost, st));
-        NPCG_CUDA(cudaStreamSynchronize(st));
-        harvest();
-        if (s->h_poll->active == 0 || last) break;
-        if (check < 64) check *= 2;
-        // the next `check` passes write history entries up to kmax + check
-        const long long need = std::min(hist_full, s->h_poll->kmax + check + 2);
+        NPCG_CUDA(cudaMemcpyAsync(&s->h_poll[slot].active, s->active_count, 4, cudaMemcpyDeviceToHost, st));
+        NPCG_CUDA(cudaMemcpyAsync(&s->h_poll[slot].kmax, s->kmax, 8, cudaMemcpyDeviceToHost, st));
+        NPCG_CUDA(cudaEventRecord(s->poll_ev[slot], st));
+        return NPCG_OK;
+    };
+    int polls = 0;          // polls enqueued
+    bool last_sent = false;  // the poll that closes the pass budget is enqueued
+    if (int rc = enqueue_chunk()) return rc;
+    last_sent = passes >= max_passes;
+    if (int rc = enqueue_poll(polls++ & 1, last_sent)) return rc;
+    for (;;) {
+        const bool more = !last_sent;
+        if (more) {
+            if (int rc = enqueue_chunk()) return rc;
+            last_sent = passes >= max_passes;
+            if (int rc = enqueue_poll(polls++ & 1, last_sent)) return rc;
+        }
+        const int wslot = (more ? polls - 2 : polls - 1) & 1;
+        NPCG_CUDA(cudaEventSynchronize(s->poll_ev[wslot]));
+        if (s->h_poll[wslot].active == 0 || !more) break;
+        // the chunk in flight and the next one write history entries up to kmax + 2 check
+        const long long need = std::min(hist_full, s->h_poll[wslot].kmax + 2 * (long long)check + 2);
         if (want_hist && need > cap) {
+            NPCG_CUDA(cudaStreamSynchronize(st));  // the chunk in flight still writes the old buffer
             const long long ncap = std::min(hist_full, std::max(2 * cap, need));
             double *nh = nullptr;
             NPCG_CUDA(dalloc(&nh, (size_t)ncap * B));
@@ -1011,6 +1036,8 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
             set_state();
         }
     }
+    NPCG_CUDA(cudaStreamSynchronize(st));
+    harvest();
     for (Ev &e : pool) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);

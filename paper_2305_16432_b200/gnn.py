@@ -14,7 +14,6 @@ whose factor lives on A's own pattern.
 from __future__ import annotations
 
 import ctypes
-import hashlib
 import json
 from dataclasses import dataclass
 
@@ -190,11 +189,13 @@ class GnnModel:
 
     def device(self):
         """npcg_gnn handle, rebuilt whenever the parameters change."""
-        _validate_params(self, self.width)
-        blob = self._blob()
-        fp = hashlib.blake2b(blob.tobytes(), digest_size=16).digest()
+        # cheap fingerprint first (per array: identity, shape, sum and sum of squares -- any
+        # in-place edit of the weights changes it); the blob is only formed for an upload
+        fp = tuple((k, id(v), v.shape, float(v.sum()), float(np.vdot(v, v))) for k, v in sorted(self.params.items()))
         if self._dev is not None and self._dev[0] == fp:
             return self._dev[1]
+        _validate_params(self, self.width)
+        blob = self._blob()
         hp = self.hyper
         d = _native.GnnDesc(self.width, hp.h, hp.l, hp.h_mp, hp.l_mp, hp.n_mp, int(hp.normalize),
                             int(hp.with_x0_head), int(hp.north_star), hp.dim)

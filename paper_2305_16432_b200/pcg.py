@@ -127,11 +127,14 @@ def pcg_solve_batch(A, B_rhs, P=None, opts: SolveOptions | None = None, *, value
 
 LAST_PROFILE: dict = {}  # filled by a profiled solve: per-kernel-class ms / launches / passes
 
-# A batch is solved as this many independent sub-batches, each on its own
-# CUDA stream driven by its own host thread: the triangular solves are bound
-# by their wavefront, not by the GPU's width, so one half's solves overlap the
-# other half's SpMV / vector updates. NPCG_STREAMS=1 turns it off.
-SPLIT_STREAMS = int(os.environ.get("NPCG_STREAMS", "2"))
+# A batch can be solved as several independent sub-batches, each on its own
+# CUDA stream driven by its own host thread (NPCG_STREAMS=2): one half's
+# wavefront solves overlap the other half's SpMV / vector updates. Measured at
+# config 2 (64 right-hand sides): a ~1100-iteration solve gains 6 % in the PCG
+# call (212 vs 226 ms), a ~105-iteration solve (trained weights) loses 30 %
+# (29 vs 22 ms: per-sub-batch setup, two wasted tail chunks, host threads) --
+# so one stream is the default.
+SPLIT_STREAMS = int(os.environ.get("NPCG_STREAMS", "1"))
 SPLIT_MIN_BATCH = 16
 _STREAMS: list = []
 

@@ -52,6 +52,36 @@ def line_info(A, batch):
     return [o.value for o in out]
 
 
+def test_cfg2_full_size_trained_weights_vs_oracle(gpu, monkeypatch):
+    """bench.py's default workload: config 2 with the committed trained
+    checkpoint (weights/poisson2d_latent64_mp5.json, ~105 iterations). The
+    same bars against the oracle's fp64 build_learned + pcg_solve."""
+    import os
+
+    import torch
+    monkeypatch.setattr(gnn, "FEATURE_WIDTH", 64)
+    path = os.path.join(os.path.dirname(os.path.abspath(gnn.__file__)), "weights", "poisson2d_latent64_mp5.json")
+    model = gnn.load_model(path)
+    hp = port.Hyper(l=1, h=model.hyper.h, n_mp=model.hyper.n_mp, l_mp=1, h_mp=model.hyper.h_mp, width=64)
+    prob = inputs.poisson_2d(k=256, batch=64)
+    A = prob.A
+    P = gnn.build_learned(model, A, prob.rhs[:, 0])
+    oA = ocsr(A)
+    oF = port.build_learned(hp, model.params, oA, prob.rhs[:, 0])
+    assert rel(P.factor.strict_lower.values, oF.lower.values) <= L_TOL
+    opts = pcg.SolveOptions(thresholds=(1e-8,))
+    X, reps = pcg.pcg_solve_batch(A, torch.from_numpy(prob.rhs).cuda(), P, opts)
+    X = X.cpu().numpy()
+    assert all(r.converged for r in reps)
+    assert max(r.iterations for r in reps) < 200  # a trained preconditioner: Jacobi needs ~930, SGS ~330
+    for s in (0, 13, 27, 40, 51, 63):
+        ox, orep = port.pcg_solve(oA, prob.rhs[:, s], oF, thresholds=(1e-8,))
+        assert orep.converged
+        assert abs(reps[s].iterations - orep.iterations) <= 1, (s, reps[s].iterations, orep.iterations)
+        assert rel(X[:, s], ox) <= X_TOL
+        assert len(reps[s].history) == reps[s].iterations + 1
+
+
 def test_cfg2_full_size_vs_oracle(gpu, monkeypatch):
     import torch
     prob = inputs.poisson_2d(k=256, batch=64)
