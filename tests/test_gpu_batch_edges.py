@@ -103,8 +103,8 @@ def test_sub_batches_on_side_streams_match_one_stream(gpu, monkeypatch, streams)
     thread and a CUDA stream each) against the one-stream solve, uneven
     split. Not bitwise: ||b|| and the dot products are reduced in an order
     that depends on the batch width, so a column may cross the threshold an
-    iteration earlier or later -- the reference bars apply (iterations +-1,
-    x within 1e-8)."""
+    iteration earlier or later -- the reference bars apply to each solve
+    (iterations +-1 and x within 1e-8 of the oracle), hence +-2 between them."""
     import torch
     prob, A, P, oA, oF = setup(40, 19, seed=4)
     opts = pcg.SolveOptions(thresholds=(1e-4, 1e-9), max_iter=3000)
@@ -114,10 +114,11 @@ def test_sub_batches_on_side_streams_match_one_stream(gpu, monkeypatch, streams)
     monkeypatch.setattr(pcg, "SPLIT_STREAMS", streams)
     X2, r2 = pcg.pcg_solve_batch(A, rhs, P, opts)
     assert all(r.converged for r in r1) and all(r.converged for r in r2)
-    assert max(abs(a.iterations - b.iterations) for a, b in zip(r1, r2)) <= 1
+    assert max(abs(a.iterations - b.iterations) for a, b in zip(r1, r2)) <= 2
     for t in opts.thresholds:
-        assert max(abs(a.iterations_to[t] - b.iterations_to[t]) for a, b in zip(r1, r2)) <= 1
+        assert max(abs(a.iterations_to[t] - b.iterations_to[t]) for a, b in zip(r1, r2)) <= 2
     err = (X1 - X2).norm(dim=0) / X1.norm(dim=0)
     assert float(err.max()) <= 1e-8
     assert all(len(r.history) == r.iterations + 1 for r in r2)
+    check(X1.cpu().numpy(), r1, prob.rhs, oA, oF, opts.thresholds, 3000, (0, 7, 18))
     check(X2.cpu().numpy(), r2, prob.rhs, oA, oF, opts.thresholds, 3000, (0, 7, 18))
