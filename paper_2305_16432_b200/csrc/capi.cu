@@ -159,6 +159,9 @@ struct npcg_solver {
     double *Dl = nullptr, *rDl = nullptr;  // diag in line order ([b][nslot] or [nslot]) and 1 / diag
     size_t Dl_cap = 0;
     int *xpend = nullptr;
+    int *xgo = nullptr;                    // line path: epoch of the pass whose x update is due (common.cuh)
+    cudaStream_t side = nullptr;           // the x updates run here, beside the P^{-1} launch
+    cudaEvent_t ev_spmv = nullptr, ev_x = nullptr;
     double *ones = nullptr;   // identity preconditioner: D = 1 (per solver: no shared state between threads)
     long long *kmax = nullptr;  // largest k of the batch at the last poll
     struct Poll {
@@ -176,6 +179,10 @@ struct npcg_solver {
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (h_poll) cudaFreeHost(h_poll);
+        if (xgo) cudaFree(xgo);
+        if (side) cudaStreamDestroy(side);
+        if (ev_spmv) cudaEventDestroy(ev_spmv);
+        if (ev_x) cudaEventDestroy(ev_x);
         for (cudaEvent_t e : poll_ev)
             if (e) cudaEventDestroy(e);
     }
@@ -484,6 +491,16 @@ int npcg_solver_create(const npcg_pattern *A, const npcg_pattern *F, int B, npcg
     }
     NPCG_CUDA(dalloc(&s->status, B));
     NPCG_CUDA(dalloc(&s->xpend, B));
+    if (s->ls) {  // x updates beside the P^{-1} launch (NPCG_XUPD_STREAM=0: inside pupd)
+        bool on = true;
+        if (const char *env = std::getenv("NPCG_XUPD_STREAM")) on = std::atoi(env) != 0;
+        if (on) {
+            NPCG_CUDA(dalloc(&s->xgo, B));
+            NPCG_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+            NPCG_CUDA(cudaEventCreateWithFlags(&s->ev_spmv, cudaEventDisableTiming));
+            NPCG_CUDA(cudaEventCreateWithFlags(&s->ev_x, cudaEventDisableTiming));
+        }
+    }
 
     NPCG_CUDA(dalloc(&s->phase, B));
     NPCG_CUDA(dalloc(&s->pflag, B));
@@ -535,6 +552,8 @@ static SolveState make_state(npcg_solver *s, const npcg_solve_opts *o) {
     SolveState st{};
     st.status = s->status;
     st.xpend = s->xpend;
+    st.xgo = s->xgo;
+    st.epoch = 0;
 
     st.phase = s->phase;
     st.pflag = s->pflag;
@@ -959,7 +978,7 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
         used.clear();
     };
     auto pupd = [&]() {
-        if (s->ls) return launch_pupd_ell(s->ls->nslot, B, s->Z, s->P, s->XL, sst, st);
+        if (s->ls) return launch_pupd_ell(s->ls->nslot, B, s->Z, s->P, s->xgo ? nullptr : s->XL, sst, st);
         note_launch();
         pupd_kernel<<<ew_grid, 256, 0, st>>>(nB, B, s->Z, s->P, x, sst, 1);
         return cudaGetLastError();
@@ -980,11 +999,21 @@ int npcg_pcg_solve(npcg_solver *s, const double *A_vals, int ab, const double *S
     // restarts takes three passes (iterate, restart, re-init)
     const long long max_passes = 3 * o->max_iter + 16;
     long long passes = 0;
+    int epoch = 0;
+    if (s->xgo) NPCG_CUDA(cudaMemsetAsync(s->xgo, 0, (size_t)B * sizeof(int), st));
     auto enqueue_chunk = [&]() -> int {
         for (int q = 0; q < check; ++q) {
+            apdot.st.epoch = ++epoch;
             NPCG_CUDA(timed(NPCG_PROF_SPMV_APDOT, [&] { return launch_spmv(apdot, st); }));
-            if (s->ls) {  // P^{-1} in one launch, then the x / p updates
+            if (s->ls) {  // P^{-1} in one launch, then the p update; x += alpha p beside it
+                if (s->xgo) {
+                    NPCG_CUDA(cudaEventRecord(s->ev_spmv, st));
+                    NPCG_CUDA(cudaStreamWaitEvent(s->side, s->ev_spmv, 0));
+                    NPCG_CUDA(launch_xupd_ell(s->ls->nslot, B, s->P, s->XL, apdot.st, s->side));
+                    NPCG_CUDA(cudaEventRecord(s->ev_x, s->side));
+                }
                 NPCG_CUDA(timed(NPCG_PROF_TRSV_FWD, [&] { return launch_ldlt_line(ll, st); }));
+                if (s->xgo) NPCG_CUDA(cudaStreamWaitEvent(st, s->ev_x, 0));  // p_k is read until here
                 NPCG_CUDA(timed(NPCG_PROF_PUPD, pupd));
                 continue;
             }

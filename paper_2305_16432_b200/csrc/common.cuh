@@ -47,6 +47,11 @@ struct SolveState {
     // per column [B]
     int *status, *phase, *pflag;
     int *xpend;                // 1 while this pass's x += alpha p is pending
+    // line path: the x update runs as its own launch on a side stream, concurrent with the
+    // P^{-1} launch (it needs alpha and p_k only). xgo[b] == epoch marks the columns whose
+    // alpha this pass's SpMV formed; null: the update stays in pupd.
+    int *xgo;
+    int epoch;
     long long *k;              // iterations
     long long *breakdown_at;
     double *scale, *rz, *alpha, *beta, *rel, *final_rel;

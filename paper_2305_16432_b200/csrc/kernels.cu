@@ -56,6 +56,7 @@ __device__ void spmv_epilogue(const SpmvArgs &a, int b, double total) {
             }
             st.alpha[b] = st.rz[b] / pAp;
             st.xpend[b] = 1;  // x += alpha p happens in pupd (pcg.py:141)
+            if (st.xgo) st.xgo[b] = st.epoch;  // ... or in this pass's xupd launch
             return;
         }
         case SPMV_RESID_INIT: {  // pcg.py:111-126
@@ -995,10 +996,13 @@ static cudaError_t launch_spmv_ell(const SpmvArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// p = z + beta p | p = z ; x += alpha p, every vector in line order (pcg.py:129, 141, 170)
+// p = z + beta p | p = z ; x += alpha p, every vector in line order (pcg.py:129, 141, 170);
+// x == nullptr: the x update is xupd_ell_kernel's
 __global__ void __launch_bounds__(256) pupd_ell_kernel(int nslot, const double *z, double *p, double *x,
                                                         SolveState st) {
-    const int b = blockIdx.y, f = st.pflag[b];
+    const int b = blockIdx.y;
+    int f = st.pflag[b];
+    if (!x) f &= ~PF_X;
     if (f == PF_NONE) return;
     const double al = st.alpha[b], be = st.beta[b];
     const size_t vb = (size_t)b * nslot;
@@ -1031,6 +1035,32 @@ cudaError_t launch_pupd_ell(int nslot, int B, const double *z, double *p, double
     const int gx = std::max(1, std::min(per, (4 * num_sms() + B - 1) / B));
     note_launch();
     pupd_ell_kernel<<<dim3(gx, B), 256, 0, s>>>(nslot, z, p, x, st);
+    return cudaGetLastError();
+}
+
+// x += alpha p (pcg.py:141) for the columns whose alpha this pass's SpMV formed (st.xgo[b] ==
+// st.epoch): needs p_k and alpha only, so it runs beside the P^{-1} launch on a side stream
+__global__ void __launch_bounds__(256) xupd_ell_kernel(int nslot, const double *p, double *x, SolveState st) {
+    const int b = blockIdx.y;
+    if (st.xgo[b] != st.epoch) return;
+    const double al = st.alpha[b];
+    const size_t vb = (size_t)b * nslot;
+    const double2 *p2 = reinterpret_cast<const double2 *>(p + vb);
+    double2 *x2 = reinterpret_cast<double2 *>(x + vb);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nslot / 2; i += gridDim.x * blockDim.x) {
+        const double2 pq = p2[i];
+        double2 xq = x2[i];
+        xq.x = __dadd_rn(xq.x, __dmul_rn(al, pq.x));
+        xq.y = __dadd_rn(xq.y, __dmul_rn(al, pq.y));
+        x2[i] = xq;
+    }
+}
+
+cudaError_t launch_xupd_ell(int nslot, int B, const double *p, double *x, const SolveState &st, cudaStream_t s) {
+    const int per = (nslot / 2 + 255) / 256;
+    const int gx = std::max(1, std::min(per, (2 * num_sms() + B - 1) / B));
+    note_launch();
+    xupd_ell_kernel<<<dim3(gx, B), 256, 0, s>>>(nslot, p, x, st);
     return cudaGetLastError();
 }
 

@@ -67,6 +67,7 @@ cudaError_t launch_to_line(int nslot, int B, const int *rowof, const double *src
                            double *dst, cudaStream_t s);
 cudaError_t launch_from_line(int nslot, int B, const int *rowof, const double *src, double *dst, cudaStream_t s);
 // all-line-order PCG vectors: p / x update, and value gathers into a packed order
+cudaError_t launch_xupd_ell(int nslot, int B, const double *p, double *x, const SolveState &st, cudaStream_t s);
 cudaError_t launch_pupd_ell(int nslot, int B, const double *z, double *p, double *x, const SolveState &st,
                             cudaStream_t s);
 void launch_gather_rows(long long count, int B, const int *sel, const double *src, double *dst, cudaStream_t s);

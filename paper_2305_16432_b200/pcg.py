@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _native
 from .errors import BreakdownError, DimensionMismatchError
-from .sparse import SparseMatrixCsr, is_device, spmv_device, to_device, _torch
+from .sparse import SparseMatrixCsr, is_device, spmv_device, to_device, to_host, _torch
 
 DEFAULT_THRESHOLDS = (1e-2, 1e-4, 1e-6, 1e-8, 1e-10, 1e-12)
 
@@ -103,7 +103,7 @@ def pcg_solve(A: SparseMatrixCsr, b, P=None, opts: SolveOptions | None = None):
     if rep.status == _native.STATUS_BREAKDOWN:
         raise BreakdownError(
             f"p'Ap <= 0 at iteration {rep.iterations}: matrix not SPD or preconditioner invalid")
-    return (x if on_dev else x.cpu().numpy()), rep
+    return (x if on_dev else to_host(x)), rep
 
 
 def pcg_solve_batch(A, B_rhs, P=None, opts: SolveOptions | None = None, *, values=None,
@@ -122,7 +122,7 @@ def pcg_solve_batch(A, B_rhs, P=None, opts: SolveOptions | None = None, *, value
         raise TypeError("pcg_solve_batch needs a device preconditioner (FactorPreconditioner) or None")
     X, reps = _pcg_device(A, Bm, fac, opts, batch=Bm.shape[1], values=values,
                           with_history=with_history, profile=profile)
-    return (X if on_dev else X.cpu().numpy()), reps
+    return (X if on_dev else to_host(X)), reps
 
 
 LAST_PROFILE: dict = {}  # filled by a profiled solve: per-kernel-class ms / launches / passes

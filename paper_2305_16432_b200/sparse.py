@@ -43,6 +43,42 @@ def to_device(x, dtype=None):
     return t.to(dtype or torch.float64).contiguous()
 
 
+_VALIDATED: dict = {}  # (id(row_ptr), id(col_idx), n) -> (row_ptr, col_idx) that passed the index checks
+
+# Pinned host buffers for results handed back as numpy arrays: a device -> pageable copy of a
+# fresh 33 MB array runs at ~2 GB/s (page faults + staging; 14.7 ms for config 2's solutions),
+# a copy into pinned memory at the link rate (1.3 ms). A buffer is reused once the array that
+# was handed out on it (and every view of it) is gone.
+_HOST_POOL: list = []  # [pinned tensor, weakref to the array last handed out | None]
+_HOST_POOL_MAX = 6
+
+
+def to_host(t):
+    """CUDA tensor -> numpy array (same shape) backed by pooled pinned memory."""
+    import weakref
+    torch = _torch()
+    t = t.contiguous()
+    n, slot = t.numel(), None
+    for entry in _HOST_POOL:
+        buf, ref = entry
+        if buf.dtype == t.dtype and buf.numel() >= n and (ref is None or ref() is None):
+            if slot is None or buf.numel() < slot[0].numel():
+                slot = entry
+    if slot is None:
+        if len(_HOST_POOL) >= _HOST_POOL_MAX:  # drop a free buffer (or fall back to a pageable copy)
+            free = [e for e in _HOST_POOL if e[1] is None or e[1]() is None]
+            if not free:
+                return t.cpu().numpy()
+            _HOST_POOL.remove(min(free, key=lambda e: e[0].numel()))
+        slot = [torch.empty(max(n, 1), dtype=t.dtype, pin_memory=True), None]
+        _HOST_POOL.append(slot)
+    view = slot[0][:n].view(t.shape)
+    view.copy_(t)
+    arr = view.numpy()
+    slot[1] = weakref.ref(arr)
+    return arr
+
+
 def is_device(x) -> bool:
     try:
         import torch
@@ -149,6 +185,17 @@ class SparseMatrixCsr:
         object.__setattr__(self, "col_idx", np.ascontiguousarray(self.col_idx, dtype=np.int64))
         object.__setattr__(self, "values", np.ascontiguousarray(self.values, dtype=np.float64))
         n, rp, ci = self.n, self.row_ptr, self.col_idx
+        object.__setattr__(self, "_dev_vals", None)
+        object.__setattr__(self, "_sym", None)
+        # index arrays already validated (same objects: one mesh, many matrices) are not
+        # walked again; like the device pattern, the cache is keyed on array identity and
+        # holds the arrays
+        key = (id(rp), id(ci), int(n))
+        hit = _VALIDATED.get(key)
+        if hit is not None and hit[0] is rp and hit[1] is ci:
+            if len(ci) != len(self.values):
+                raise DimensionMismatchError("row_ptr endpoints disagree with nnz")
+            return
         if n < 0 or rp.shape != (n + 1,):
             raise DimensionMismatchError(f"row_ptr must have length n+1={n + 1}")
         if rp[0] != 0 or rp[-1] != len(ci) or len(ci) != len(self.values):
@@ -164,8 +211,9 @@ class SparseMatrixCsr:
             ok[heads - 1] = True  # pairs straddling a row boundary are exempt
             if not np.all(ok):
                 raise DimensionMismatchError("columns must strictly increase within rows")
-        object.__setattr__(self, "_dev_vals", None)
-        object.__setattr__(self, "_sym", None)
+        _VALIDATED[key] = (rp, ci)
+        while len(_VALIDATED) > 64:
+            _VALIDATED.pop(next(iter(_VALIDATED)))
 
     # -- constructors (sparse.py:69-108) --------------------------------------
 
