@@ -15,10 +15,31 @@ __device__ __forceinline__ void st_gen(double *p, double v) {
 }
 __device__ __forceinline__ int tile_elem(int q, int t) { return (q >> 1) * 64 + t * 2 + (q & 1); }
 
+__device__ volatile int g_stop;
+
 template <int FLAGS, int KR>
-__global__ void __launch_bounds__(128, 1) step_kernel(double *out, long long *cyc, int Q0, int Q1, int R) {
+__global__ void __launch_bounds__(256, 1) step_kernel(double *out, long long *cyc, int Q0, int Q1, int R, int nline,
+                                                      int noise_gap) {
     extern __shared__ __align__(128) double sm[];
     const int t = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (w >= nline) {  // helper-like traffic: 16-byte shared loads / stores, `noise_gap` idle cycles between bursts
+        double2 *buf = reinterpret_cast<double2 *>(sm + (size_t)w * (G * (kKinds + 3 * KR) * kTileSlots + 64 * KR));
+        double2 a = make_double2(1.0, 2.0);
+        for (int it = 0; it < 20000; ++it) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                double2 v = buf[t + 32 * k];
+                a.x += v.x;
+                a.y += v.y;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) buf[t + 32 * (8 + k)] = a;
+            if (noise_gap) __nanosleep(noise_gap);
+            if (g_stop) break;
+        }
+        out[blockIdx.x * blockDim.x + threadIdx.x] = a.x + a.y;
+        return;
+    }
     double *f = sm + (size_t)w * (G * (kKinds + 3 * KR) * kTileSlots + 64 * KR);
     double *vin = f + G * kKinds * kTileSlots;
     double *ring = f + G * (kKinds + 3 * KR) * kTileSlots;
@@ -111,22 +132,30 @@ __global__ void __launch_bounds__(128, 1) step_kernel(double *out, long long *cy
     double s = 0;
     for (int c = 0; c < KR; ++c) s += h0[c] + lp[c];
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
-    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        *cyc = t1 - t0;
+        g_stop = 1;
+    }
 }
 
 template <int FLAGS, int KR>
-void run(const char *name, int warps = 1) {
+void run(const char *name, int warps = 1, int noise = 0, int gap = 0) {
     double *out;
     long long *cyc, h;
     cudaMalloc(&out, 8 * 1024 * 32);
     cudaMalloc(&cyc, 8);
     auto k = step_kernel<FLAGS, KR>;
-    const int smem = warps * (G * (kKinds + 3 * KR) * kTileSlots + 64 * KR) * 8;
+    const int smem = (warps + noise) * (G * (kKinds + 3 * KR) * kTileSlots + 64 * KR) * 8;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int r = 0; r < 2; ++r) k<<<1, 32 * warps, smem>>>(out, cyc, 64, 1 << 30, 64);
+    for (int r = 0; r < 2; ++r) {
+        int zero = 0;
+        cudaMemcpyToSymbol(g_stop, &zero, sizeof(int));
+        k<<<1, 32 * (warps + noise), smem>>>(out, cyc, 64, 1 << 30, 64, warps, gap);
+    }
     cudaError_t e = cudaDeviceSynchronize();
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
-    printf("%-58s KR=%d warps=%d  %.1f cycles/step  %s\n", name, KR, warps, (double)h / (kStages * STEPS),
+    printf("%-58s KR=%d warps=%d noise=%d gap=%d  %.1f cycles/step  %s\n", name, KR, warps, noise, gap,
+           (double)h / (kStages * STEPS),
            e == cudaSuccess ? "" : cudaGetErrorString(e));
     cudaFree(out);
     cudaFree(cyc);
@@ -148,5 +177,10 @@ int main() {
     run<F_LDS | F_STS | F_XL | F_RING, 1>("everything", 4);
     run<F_LDS | F_STS | F_XL | F_RING, 2>("everything", 4);
     run<F_LDS | F_STS | F_XL | F_RING, 4>("everything");
+    // four line warps next to four warps of helper-like shared-memory traffic
+    run<F_LDS | F_STS | F_XL | F_RING | F_GENERIC, 1>("everything + 4 noise warps, back to back", 4, 4, 0);
+    run<F_LDS | F_STS | F_XL | F_RING | F_GENERIC, 1>("everything + 4 noise warps, 200 ns gaps", 4, 4, 200);
+    run<F_LDS | F_STS | F_XL | F_RING | F_GENERIC, 1>("everything + 4 noise warps, 1 us gaps", 4, 4, 1000);
+    run<F_LDS | F_STS | F_XL | F_RING | F_GENERIC, 1>("everything, no noise", 4, 0, 0);
     return 0;
 }
