@@ -510,7 +510,12 @@ __device__ __forceinline__ void line_helper(const LineDirIO &io, const int t, co
                         r[k].x = __dsub_rn(r[k].x, __dmul_rn(alpha, ap[k].x));  // pcg.py:142
                         r[k].y = __dsub_rn(r[k].y, __dmul_rn(alpha, ap[k].y));
                         part[k] = t + 32 * k < nc ? __dadd_rn(__dmul_rn(r[k].x, r[k].x), __dmul_rn(r[k].y, r[k].y)) : 0.0;
-                        if (t + 32 * k < nc) v0[t + 32 * k] = r[k];
+                        if (t + 32 * k < nc) {
+                            v0[t + 32 * k] = r[k];
+                            // r_{k+1} goes to global memory from the registers here (the write-back
+                            // would read it from the slot again)
+                            if (rhs.act[c]) reinterpret_cast<double2 *>(io.rg + c * io.sys + (size_t)lo * kTileSlots)[t + 32 * k] = r[k];
+                        }
                     }
 #pragma unroll
                     for (int h = 1; h < K; h <<= 1)  // |r_{k+1}|^2 (pcg.py:143), fixed pairwise order
@@ -555,7 +560,6 @@ __device__ __forceinline__ void line_helper(const LineDirIO &io, const int t, co
                 for (int k = 0; k < K; ++k) {
                     const int q = t + 32 * k < nc ? t + 32 * k : t;
                     res[c][k] = v1[q];
-                    if (!UPPER && PCG) rk[c][k] = v0[q];
                     if (UPPER && PCG) rk[c][k] = v2[q];
                 }
             }
@@ -572,8 +576,6 @@ __device__ __forceinline__ void line_helper(const LineDirIO &io, const int t, co
                 for (int k = 0; k < K; ++k) {
                     const bool ok = t + 32 * k < nc;
                     if (ok) og[t + 32 * k] = res[c][k];  // y | z
-                    if (!UPPER && PCG && rhs.upd[c] && ok)
-                        reinterpret_cast<double2 *>(io.rg + c * io.sys + (size_t)lo * kTileSlots)[t + 32 * k] = rk[c][k];
                     part[k] = (UPPER && PCG && ok) ? __dadd_rn(__dmul_rn(rk[c][k].x, res[c][k].x), __dmul_rn(rk[c][k].y, res[c][k].y)) : 0.0;
                 }
                 if (UPPER && PCG) {  // r.z (pcg.py:167), fixed pairwise order
