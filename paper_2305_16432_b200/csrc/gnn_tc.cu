@@ -52,6 +52,10 @@ constexpr int kTcF = 64, kTcH = 64;     // latent width, processor hidden width
 template <bool NODE>
 constexpr int tc_k1() { return NODE ? 2 * kTcF : 3 * kTcF; }  // layer-1 fan-in
 constexpr int kAtomBytes = kTcRows * 128;  // one 32-wide K chunk of 128 rows (16 KB)
+#ifndef NPCG_TC_AHEAD
+#define NPCG_TC_AHEAD 2
+#endif
+constexpr int kTcAhead = NPCG_TC_AHEAD;  // K chunks a row's loads run ahead of the MMAs
 
 // byte offsets in dynamic shared memory
 template <bool NODE>
@@ -239,18 +243,18 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
                 }
             }
         };
-        // ---- layer 1: K chunks of 32, double-buffered, loads one chunk ahead ----
-        float4 xa[8];
-        load_chunk(0, xa);
-#pragma unroll 1
-        for (int c = 0; c < kTcK1 / 32; ++c) {
-            const int u = c & 1;
-            float4 xb[8];
-            if (c + 1 < kTcK1 / 32) load_chunk(c + 1, xb);
-            if (use[u] > 0) mbar_wait(&bar[u], (use[u] - 1) & 1);  // the MMAs that last read this buffer are done
-            store_split(abuf(u, 0), abuf(u, 1), t, xa);
+        // ---- layer 1: K chunks of 32, double-buffered A operand, row loads kTcAhead chunks
+        // ahead (the kernel is bound by the latency of these gathers: one warp per scheduler) ----
+        constexpr int kNC = kTcK1 / 32;
+        float4 xq[kTcAhead + 1][8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) xa[j] = xb[j];
+        for (int c = 0; c < kTcAhead && c < kNC; ++c) load_chunk(c, xq[c]);
+#pragma unroll
+        for (int c = 0; c < kNC; ++c) {
+            const int u = c & 1;
+            if (c + kTcAhead < kNC) load_chunk(c + kTcAhead, xq[(c + kTcAhead) % (kTcAhead + 1)]);
+            if (use[u] > 0) mbar_wait(&bar[u], (use[u] - 1) & 1);  // the MMAs that last read this buffer are done
+            store_split(abuf(u, 0), abuf(u, 1), t, xq[c % (kTcAhead + 1)]);
             fence_proxy_async();
             __syncthreads();
             if (t == 0) {
