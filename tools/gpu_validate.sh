@@ -1,3 +1,5 @@
+# End-of-round validation on one B200 (under gpurun): smoke, every GPU test, the bench arms,
+# the ncu launch list of the default step and one full capture of the PCG kernels.
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
