@@ -25,6 +25,9 @@ GAIN = float(os.environ.get("GAIN", "1.0"))
 EVAL_K = int(os.environ.get("EVAL_K", "256"))
 PROBLEM = os.environ.get("PROBLEM", "poisson")  # "poisson" (config 2) or "wave" (config 3: a matrix per system)
 OUT = os.environ.get("OUT", "gpurun_out/poisson_f64_trained.json")
+# extra tuples per mesh with a white-noise x (b = A x): ||(P - A) x||^2 over white x estimates the
+# Frobenius ("naive") objective, the solution vectors alone weight the smooth modes only
+NOISE = int(os.environ.get("NOISE", "0"))
 
 
 def problem(k, batch, cfg):
@@ -55,6 +58,12 @@ def make_tuples():
                                    pcg.SolveOptions(thresholds=(1e-12,), max_iter=20000))
             assert rep.converged
             out.append(Tup(A, prob.rhs[:, c].copy(), x))
+        rng = np.random.default_rng(9000 + j)
+        for c in range(NOISE):
+            A = system(prob, c % PER_MESH)
+            xn = rng.standard_normal(A.n) * float(np.linalg.norm(out[-1].x) / np.sqrt(A.n))
+            from paper_2305_16432_b200 import sparse as _sp
+            out.append(Tup(A, _sp.spmv(A, xn), xn))
     return out
 
 
