@@ -86,6 +86,38 @@ def levelsync(monkeypatch):
     monkeypatch.setenv("NPCG_LEVELSYNC", "1")
 
 
+def test_poisson_3d_trained_checkpoint(gpu, levelsync, monkeypatch):
+    """tools/bench_3d.py's config-4 weights (weights/poisson3d_latent64_mp5.json,
+    trained by the device training step on 6^3 .. 12^3 cubes): latent-64
+    tensor-core GNN + level-path PCG against the oracle on a 14^3 cube, and the
+    trained factor beats Jacobi by a wide margin."""
+    import os
+
+    import torch
+
+    from paper_2305_16432_b200 import preconditioners
+    monkeypatch.setattr(gnn, "FEATURE_WIDTH", 64)
+    path = os.path.join(os.path.dirname(os.path.abspath(gnn.__file__)), "weights", "poisson3d_latent64_mp5.json")
+    model = gnn.load_model(path)
+    ohp = port.Hyper(l=1, h=model.hyper.h, n_mp=model.hyper.n_mp, l_mp=1, h_mp=model.hyper.h_mp, width=64)
+    prob = inputs.poisson_3d(k=14, batch=6)
+    A = prob.A
+    P = gnn.build_learned(model, A, prob.rhs[:, 0])
+    oA = port.Csr(A.n, A.row_ptr, A.col_idx, A.values)
+    oF = port.build_learned(ohp, model.params, oA, prob.rhs[:, 0])
+    assert rel(P.factor.strict_lower.values, oF.lower.values) <= L_TOL
+    thr = (1e-8,)
+    X, reps = pcg.pcg_solve_batch(A, torch.from_numpy(prob.rhs).cuda(), P, pcg.SolveOptions(thresholds=thr, max_iter=2000))
+    X = X.cpu().numpy()
+    _, jac = pcg.pcg_solve(A, prob.rhs[:, 0], preconditioners.build_jacobi(A), pcg.SolveOptions(thresholds=thr))
+    for s in (0, 3, 5):
+        ox, orep = port.pcg_solve(oA, prob.rhs[:, s], oF, thresholds=thr, max_iter=2000)
+        assert reps[s].converged and orep.converged
+        assert abs(reps[s].iterations - orep.iterations) <= 1, (s, reps[s].iterations, orep.iterations)
+        assert rel(X[:, s], ox) <= X_TOL
+    assert 3 * max(r.iterations for r in reps) < jac.iterations
+
+
 def test_level_sync_apply_inverse_bitwise(gpu, levelsync):
     import torch
     A = inputs.poisson_3d(k=9, batch=1).A

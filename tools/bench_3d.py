@@ -14,9 +14,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def model_for(gain):
+def model_for(gain, cfg=4):
     from paper_2305_16432_b200 import gnn
     gnn.FEATURE_WIDTH = 64
+    if cfg == 4 and os.environ.get("WEIGHTS", "trained") == "trained":
+        # trained on 6^3 .. 12^3 Poisson cubes by the device training step
+        # (PROBLEM=poisson3d tools/train_bench_weights.py; log in profiles/r2_train_poisson3d_weights.log)
+        return gnn.load_model(os.path.join(ROOT, "paper_2305_16432_b200", "weights", "poisson3d_latent64_mp5.json"))
     hyper = gnn.GnnHyperParams(l=1, h=64, n_mp=5, l_mp=1, h_mp=64)
     model = gnn.create_model(hyper, seed=3)
     for r in range(5):
@@ -33,7 +37,7 @@ def run(cfg, k, batch, gain, steps):
     prob = inputs.poisson_3d(k=k, batch=batch) if cfg == 4 else inputs.heat_3d(k=k, batch=batch)
     gen_s = time.time() - t
     A = prob.A
-    model = model_for(gain)
+    model = model_for(gain, cfg)
     rhs = torch.from_numpy(prob.rhs).cuda()
     vals = torch.from_numpy(prob.values).cuda() if prob.values is not None else None
     opts = pcg.SolveOptions(thresholds=(prob.rtol,))
@@ -104,6 +108,7 @@ def run(cfg, k, batch, gain, steps):
     pcg_mean = float(np.mean(p_ms))
     line = {"config": cfg, "k": k, "n": n, "nnz": nnz, "batch": Bn, "distinct_systems": distinct,
             "rtol": prob.rtol, "gain": gain, "gen_s": round(gen_s, 1),
+            "weights": "trained" if cfg == 4 and os.environ.get("WEIGHTS", "trained") == "trained" else "seeded",
             "value": round(Bn / (np.mean(times) * 1e-3), 3), "unit": "systems/s", "ms_per_step": round(float(np.mean(times)), 3),
             "gnn_ms": round(float(np.mean(g_ms)), 3), "pcg_ms": round(pcg_mean, 3),
             "iterations": {"min": int(its.min()), "max": int(its.max()), "mean": float(its.mean())},

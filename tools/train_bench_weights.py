@@ -33,6 +33,8 @@ NOISE = int(os.environ.get("NOISE", "0"))
 def problem(k, batch, cfg):
     if PROBLEM == "wave":
         return inputs.wave_2d(k=k, batch=batch, cfg=cfg)
+    if PROBLEM == "poisson3d":
+        return inputs.poisson_3d(k=k, batch=batch, cfg=cfg)
     return inputs.poisson_2d(k=k, batch=batch, cfg=cfg)
 
 
@@ -68,7 +70,7 @@ def make_tuples():
 
 
 def evaluate(model, tag):
-    prob = problem(EVAL_K, 16 if PROBLEM == "poisson" else 4, 2 if PROBLEM == "poisson" else 3)
+    prob = problem(EVAL_K, 4 if PROBLEM == "wave" else 16, {"poisson": 2, "wave": 3, "poisson3d": 4}[PROBLEM])
     A = prob.A
     rhs = torch.from_numpy(prob.rhs).cuda()
     opts = pcg.SolveOptions(thresholds=(1e-8,), max_iter=6000)
@@ -101,7 +103,7 @@ def main():
     tuples = make_tuples()
     print(f"{len(tuples)} tuples in {time.time() - t0:.1f}s", flush=True)
     for kind in ("jacobi", "gauss_seidel"):
-        prob = problem(EVAL_K, 4, 2 if PROBLEM == "poisson" else 3)
+        prob = problem(EVAL_K, 4, {"poisson": 2, "wave": 3, "poisson3d": 4}[PROBLEM])
         its = []
         for c in range(4):
             A = system(prob, c)
