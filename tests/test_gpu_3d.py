@@ -118,6 +118,31 @@ def test_poisson_3d_trained_checkpoint(gpu, levelsync, monkeypatch):
     assert 3 * max(r.iterations for r in reps) < jac.iterations
 
 
+def test_heat_3d_trained_checkpoint(gpu, levelsync, monkeypatch):
+    """Config 5's weights (weights/heat3d_latent64_mp5.json: trained on small
+    cubes with dt scaled to config 5's mass : stiffness balance): distinct
+    systems, per-system L' from the tensor-core GNN, rtol 1e-10, against the
+    oracle."""
+    import os
+    monkeypatch.setattr(gnn, "FEATURE_WIDTH", 64)
+    path = os.path.join(os.path.dirname(os.path.abspath(gnn.__file__)), "weights", "heat3d_latent64_mp5.json")
+    model = gnn.load_model(path)
+    ohp = port.Hyper(l=1, h=model.hyper.h, n_mp=model.hyper.n_mp, l_mp=1, h_mp=model.hyper.h_mp, width=64)
+    prob = inputs.heat_3d(k=12, batch=3, dt=1e-3 * (128.0 / 12) ** 2)
+    A, vals = prob.A, prob.values
+    P = gnn.build_learned_batch(model, A, prob.rhs, values=vals)
+    thr = (1e-10,)
+    X, reps = pcg.pcg_solve_batch(A, prob.rhs, P, pcg.SolveOptions(thresholds=thr, max_iter=3000), values=vals)
+    for s, rep in enumerate(reps):
+        oA = port.Csr(A.n, A.row_ptr, A.col_idx, np.ascontiguousarray(vals[:, s]))
+        oF = port.build_learned(ohp, model.params, oA, prob.rhs[:, s])
+        assert rel(P.system_factor(s).strict_lower.values, oF.lower.values) <= L_TOL
+        ox, orep = port.pcg_solve(oA, prob.rhs[:, s], oF, thresholds=thr, max_iter=3000)
+        assert rep.converged and orep.converged
+        assert abs(rep.iterations - orep.iterations) <= 1, (s, rep.iterations, orep.iterations)
+        assert rel(X[:, s], ox) <= X_TOL
+
+
 def test_level_sync_apply_inverse_bitwise(gpu, levelsync):
     import torch
     A = inputs.poisson_3d(k=9, batch=1).A

@@ -17,10 +17,11 @@ sys.path.insert(0, ROOT)
 def model_for(gain, cfg=4):
     from paper_2305_16432_b200 import gnn
     gnn.FEATURE_WIDTH = 64
-    if cfg == 4 and os.environ.get("WEIGHTS", "trained") == "trained":
-        # trained on 6^3 .. 12^3 Poisson cubes by the device training step
-        # (PROBLEM=poisson3d tools/train_bench_weights.py; log in profiles/r2_train_poisson3d_weights.log)
-        return gnn.load_model(os.path.join(ROOT, "paper_2305_16432_b200", "weights", "poisson3d_latent64_mp5.json"))
+    if os.environ.get("WEIGHTS", "trained") == "trained":
+        # trained on 6^3 .. 12^3 cubes by the device training step (PROBLEM=poisson3d | heat3d
+        # tools/train_bench_weights.py; logs in profiles/r2_train_*3d_weights.log)
+        name = "poisson3d_latent64_mp5.json" if cfg == 4 else "heat3d_latent64_mp5.json"
+        return gnn.load_model(os.path.join(ROOT, "paper_2305_16432_b200", "weights", name))
     hyper = gnn.GnnHyperParams(l=1, h=64, n_mp=5, l_mp=1, h_mp=64)
     model = gnn.create_model(hyper, seed=3)
     for r in range(5):
@@ -108,7 +109,7 @@ def run(cfg, k, batch, gain, steps):
     pcg_mean = float(np.mean(p_ms))
     line = {"config": cfg, "k": k, "n": n, "nnz": nnz, "batch": Bn, "distinct_systems": distinct,
             "rtol": prob.rtol, "gain": gain, "gen_s": round(gen_s, 1),
-            "weights": "trained" if cfg == 4 and os.environ.get("WEIGHTS", "trained") == "trained" else "seeded",
+            "weights": "trained" if os.environ.get("WEIGHTS", "trained") == "trained" else "seeded",
             "value": round(Bn / (np.mean(times) * 1e-3), 3), "unit": "systems/s", "ms_per_step": round(float(np.mean(times)), 3),
             "gnn_ms": round(float(np.mean(g_ms)), 3), "pcg_ms": round(pcg_mean, 3),
             "iterations": {"min": int(its.min()), "max": int(its.max()), "mean": float(its.mean())},

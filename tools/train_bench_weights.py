@@ -35,6 +35,10 @@ def problem(k, batch, cfg):
         return inputs.wave_2d(k=k, batch=batch, cfg=cfg)
     if PROBLEM == "poisson3d":
         return inputs.poisson_3d(k=k, batch=batch, cfg=cfg)
+    if PROBLEM == "heat3d":
+        # config 5 is 128^3 cells with dt = 1e-3: the mass : dt-stiffness balance goes with dt / h^2,
+        # so a k^3 training cube gets dt scaled to keep config 5's balance
+        return inputs.heat_3d(k=k, batch=batch, cfg=cfg, dt=1e-3 * (128.0 / k) ** 2)
     return inputs.poisson_2d(k=k, batch=batch, cfg=cfg)
 
 
@@ -70,7 +74,7 @@ def make_tuples():
 
 
 def evaluate(model, tag):
-    prob = problem(EVAL_K, 4 if PROBLEM == "wave" else 16, {"poisson": 2, "wave": 3, "poisson3d": 4}[PROBLEM])
+    prob = problem(EVAL_K, 4 if PROBLEM in ("wave", "heat3d") else 16, {"poisson": 2, "wave": 3, "poisson3d": 4, "heat3d": 5}[PROBLEM])
     A = prob.A
     rhs = torch.from_numpy(prob.rhs).cuda()
     opts = pcg.SolveOptions(thresholds=(1e-8,), max_iter=6000)
@@ -103,7 +107,7 @@ def main():
     tuples = make_tuples()
     print(f"{len(tuples)} tuples in {time.time() - t0:.1f}s", flush=True)
     for kind in ("jacobi", "gauss_seidel"):
-        prob = problem(EVAL_K, 4, {"poisson": 2, "wave": 3, "poisson3d": 4}[PROBLEM])
+        prob = problem(EVAL_K, 4, {"poisson": 2, "wave": 3, "poisson3d": 4, "heat3d": 5}[PROBLEM])
         its = []
         for c in range(4):
             A = system(prob, c)
