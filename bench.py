@@ -64,7 +64,7 @@ def args_():
     ap.add_argument("--k", type=int, default=None, help="mesh cells per side (default 256 / 512)")
     ap.add_argument("--batch", type=int, default=None, help="RHS (config 2) or systems (config 3) per GPU")
     ap.add_argument("--weights", default="trained", choices=["trained", "seeded"],
-                    help="config 2 GNN weights: the committed trained checkpoint (default) or the seeded "
+                    help="GNN weights: the committed trained checkpoint of the config (default) or the seeded "
                          "create_model draws with the processor gain cancelled (round 1 / early round 2 lines)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -78,6 +78,7 @@ def args_():
 
 WEIGHTS = "trained"  # --weights: "trained" (config 2: the committed checkpoint) or "seeded"
 TRAINED_WEIGHTS = os.path.join(ROOT, "paper_2305_16432_b200", "weights", "poisson2d_latent64_mp5.json")
+TRAINED_WEIGHTS_CFG3 = os.path.join(ROOT, "paper_2305_16432_b200", "weights", "wave2d_latent64_mp5.json")
 
 
 def workload(k, batch, rank=0, config=2):
@@ -87,10 +88,11 @@ def workload(k, batch, rank=0, config=2):
     else:
         prob = inputs.poisson_2d(k=k, batch=batch, first=rank * batch)
     gnn.FEATURE_WIDTH = CFG["width"]
-    if config == 2 and WEIGHTS == "trained":
-        # trained on 24^2 .. 48^2 Poisson tuples by the device training step
-        # (tools/train_bench_weights.py, log in profiles/r2_train_bench_weights.log)
-        model = gnn.load_model(TRAINED_WEIGHTS)
+    if WEIGHTS == "trained":
+        # trained on 24^2 .. 48^2 tuples by the device training step (tools/train_bench_weights.py,
+        # logs in profiles/r2_train_bench_weights.log / r2_train_wave2d_weights.log; config 3's
+        # training meshes scale dt to keep the 512^2 problem's mass : stiffness balance)
+        model = gnn.load_model(TRAINED_WEIGHTS if config == 2 else TRAINED_WEIGHTS_CFG3)
         hp = model.hyper
         assert (hp.h, hp.n_mp, hp.h_mp, model.width) == (CFG["h"], CFG["n_mp"], CFG["h"], CFG["width"])
         return prob, model
@@ -104,10 +106,10 @@ def workload(k, batch, rank=0, config=2):
 
 def config_dict(prob, k, batch, world, config=2):
     A = prob.A
-    if config == 2 and WEIGHTS == "trained":
+    if WEIGHTS == "trained":
         gnn_desc = (f"reference-mode F={CFG['width']} h={CFG['h']} n_mp={CFG['n_mp']}, trained checkpoint "
-                    f"weights/poisson2d_latent64_mp5.json (data loss, Adam, 24^2..48^2 Poisson tuples, device "
-                    f"training step)")
+                    f"weights/{'poisson2d' if config == 2 else 'wave2d'}_latent64_mp5.json (data loss, Adam, "
+                    f"24^2..48^2 tuples, device training step)")
     else:
         gnn_desc = (f"reference-mode F={CFG['width']} h={CFG['h']} n_mp={CFG['n_mp']}, "
                     f"create_model(seed={CFG['seed']}) with processor output layers x10")
@@ -372,7 +374,7 @@ def reference_arm(a):
         sample = (f"oracle port of the reference (numpy GNN + sequential C kernels, fp64): every timed step is the "
                   f"whole job -- the GNN once (all BLAS threads) then all {batch} right-hand sides solved on "
                   f"{info['rhs_per_round']} processes (one per core); wall clock per step")
-    line = {"impl": "reference", "weights": WEIGHTS if a.config == 2 else "seeded", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+    line = {"impl": "reference", "weights": WEIGHTS, "metric": METRIC, "value": round(value, 4), "unit": UNIT,
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(statistics.mean(step_s) * 1e3, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -405,7 +407,7 @@ def main():
     from paper_2305_16432_b200 import _native, gnn, pcg, sparse
     from paper_2305_16432_b200.dist import gather_solutions
     cfg3 = a.config == 3
-    if (cfg3 or WEIGHTS == "seeded") and "NPCG_STREAMS" not in os.environ:
+    if WEIGHTS == "seeded" and "NPCG_STREAMS" not in os.environ:
         pcg.SPLIT_STREAMS = 2  # long solves (~1100+ iterations): two concurrent sub-batches gain 6-12 %
     k, B = _sizes(a)
     prob, model = workload(k, B, rank, config=a.config)
@@ -614,11 +616,11 @@ def main():
         cpu = {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "port", "sample": sample, **info}
     total_launches = int(reduce(launches, dist.ReduceOp.SUM if world > 1 else None))
     if rank == 0:
-        line = {"metric": METRIC, "weights": WEIGHTS if a.config == 2 else "seeded", "value": round(value, 3),
+        line = {"metric": METRIC, "weights": WEIGHTS, "value": round(value, 3),
                 "unit": UNIT, "n_gpus": world,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded jittered mesh + GRF loads / coefficients; seeded GNN weights)",
+                "data": "synthetic (seeded jittered mesh + GRF loads / coefficients; GNN weights as config.gnn says)",
                 "config": config_dict(prob, k, B, world, a.config), "roofline": roof, "gnn": gnn_line,
                 "cpu_baseline": cpu, "e2e": e2e, "e2e_from_coefficients": e2e_coef, "context": context, "gpu_launches": total_launches, "clocks": clk,
                 "iterations": {"min": int(iters.min()), "max": int(iters.max()), "mean": float(iters.mean())},

@@ -150,3 +150,25 @@ def test_cfg3_two_distinct_systems_end_to_end(gpu, monkeypatch, cfg3):
         assert reps[s].converged and orep.converged
         assert abs(reps[s].iterations - orep.iterations) <= 1, (s, reps[s].iterations, orep.iterations)
         assert rel(X[:, s], ox) <= X_TOL
+
+
+def test_cfg3_trained_checkpoint_end_to_end(gpu, monkeypatch, cfg3):
+    """bench.py --config 3's default weights (weights/wave2d_latent64_mp5.json,
+    ~11 iterations): one of the 513^2 systems end to end against the oracle."""
+    import os
+    monkeypatch.setattr(gnn, "FEATURE_WIDTH", 64)
+    path = os.path.join(os.path.dirname(os.path.abspath(gnn.__file__)), "weights", "wave2d_latent64_mp5.json")
+    model = gnn.load_model(path)
+    hp = port.Hyper(l=1, h=model.hyper.h, n_mp=model.hyper.n_mp, l_mp=1, h_mp=model.hyper.h_mp, width=64)
+    A, vals = cfg3.A, cfg3.values
+    P = gnn.build_learned_batch(model, A, cfg3.rhs, values=vals)
+    X, reps = pcg.pcg_solve_batch(A, cfg3.rhs, P, pcg.SolveOptions(thresholds=(1e-8,)), values=vals)
+    assert all(r.converged for r in reps) and max(r.iterations for r in reps) < 20  # Jacobi needs ~22
+    s = 1
+    oA = ocsr(A, vals[:, s])
+    oF = port.build_learned(hp, model.params, oA, cfg3.rhs[:, s])
+    assert rel(P.system_factor(s).strict_lower.values, oF.lower.values) <= L_TOL
+    ox, orep = port.pcg_solve(oA, cfg3.rhs[:, s], oF, thresholds=(1e-8,))
+    assert orep.converged
+    assert abs(reps[s].iterations - orep.iterations) <= 1, (reps[s].iterations, orep.iterations)
+    assert rel(X[:, s], ox) <= X_TOL

@@ -32,7 +32,9 @@ NOISE = int(os.environ.get("NOISE", "0"))
 
 def problem(k, batch, cfg):
     if PROBLEM == "wave":
-        return inputs.wave_2d(k=k, batch=batch, cfg=cfg)
+        # config 3 is 512^2 cells with dt = 1e-3: the mass : dt^2-stiffness balance goes with
+        # (dt / h)^2, so a k^2 training mesh gets dt scaled to keep config 3's balance
+        return inputs.wave_2d(k=k, batch=batch, cfg=cfg, dt=1e-3 * 512.0 / k)
     if PROBLEM == "poisson3d":
         return inputs.poisson_3d(k=k, batch=batch, cfg=cfg)
     if PROBLEM == "heat3d":
