@@ -7,7 +7,7 @@ timeout 2400 python -m pytest tests -m gpu -q --durations=5 > gpurun_out/gputest
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo bench=$?
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref=$?
 timeout 900 python bench.py --weights seeded --no-cpu-baseline > gpurun_out/bench_seeded.log 2>&1; echo seeded=$?
-timeout 900 python bench.py --config 3 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_cfg3.log 2>&1; echo cfg3=$?
+timeout 900 python bench.py --config 3 --steps 5 --warmup 2 --no-cpu-baseline > gpurun_out/bench_cfg3.log 2>&1; echo cfg3=$?
 timeout 300 python bench.py --profile-only > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 420 --csv --log-file gpurun_out/r2_launches_final.csv python bench.py --profile-only > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ldlt_line|spmv_ell_kernel<7, 0, 1>|pupd_ell|mp_tc_kernel" -s 10 -c 5 -o gpurun_out/r2_prof_final python bench.py --profile-only > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
