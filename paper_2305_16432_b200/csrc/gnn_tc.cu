@@ -200,59 +200,80 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
     uint32_t use[2] = {0, 0}, ph2 = 0;  // completed-use counts (mbarrier parity)
     const long long items = NODE ? (long long)n : m;
     const long long tiles_per = (items + kTcRows - 1) / kTcRows, tiles = tiles_per * B;
-    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int b = (int)(tile / tiles_per);
+    // a tile's row of this thread: where its input chunks come from
+    struct Row {
+        int b = 0, p0 = 0, p1 = 0;
+        long long it = 0;
+        bool live = false;
+        const float *eb = nullptr, *vb = nullptr, *xrow[3] = {nullptr, nullptr, nullptr};
+    };
+    auto setup = [&](long long tile) {
+        Row r;
+        r.b = (int)(tile / tiles_per);
         const long long item = (tile % tiles_per) * kTcRows + t;
-        const bool live = item < items;
-        const long long it = live ? item : 0;
-        const float *eb = e + ((size_t)b * m) * kTcF;
-        const float *vb = v + ((size_t)b * n) * kTcF;
-        const float *xrow[3];
-        int p0 = 0, p1 = 0;
+        r.live = item < items;
+        r.it = r.live ? item : 0;
+        r.eb = e + ((size_t)r.b * m) * kTcF;
+        r.vb = v + ((size_t)r.b * n) * kTcF;
         if (NODE) {
-            xrow[0] = vb + (size_t)it * kTcF;
-            p0 = live ? rp[it] : 0;
-            p1 = live ? rp[it + 1] : 0;
+            r.xrow[0] = r.vb + (size_t)r.it * kTcF;
+            r.p0 = r.live ? rp[r.it] : 0;
+            r.p1 = r.live ? rp[r.it + 1] : 0;
         } else {
-            xrow[0] = eb + (size_t)it * kTcF;
-            xrow[1] = vb + (size_t)(live ? src[it] : 0) * kTcF;
-            xrow[2] = vb + (size_t)(live ? col[it] : 0) * kTcF;
+            r.xrow[0] = r.eb + (size_t)r.it * kTcF;
+            r.xrow[1] = r.vb + (size_t)(r.live ? src[r.it] : 0) * kTcF;
+            r.xrow[2] = r.vb + (size_t)(r.live ? col[r.it] : 0) * kTcF;
         }
-        // chunk c of this row's input: 32 consecutive features
-        auto load_chunk = [&](int c, float4 (&x)[8]) {
-            if (!NODE || c < 2) {
-                const float4 *p = reinterpret_cast<const float4 *>(xrow[c >> 1] + (c & 1) * 32);
+        return r;
+    };
+    // chunk c of a row's input: 32 consecutive features
+    auto load_chunk = [&](const Row &r, int c, float4 (&x)[8]) {
+        if (!NODE || c < 2) {
+            const float4 *p = reinterpret_cast<const float4 *>(r.xrow[c >> 1] + (c & 1) * 32);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) x[j] = live ? p[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {  // agg_i = sum_p e_p * v_col(p), CSR order (autodiff.py:174, 209, 221-243)
-                const int f0 = (c & 1) * 32;
+            for (int j = 0; j < 8; ++j) x[j] = r.live ? p[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {  // agg_i = sum_p e_p * v_col(p), CSR order (autodiff.py:174, 209, 221-243)
+            const int f0 = (c & 1) * 32;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) x[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = 0; j < 8; ++j) x[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 2
-                for (int p = p0; p < p1; ++p) {
-                    const float4 *ep = reinterpret_cast<const float4 *>(eb + (size_t)p * kTcF + f0);
-                    const float4 *vp = reinterpret_cast<const float4 *>(vb + (size_t)col[p] * kTcF + f0);
+            for (int p = r.p0; p < r.p1; ++p) {
+                const float4 *ep = reinterpret_cast<const float4 *>(r.eb + (size_t)p * kTcF + f0);
+                const float4 *vp = reinterpret_cast<const float4 *>(r.vb + (size_t)col[p] * kTcF + f0);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 a = ep[j], q = vp[j];
-                        x[j].x = fmaf(a.x, q.x, x[j].x);
-                        x[j].y = fmaf(a.y, q.y, x[j].y);
-                        x[j].z = fmaf(a.z, q.z, x[j].z);
-                        x[j].w = fmaf(a.w, q.w, x[j].w);
-                    }
+                for (int j = 0; j < 8; ++j) {
+                    const float4 a = ep[j], q = vp[j];
+                    x[j].x = fmaf(a.x, q.x, x[j].x);
+                    x[j].y = fmaf(a.y, q.y, x[j].y);
+                    x[j].z = fmaf(a.z, q.z, x[j].z);
+                    x[j].w = fmaf(a.w, q.w, x[j].w);
                 }
             }
-        };
-        // ---- layer 1: K chunks of 32, double-buffered A operand, row loads kTcAhead chunks
-        // ahead (the kernel is bound by the latency of these gathers: one warp per scheduler) ----
-        constexpr int kNC = kTcK1 / 32;
-        float4 xq[kTcAhead + 1][8];
+        }
+    };
+    // Row loads run kTcAhead chunks ahead of the MMAs (the kernel is bound by the latency of
+    // these gathers: one warp per scheduler), across tiles too: the next tile's first chunks
+    // are requested before this tile's epilogues.
+    constexpr int kNC = kTcK1 / 32;
+    constexpr int kPre = kTcAhead < 2 ? kTcAhead : 2;  // chunks fetched across the tile boundary (plain row loads)
+    float4 xq[kTcAhead + 1][8];
+    Row cur;
+    if ((long long)blockIdx.x < tiles) {
+        cur = setup(blockIdx.x);
 #pragma unroll
-        for (int c = 0; c < kTcAhead && c < kNC; ++c) load_chunk(c, xq[c]);
+        for (int c = 0; c < kPre; ++c) load_chunk(cur, c, xq[c]);
+    }
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int b = cur.b;
+        const long long it = cur.it;
+        const bool live = cur.live;
+        // ---- layer 1: K chunks of 32, double-buffered A operand ----
+#pragma unroll
+        for (int c = kPre; c < kTcAhead && c < kNC; ++c) load_chunk(cur, c, xq[c]);
 #pragma unroll
         for (int c = 0; c < kNC; ++c) {
             const int u = c & 1;
-            if (c + kTcAhead < kNC) load_chunk(c + kTcAhead, xq[(c + kTcAhead) % (kTcAhead + 1)]);
+            if (c + kTcAhead < kNC) load_chunk(cur, c + kTcAhead, xq[(c + kTcAhead) % (kTcAhead + 1)]);
             if (use[u] > 0) mbar_wait(&bar[u], (use[u] - 1) & 1);  // the MMAs that last read this buffer are done
             store_split(abuf(u, 0), abuf(u, 1), t, xq[c % (kTcAhead + 1)]);
             fence_proxy_async();
@@ -271,6 +292,14 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
                 mma_commit(&bar[u]);
             }
             ++use[u];
+        }
+        // the next tile's first chunks: in flight during this tile's epilogues
+        const long long ntile = tile + gridDim.x;
+        Row nxt;
+        if (ntile < tiles) {
+            nxt = setup(ntile);
+#pragma unroll
+            for (int c = 0; c < kPre; ++c) load_chunk(nxt, c, xq[c]);
         }
         // every layer-1 MMA done (the last commit of each buffer)
         mbar_wait(&bar[0], (use[0] - 1) & 1);
@@ -364,6 +393,7 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
         }
         tc_fence_before();
         __syncthreads();  // TMEM reads done before the next tile's MMAs overwrite it
+        cur = nxt;
     }
     tc_fence_after();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
