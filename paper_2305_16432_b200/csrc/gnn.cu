@@ -484,7 +484,8 @@ cudaError_t launch_mp_edge_tc(int n, long long m, int B, const int *src, const i
                               const float *ln_b, float *e, const float *v, cudaStream_t s);
 cudaError_t launch_mp_node_tc(int n, long long m, int B, const int *rp, const int *col, const float *W1,
                               const float *b1, const float *W2, const float *b2, const float *ln_g,
-                              const float *ln_b, const float *e, const float *v, float *v_out, cudaStream_t s);
+                              const float *ln_b, const float *e, const float *v, float *v_out, float *agg_buf,
+                              cudaStream_t s);
 static bool gnn_tc_enabled() {
     static int on = -1;
     if (on < 0) {
@@ -527,7 +528,7 @@ __global__ void exp_factor_kernel(long long nnz, int B, const int *pair, const i
 
 // ---------------------------------------------------------------------------
 template <int F, int H, int TE>
-static cudaError_t run_rounds(const GnnDev &g, const Pattern &A, int B, float *e, float *v, float *v2,
+static cudaError_t run_rounds(const GnnDev &g, const Pattern &A, int B, float *aggbuf, float *e, float *v, float *v2,
                               float **v_final, cudaStream_t s) {
     const int n = (int)A.n;
     const long long m = A.nnz;
@@ -556,7 +557,8 @@ static cudaError_t run_rounds(const GnnDev &g, const Pattern &A, int B, float *e
         const float *lng_e = ln ? w + g.ln_mp_edge[r].w : nullptr, *lnb_e = ln ? w + g.ln_mp_edge[r].b : nullptr;
         if (tc) {
             cudaError_t c = launch_mp_node_tc(n, m, B, A.rp, A.col, w + g.mp_node[r][0].w, w + g.mp_node[r][0].b,
-                                              w + g.mp_node[r][1].w, w + g.mp_node[r][1].b, lng_n, lnb_n, e, v, v2, s);
+                                              w + g.mp_node[r][1].w, w + g.mp_node[r][1].b, lng_n, lnb_n, e, v, v2,
+                                              aggbuf, s);
             if (c != cudaSuccess) return c;
         } else {
             note_launch(); mp_kernel<F, H, TE, true><<<gn, kGnnThreads, smem_node, s>>>(
@@ -645,6 +647,14 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
               ck(cudaMallocAsync((void **)&M, sizeof(double) * std::max<long long>(m * B, 1), s)) &&
               ck(cudaMallocAsync((void **)&st, sizeof(double) * (16 * B + 2 * num_sms() * (size_t)B + 8), s)) &&
               ck(cudaMallocAsync((void **)&flags, sizeof(int) * 4, s));
+    // tensor-core path: the aggregated messages of a round, formed by their own full-occupancy
+    // kernel (NPCG_GNN_AGG=0: inside the node kernel)
+    float *aggbuf = nullptr;
+    {
+        bool sep = F == 64 && g.d.h_mp == 64 && gnn_tc_enabled();
+        if (const char *env = std::getenv("NPCG_GNN_AGG")) sep = sep && std::atoi(env) != 0;
+        if (ok && sep) ok = ck(cudaMallocAsync((void **)&aggbuf, sizeof(float) * std::max<long long>((long long)n * F * B, 1), s));
+    }
     double *geo = nullptr, *dl = nullptr;  // north_star: edge geometry [dim+1][m], diag(L) [n][B]
     if (ok && ns)
         ok = ck(cudaMallocAsync((void **)&geo, sizeof(double) * std::max<long long>((long long)(g.d.dim + 1) * m, 1), s)) &&
@@ -695,11 +705,11 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
         if (ok) {
             const int hm = g.d.h_mp;
             cudaError_t c = cudaErrorInvalidValue;
-            if (F == 16 && hm == 16) c = run_rounds<16, 16, 64>(g, A, B, e, v, v2, &vfin, s);
-            else if (F == 16 && hm == 8) c = run_rounds<16, 8, 64>(g, A, B, e, v, v2, &vfin, s);
-            else if (F == 16 && hm == 32) c = run_rounds<16, 32, 64>(g, A, B, e, v, v2, &vfin, s);
-            else if (F == 64 && hm == 64) c = run_rounds<64, 64, 32>(g, A, B, e, v, v2, &vfin, s);
-            else if (F == 64 && hm == 32) c = run_rounds<64, 32, 32>(g, A, B, e, v, v2, &vfin, s);
+            if (F == 16 && hm == 16) c = run_rounds<16, 16, 64>(g, A, B, aggbuf, e, v, v2, &vfin, s);
+            else if (F == 16 && hm == 8) c = run_rounds<16, 8, 64>(g, A, B, aggbuf, e, v, v2, &vfin, s);
+            else if (F == 16 && hm == 32) c = run_rounds<16, 32, 64>(g, A, B, aggbuf, e, v, v2, &vfin, s);
+            else if (F == 64 && hm == 64) c = run_rounds<64, 64, 32>(g, A, B, aggbuf, e, v, v2, &vfin, s);
+            else if (F == 64 && hm == 32) c = run_rounds<64, 32, 32>(g, A, B, aggbuf, e, v, v2, &vfin, s);
             ok = ck(c);
         }
         double *Mout = edge_out ? edge_out : M;
@@ -727,6 +737,7 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
     cudaFreeAsync(M, s);
     cudaFreeAsync(st, s);
     cudaFreeAsync(flags, s);
+    if (aggbuf) cudaFreeAsync(aggbuf, s);
     if (geo) cudaFreeAsync(geo, s);
     if (dl) cudaFreeAsync(dl, s);
     if (!ok) return NPCG_ERR_CUDA;

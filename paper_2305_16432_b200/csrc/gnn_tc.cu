@@ -145,7 +145,8 @@ template <bool NODE>
 __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B, const int *rp, const int *src,
                                                        const int *col, const float *W1, const float *b1,
                                                        const float *W2, const float *b2, const float *ln_g,
-                                                       const float *ln_b, float *e, const float *v, float *v_out) {
+                                                       const float *ln_b, float *e, const float *v, float *v_out,
+                                                       const float *agg) {
     constexpr int kTcK1 = tc_k1<NODE>();
     using L = TcSmem<NODE>;
     constexpr int kW1Hi = L::W1Hi, kW1Lo = L::W1Lo, kW2Hi = L::W2Hi, kW2Lo = L::W2Lo, kABuf = L::ABuf;
@@ -217,8 +218,12 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
         r.vb = v + ((size_t)r.b * n) * kTcF;
         if (NODE) {
             r.xrow[0] = r.vb + (size_t)r.it * kTcF;
-            r.p0 = r.live ? rp[r.it] : 0;
-            r.p1 = r.live ? rp[r.it + 1] : 0;
+            if (agg) {  // aggregated messages formed by agg_rows_kernel: a plain row like v
+                r.xrow[1] = agg + ((size_t)r.b * n + (size_t)r.it) * kTcF;
+            } else {
+                r.p0 = r.live ? rp[r.it] : 0;
+                r.p1 = r.live ? rp[r.it + 1] : 0;
+            }
         } else {
             r.xrow[0] = r.eb + (size_t)r.it * kTcF;
             r.xrow[1] = r.vb + (size_t)(r.live ? src[r.it] : 0) * kTcF;
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
     };
     // chunk c of a row's input: 32 consecutive features
     auto load_chunk = [&](const Row &r, int c, float4 (&x)[8]) {
-        if (!NODE || c < 2) {
+        if (!NODE || c < 2 || agg) {
             const float4 *p = reinterpret_cast<const float4 *>(r.xrow[c >> 1] + (c & 1) * 32);
 #pragma unroll
             for (int j = 0; j < 8; ++j) x[j] = r.live ? p[j] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -399,11 +404,37 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// agg[b][i][:] = sum over row i's entries p of e[b][p][:] * v[b][col p][:] (gnn.py:250-251: mul,
+// segment_sum), in CSR order with one fma per term like the in-kernel form. 16 threads per
+// node, a float4 each: every load is a full 256-byte row -- the gathers are coalesced and the
+// kernel runs at full occupancy, which the 128-thread tensor-core kernel cannot offer them.
+__global__ void __launch_bounds__(256) agg_rows_kernel(int n, long long m, int B, const int *rp, const int *col,
+                                                       const float *e, const float *v, float *agg) {
+    const long long total = (long long)B * n * 16;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total; q += (long long)gridDim.x * blockDim.x) {
+        const long long node = q >> 4;
+        const int j = (int)(q & 15), b = (int)(node / n), i = (int)(node - (long long)b * n);
+        const float4 *eb = reinterpret_cast<const float4 *>(e + ((size_t)b * m) * kTcF) + j;
+        const float4 *vb = reinterpret_cast<const float4 *>(v + ((size_t)b * n) * kTcF) + j;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int p0 = rp[i], p1 = rp[i + 1];
+#pragma unroll 4
+        for (int p = p0; p < p1; ++p) {
+            const float4 a = eb[(size_t)p * (kTcF / 4)], x = vb[(size_t)col[p] * (kTcF / 4)];
+            acc.x = fmaf(a.x, x.x, acc.x);
+            acc.y = fmaf(a.y, x.y, acc.y);
+            acc.z = fmaf(a.z, x.z, acc.z);
+            acc.w = fmaf(a.w, x.w, acc.w);
+        }
+        reinterpret_cast<float4 *>(agg)[node * 16 + j] = acc;
+    }
+}
+
 template <bool NODE>
 static cudaError_t launch_mp_tc_t(int n, long long m, int B, const int *rp, const int *src, const int *col,
                                   const float *W1, const float *b1, const float *W2, const float *b2,
                                   const float *ln_g, const float *ln_b, float *e, const float *v, float *v_out,
-                                  cudaStream_t s) {
+                                  const float *agg, cudaStream_t s) {
     static bool configured = false;
     const int smem = TcSmem<NODE>::Total;
     if (!configured) {
@@ -415,21 +446,30 @@ static cudaError_t launch_mp_tc_t(int n, long long m, int B, const int *rp, cons
     const long long tiles = (items + kTcRows - 1) / kTcRows * B;
     const int grid = (int)std::max<long long>(1, std::min<long long>(tiles, num_sms()));
     note_launch();
-    mp_tc_kernel<NODE><<<grid, 128, smem, s>>>(n, m, B, rp, src, col, W1, b1, W2, b2, ln_g, ln_b, e, v, v_out);
+    mp_tc_kernel<NODE><<<grid, 128, smem, s>>>(n, m, B, rp, src, col, W1, b1, W2, b2, ln_g, ln_b, e, v, v_out, agg);
     return cudaGetLastError();
 }
 
 cudaError_t launch_mp_edge_tc(int n, long long m, int B, const int *src, const int *col, const float *W1,
                               const float *b1, const float *W2, const float *b2, const float *ln_g,
                               const float *ln_b, float *e, const float *v, cudaStream_t s) {
-    return launch_mp_tc_t<false>(n, m, B, nullptr, src, col, W1, b1, W2, b2, ln_g, ln_b, e, v, nullptr, s);
+    return launch_mp_tc_t<false>(n, m, B, nullptr, src, col, W1, b1, W2, b2, ln_g, ln_b, e, v, nullptr, nullptr, s);
 }
 
+// agg_buf: [B][n][64] floats of scratch (the aggregated messages), or null to form them inside
+// the node kernel
 cudaError_t launch_mp_node_tc(int n, long long m, int B, const int *rp, const int *col, const float *W1,
                               const float *b1, const float *W2, const float *b2, const float *ln_g,
-                              const float *ln_b, const float *e, const float *v, float *v_out, cudaStream_t s) {
+                              const float *ln_b, const float *e, const float *v, float *v_out, float *agg_buf,
+                              cudaStream_t s) {
+    if (agg_buf) {
+        const long long total = (long long)B * n * 16;
+        note_launch();
+        agg_rows_kernel<<<(int)std::min<long long>((total + 255) / 256, 16LL * num_sms()), 256, 0, s>>>(n, m, B, rp, col, e,
+                                                                                                       v, agg_buf);
+    }
     return launch_mp_tc_t<true>(n, m, B, rp, nullptr, col, W1, b1, W2, b2, ln_g, ln_b, const_cast<float *>(e), v,
-                                v_out, s);
+                                v_out, agg_buf, s);
 }
 
 }  // namespace npcg
