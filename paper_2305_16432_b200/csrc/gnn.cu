@@ -648,13 +648,10 @@ static int build_F(const GnnDev &g, const Pattern &A, int B, const double *A_val
               ck(cudaMallocAsync((void **)&st, sizeof(double) * (16 * B + 2 * num_sms() * (size_t)B + 8), s)) &&
               ck(cudaMallocAsync((void **)&flags, sizeof(int) * 4, s));
     // tensor-core path: the aggregated messages of a round, formed by their own full-occupancy
-    // kernel (NPCG_GNN_AGG=0: inside the node kernel)
+    // kernel (gnn_tc.cu agg_rows_kernel)
     float *aggbuf = nullptr;
-    {
-        bool sep = F == 64 && g.d.h_mp == 64 && gnn_tc_enabled();
-        if (const char *env = std::getenv("NPCG_GNN_AGG")) sep = sep && std::atoi(env) != 0;
-        if (ok && sep) ok = ck(cudaMallocAsync((void **)&aggbuf, sizeof(float) * std::max<long long>((long long)n * F * B, 1), s));
-    }
+    if (ok && F == 64 && g.d.h_mp == 64 && gnn_tc_enabled())
+        ok = ck(cudaMallocAsync((void **)&aggbuf, sizeof(float) * std::max<long long>((long long)n * F * B, 1), s));
     double *geo = nullptr, *dl = nullptr;  // north_star: edge geometry [dim+1][m], diag(L) [n][B]
     if (ok && ns)
         ok = ck(cudaMallocAsync((void **)&geo, sizeof(double) * std::max<long long>((long long)(g.d.dim + 1) * m, 1), s)) &&

@@ -18,8 +18,9 @@
 // the FFMA tiles give 2e-6. L' parity (1e-5 normwise) is held by
 // tests/test_gpu_parity.py and tests/test_gpu_fullsize.py.
 //
-// One persistent CTA per SM, 4 warps (128 threads = the 128 rows -- edges or
-// nodes -- of a tile, thread t owns row t). Shared memory (1024-byte
+// One persistent CTA per SM, 4 warps (128 threads; a tile is 128 rows -- edges
+// or nodes: thread t owns row t in the epilogues, the gathers are
+// warp-cooperative, eight lanes per row). Shared memory (1024-byte
 // aligned, every operand in the canonical K-major 128-byte-swizzle layout:
 // 8-row groups 1024 B apart, a row's 16-byte chunk j stored at chunk
 // j ^ (row % 8)):
@@ -27,8 +28,8 @@
 //   W2^T hi / lo [64 x 64]  16 KB each  (B operand of layer 2)
 //   two A buffers of one 32-wide K chunk, hi + lo [128 x 32] each (32 KB)
 // Per tile: the K chunks of X ([e | v_src | v_dst], or [v | agg] with agg
-// formed by the row's thread from its CSR row in stored order) are
-// gathered, split and stored while the previous chunk's MMAs run
+// formed in CSR order by agg_rows_kernel) are gathered, split and stored while
+// the previous chunk's MMAs run
 // (double-buffered, completion via tcgen05.commit -> mbarrier); layer 1
 // accumulates chunk c's big terms in TMEM columns [64 c, 64 c + 64) and all
 // corrections in [448, 512); the epilogue sums them with b1, applies ReLU,
@@ -123,15 +124,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// store 32 consecutive fp32 values (one K chunk of one row) split hi / lo
-__device__ __forceinline__ void store_split(char *hi, char *lo, int r, const float4 (&x)[8]) {
+// store a lane's eight gathered 16-byte pieces (rows r0 + 4 i, piece j of the 32-wide K chunk)
+// split hi / lo
+__device__ __forceinline__ void store_split(char *hi, char *lo, int r0, int j, const float4 (&x)[8]) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int i = 0; i < 8; ++i) {
+        const int r = r0 + 4 * i;
         float4 h, l;
-        h.x = tf32_rna(x[j].x), l.x = tf32_rna(x[j].x - h.x);
-        h.y = tf32_rna(x[j].y), l.y = tf32_rna(x[j].y - h.y);
-        h.z = tf32_rna(x[j].z), l.z = tf32_rna(x[j].z - h.z);
-        h.w = tf32_rna(x[j].w), l.w = tf32_rna(x[j].w - h.w);
+        h.x = tf32_rna(x[i].x), l.x = tf32_rna(x[i].x - h.x);
+        h.y = tf32_rna(x[i].y), l.y = tf32_rna(x[i].y - h.y);
+        h.z = tf32_rna(x[i].z), l.z = tf32_rna(x[i].z - h.z);
+        h.w = tf32_rna(x[i].w), l.w = tf32_rna(x[i].w - h.w);
         *reinterpret_cast<float4 *>(hi + sw128(r, j)) = h;
         *reinterpret_cast<float4 *>(lo + sw128(r, j)) = l;
     }
@@ -201,59 +204,46 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
     uint32_t use[2] = {0, 0}, ph2 = 0;  // completed-use counts (mbarrier parity)
     const long long items = NODE ? (long long)n : m;
     const long long tiles_per = (items + kTcRows - 1) / kTcRows, tiles = tiles_per * B;
-    // a tile's row of this thread: where its input chunks come from
-    struct Row {
-        int b = 0, p0 = 0, p1 = 0;
-        long long it = 0;
+    // Gathers are warp-cooperative: warp w stages rows 32 w .. 32 w + 31 of a tile, eight lanes
+    // per row (lane l: row 4 i + l / 8 of the warp at its i-th load, 16-byte piece l % 8 of the
+    // 128-byte chunk), so one load instruction fetches four complete 128-byte lines instead of
+    // a 16-byte piece of 32 lines. A lane keeps its eight rows' indices, not pointers.
+    const int lane = t & 31, piece = lane & 7, rsub = lane >> 3;
+    struct Rows {
+        int b = 0;
+        long long it = 0;        // this THREAD's row (epilogue: TMEM lane = row t)
         bool live = false;
-        const float *eb = nullptr, *vb = nullptr, *xrow[3] = {nullptr, nullptr, nullptr};
+        unsigned mask = 0;       // bit i: the lane's i-th gathered row exists
+        int i0[8], i1[8], i2[8];  // row index per source: e | v_src | v_dst (edge), v | agg (node)
     };
     auto setup = [&](long long tile) {
-        Row r;
+        Rows r;
         r.b = (int)(tile / tiles_per);
-        const long long item = (tile % tiles_per) * kTcRows + t;
-        r.live = item < items;
-        r.it = r.live ? item : 0;
-        r.eb = e + ((size_t)r.b * m) * kTcF;
-        r.vb = v + ((size_t)r.b * n) * kTcF;
-        if (NODE) {
-            r.xrow[0] = r.vb + (size_t)r.it * kTcF;
-            if (agg) {  // aggregated messages formed by agg_rows_kernel: a plain row like v
-                r.xrow[1] = agg + ((size_t)r.b * n + (size_t)r.it) * kTcF;
-            } else {
-                r.p0 = r.live ? rp[r.it] : 0;
-                r.p1 = r.live ? rp[r.it + 1] : 0;
-            }
-        } else {
-            r.xrow[0] = r.eb + (size_t)r.it * kTcF;
-            r.xrow[1] = r.vb + (size_t)(r.live ? src[r.it] : 0) * kTcF;
-            r.xrow[2] = r.vb + (size_t)(r.live ? col[r.it] : 0) * kTcF;
+        const long long row0 = (tile % tiles_per) * kTcRows;
+        r.live = row0 + t < items;
+        r.it = r.live ? row0 + t : 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const long long item = row0 + warp * 32 + 4 * i + rsub;
+            const bool ok = item < items;
+            r.mask |= ok ? 1u << i : 0u;
+            r.i0[i] = ok ? (int)item : 0;
+            r.i1[i] = NODE ? r.i0[i] : (ok ? src[item] : 0);
+            r.i2[i] = NODE ? 0 : (ok ? col[item] : 0);
         }
         return r;
     };
-    // chunk c of a row's input: 32 consecutive features
-    auto load_chunk = [&](const Row &r, int c, float4 (&x)[8]) {
-        if (!NODE || c < 2 || agg) {
-            const float4 *p = reinterpret_cast<const float4 *>(r.xrow[c >> 1] + (c & 1) * 32);
+    // chunk c (32 consecutive features) of the lane's eight rows
+    auto load_chunk = [&](const Rows &r, int c, float4 (&x)[8]) {
+        const int sidx = c >> 1;
+        const float *base = NODE ? (sidx == 0 ? v + ((size_t)r.b * n) * kTcF : agg + ((size_t)r.b * n) * kTcF)
+                                 : (sidx == 0 ? e + ((size_t)r.b * m) * kTcF : v + ((size_t)r.b * n) * kTcF);
+        const int off = (c & 1) * 32 + piece * 4;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = r.live ? p[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {  // agg_i = sum_p e_p * v_col(p), CSR order (autodiff.py:174, 209, 221-243)
-            const int f0 = (c & 1) * 32;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 2
-            for (int p = r.p0; p < r.p1; ++p) {
-                const float4 *ep = reinterpret_cast<const float4 *>(r.eb + (size_t)p * kTcF + f0);
-                const float4 *vp = reinterpret_cast<const float4 *>(r.vb + (size_t)col[p] * kTcF + f0);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float4 a = ep[j], q = vp[j];
-                    x[j].x = fmaf(a.x, q.x, x[j].x);
-                    x[j].y = fmaf(a.y, q.y, x[j].y);
-                    x[j].z = fmaf(a.z, q.z, x[j].z);
-                    x[j].w = fmaf(a.w, q.w, x[j].w);
-                }
-            }
+        for (int i = 0; i < 8; ++i) {
+            const int idx = sidx == 0 ? r.i0[i] : (sidx == 1 ? r.i1[i] : r.i2[i]);
+            x[i] = (r.mask >> i) & 1u ? *reinterpret_cast<const float4 *>(base + (size_t)idx * kTcF + off)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
     // Row loads run kTcAhead chunks ahead of the MMAs (the kernel is bound by the latency of
@@ -262,7 +252,7 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
     constexpr int kNC = kTcK1 / 32;
     constexpr int kPre = kTcAhead < 2 ? kTcAhead : 2;  // chunks fetched across the tile boundary (plain row loads)
     float4 xq[kTcAhead + 1][8];
-    Row cur;
+    Rows cur;
     if ((long long)blockIdx.x < tiles) {
         cur = setup(blockIdx.x);
 #pragma unroll
@@ -280,7 +270,7 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
             const int u = c & 1;
             if (c + kTcAhead < kNC) load_chunk(cur, c + kTcAhead, xq[(c + kTcAhead) % (kTcAhead + 1)]);
             if (use[u] > 0) mbar_wait(&bar[u], (use[u] - 1) & 1);  // the MMAs that last read this buffer are done
-            store_split(abuf(u, 0), abuf(u, 1), t, xq[c % (kTcAhead + 1)]);
+            store_split(abuf(u, 0), abuf(u, 1), warp * 32 + rsub, piece, xq[c % (kTcAhead + 1)]);
             fence_proxy_async();
             __syncthreads();
             if (t == 0) {
@@ -300,7 +290,7 @@ __global__ void __launch_bounds__(128, 1) mp_tc_kernel(int n, long long m, int B
         }
         // the next tile's first chunks: in flight during this tile's epilogues
         const long long ntile = tile + gridDim.x;
-        Row nxt;
+        Rows nxt;
         if (ntile < tiles) {
             nxt = setup(ntile);
 #pragma unroll
@@ -456,18 +446,16 @@ cudaError_t launch_mp_edge_tc(int n, long long m, int B, const int *src, const i
     return launch_mp_tc_t<false>(n, m, B, nullptr, src, col, W1, b1, W2, b2, ln_g, ln_b, e, v, nullptr, nullptr, s);
 }
 
-// agg_buf: [B][n][64] floats of scratch (the aggregated messages), or null to form them inside
-// the node kernel
+// agg_buf: [B][n][64] floats of scratch (the aggregated messages)
 cudaError_t launch_mp_node_tc(int n, long long m, int B, const int *rp, const int *col, const float *W1,
                               const float *b1, const float *W2, const float *b2, const float *ln_g,
                               const float *ln_b, const float *e, const float *v, float *v_out, float *agg_buf,
                               cudaStream_t s) {
-    if (agg_buf) {
-        const long long total = (long long)B * n * 16;
-        note_launch();
-        agg_rows_kernel<<<(int)std::min<long long>((total + 255) / 256, 16LL * num_sms()), 256, 0, s>>>(n, m, B, rp, col, e,
-                                                                                                       v, agg_buf);
-    }
+    if (!agg_buf) return cudaErrorInvalidValue;
+    const long long total = (long long)B * n * 16;
+    note_launch();
+    agg_rows_kernel<<<(int)std::min<long long>((total + 255) / 256, 16LL * num_sms()), 256, 0, s>>>(n, m, B, rp, col, e, v,
+                                                                                                   agg_buf);
     return launch_mp_tc_t<true>(n, m, B, rp, nullptr, col, W1, b1, W2, b2, ln_g, ln_b, const_cast<float *>(e), v,
                                 v_out, agg_buf, s);
 }
