@@ -13,3 +13,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 420 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ldlt_line|spmv_ell_kernel<7, 0, 1>|pupd_ell|mp_tc_kernel" -s 10 -c 5 -o gpurun_out/r2_prof_final python bench.py --profile-only > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
 ncu -i gpurun_out/r2_prof_final.ncu-rep --page details > gpurun_out/r2_prof_final_details.txt 2>&1
 ncu -i gpurun_out/r2_prof_final.ncu-rep --page raw --csv > gpurun_out/r2_prof_final_raw.csv 2>&1
+CFG=4 timeout 700 python tools/bench_3d.py > gpurun_out/bench_cfg4.log 2>&1; echo c4=$?
+CFG=5 timeout 1500 python tools/bench_3d.py > gpurun_out/bench_cfg5.log 2>&1; echo c5=$?
+timeout 300 python tools/bench_train.py > gpurun_out/bench_train.log 2>&1; echo train=$?
