@@ -203,40 +203,67 @@ __global__ void __launch_bounds__(kGnnThreads) encode_kernel(long long count, in
         sb[k] = ln_b ? ln_b[k] : 0.f;
     }
     __syncthreads();
-    const long long total = count * B;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
-         q += (long long)gridDim.x * blockDim.x) {
-        const int b = (int)(q / count);
-        const long long i = q % count;
-        float xf[WIN];
+    // two rows per thread: every weight read from shared memory feeds two rows' FMAs (the
+    // broadcast loads are what the one-row form waits on)
+    constexpr int R = 2;
+    const long long total = count * B, pairs = (total + R - 1) / R;
+    for (long long qp = blockIdx.x * (long long)blockDim.x + threadIdx.x; qp < pairs;
+         qp += (long long)gridDim.x * blockDim.x) {
+        float xf[R][WIN];
+        bool on[R];
 #pragma unroll
-        for (int k = 0; k < WIN; ++k) {
-            double xv = in.xb[k] ? in.x[k][(size_t)i * B + b] : in.x[k][i];
-            if (normalize) xv = (xv - in.mean[k][b]) / in.sd[k][b];
-            xf[k] = (float)xv;
+        for (int r = 0; r < R; ++r) {
+            const long long q = qp * R + r;
+            on[r] = q < total;
+            const long long qq = on[r] ? q : 0;
+            const int b = (int)(qq / count);
+            const long long i = qq % count;
+#pragma unroll
+            for (int k = 0; k < WIN; ++k) {
+                double xv = in.xb[k] ? in.x[k][(size_t)i * B + b] : in.x[k][i];
+                if (normalize) xv = (xv - in.mean[k][b]) / in.sd[k][b];
+                xf[r][k] = (float)xv;
+            }
         }
-        float acc[F];
+        float acc[R][F];
 #pragma unroll
-        for (int f = 0; f < F; ++f) acc[f] = sb2[f];
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int f = 0; f < F; ++f) acc[r][f] = sb2[f];
         for (int k = 0; k < h; ++k) {
-            float a = sb1[k];
+            float hk[R];
 #pragma unroll
-            for (int c = 0; c < WIN; ++c) a = fmaf(xf[c], sW1[c * h + k], a);
-            const float hk = fmaxf(a, 0.0f);
+            for (int r = 0; r < R; ++r) {
+                float a = sb1[k];
+#pragma unroll
+                for (int c = 0; c < WIN; ++c) a = fmaf(xf[r][c], sW1[c * h + k], a);
+                hk[r] = fmaxf(a, 0.0f);
+            }
             const float4 *w4 = reinterpret_cast<const float4 *>(sW2 + k * F);
 #pragma unroll
             for (int f4 = 0; f4 < F / 4; ++f4) {
                 const float4 w = w4[f4];
-                acc[4 * f4 + 0] = fmaf(hk, w.x, acc[4 * f4 + 0]);
-                acc[4 * f4 + 1] = fmaf(hk, w.y, acc[4 * f4 + 1]);
-                acc[4 * f4 + 2] = fmaf(hk, w.z, acc[4 * f4 + 2]);
-                acc[4 * f4 + 3] = fmaf(hk, w.w, acc[4 * f4 + 3]);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    acc[r][4 * f4 + 0] = fmaf(hk[r], w.x, acc[r][4 * f4 + 0]);
+                    acc[r][4 * f4 + 1] = fmaf(hk[r], w.y, acc[r][4 * f4 + 1]);
+                    acc[r][4 * f4 + 2] = fmaf(hk[r], w.z, acc[r][4 * f4 + 2]);
+                    acc[r][4 * f4 + 3] = fmaf(hk[r], w.w, acc[r][4 * f4 + 3]);
+                }
             }
         }
-        if (ln_g) layer_norm_row<F>(acc, sg, sb);
-        float4 *o4 = reinterpret_cast<float4 *>(out + ((size_t)b * count + i) * F);
 #pragma unroll
-        for (int f4 = 0; f4 < F / 4; ++f4) o4[f4] = make_float4(acc[4 * f4], acc[4 * f4 + 1], acc[4 * f4 + 2], acc[4 * f4 + 3]);
+        for (int r = 0; r < R; ++r) {
+            if (!on[r]) continue;
+            const long long q = qp * R + r;
+            const int b = (int)(q / count);
+            const long long i = q % count;
+            if (ln_g) layer_norm_row<F>(acc[r], sg, sb);
+            float4 *o4 = reinterpret_cast<float4 *>(out + ((size_t)b * count + i) * F);
+#pragma unroll
+            for (int f4 = 0; f4 < F / 4; ++f4)
+                o4[f4] = make_float4(acc[r][4 * f4], acc[r][4 * f4 + 1], acc[r][4 * f4 + 2], acc[r][4 * f4 + 3]);
+        }
     }
 }
 
@@ -414,36 +441,59 @@ __global__ void __launch_bounds__(kGnnThreads) decode_kernel(long long count, in
     }
     __syncthreads();
     const float bout = b2[0];
-    const long long total = count * B;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
-         q += (long long)gridDim.x * blockDim.x) {
-        const int b = (int)(q / count);
-        const long long i = q % count;
-        float xr[F];
-        const float4 *x4 = reinterpret_cast<const float4 *>(x + ((size_t)b * count + i) * F);
+    constexpr int R = 2;  // rows per thread (see encode_kernel)
+    const long long total = count * B, pairs = (total + R - 1) / R;
+    for (long long qp = blockIdx.x * (long long)blockDim.x + threadIdx.x; qp < pairs;
+         qp += (long long)gridDim.x * blockDim.x) {
+        float xr[R][F];
+        bool on[R];
 #pragma unroll
-        for (int f4 = 0; f4 < F / 4; ++f4) {
-            const float4 t = x4[f4];
-            xr[4 * f4] = t.x;
-            xr[4 * f4 + 1] = t.y;
-            xr[4 * f4 + 2] = t.z;
-            xr[4 * f4 + 3] = t.w;
+        for (int r = 0; r < R; ++r) {
+            const long long q = qp * R + r;
+            on[r] = q < total;
+            const long long qq = on[r] ? q : 0;
+            const int b = (int)(qq / count);
+            const long long i = qq % count;
+            const float4 *x4 = reinterpret_cast<const float4 *>(x + ((size_t)b * count + i) * F);
+#pragma unroll
+            for (int f4 = 0; f4 < F / 4; ++f4) {
+                const float4 t = x4[f4];
+                xr[r][4 * f4] = t.x;
+                xr[r][4 * f4 + 1] = t.y;
+                xr[r][4 * f4 + 2] = t.z;
+                xr[r][4 * f4 + 3] = t.w;
+            }
         }
-        float o = bout;
+        float o[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) o[r] = bout;
         for (int k = 0; k < h; ++k) {
-            float a = sb1[k];
+            float a[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) a[r] = sb1[k];
             const float4 *w4 = reinterpret_cast<const float4 *>(sW1T + k * F);
 #pragma unroll
             for (int f4 = 0; f4 < F / 4; ++f4) {
                 const float4 w = w4[f4];
-                a = fmaf(xr[4 * f4], w.x, a);
-                a = fmaf(xr[4 * f4 + 1], w.y, a);
-                a = fmaf(xr[4 * f4 + 2], w.z, a);
-                a = fmaf(xr[4 * f4 + 3], w.w, a);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    a[r] = fmaf(xr[r][4 * f4], w.x, a[r]);
+                    a[r] = fmaf(xr[r][4 * f4 + 1], w.y, a[r]);
+                    a[r] = fmaf(xr[r][4 * f4 + 2], w.z, a[r]);
+                    a[r] = fmaf(xr[r][4 * f4 + 3], w.w, a[r]);
+                }
             }
-            o = fmaf(fmaxf(a, 0.0f), sW2[k], o);
+#pragma unroll
+            for (int r = 0; r < R; ++r) o[r] = fmaf(fmaxf(a[r], 0.0f), sW2[k], o[r]);
         }
-        out[(size_t)i * B + b] = (double)o;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (!on[r]) continue;
+            const long long q = qp * R + r;
+            const int b = (int)(q / count);
+            const long long i = q % count;
+            out[(size_t)i * B + b] = (double)o[r];
+        }
     }
 }
 
